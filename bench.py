@@ -1,0 +1,363 @@
+"""Benchmark of the RSR hot path on B200 (driver contract: one JSON line).
+
+Default workload (N=1): BASELINE config 1 -- ternary 16384x16384 RSR matvec,
+bf16 vector, k=6 (the k with the fewest artifact bytes), seed 0, matrix from
+the reference generator (bench.py:102-113 of rsrmv).  A "step" is one
+single-vector multiply.  ``value`` is matvecs/s with the artifact resident
+in HBM; L2 is defeated by rotating >= 3 artifact copies (each ~92 MB, L2 is
+126 MB).  ``e2e`` is the same metric through the public API with a host
+(numpy float32) vector and a host result.
+
+--gpus N > 1 (torchrun): the same matrix is row-block sharded (balanced by
+stream bytes) and each step ends with an NCCL all-gather of the output
+slices (strong scaling).  --impl reference times the CPU restatement of the
+reference float path (oracle/, all host cores) on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(workload="ternary 16384x16384 RSR matvec, bf16 vector, single vector",
+               m=16384, n=16384, bitwidth="ternary", k=6, vdtype="bf16"),
+    "c1": dict(workload="binary 4096x4096 RSR matvec, fp32 vector, k=8",
+               m=4096, n=4096, bitwidth="binary", k=8, vdtype="f32"),
+    "c4": dict(workload="ternary 8192x8192 RSR matvec, bf16 vector, single vector",
+               m=8192, n=8192, bitwidth="ternary", k=5, vdtype="bf16"),
+}
+METRIC = "ternary matvec/s & %HBM roofline at 16384^2"
+UNIT = "matvec/s"
+
+
+def random_packed(m, n, bitwidth, seed, density=0.5):
+    """Reference generator (rsrmv bench.py:102-113) + packing (matcore.py:114-125)."""
+    rng = np.random.default_rng(seed)
+    u = rng.random((m, n))
+    if bitwidth == "binary":
+        ent = (u < density).astype(np.uint8)
+        return np.packbits(ent, axis=1, bitorder="little")
+    codes = (u < density / 2).astype(np.uint8) | ((u > 1 - density / 2).astype(np.uint8) << 1)
+    del u
+    pad = (-n) % 4
+    if pad:
+        codes = np.concatenate([codes, np.zeros((m, pad), np.uint8)], axis=1)
+    c4 = codes.reshape(m, -1, 4)
+    return np.ascontiguousarray(c4[:, :, 0] | (c4[:, :, 1] << 2) | (c4[:, :, 2] << 4)
+                                | (c4[:, :, 3] << 6))
+
+
+def random_vector(n, seed):
+    """rsrmv bench.py:116-117."""
+    return np.random.default_rng(seed ^ 0x5EED).standard_normal(n).astype(np.float32)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_run(cfg, steps, warmup, seconds=None):
+    """Time the CPU restatement of the reference float path (oracle/, all
+    host threads; float64 accumulation exactly as rsrmv matvec_f32)."""
+    from oracle import rsr_oracle as orc
+    data = random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0)
+    p = orc.Packed(cfg["m"], cfg["n"], cfg["bitwidth"], data)
+    a = orc.preprocess(p, cfg["k"])
+    v = random_vector(cfg["n"], 0)
+    if cfg["vdtype"] == "bf16":
+        b = v.view(np.uint32).astype(np.uint64)
+        v = ((((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16).astype(np.uint32)).view(np.float32)
+    threads = orc.max_threads()
+    for _ in range(max(warmup, 1)):
+        orc.matvec_f32(a, v, threads=threads)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        orc.matvec_f32(a, v, threads=threads)
+        n += 1
+        el = time.perf_counter() - t0
+        if (seconds is None and n >= steps) or (seconds is not None and el >= seconds):
+            break
+    return n / el, threads, n, el
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.k:
+        cfg["k"] = args.k
+    warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    config = {"workload": cfg["workload"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
+              "bitwidth": cfg["bitwidth"], "vector_dtype": cfg["vdtype"], "seed": 0,
+              "density": 0.5}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        val, threads, n, el = cpu_reference_run(cfg, args.steps, warmup)
+        line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": n, "warmup": warmup, "ms_per_step": 1e3 * el / n,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (rsrmv random_matrix seed 0)",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+                                 "sample": f"{n} full {cfg['m']}x{cfg['n']} float-path "
+                                           f"matvecs (C restatement of rsrmv matvec_f32, "
+                                           f"block-parallel, float64 accumulation)"},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2603_27462_b200 as rsr
+    from paper_2603_27462_b200 import kernels as kn
+    from paper_2603_27462_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    data = random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0)
+    mat = rsr.PackedMatrix(cfg["m"], cfg["n"], cfg["bitwidth"], data)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a = rsr.preprocess(mat, cfg["k"])
+    torch.cuda.synchronize()
+    preprocess_ms = 1e3 * (time.perf_counter() - t0)
+    del data
+
+    # ---- shard by stream bytes (row blocks), one contiguous range per rank
+    bc = a.plan.block_count
+    if world > 1:
+        e_off = a.e_off_d.cpu().numpy()
+        tc = a.plan.tile_count
+        cum = e_off[::tc]  # entry offset at the start of each block
+        bounds = [0] + [int(np.searchsorted(cum, cum[-1] * r / world)) for r in range(1, world)] + [bc]
+        b0, b1 = bounds[rank], bounds[rank + 1]
+    else:
+        b0, b1 = 0, bc
+    nb = b1 - b0
+    k = cfg["k"]
+    rows_per_rank = -(-bc // world) * k  # padded slice for the all-gather
+
+    # ---- L2 defeat: rotate copies of the stream arrays
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    sb = a.stream_bytes() * nb // max(bc, 1)
+    ncopies = int(max(3, min(16, -(-3 * l2 // max(sb, 1)))))
+    views, keep = [], []
+    for c in range(ncopies):
+        if c == 0:
+            ent, gs, eo, go = a.entries_d, a.gsigns_d, a.e_off_d, a.g_off_d
+        else:
+            ent, gs, eo, go = (a.entries_d.clone(), a.gsigns_d.clone(), a.e_off_d.clone(),
+                               a.g_off_d.clone())
+        keep.append((ent, gs, eo, go))
+        v = a.view(b0, nb)
+        v.entries, v.gsigns = _lib.ptr(ent), _lib.ptr(gs)
+        v.e_off = _lib.ptr(eo) + 8 * b0 * a.plan.tile_count
+        v.g_off = _lib.ptr(go) + 8 * b0 * a.plan.tile_count
+        views.append(v)
+
+    vf = random_vector(cfg["n"], 0)
+    vt = torch.from_numpy(vf).to(dev)
+    if cfg["vdtype"] == "bf16":
+        vt = vt.to(torch.bfloat16)
+    y_local = torch.zeros(rows_per_rank, dtype=torch.float32, device=dev)
+    y_all = torch.zeros(rows_per_rank * world, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+
+    def step(i):
+        kn.matvec_into(a, vt, y_local, view=views[i % ncopies], stream=sptr)
+        if world > 1:
+            dist.all_gather_into_tensor(y_all, y_local)
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # per-launch kernel durations (CUDA events on the launching stream)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(min(args.steps, 100))]
+    for i, (e0, e1) in enumerate(kev):
+        e0.record(stream)
+        kn.matvec_into(a, vt, y_local, view=views[i % ncopies], stream=sptr)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    kernel_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in kev]))
+
+    # ---- timed region: exactly K steps
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        end.record(stream)
+        torch.cuda.synchronize()
+        # keep the GPU loaded for the sampler's benefit (untimed)
+        t_hold = time.perf_counter()
+        while time.perf_counter() - t_hold < 0.5:
+            for i in range(50):
+                step(i)
+            torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    total_ms = start.elapsed_time(end)
+    if dist:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = 1e3 / ms_per_step  # matvecs/s of the whole job (each step = one full matvec)
+
+    # ---- e2e through the public API with host buffers (rank 0, unsharded)
+    e2e = None
+    if rank == 0:
+        vh = vf.copy()
+        for _ in range(5):
+            rsr.rsr_matvec(a, vh)
+        torch.cuda.synchronize()
+        ne = max(20, min(args.steps, 200))
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            yh = rsr.rsr_matvec(a, vh)
+        e2e_s = (time.perf_counter() - t0) / ne
+        e2e = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(vh.nbytes),
+               "d2h_bytes_per_step": int(yh.nbytes),
+               "api": "paper_2603_27462_b200.rsr_matvec(artifact, numpy float32 v)"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    hbm, peak_kind = peaks()
+    vbytes = 2 if cfg["vdtype"] == "bf16" else 4
+    alg_bytes = (a.file_bytes() - 24) + cfg["n"] * vbytes + cfg["m"] * 4
+    if world > 1:
+        alg_bytes = alg_bytes * nb // bc
+    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+    own_bytes = a.stream_bytes() * nb // bc + cfg["n"] * vbytes + nb * k * 4
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.config}_k{k}")
+    except Exception:
+        pass
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+            "algorithmic_bytes": int(alg_bytes), "stream_bytes": int(own_bytes),
+            "achieved_own_bytes_gbs": own_bytes / (kernel_ms * 1e-3) / 1e9,
+            "kernel_us": kernel_ms * 1e3, "frac_of_8TBs_nominal": achieved / 8000.0}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        val, threads, n, el = cpu_reference_run(cfg, 0, 1, seconds=args.cpu_seconds)
+        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{n} full {cfg['m']}x{cfg['n']} float-path matvecs in {el:.1f}s "
+                         f"(C restatement of rsrmv matvec_f32, block-parallel, f64 accum)"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": dict(config, l2_defeat=f"rotating {ncopies} stream copies "
+                                              f"({sb / 1e6:.1f} MB each, L2 {l2 / 1e6:.0f} MB)",
+                           parallelism=f"rowblock{world}" if world > 1 else "single"),
+            "preprocess_ms": preprocess_ms, "gpu_launches": args.steps,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,151 @@
+/*
+ * rsr_b200.h -- C ABI of the B200-native (sm_100a) RSR matvec library.
+ *
+ * Drop-in boundary for the reference package `rsrmv`'s native seam
+ * (pkg/src/rsrmv/_native.py): the reference binds flat numpy arrays and
+ * scalars into numba cores; this library takes flat DEVICE arrays, sizes and
+ * a cudaStream_t.  No torch types cross this boundary.  Every entry point is
+ * stream-ordered, never synchronizes, never allocates, and returns an
+ * rsr_status (0 = success).  The Python shim (paper_2603_27462_b200/_lib.py)
+ * maps status codes onto the reference's exception kinds
+ * (pkg/src/rsrmv/errors.py:23-74).
+ *
+ * Layout conventions follow the reference exactly:
+ *   packed matrix : uint8[rows][row_bytes], row-major, LSB-first;
+ *                   binary 1 bit/entry, ternary 2-bit codes 0->00 +1->01 -1->10
+ *                   (matcore.py:24-26, :77-78, :114-125)
+ *   group word    : u64 = perm_start | perm_len<<16 | pos_mask<<32 | neg_mask<<48
+ *                   (_native.py:4-9, preproc.py:31-41)
+ *   cells         : tile-major, cell = t * block_count + b (preproc.py:120-122)
+ *
+ * The multiply kernels consume a device-only "stream" layout derived from the
+ * reference arrays once per artifact (rsr_stream_build): block-major cells,
+ * u16 entries = tile-local column | head-of-group<<15 (u32 entries with bit
+ * 31 for tiles wider than 32768 columns), a u32 sign word per group
+ * (pos | neg<<16), every cell padded to 32 bytes of entries.  See DESIGN.md.
+ */
+#ifndef RSR_B200_H
+#define RSR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *rsr_stream_t; /* a cudaStream_t */
+
+typedef enum {
+    RSR_OK = 0,
+    RSR_ERR_TILE_TOO_WIDE = 1,  /* a group longer than 65535 columns (preproc.py:271-276) */
+    RSR_ERR_K_TOO_LARGE = 2,    /* k above 16 binary / 10 ternary (preproc.py:102-103) */
+    RSR_ERR_INVALID = 3,        /* bad argument (shape, null pointer, dtype) */
+    RSR_ERR_DIMENSION = 4,      /* vector length != columns (kernels.py:52-56) */
+    RSR_ERR_CUDA = 5,           /* a CUDA launch failed; see rsr_last_cuda_error() */
+    RSR_ERR_WORKSPACE = 6       /* workspace smaller than the *_workspace_bytes() query */
+} rsr_status;
+
+typedef enum { RSR_BINARY = 0, RSR_TERNARY = 1 } rsr_bitwidth;
+
+/* Element types of vectors crossing the boundary. */
+typedef enum {
+    RSR_F32 = 0,
+    RSR_BF16 = 1,
+    RSR_F16 = 2,
+    RSR_I8 = 3,
+    RSR_I32 = 4
+} rsr_dtype;
+
+/* Device view of a matrix's stream layout (built by rsr_stream_build). */
+typedef struct {
+    int64_t m, n;              /* rows, cols */
+    int32_t k, bitwidth;       /* block height, rsr_bitwidth */
+    int64_t tile_width, block_count, tile_count;
+    int32_t entry_bytes;       /* 2 (u16 entries) or 4 (u32 entries, tile_width > 32768) */
+    int32_t reserved;
+    const void *entries;       /* device, entry_bytes each */
+    const uint32_t *gsigns;    /* device, one sign word per group (incl. padding groups) */
+    const int64_t *e_off;      /* device, cells+1 entry offsets, block-major cell order */
+    const int64_t *g_off;      /* device, cells+1 group offsets, block-major cell order */
+    int64_t row_begin_block;   /* first block this view covers (row-block sharding) */
+    int64_t n_blocks;          /* blocks covered (== block_count unless sharded) */
+} rsr_stream_view;
+
+/* ---- library info ---------------------------------------------------- */
+const char *rsr_version(void);
+const char *rsr_last_cuda_error(void);
+int rsr_device_sm_count(int device);
+
+/* ---- offline preprocessing ------------------------------------------------
+ * Replaces preproc.preprocess's per-cell loop over
+ * _native.group_block_{binary,ternary} (preproc.py:239-289,
+ * _native.py:25-161).  Two phases so the caller can size the outputs:
+ *   1. rsr_group_count: per-cell group / retained counts, exclusive-scanned
+ *      into go[cells+1] and po[cells+1] (int64, device), plus per-cell
+ *      sort_steps exactly as the reference tallies them.  *status_dev
+ *      (int32, device) receives RSR_ERR_TILE_TOO_WIDE when any group would
+ *      exceed 65535 columns.
+ *   2. rsr_group_fill: words[go[cells]] and perm[po[cells]], byte-identical to
+ *      the reference artifact.
+ * data is the packed matrix on the device (uint8[rows][row_bytes]).       */
+size_t rsr_group_workspace_bytes(int64_t rows, int64_t cols, int32_t bitwidth, int32_t k,
+                                 int64_t tile_width);
+rsr_status rsr_group_count(const uint8_t *data, int64_t rows, int64_t cols, int64_t row_bytes,
+                           int32_t bitwidth, int32_t k, int64_t tile_width,
+                           int64_t *go, int64_t *po, int64_t *sort_steps, int32_t *status_dev,
+                           void *workspace, size_t workspace_bytes, rsr_stream_t stream);
+rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64_t row_bytes,
+                          int32_t bitwidth, int32_t k, int64_t tile_width,
+                          const int64_t *go, const int64_t *po, uint64_t *words, uint16_t *perm,
+                          void *workspace, size_t workspace_bytes, rsr_stream_t stream);
+
+/* ---- stream layout (device-only multiply format) ----------------------------
+ * rsr_stream_count fills e_off/g_off (cells+1, block-major); the caller reads
+ * e_off[cells], g_off[cells] to size entries/gsigns, then rsr_stream_build
+ * fills them from the reference arrays.                                      */
+rsr_status rsr_stream_count(const int64_t *go, const int64_t *po, int64_t block_count,
+                            int64_t tile_count, int32_t entry_bytes, int64_t *e_off,
+                            int64_t *g_off, rsr_stream_t stream);
+rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                            const int64_t *po, int64_t block_count, int64_t tile_count,
+                            int32_t entry_bytes, const int64_t *e_off, const int64_t *g_off,
+                            void *entries, uint32_t *gsigns, rsr_stream_t stream);
+
+/* ---- online multiply --------------------------------------------------------
+ * rsr_matvec: y (+)= A . v  over the view's row blocks.
+ *   v dtype RSR_I8  -> y int32, exact   (replaces _native.matvec_i8 /
+ *                                        matvec_i8_par, _native.py:167-285)
+ *   v dtype F32/BF16/F16 -> y float32, fp32 accumulation (replaces
+ *                                        _native.matvec_f32, _native.py:214-242)
+ * y holds rows [row_begin_block*k, ...) of the full output; accumulate=0
+ * overwrites, 1 adds (the reference cores add into caller-zeroed y).
+ * workspace: rsr_matvec_workspace_bytes(view) bytes of device scratch
+ * (only needed when tile_count > 1).                                         */
+size_t rsr_matvec_workspace_bytes(const rsr_stream_view *view);
+rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtype, void *y,
+                      int32_t accumulate, void *workspace, size_t workspace_bytes,
+                      rsr_stream_t stream);
+
+/* rsr_fused_matvec: absmax-quantize v (float64 math, half away from zero,
+ * +-127), exact int32 multiply, out[i] = f32(f64(y_i) * (beta / scale)).
+ * Bit-identical to _native.fused_matvec (_native.py:339-353).  The
+ * quantization is fused into every CTA's prologue (no separate pass).
+ * scale_out (device f64, may be NULL) receives the activation scale.       */
+rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtype,
+                            double beta, float *out, double *scale_out, void *workspace,
+                            size_t workspace_bytes, rsr_stream_t stream);
+
+/* ---- helpers ---------------------------------------------------------------- */
+/* _native.count_ops (_native.py:288-307): out3 (device int64[3]) =
+ * gather adds, scatter adds, groups.                                         */
+rsr_status rsr_count_ops(const uint64_t *words, int64_t n_words, int64_t *out3,
+                         rsr_stream_t stream);
+/* _native.absmax_quantize (_native.py:313-336): q int8[n], *scale_out f64.  */
+rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t *q,
+                               double *scale_out, rsr_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSR_B200_H */

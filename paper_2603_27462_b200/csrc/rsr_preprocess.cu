@@ -1,0 +1,470 @@
+// rsr_preprocess.cu -- GPU offline preprocessing, bit-exact with the reference.
+//
+// Replaces the per-cell counting sort of the reference
+// (pkg/src/rsrmv/_native.py:25-161, driven by preproc.py:239-289).  One warp
+// owns one (tile, block) cell:
+//   1. pattern keys of the cell's columns (binary: 2^i weights; ternary:
+//      base-3 digits, whose order equals the reference's 4^h code-key order),
+//   2. a histogram in a warp-private table (shared memory, or global scratch
+//      for the 3^9 / 3^10 / 2^13.. pattern spaces),
+//   3. an ascending-key exclusive scan over the non-zero keys that emits the
+//      group words in key order (ballot compaction),
+//   4. a STABLE scatter of column ids: columns are visited in ascending order
+//      32 at a time; __match_any_sync ranks equal keys inside the chunk and
+//      the chunk leader advances the bucket cursor, so columns of one group
+//      land in ascending order exactly as the serial counting sort puts them.
+// Two launches (count, fill) bracket an int64 scan so outputs are sized
+// exactly; the stream-layout builder for the multiply kernels lives here too.
+
+#include "rsr_common.cuh"
+
+namespace rsr {
+
+constexpr int PP_WARPS = 8;                    // warps (cells in flight) per CTA
+constexpr int64_t PP_SMEM_TABLE_MAX = 6144;    // buckets per warp kept in smem
+
+// Pattern key of tile-local column j of the block starting at row r0.
+// Ternary keys are base-3 (digit = 2-bit code); *bad is set on code 3.
+__device__ __forceinline__ uint32_t column_key(const uint8_t *__restrict__ data,
+                                               int64_t row_bytes, int64_t r0, int h,
+                                               int64_t c, int bitwidth, bool *bad) {
+    uint32_t key = 0;
+    if (bitwidth == RSR_BINARY) {
+        const uint8_t *p = data + r0 * row_bytes + (c >> 3);
+        const int sh = (int)(c & 7);
+        for (int i = 0; i < h; ++i) key |= (uint32_t)((__ldg(p + i * row_bytes) >> sh) & 1u) << i;
+    } else {
+        const uint8_t *p = data + r0 * row_bytes + (c >> 2);
+        const int sh = (int)((c & 3) << 1);
+        uint32_t w = 1;
+        for (int i = 0; i < h; ++i) {
+            uint32_t code = (__ldg(p + i * row_bytes) >> sh) & 3u;
+            if (code == 3u) *bad = true;
+            key += code * w;
+            w *= 3u;
+        }
+    }
+    return key;
+}
+
+// pos | neg<<16 of a pattern key (binary: key itself).
+__device__ __forceinline__ uint32_t key_masks(uint32_t key, int bitwidth, int h) {
+    if (bitwidth == RSR_BINARY) return key;
+    uint32_t pos = 0, neg = 0;
+    for (int i = 0; i < h; ++i) {
+        uint32_t q = key / 3u, d = key - 3u * q;
+        key = q;
+        if (d == 1u) pos |= 1u << i;
+        else if (d == 2u) neg |= 1u << i;
+    }
+    return pos | (neg << 16);
+}
+
+struct CellGeom {
+    int64_t r0, c0, tn;
+    int h;
+};
+
+__device__ __forceinline__ CellGeom cell_geom(int64_t cell, int64_t rows, int64_t cols, int k,
+                                              int64_t tw, int64_t bc) {
+    CellGeom g;
+    const int64_t t = cell / bc, b = cell - t * bc;
+    g.r0 = b * k;
+    g.h = (int)min((int64_t)k, rows - g.r0);
+    g.c0 = t * tw;
+    g.tn = min(tw, cols - g.c0);
+    return g;
+}
+
+__device__ __forceinline__ uint32_t *warp_table(uint32_t *smem_tab, uint32_t *gmem_tab,
+                                                int64_t bk, int warp_in_cta) {
+    if (smem_tab) return smem_tab + (int64_t)warp_in_cta * bk;
+    const int64_t gw = (int64_t)blockIdx.x * PP_WARPS + warp_in_cta;
+    return gmem_tab + gw * bk;
+}
+
+// Histogram of one cell into tab[0..B) (tab zeroed here first).
+__device__ __forceinline__ void cell_histogram(const uint8_t *data, int64_t row_bytes,
+                                               const CellGeom &g, int bitwidth, int64_t B,
+                                               uint32_t *tab, uint32_t lane, bool *bad) {
+    for (int64_t d = lane; d < B; d += 32) tab[d] = 0u;
+    __syncwarp();
+    for (int64_t j = lane; j < g.tn; j += 32) {
+        uint32_t key = column_key(data, row_bytes, g.r0, g.h, g.c0 + j, bitwidth, bad);
+        atomicAdd(tab + key, 1u);
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(PP_WARPS * 32)
+group_count_kernel(const uint8_t *__restrict__ data, int64_t rows, int64_t cols,
+                   int64_t row_bytes, int bitwidth, int k, int64_t tw, int64_t bc,
+                   int64_t cells, int64_t bk, uint32_t *gmem_tab, int64_t *go, int64_t *po,
+                   int64_t *steps, int32_t *status) {
+    extern __shared__ uint32_t pp_smem[];
+    const uint32_t lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    uint32_t *tab = warp_table(gmem_tab ? nullptr : pp_smem, gmem_tab, bk, warp);
+    for (int64_t cell = (int64_t)blockIdx.x * PP_WARPS + warp; cell < cells;
+         cell += (int64_t)gridDim.x * PP_WARPS) {
+        const CellGeom g = cell_geom(cell, rows, cols, k, tw, bc);
+        const int64_t B = bucket_count(bitwidth, g.h);
+        bool bad = false;
+        cell_histogram(data, row_bytes, g, bitwidth, B, tab, lane, &bad);
+        uint32_t ng = 0, over = 0;
+        for (int64_t d = 1 + lane; d < B; d += 32) {
+            const uint32_t c = tab[d];
+            ng += c > 0u;
+            over |= c > 0xFFFFu;
+        }
+        ng = warp_sum(ng);
+        over = __any_sync(RSR_FULL_MASK, over != 0u);
+        const bool anybad = __any_sync(RSR_FULL_MASK, bad);
+        if (lane == 0) {
+            const int64_t nret = g.tn - (int64_t)tab[0];
+            go[cell + 1] = ng;
+            po[cell + 1] = nret;
+            // the reference's step tally (_native.py:45-81 / :109-153)
+            const int64_t dsize = bitwidth == RSR_BINARY ? ((int64_t)1 << g.h)
+                                                         : ((int64_t)1 << (2 * g.h));
+            const int64_t per_group = bitwidth == RSR_BINARY ? 1 : 1 + g.h;
+            steps[cell] = 3 * g.tn + 2 * dsize + nret + (int64_t)ng * per_group;
+            if (over) atomicExch(status, (int32_t)RSR_ERR_TILE_TOO_WIDE);
+            if (anybad) atomicCAS(status, 0, (int32_t)RSR_ERR_INVALID);
+            if (cell == 0) {
+                go[0] = 0;
+                po[0] = 0;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(PP_WARPS * 32)
+group_fill_kernel(const uint8_t *__restrict__ data, int64_t rows, int64_t cols,
+                  int64_t row_bytes, int bitwidth, int k, int64_t tw, int64_t bc,
+                  int64_t cells, int64_t bk, uint32_t *gmem_tab, const int64_t *__restrict__ go,
+                  const int64_t *__restrict__ po, uint64_t *__restrict__ words,
+                  uint16_t *__restrict__ perm) {
+    extern __shared__ uint32_t pp_smem[];
+    const uint32_t lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    const int warp = threadIdx.x >> 5;
+    uint32_t *tab = warp_table(gmem_tab ? nullptr : pp_smem, gmem_tab, bk, warp);
+    for (int64_t cell = (int64_t)blockIdx.x * PP_WARPS + warp; cell < cells;
+         cell += (int64_t)gridDim.x * PP_WARPS) {
+        const CellGeom g = cell_geom(cell, rows, cols, k, tw, bc);
+        const int64_t B = bucket_count(bitwidth, g.h);
+        bool bad = false;
+        cell_histogram(data, row_bytes, g, bitwidth, B, tab, lane, &bad);
+        // ascending-key exclusive scan over non-zero keys; emit words.
+        uint64_t *wout = words + go[cell];
+        uint32_t running = 0, nw = 0;
+        for (int64_t d0 = 0; d0 < B; d0 += 32) {
+            const int64_t d = d0 + lane;
+            const uint32_t c = (d < B && d != 0) ? tab[d] : 0u;
+            const uint32_t incl = warp_inclusive_scan(c, lane);
+            const uint32_t start = running + incl - c;
+            const uint32_t ball = __ballot_sync(RSR_FULL_MASK, c > 0u);
+            if (c > 0u) {
+                const uint32_t m = key_masks((uint32_t)d, bitwidth, g.h);
+                wout[nw + __popc(ball & lt)] =
+                    (uint64_t)start | ((uint64_t)c << 16) | ((uint64_t)(m & 0xFFFFu) << 32) |
+                    ((uint64_t)(m >> 16) << 48);
+                tab[d] = start;  // becomes the scatter cursor of this key
+            }
+            running += __shfl_sync(RSR_FULL_MASK, incl, 31);
+            nw += __popc(ball);
+        }
+        __syncwarp();
+        // stable scatter of tile-local column ids
+        uint16_t *pout = perm + po[cell];
+        for (int64_t j0 = 0; j0 < g.tn; j0 += 32) {
+            const int64_t j = j0 + lane;
+            const bool valid = j < g.tn;
+            uint32_t key = valid ? column_key(data, row_bytes, g.r0, g.h, g.c0 + j, bitwidth, &bad)
+                                 : 0xFFFFFFFFu;
+            const uint32_t peers = __match_any_sync(RSR_FULL_MASK, key);
+            const bool live = valid && key != 0u;
+            uint32_t base = 0;
+            if (live) {
+                base = tab[key];
+                pout[base + __popc(peers & lt)] = (uint16_t)j;
+            }
+            __syncwarp();
+            if (live && (peers & lt) == 0u) tab[key] = base + __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
+// Single-CTA inclusive scan of a[1..cells] in place (a[0] already 0), for
+// two int64 arrays at once.
+__global__ void __launch_bounds__(1024)
+scan2_kernel(int64_t *a, int64_t *b, int64_t cells) {
+    __shared__ int64_t wa[32], wb[32];
+    __shared__ int64_t carry_a, carry_b;
+    const uint32_t lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        carry_a = 0;
+        carry_b = 0;
+        a[0] = 0;
+        if (b) b[0] = 0;
+    }
+    __syncthreads();
+    for (int64_t base = 0; base < cells; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        int64_t xa = i < cells ? a[i + 1] : 0, xb = (b && i < cells) ? b[i + 1] : 0;
+        xa = warp_inclusive_scan(xa, lane);
+        xb = warp_inclusive_scan(xb, lane);
+        if (lane == 31) {
+            wa[warp] = xa;
+            wb[warp] = xb;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int64_t sa = wa[lane], sb = wb[lane];
+            sa = warp_inclusive_scan(sa, lane);
+            sb = warp_inclusive_scan(sb, lane);
+            wa[lane] = sa;
+            wb[lane] = sb;
+        }
+        __syncthreads();
+        const int64_t pa = (warp ? wa[warp - 1] : 0) + carry_a;
+        const int64_t pb = (warp ? wb[warp - 1] : 0) + carry_b;
+        if (i < cells) {
+            a[i + 1] = xa + pa;
+            if (b) b[i + 1] = xb + pb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            carry_a = xa + pa;
+            carry_b = xb + pb;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stream layout: block-major cells, entries padded to 32 bytes per cell.
+
+__global__ void stream_count_kernel(const int64_t *__restrict__ go, const int64_t *__restrict__ po,
+                                    int64_t bc, int64_t tc, int entry_bytes, int64_t *e_off,
+                                    int64_t *g_off) {
+    const int64_t cells = bc * tc;
+    const int64_t per_chunk = 32 / entry_bytes;
+    for (int64_t dc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; dc < cells;
+         dc += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = dc / tc, t = dc - b * tc;
+        const int64_t src = t * bc + b;
+        const int64_t nret = po[src + 1] - po[src];
+        const int64_t ng = go[src + 1] - go[src];
+        const int64_t elen = (nret + per_chunk - 1) / per_chunk * per_chunk;
+        e_off[dc + 1] = elen;
+        g_off[dc + 1] = ng + (elen != nret ? 1 : 0);
+    }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(256)
+stream_build_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
+                    const uint16_t *__restrict__ perm, const int64_t *__restrict__ po, int64_t bc,
+                    int64_t tc, const int64_t *__restrict__ e_off,
+                    const int64_t *__restrict__ g_off, E *__restrict__ entries,
+                    uint32_t *__restrict__ gsigns) {
+    constexpr E HEAD = (E)1 << (8 * sizeof(E) - 1);
+    const uint32_t lane = lane_id();
+    const int64_t cells = bc * tc;
+    for (int64_t dc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; dc < cells;
+         dc += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b = dc / tc, t = dc - b * tc;
+        const int64_t src = t * bc + b;
+        const int64_t p0 = po[src], nret = po[src + 1] - p0;
+        const int64_t w0 = go[src], ng = go[src + 1] - w0;
+        const int64_t e0 = e_off[dc], elen = e_off[dc + 1] - e0;
+        const int64_t g0 = g_off[dc];
+        for (int64_t i = lane; i < elen; i += 32)
+            entries[e0 + i] = i < nret ? (E)perm[p0 + i] : (i == nret ? HEAD : (E)0);
+        __syncwarp();
+        for (int64_t gi = lane; gi < ng; gi += 32) {
+            const uint64_t w = words[w0 + gi];
+            entries[e0 + (int64_t)(w & 0xFFFFu)] |= HEAD;
+            gsigns[g0 + gi] = (uint32_t)(w >> 32);
+        }
+        if (lane == 0 && elen != nret) gsigns[g0 + ng] = 0u;
+    }
+}
+
+__global__ void count_ops_kernel(const uint64_t *__restrict__ words, int64_t n, int64_t *out3) {
+    int64_t g = 0, s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = words[i];
+        g += (int64_t)((w >> 16) & 0xFFFFu);
+        s += __popcll(w >> 32);
+    }
+    g = warp_sum(g);
+    s = warp_sum(s);
+    if (lane_id() == 0) {
+        atomicAdd((unsigned long long *)out3, (unsigned long long)g);
+        atomicAdd((unsigned long long *)(out3 + 1), (unsigned long long)s);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd((unsigned long long *)(out3 + 2), (unsigned long long)n);
+}
+
+struct GroupLaunch {
+    int64_t bc, tc, cells, bk;
+    bool smem;
+    int grid;
+    size_t smem_bytes;
+};
+
+static GroupLaunch group_launch(int64_t rows, int64_t cols, int32_t bitwidth, int32_t k,
+                                int64_t tw) {
+    GroupLaunch L;
+    L.bc = (rows + k - 1) / k;
+    L.tc = (cols + tw - 1) / tw;
+    L.cells = L.bc * L.tc;
+    L.bk = bucket_count(bitwidth, k);
+    L.smem = L.bk <= PP_SMEM_TABLE_MAX;
+    const int sms = sm_count();
+    const int64_t need = (L.cells + PP_WARPS - 1) / PP_WARPS;
+    if (L.smem) {
+        L.grid = (int)std::min<int64_t>(need, (int64_t)sms * 16);
+        L.smem_bytes = (size_t)L.bk * 4 * PP_WARPS;
+    } else {
+        L.grid = (int)std::min<int64_t>(need, (int64_t)sms * 2);
+        L.smem_bytes = 0;
+    }
+    if (L.grid < 1) L.grid = 1;
+    return L;
+}
+
+static rsr_status check_plan(int64_t rows, int64_t cols, int64_t row_bytes, int32_t bitwidth,
+                             int32_t k, int64_t tw) {
+    if (rows < 1 || cols < 1 || tw < 1) return RSR_ERR_INVALID;
+    if (bitwidth != RSR_BINARY && bitwidth != RSR_TERNARY) return RSR_ERR_INVALID;
+    if (k < 1) return RSR_ERR_INVALID;
+    if (k > (bitwidth == RSR_BINARY ? 16 : 10)) return RSR_ERR_K_TOO_LARGE;
+    if (tw > 65536) return RSR_ERR_TILE_TOO_WIDE;
+    const int64_t need = bitwidth == RSR_BINARY ? (cols + 7) / 8 : (cols + 3) / 4;
+    if (row_bytes < need) return RSR_ERR_INVALID;
+    return RSR_OK;
+}
+
+}  // namespace rsr
+
+using namespace rsr;
+
+extern "C" {
+
+size_t rsr_group_workspace_bytes(int64_t rows, int64_t cols, int32_t bitwidth, int32_t k,
+                                 int64_t tile_width) {
+    if (rows < 1 || cols < 1 || k < 1 || tile_width < 1) return 0;
+    GroupLaunch L = group_launch(rows, cols, bitwidth, k, tile_width);
+    if (L.smem) return 0;
+    return (size_t)L.grid * PP_WARPS * (size_t)L.bk * 4;
+}
+
+rsr_status rsr_group_count(const uint8_t *data, int64_t rows, int64_t cols, int64_t row_bytes,
+                           int32_t bitwidth, int32_t k, int64_t tile_width, int64_t *go,
+                           int64_t *po, int64_t *sort_steps, int32_t *status_dev,
+                           void *workspace, size_t workspace_bytes, rsr_stream_t stream) {
+    rsr_status st = check_plan(rows, cols, row_bytes, bitwidth, k, tile_width);
+    if (st != RSR_OK) return st;
+    if (!data || !go || !po || !sort_steps || !status_dev) return RSR_ERR_INVALID;
+    GroupLaunch L = group_launch(rows, cols, bitwidth, k, tile_width);
+    uint32_t *gtab = nullptr;
+    if (!L.smem) {
+        if (workspace_bytes < rsr_group_workspace_bytes(rows, cols, bitwidth, k, tile_width) ||
+            !workspace)
+            return RSR_ERR_WORKSPACE;
+        gtab = (uint32_t *)workspace;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (L.smem_bytes > 48 * 1024)
+        cudaFuncSetAttribute(group_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)L.smem_bytes);
+    cudaMemsetAsync(status_dev, 0, sizeof(int32_t), s);
+    group_count_kernel<<<L.grid, PP_WARPS * 32, L.smem_bytes, s>>>(
+        data, rows, cols, row_bytes, bitwidth, k, tile_width, L.bc, L.cells, L.bk, gtab, go, po,
+        sort_steps, status_dev);
+    scan2_kernel<<<1, 1024, 0, s>>>(go, po, L.cells);
+    return launch_status();
+}
+
+rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64_t row_bytes,
+                          int32_t bitwidth, int32_t k, int64_t tile_width, const int64_t *go,
+                          const int64_t *po, uint64_t *words, uint16_t *perm, void *workspace,
+                          size_t workspace_bytes, rsr_stream_t stream) {
+    rsr_status st = check_plan(rows, cols, row_bytes, bitwidth, k, tile_width);
+    if (st != RSR_OK) return st;
+    if (!data || !go || !po) return RSR_ERR_INVALID;
+    GroupLaunch L = group_launch(rows, cols, bitwidth, k, tile_width);
+    uint32_t *gtab = nullptr;
+    if (!L.smem) {
+        if (workspace_bytes < rsr_group_workspace_bytes(rows, cols, bitwidth, k, tile_width) ||
+            !workspace)
+            return RSR_ERR_WORKSPACE;
+        gtab = (uint32_t *)workspace;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (L.smem_bytes > 48 * 1024)
+        cudaFuncSetAttribute(group_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)L.smem_bytes);
+    group_fill_kernel<<<L.grid, PP_WARPS * 32, L.smem_bytes, s>>>(
+        data, rows, cols, row_bytes, bitwidth, k, tile_width, L.bc, L.cells, L.bk, gtab, go, po,
+        words, perm);
+    return launch_status();
+}
+
+rsr_status rsr_stream_count(const int64_t *go, const int64_t *po, int64_t block_count,
+                            int64_t tile_count, int32_t entry_bytes, int64_t *e_off,
+                            int64_t *g_off, rsr_stream_t stream) {
+    if (!go || !po || !e_off || !g_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
+    if (entry_bytes != 2 && entry_bytes != 4) return RSR_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t cells = block_count * tile_count;
+    const int grid = (int)std::min<int64_t>((cells + 255) / 256, 4096);
+    stream_count_kernel<<<grid, 256, 0, s>>>(go, po, block_count, tile_count, entry_bytes, e_off,
+                                             g_off);
+    scan2_kernel<<<1, 1024, 0, s>>>(e_off, g_off, cells);
+    return launch_status();
+}
+
+rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                            const int64_t *po, int64_t block_count, int64_t tile_count,
+                            int32_t entry_bytes, const int64_t *e_off, const int64_t *g_off,
+                            void *entries, uint32_t *gsigns, rsr_stream_t stream) {
+    if (!go || !po || !e_off || !g_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t cells = block_count * tile_count;
+    const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 32);
+    if (entry_bytes == 2)
+        stream_build_kernel<uint16_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
+                                                           tile_count, e_off, g_off,
+                                                           (uint16_t *)entries, gsigns);
+    else if (entry_bytes == 4)
+        stream_build_kernel<uint32_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
+                                                           tile_count, e_off, g_off,
+                                                           (uint32_t *)entries, gsigns);
+    else
+        return RSR_ERR_INVALID;
+    return launch_status();
+}
+
+rsr_status rsr_count_ops(const uint64_t *words, int64_t n_words, int64_t *out3,
+                         rsr_stream_t stream) {
+    if (!out3 || n_words < 0) return RSR_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(out3, 0, 3 * sizeof(int64_t), s);
+    if (n_words > 0) {
+        const int grid = (int)std::min<int64_t>((n_words + 255) / 256, (int64_t)sm_count() * 4);
+        count_ops_kernel<<<grid, 256, 0, s>>>(words, n_words, out3);
+    }
+    return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,269 @@
+"""Online multiply API on the GPU (operator API of reference kernels.py).
+
+Same names, arguments, dtypes and errors as pkg/src/rsrmv/kernels.py:
+``rsr_matvec`` (int8 -> exact int32; real -> float32), ``rsr_matvec_fused``
+(ternary only; quantize -> exact int multiply -> f32(f64(y)*beta/scale)),
+``batched_preprocess``, ``Multiplier`` / ``multiplier_multiply`` and
+``OpCounter``.  Every multiply runs the sm_100a kernels of
+csrc/rsr_matvec.cu through the C ABI; there is no CPU path.
+
+Vectors may be numpy arrays (copied to the artifact's device, result copied
+back -- the reference-facing, host-buffer call) or CUDA tensors (result stays
+on the device, nothing synchronizes).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionMismatch, HeterogeneousSiblings
+from .matcore import (BINARY, TERNARY, PackedMatrix, _is_torch, dense_device,
+                      naive_matvec, quantize_activations)
+from .preproc import RsrArtifact, preprocess
+
+NAIVE_F32 = "NaiveF32"
+NAIVE_I8 = "NaiveI8"
+RSR_BINARY = "RsrBinary"
+RSR_TERNARY = "RsrTernary"
+KINDS = (NAIVE_F32, NAIVE_I8, RSR_BINARY, RSR_TERNARY)
+
+
+@dataclass
+class OpCounter:
+    """Add/visit counts over one or more multiplies (reference kernels.py:30-36)."""
+    gather_adds: int = 0
+    scatter_adds: int = 0
+    groups_visited: int = 0
+
+
+def thread_count() -> int:
+    """RSR_THREADS (reference kernels.py:39-45).  Kept for API compatibility:
+    the GPU kernels ignore it (the whole device is used)."""
+    try:
+        t = int(os.environ.get("RSR_THREADS", "1"))
+    except ValueError:
+        return 1
+    return max(1, t)
+
+
+def _count(a: RsrArtifact, counter: OpCounter | None):
+    if counter is not None:
+        g, s, ng = a.op_totals()
+        counter.gather_adds += g
+        counter.scatter_adds += s
+        counter.groups_visited += ng
+
+
+class _Workspace:
+    """Per-device scratch for tile partials (grown on demand, reused)."""
+    _bufs: dict = {}
+
+    @classmethod
+    def get(cls, device, nbytes: int):
+        import torch
+        if nbytes <= 0:
+            return None, 0
+        key = str(device)
+        b = cls._bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            cls._bufs[key] = b
+        return b, nbytes
+
+
+def _prepare_vec(a: RsrArtifact, v):
+    """-> (device tensor, is_host, kind) with kind 'int' or 'float'."""
+    import torch
+    host = not _is_torch(v)
+    if host:
+        vn = np.asarray(v)
+        if vn.ndim != 1 or vn.shape[0] != a.n:
+            raise DimensionMismatch(f"vector of length {vn.size} against {a.n} columns")
+        if np.issubdtype(vn.dtype, np.integer):
+            if vn.dtype != np.int8:
+                raise DimensionMismatch("integer vectors must be int8")
+            t = torch.from_numpy(np.ascontiguousarray(vn))
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(vn.astype(np.float32, copy=False)))
+        return t.to(a.device, non_blocking=False), True
+    t = v
+    if t.dim() != 1 or t.shape[0] != a.n:
+        raise DimensionMismatch(f"vector of length {t.numel()} against {a.n} columns")
+    if not (t.is_floating_point() or t.is_complex()):
+        if t.dtype != torch.int8:
+            raise DimensionMismatch("integer vectors must be int8")
+    elif t.dtype not in (torch.float32, torch.bfloat16, torch.float16):
+        t = t.to(torch.float32)
+    if t.device != a.device:
+        t = t.to(a.device)
+    return t.contiguous(), False
+
+
+def matvec_into(a: RsrArtifact, vt, y, accumulate: bool = False, view=None, stream=None):
+    """Launch the multiply on device tensors: y (+)= A.v (no checks, no sync).
+
+    vt: int8 -> y int32; float32/bfloat16/float16 -> y float32.
+    """
+    from .matcore import _dtype_code
+    vw = a._view if view is None else view
+    L = _lib.lib()
+    import ctypes
+    wsb = int(L.rsr_matvec_workspace_bytes(ctypes.byref(vw)))
+    ws, wsb = _Workspace.get(a.device, wsb)
+    s = _lib.current_stream_ptr(a.device) if stream is None else stream
+    _lib.check(L.rsr_matvec(ctypes.byref(vw), _lib.ptr(vt), _dtype_code(vt), _lib.ptr(y),
+                            int(accumulate), _lib.ptr(ws), wsb, s), "rsr_matvec")
+    return y
+
+
+def fused_into(a: RsrArtifact, vt, out, beta: float | None = None, view=None, stream=None,
+               scale_out=None):
+    """Launch the fused quantize/multiply/dequantize kernel on device tensors."""
+    from .matcore import _dtype_code
+    import ctypes
+    vw = a._view if view is None else view
+    L = _lib.lib()
+    wsb = int(L.rsr_matvec_workspace_bytes(ctypes.byref(vw)))
+    ws, wsb = _Workspace.get(a.device, wsb)
+    s = _lib.current_stream_ptr(a.device) if stream is None else stream
+    b = float(a.weight_scale) if beta is None else float(beta)
+    _lib.check(L.rsr_fused_matvec(ctypes.byref(vw), _lib.ptr(vt), _dtype_code(vt), b,
+                                  _lib.ptr(out), _lib.ptr(scale_out), _lib.ptr(ws), wsb, s),
+               "rsr_matvec_fused")
+    return out
+
+
+def rsr_matvec(a: RsrArtifact, v, counter: OpCounter | None = None,
+               threads: int | None = None):
+    """Multiply a preprocessed matrix by v on the GPU (reference kernels.py:59-102).
+
+    int8 vectors take the exact integer path (int32 result); real vectors
+    the float path (float32 result, fp32 accumulation -- see DESIGN.md for
+    the stated tolerance).  ``threads`` is accepted for API compatibility.
+    """
+    import torch
+    vt, host = _prepare_vec(a, v)
+    _count(a, counter)
+    if vt.dtype == torch.int8:
+        y = torch.empty(a.m, dtype=torch.int32, device=a.device)
+    else:
+        y = torch.empty(a.m, dtype=torch.float32, device=a.device)
+    matvec_into(a, vt, y)
+    return y.cpu().numpy() if host else y
+
+
+def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
+    """Quantize v to int8, multiply exactly, rescale by weight_scale/scale
+    (reference kernels.py:105-125), in one kernel launch."""
+    import torch
+    if a.bitwidth != TERNARY:
+        raise ValueError("fused path requires a ternary artifact")
+    vt, host = _prepare_vec(a, v)
+    _count(a, counter)
+    if vt.dtype == torch.int8:
+        vt = vt.to(torch.float32)
+    out = torch.empty(a.m, dtype=torch.float32, device=a.device)
+    fused_into(a, vt, out)
+    return out.cpu().numpy() if host else out
+
+
+def batched_preprocess(mats: list, k: int, tile_width: int | None = None):
+    """Stack sibling matrices sharing an input (reference kernels.py:128-160).
+
+    Returns (artifact, offsets); the stacked artifact's weight_scale is 1.0
+    and callers apply per-matrix scales after splitting at ``offsets``.
+    """
+    if not mats:
+        raise HeterogeneousSiblings("no matrices to batch")
+    n = mats[0].cols
+    bw = mats[0].bitwidth
+    for mm in mats[1:]:
+        if mm.cols != n or mm.bitwidth != bw:
+            raise HeterogeneousSiblings(
+                f"expected all {bw} matrices with {n} columns, got {mm.bitwidth} with {mm.cols}")
+    if any(_is_torch(mm.data) for mm in mats):
+        import torch
+        data = torch.cat([mm.device_data() for mm in mats], 0)
+    else:
+        data = np.vstack([mm.host_data() for mm in mats])
+    stacked = PackedMatrix(sum(mm.rows for mm in mats), n, bw, data)
+    offsets = [0]
+    for mm in mats:
+        offsets.append(offsets[-1] + mm.rows)
+    return preprocess(stacked, k, tile_width), offsets
+
+
+class Multiplier:
+    """One matrix bound to one multiplication strategy (reference kernels.py:163-217).
+
+    RSR kinds hold a GPU artifact; naive kinds hold a dense device copy.
+    For real input every kind computes weight_scale * (M @ v) (NaiveF32 in
+    float64, the int8 kinds through activation quantization); int8 input
+    gives the raw int32 product.
+    """
+
+    def __init__(self, kind: str, matrix: PackedMatrix, k: int = 4,
+                 tile_width: int | None = None):
+        if kind not in KINDS:
+            raise ValueError(f"unknown multiplier kind {kind!r}")
+        if kind == RSR_BINARY and matrix.bitwidth != BINARY:
+            raise ValueError("RsrBinary needs a binary matrix")
+        if kind == RSR_TERNARY and matrix.bitwidth != TERNARY:
+            raise ValueError("RsrTernary needs a ternary matrix")
+        import torch
+        self.kind = kind
+        self.matrix = matrix
+        self.artifact = None
+        self._dense = None
+        if kind in (RSR_BINARY, RSR_TERNARY):
+            self.artifact = preprocess(matrix, k, tile_width)
+        else:
+            self._dense = dense_device(matrix).to(torch.float64)
+
+    def multiply(self, v, counter: OpCounter | None = None):
+        import torch
+        host = not _is_torch(v)
+        shape = tuple(np.asarray(v).shape) if host else tuple(v.shape)
+        if len(shape) != 1 or shape[0] != self.matrix.cols:
+            raise DimensionMismatch(
+                f"vector of length {int(np.prod(shape))} against {self.matrix.cols} columns")
+        beta = self.matrix.weight_scale
+        if host:
+            vn = np.asarray(v)
+            is_int = np.issubdtype(vn.dtype, np.integer)
+        else:
+            is_int = not (v.is_floating_point() or v.is_complex())
+        if self.kind in (NAIVE_F32, NAIVE_I8):
+            vt = torch.from_numpy(np.ascontiguousarray(v)).cuda() if host else v
+            if is_int:
+                y = (self._dense @ vt.to(torch.float64)).to(torch.int32)
+            elif self.kind == NAIVE_F32:
+                y = beta * (self._dense @ vt.to(torch.float64))
+            else:
+                q = quantize_activations(vt)
+                yi = self._dense @ q.values.to(torch.float64)
+                y = ((beta / q.scale) * yi).to(torch.float32)
+            return y.cpu().numpy() if host else y
+        if is_int:
+            return rsr_matvec(self.artifact, v, counter)
+        if self.kind == RSR_TERNARY:
+            return rsr_matvec_fused(self.artifact, v, counter)
+        y = rsr_matvec(self.artifact, v, counter)
+        if beta == 1.0:
+            return y
+        if host:
+            return (beta * y.astype(np.float64)).astype(np.float32)
+        return (beta * y.to(torch.float64)).to(torch.float32)
+
+
+def multiplier_multiply(mul: Multiplier, v, counter: OpCounter | None = None):
+    """Function form of Multiplier.multiply (reference kernels.py:220-222)."""
+    return mul.multiply(v, counter)
+
+
+def naive_reference(matrix: PackedMatrix, v):
+    return naive_matvec(matrix, v)

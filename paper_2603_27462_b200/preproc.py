@@ -1,0 +1,472 @@
+"""Offline preprocessing on the GPU (operator API of reference preproc.py).
+
+``preprocess(m, k, tile_width=None) -> RsrArtifact`` keeps the reference
+signature, plans, caps and errors (pkg/src/rsrmv/preproc.py:26-114,
+:239-289) and produces the SAME flat arrays -- ``words`` u64, ``perm`` u16
+(tile-local column ids), ``group_offsets`` / ``perm_offsets`` int64 and
+``sort_steps`` -- byte for byte, but computes them with the sm_100a grouping
+kernels (csrc/rsr_preprocess.cu).  The artifact lives on the device; the
+reference attribute names return host numpy copies on first access so code
+written against the reference (validate_artifact, reconstruct, .rsra I/O)
+works unchanged.
+
+On top of the reference arrays every artifact carries the device-only stream
+layout the multiply kernels read (block-major cells, u16 column|head entries,
+u32 group sign words); see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import CorruptArtifact, DimensionMismatch, KTooLarge, TileTooWide
+from .matcore import BINARY, TERNARY, PackedMatrix, _is_torch, encode
+
+MAX_TILE_WIDTH = 65536          # reference preproc.py:26
+DEFAULT_WIDE_TILE = 32768       # reference preproc.py:27
+K_CAP = {BINARY: 16, TERNARY: 10}   # reference preproc.py:28
+STREAM_MAX_TILE = 32768         # widest tile the u16 stream entries address
+
+
+def pack_group(perm_start: int, perm_len: int, pos_mask: int, neg_mask: int) -> int:
+    """Pack one group record: bits [0,16) perm_start, [16,32) perm_len,
+    [32,48) pos_mask, [48,64) neg_mask (reference preproc.py:31-41)."""
+    for name, val in (("perm_start", perm_start), ("perm_len", perm_len),
+                      ("pos_mask", pos_mask), ("neg_mask", neg_mask)):
+        if not 0 <= val <= 0xFFFF:
+            raise ValueError(f"{name}={val} does not fit u16")
+    return perm_start | (perm_len << 16) | (pos_mask << 32) | (neg_mask << 48)
+
+
+def unpack_group(word: int) -> tuple[int, int, int, int]:
+    """Inverse of pack_group (reference preproc.py:44-48)."""
+    word = int(word)
+    return (word & 0xFFFF, (word >> 16) & 0xFFFF, (word >> 32) & 0xFFFF, (word >> 48) & 0xFFFF)
+
+
+@dataclass(frozen=True)
+class GroupRecord:
+    perm_start: int
+    perm_len: int
+    pos_mask: int
+    neg_mask: int
+
+
+@dataclass(frozen=True)
+class BlockMeta:
+    perm: np.ndarray
+    groups: tuple
+
+
+@dataclass
+class StepCounter:
+    steps: int = 0
+
+
+@dataclass(frozen=True)
+class BlockPlan:
+    """Block/tile layout of one matrix (reference preproc.py:80-94)."""
+    k: int
+    block_count: int
+    last_block_height: int
+    tile_width: int
+    tile_count: int
+
+    def __post_init__(self):
+        if not 1 <= self.k <= 16:
+            raise ValueError(f"k={self.k} outside [1, 16]")
+        if not 1 <= self.tile_width <= MAX_TILE_WIDTH:
+            raise TileTooWide(f"tile_width={self.tile_width}", n_tile=self.tile_width)
+        if not 1 <= self.last_block_height <= self.k:
+            raise ValueError("last block height inconsistent with k")
+
+
+def make_plan(m_rows: int, n_cols: int, k: int, bitwidth: str,
+              tile_width: int | None = None) -> BlockPlan:
+    """Validate caps and lay out blocks/tiles (reference preproc.py:97-114)."""
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    if k > K_CAP[bitwidth]:
+        raise KTooLarge(k, bitwidth)
+    if tile_width is None:
+        tile_width = n_cols if n_cols <= MAX_TILE_WIDTH else DEFAULT_WIDE_TILE
+    if not 1 <= tile_width <= MAX_TILE_WIDTH:
+        raise TileTooWide(f"tile_width={tile_width} outside [1, {MAX_TILE_WIDTH}]",
+                          n_tile=tile_width)
+    bc = -(-m_rows // k)
+    tc = -(-n_cols // tile_width)
+    return BlockPlan(k, bc, m_rows - k * (bc - 1), tile_width, tc)
+
+
+def _u64_host(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
+
+
+def _u16_host(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint16)
+
+
+class RsrArtifact:
+    """Preprocessed matrix: reference flat arrays + device stream layout.
+
+    Device tensors: ``words_d`` (int64 storage of u64 words), ``perm_d``
+    (int16 storage of u16), ``go_d``/``po_d`` (int64, cells+1), and the
+    stream layout ``entries_d``/``gsigns_d``/``e_off_d``/``g_off_d``.  The
+    reference attribute names (``words``, ``perm``, ``group_offsets``,
+    ``perm_offsets``, ``sort_steps``) are host numpy views fetched lazily.
+    Cells are tile-major exactly as in the reference (cell = t*bc + b).
+    """
+
+    def __init__(self, m, n, k, bitwidth, weight_scale, plan, words_d, perm_d, go_d, po_d,
+                 steps_d=None, n_words=None, n_perm=None):
+        self.m = m
+        self.n = n
+        self.k = k
+        self.bitwidth = bitwidth
+        self.weight_scale = weight_scale
+        self.plan = plan
+        self.words_d = words_d
+        self.perm_d = perm_d
+        self.go_d = go_d
+        self.po_d = po_d
+        self.steps_d = steps_d
+        self.n_words = int(words_d.numel()) if n_words is None else n_words
+        self.n_perm = int(perm_d.numel()) if n_perm is None else n_perm
+        self.device = go_d.device
+        self._host = {}
+        self._build_stream()
+
+    # ---- reference attribute surface (host numpy, lazily copied) ----------
+    def _h(self, key, fn):
+        if key not in self._host:
+            self._host[key] = fn()
+        return self._host[key]
+
+    @property
+    def words(self) -> np.ndarray:
+        return self._h("words", lambda: _u64_host(self.words_d))
+
+    @property
+    def perm(self) -> np.ndarray:
+        return self._h("perm", lambda: _u16_host(self.perm_d))
+
+    @property
+    def group_offsets(self) -> np.ndarray:
+        return self._h("go", lambda: self.go_d.cpu().numpy())
+
+    @property
+    def perm_offsets(self) -> np.ndarray:
+        return self._h("po", lambda: self.po_d.cpu().numpy())
+
+    @property
+    def sort_steps(self):
+        if self.steps_d is None:
+            return None
+        return self._h("steps", lambda: self.steps_d.cpu().numpy())
+
+    @property
+    def cells(self) -> int:
+        return self.plan.tile_count * self.plan.block_count
+
+    def cell_index(self, tile: int, block: int) -> int:
+        return tile * self.plan.block_count + block
+
+    def block_meta(self, tile: int, block: int) -> BlockMeta:
+        c = self.cell_index(tile, block)
+        go, po = self.group_offsets, self.perm_offsets
+        groups = tuple(GroupRecord(*unpack_group(w)) for w in self.words[go[c]:go[c + 1]])
+        return BlockMeta(self.perm[po[c]:po[c + 1]].copy(), groups)
+
+    def op_totals(self) -> tuple[int, int, int]:
+        """(gather adds, scatter adds, groups) of one multiply, counted on the
+        GPU (reference _native.count_ops, _native.py:288-307)."""
+        if "ops" not in self._host:
+            import torch
+            out = torch.zeros(3, dtype=torch.int64, device=self.device)
+            _lib.check(_lib.lib().rsr_count_ops(
+                _lib.ptr(self.words_d), self.n_words, _lib.ptr(out),
+                _lib.current_stream_ptr(self.device)), "count_ops")
+            self._host["ops"] = tuple(int(x) for x in out.cpu().tolist())
+        return self._host["ops"]
+
+    def file_bytes(self) -> int:
+        """Serialized .rsra size (reference preproc.py:161-169)."""
+        gc = np.diff(self.group_offsets)
+        pl = np.diff(self.perm_offsets)
+        return int(24 + np.sum(8 + 8 * gc + 2 * pl + (-(2 * pl)) % 4))
+
+    def stream_bytes(self) -> int:
+        """Bytes of the device stream layout one multiply reads."""
+        return int(self.entries_d.numel() * self.entries_d.element_size()
+                   + self.gsigns_d.numel() * 4 + self.e_off_d.numel() * 16)
+
+    # ---- device stream layout -------------------------------------------
+    def _build_stream(self):
+        import torch
+        p = self.plan
+        if p.tile_width > STREAM_MAX_TILE:
+            raise TileTooWide(
+                f"tile_width={p.tile_width}: the GPU multiply addresses tiles of at most "
+                f"{STREAM_MAX_TILE} columns; preprocess with tile_width<={STREAM_MAX_TILE}",
+                n_tile=p.tile_width)
+        dev = self.device
+        s = _lib.current_stream_ptr(dev)
+        cells = self.cells
+        self.entry_bytes = 2
+        e_off = torch.zeros(cells + 1, dtype=torch.int64, device=dev)
+        g_off = torch.zeros(cells + 1, dtype=torch.int64, device=dev)
+        L = _lib.lib()
+        _lib.check(L.rsr_stream_count(_lib.ptr(self.go_d), _lib.ptr(self.po_d), p.block_count,
+                                      p.tile_count, self.entry_bytes, _lib.ptr(e_off),
+                                      _lib.ptr(g_off), s), "stream_count")
+        ne, ng = (int(x) for x in torch.stack([e_off[-1], g_off[-1]]).cpu().tolist())
+        entries = torch.empty(max(ne, 8), dtype=torch.int16, device=dev)
+        gsigns = torch.empty(max(ng, 1), dtype=torch.int32, device=dev)
+        _lib.check(L.rsr_stream_build(_lib.ptr(self.words_d), _lib.ptr(self.go_d),
+                                      _lib.ptr(self.perm_d), _lib.ptr(self.po_d), p.block_count,
+                                      p.tile_count, self.entry_bytes, _lib.ptr(e_off),
+                                      _lib.ptr(g_off), _lib.ptr(entries), _lib.ptr(gsigns), s),
+                   "stream_build")
+        self.entries_d, self.gsigns_d, self.e_off_d, self.g_off_d = entries, gsigns, e_off, g_off
+        self._view = self.view()
+
+    def view(self, block_begin: int = 0, n_blocks: int | None = None) -> _lib.StreamView:
+        """C-ABI view over row blocks [block_begin, block_begin + n_blocks)."""
+        p = self.plan
+        if n_blocks is None:
+            n_blocks = p.block_count - block_begin
+        v = _lib.StreamView()
+        v.m, v.n, v.k = self.m, self.n, self.k
+        v.bitwidth = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
+        v.tile_width, v.block_count, v.tile_count = p.tile_width, p.block_count, p.tile_count
+        v.entry_bytes = self.entry_bytes
+        v.entries = _lib.ptr(self.entries_d)
+        v.gsigns = _lib.ptr(self.gsigns_d)
+        # a block range starts at cell block_begin*tc in the block-major order
+        v.e_off = _lib.ptr(self.e_off_d) + 8 * block_begin * p.tile_count
+        v.g_off = _lib.ptr(self.g_off_d) + 8 * block_begin * p.tile_count
+        v.row_begin_block = block_begin
+        v.n_blocks = n_blocks
+        return v
+
+    # ---- constructors ----------------------------------------------------
+    @classmethod
+    def from_host(cls, m, n, k, bitwidth, weight_scale, plan, words, perm, group_offsets,
+                  perm_offsets, sort_steps=None, device=None) -> "RsrArtifact":
+        """Upload reference-format host arrays (e.g. a loaded .rsra file)."""
+        import torch
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+
+        def up(a, dt, view_dt):
+            a = np.ascontiguousarray(a)
+            if a.size == 0:
+                return torch.zeros(1, dtype=view_dt, device=dev)[:0]
+            return torch.from_numpy(a.view(dt)).to(dev)
+
+        a = cls(m, n, k, bitwidth, weight_scale, plan,
+                up(np.asarray(words, np.uint64), np.int64, torch.int64),
+                up(np.asarray(perm, np.uint16), np.int16, torch.int16),
+                up(np.asarray(group_offsets, np.int64), np.int64, torch.int64),
+                up(np.asarray(perm_offsets, np.int64), np.int64, torch.int64),
+                None if sort_steps is None else
+                up(np.asarray(sort_steps, np.int64), np.int64, torch.int64))
+        return a
+
+
+def _grouping(data_d, rows, cols, row_bytes, bitwidth, k, tw, dev):
+    """Run the two-phase GPU grouping; returns device arrays."""
+    import torch
+    bw = _lib.RSR_BINARY if bitwidth == BINARY else _lib.RSR_TERNARY
+    bc = -(-rows // k)
+    tc = -(-cols // tw)
+    cells = bc * tc
+    s = _lib.current_stream_ptr(dev)
+    L = _lib.lib()
+    go = torch.empty(cells + 1, dtype=torch.int64, device=dev)
+    po = torch.empty(cells + 1, dtype=torch.int64, device=dev)
+    steps = torch.empty(cells, dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    wsb = int(L.rsr_group_workspace_bytes(rows, cols, bw, k, tw))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    _lib.check(L.rsr_group_count(_lib.ptr(data_d), rows, cols, row_bytes, bw, k, tw,
+                                 _lib.ptr(go), _lib.ptr(po), _lib.ptr(steps), _lib.ptr(status),
+                                 _lib.ptr(ws), wsb, s), "preprocess")
+    st, nw, npm = (int(x) for x in torch.stack(
+        [status[0].to(torch.int64), go[-1], po[-1]]).cpu().tolist())
+    if st == _lib.RSR_ERR_TILE_TOO_WIDE:
+        raise TileTooWide(
+            f"a group of identical columns exceeds {0xFFFF} entries; "
+            f"use a tile_width of {DEFAULT_WIDE_TILE} or less", n_tile=min(tw, cols))
+    if st != 0:
+        _lib.check(st, "preprocess")
+    words = torch.empty(nw, dtype=torch.int64, device=dev)
+    perm = torch.empty(npm, dtype=torch.int16, device=dev)
+    _lib.check(L.rsr_group_fill(_lib.ptr(data_d), rows, cols, row_bytes, bw, k, tw,
+                                _lib.ptr(go), _lib.ptr(po), _lib.ptr(words), _lib.ptr(perm),
+                                _lib.ptr(ws), wsb, s), "preprocess")
+    return words, perm, go, po, steps
+
+
+def preprocess(m: PackedMatrix, k: int, tile_width: int | None = None,
+               device=None) -> RsrArtifact:
+    """Preprocess a packed matrix into an RsrArtifact on the GPU.
+
+    Deterministic and byte-identical to the reference artifact
+    (preproc.py:239-289).  Raises KTooLarge / TileTooWide as the reference.
+    """
+    import torch
+    plan = make_plan(m.rows, m.cols, k, m.bitwidth, tile_width)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+        else torch.device(device)
+    data_d = m.device_data(dev)
+    words, perm, go, po, steps = _grouping(data_d, m.rows, m.cols, m.row_bytes, m.bitwidth, k,
+                                           plan.tile_width, dev)
+    return RsrArtifact(m.rows, m.cols, k, m.bitwidth, m.weight_scale, plan, words, perm, go,
+                       po, steps)
+
+
+def pattern_key(m: PackedMatrix, block_rows: range, col: int) -> int:
+    """Reference pattern key of one column (preproc.py:183-197): binary
+    sum bit*2^i, ternary sum code*4^i (host helper)."""
+    if not 0 <= col < m.cols:
+        raise DimensionMismatch(f"column {col} outside 0..{m.cols - 1}")
+    data = m.host_data()
+    key = 0
+    for i, r in enumerate(block_rows):
+        if m.bitwidth == BINARY:
+            key |= int((data[r, col >> 3] >> (col & 7)) & 1) << i
+        else:
+            key |= int((data[r, col >> 2] >> ((col & 3) << 1)) & 3) << (2 * i)
+    return key
+
+
+def preprocess_block(m: PackedMatrix, block_rows: range, tile_cols: range,
+                     counter: StepCounter | None = None) -> BlockMeta:
+    """Group one (block, tile) cell on the GPU (reference preproc.py:200-236)."""
+    from .matcore import decode
+    h = len(block_rows)
+    if h < 1:
+        raise ValueError("empty block")
+    if h > K_CAP[m.bitwidth]:
+        raise KTooLarge(h, m.bitwidth)
+    tn = len(tile_cols)
+    if not 1 <= tn <= MAX_TILE_WIDTH:
+        raise TileTooWide(f"tile of {tn} columns", n_tile=tn)
+    dense = decode(m)[block_rows.start:block_rows.stop, tile_cols.start:tile_cols.stop]
+    sub = encode(dense, h, tn, m.bitwidth)
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    words, perm, go, po, steps = _grouping(sub.device_data(dev), h, tn, sub.row_bytes,
+                                           m.bitwidth, h, tn, dev)
+    if counter is not None:
+        counter.steps += int(steps[0].item())
+    groups = tuple(GroupRecord(*unpack_group(w)) for w in _u64_host(words))
+    return BlockMeta(_u16_host(perm).copy(), groups)
+
+
+def _cell_key_array(words: np.ndarray, bitwidth: str) -> np.ndarray:
+    pos = ((words >> np.uint64(32)) & np.uint64(0xFFFF)).astype(np.int64)
+    neg = ((words >> np.uint64(48)) & np.uint64(0xFFFF)).astype(np.int64)
+    if bitwidth == BINARY:
+        return pos
+    key = np.zeros(words.size, np.int64)
+    for i in range(16):
+        key += (((pos >> i) & 1) + 2 * ((neg >> i) & 1)) << (2 * i)
+    return key
+
+
+def validate_artifact(a: RsrArtifact) -> None:
+    """Structural audit on host copies; raises CorruptArtifact
+    (same invariants as reference preproc.py:305-372)."""
+    def fail(msg):
+        raise CorruptArtifact(msg)
+
+    if a.bitwidth not in (BINARY, TERNARY):
+        fail(f"bad bitwidth {a.bitwidth!r}")
+    if a.m < 1 or a.n < 1:
+        fail("empty matrix dimensions")
+    if not 1 <= a.k <= K_CAP[a.bitwidth]:
+        fail(f"k={a.k} outside caps for {a.bitwidth}")
+    p = a.plan
+    if p.block_count != -(-a.m // a.k) or p.tile_count != -(-a.n // p.tile_width):
+        fail("plan grid inconsistent with matrix shape")
+    go, po = a.group_offsets, a.perm_offsets
+    words, perm = a.words, a.perm
+    cells = a.cells
+    if len(go) != cells + 1 or len(po) != cells + 1:
+        fail("offset arrays do not match the cell grid")
+    if go[0] != 0 or po[0] != 0 or go[-1] != len(words) or po[-1] != len(perm):
+        fail("offset bounds do not match array lengths")
+    if (np.diff(go) < 0).any() or (np.diff(po) < 0).any():
+        fail("offsets not monotone")
+    for t in range(p.tile_count):
+        tn = min(p.tile_width, a.n - t * p.tile_width)
+        for b in range(p.block_count):
+            c = a.cell_index(t, b)
+            h = min(a.k, a.m - b * a.k)
+            w = words[go[c]:go[c + 1]]
+            seg = perm[po[c]:po[c + 1]]
+            if w.size == 0:
+                if seg.size:
+                    fail(f"cell {c}: permutation without groups")
+                continue
+            ps = (w & np.uint64(0xFFFF)).astype(np.int64)
+            pl = ((w >> np.uint64(16)) & np.uint64(0xFFFF)).astype(np.int64)
+            pos = ((w >> np.uint64(32)) & np.uint64(0xFFFF)).astype(np.int64)
+            neg = ((w >> np.uint64(48)) & np.uint64(0xFFFF)).astype(np.int64)
+            if (pl < 1).any():
+                fail(f"cell {c}: empty group")
+            if ps[0] != 0 or (ps[1:] != ps[:-1] + pl[:-1]).any():
+                fail(f"cell {c}: permutation ranges not consecutive")
+            if ps[-1] + pl[-1] != seg.size:
+                fail(f"cell {c}: group ranges do not cover the permutation")
+            if ((pos & neg) != 0).any():
+                fail(f"cell {c}: overlapping scatter masks")
+            if ((pos | neg) == 0).any():
+                fail(f"cell {c}: stored zero pattern")
+            if h < 16 and ((pos | neg) >> h != 0).any():
+                fail(f"cell {c}: mask bits beyond block height {h}")
+            if a.bitwidth == BINARY and (neg != 0).any():
+                fail(f"cell {c}: negative mask in a binary artifact")
+            if (np.diff(_cell_key_array(w, a.bitwidth)) <= 0).any():
+                fail(f"cell {c}: group keys not strictly ascending")
+            if seg.size and int(seg.max()) >= tn:
+                fail(f"cell {c}: column index beyond tile width {tn}")
+            if np.unique(seg).size != seg.size:
+                fail(f"cell {c}: duplicate column in permutation")
+            starts = np.repeat(ps, pl)
+            idx = np.arange(seg.size)
+            inner = idx != starts
+            if inner.any() and (seg[1:][inner[1:]].astype(np.int64)
+                                <= seg[:-1][inner[1:]].astype(np.int64)).any():
+                fail(f"cell {c}: columns not ascending within a group")
+
+
+def reconstruct(a: RsrArtifact) -> PackedMatrix:
+    """Rebuild the source matrix from an artifact, auditing first
+    (reference preproc.py:375-400)."""
+    validate_artifact(a)
+    dense = np.zeros((a.m, a.n), np.int8)
+    p = a.plan
+    go, po, words, perm = a.group_offsets, a.perm_offsets, a.words, a.perm
+    for t in range(p.tile_count):
+        c0 = t * p.tile_width
+        for b in range(p.block_count):
+            c = a.cell_index(t, b)
+            r0 = b * a.k
+            h = min(a.k, a.m - r0)
+            seg = perm[po[c]:po[c + 1]]
+            for word in words[go[c]:go[c + 1]]:
+                ps, pl, pos, neg = unpack_group(word)
+                cols = c0 + seg[ps:ps + pl].astype(np.int64)
+                for i in range(h):
+                    if (pos >> i) & 1:
+                        dense[r0 + i, cols] = 1
+                    elif (neg >> i) & 1:
+                        dense[r0 + i, cols] = -1
+    out = encode(dense, a.m, a.n, a.bitwidth)
+    return PackedMatrix(a.m, a.n, a.bitwidth, out.data, weight_scale=a.weight_scale)

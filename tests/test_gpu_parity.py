@@ -1,0 +1,172 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle and
+the reference golden vectors.  Integer/byte work is bit-exact; the float path
+is held to |y - ref| <= 1e-6 * sum_j |M_ij v_j| + 1e-6 * |ref| per row
+(ref = the reference's float64 accumulation)."""
+
+import numpy as np
+import pytest
+
+from oracle import rsr_oracle as orc
+from tests import golden_data as gd
+
+pytestmark = pytest.mark.gpu
+
+FLOAT_RTOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def rsr():
+    import torch
+    import paper_2603_27462_b200 as pkg
+    torch.cuda.set_device(0)
+    return pkg
+
+
+def float_ok(y, ref_f64, dense, v):
+    cond = np.abs(dense.astype(np.float64)) @ np.abs(np.asarray(v, np.float64))
+    return np.abs(y.astype(np.float64) - ref_f64) <= FLOAT_RTOL * cond + FLOAT_RTOL * np.abs(ref_f64)
+
+
+def _golden_usable(md):
+    tw = md["tile_width"] or (md["n"] if md["n"] <= 65536 else 32768)
+    return tw <= 32768
+
+
+@pytest.mark.parametrize("i", range(19))
+def test_preprocess_bit_exact_vs_reference(rsr, i):
+    case = gd.small_case(i)
+    md = case["meta"]
+    if not _golden_usable(md):
+        pytest.skip("tile wider than 32768 columns (see DESIGN.md)")
+    m = rsr.PackedMatrix(md["m"], md["n"], md["bitwidth"], case["data"], md["weight_scale"])
+    a = rsr.preprocess(m, md["k"], md["tile_width"])
+    assert np.array_equal(a.words, case["words"])
+    assert np.array_equal(a.perm, case["perm"])
+    assert np.array_equal(a.group_offsets, case["go"])
+    assert np.array_equal(a.perm_offsets, case["po"])
+    assert np.array_equal(a.sort_steps, case["steps"])
+    assert a.file_bytes() == md["file_bytes"]
+    assert list(a.op_totals()) == md["op_totals"]
+    rsr.validate_artifact(a)
+
+
+@pytest.mark.parametrize("i", range(19))
+def test_multiply_vs_reference(rsr, i):
+    case = gd.small_case(i)
+    md = case["meta"]
+    if not _golden_usable(md):
+        pytest.skip("tile wider than 32768 columns (see DESIGN.md)")
+    m = rsr.PackedMatrix(md["m"], md["n"], md["bitwidth"], case["data"], md["weight_scale"])
+    a = rsr.preprocess(m, md["k"], md["tile_width"])
+    y = rsr.rsr_matvec(a, case["vi"])
+    assert y.dtype == np.int32
+    assert np.array_equal(y, case["y_i8"])
+    yf = rsr.rsr_matvec(a, case["vf"])
+    assert yf.dtype == np.float32
+    dense = orc.decode(orc.Packed(md["m"], md["n"], md["bitwidth"], case["data"]))
+    assert float_ok(yf, case["naive_f64"], dense, case["vf"]).all()
+    if md["bitwidth"] == "ternary":
+        assert np.array_equal(rsr.rsr_matvec_fused(a, case["vf"]), case["fused"])
+
+
+def test_known_answers(rsr):
+    m = rsr.encode(np.array([[1, 0, 1, 0], [1, 1, 0, 0]], np.int8), 2, 4, "binary")
+    a = rsr.preprocess(m, 2)
+    assert list(a.perm) == [2, 1, 0]
+    assert [(g.perm_start, g.perm_len, g.pos_mask, g.neg_mask)
+            for g in a.block_meta(0, 0).groups] == [(0, 1, 1, 0), (1, 1, 2, 0), (2, 1, 3, 0)]
+    assert a.op_totals() == (3, 4, 3)
+    assert list(rsr.rsr_matvec(a, np.array([1, 2, 3, 4], np.int8))) == [4, 3]
+    mt = rsr.PackedMatrix(2, 3, "ternary", rsr.encode(
+        np.array([[1, -1, 0], [0, 1, 1]], np.int8), 2, 3, "ternary").data, 0.5)
+    at = rsr.preprocess(mt, 2)
+    y = rsr.rsr_matvec_fused(at, np.array([2.0, 3.0, 5.0], np.float32))
+    exp = (np.array([-25, 203], np.float64) * (0.5 / 25.4)).astype(np.float32)
+    assert np.array_equal(y, exp)
+    assert list(rsr.rsr_matvec(at, np.array([2, 3, 5], np.int8))) == [-1, 8]
+
+
+def test_saturating_inputs(rsr):
+    n = 4096
+    a = rsr.preprocess(rsr.encode(np.ones((3, n), np.int8), 3, n, "binary"), 3)
+    assert list(rsr.rsr_matvec(a, np.full(n, -128, np.int8))) == [-128 * n] * 3
+
+
+def test_zero_matrix(rsr):
+    a = rsr.preprocess(rsr.encode(np.zeros((4, 8), np.int8), 4, 8, "ternary"), 3)
+    assert a.words.size == 0 and a.perm.size == 0
+    assert a.op_totals() == (0, 0, 0)
+    assert list(rsr.rsr_matvec(a, np.ones(8, np.int8))) == [0, 0, 0, 0]
+    assert list(rsr.rsr_matvec_fused(a, np.ones(8, np.float32))) == [0.0] * 4
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("bw", ["binary", "ternary"])
+def test_random_shapes_vs_oracle(rsr, seed, bw):
+    rng = np.random.default_rng(100 + seed)
+    m_, n_ = int(rng.integers(1, 300)), int(rng.integers(1, 3000))
+    k = int(rng.integers(1, (16 if bw == "binary" else 10) + 1))
+    tw = [None, 48, 1000, 777][seed % 4]
+    dens = [0.5, 0.1, 0.9, 0.69][seed % 4]
+    p = orc.random_matrix(m_, n_, bw, seed, dens)
+    ref = orc.preprocess(p, k, tw)
+    a = rsr.preprocess(rsr.PackedMatrix(m_, n_, bw, p.data, 0.37), k, tw)
+    assert np.array_equal(a.words, ref.words)
+    assert np.array_equal(a.perm, ref.perm)
+    assert np.array_equal(a.group_offsets, ref.group_offsets)
+    assert np.array_equal(a.sort_steps, ref.sort_steps)
+    vi = rng.integers(-128, 128, n_).astype(np.int8)
+    assert np.array_equal(rsr.rsr_matvec(a, vi), orc.matvec_i8(ref, vi))
+    vf = (rng.standard_normal(n_) * 3).astype(np.float32)
+    assert float_ok(rsr.rsr_matvec(a, vf), orc.matvec_f64(ref, vf), orc.decode(p), vf).all()
+    if bw == "ternary":
+        ref.weight_scale = 0.37
+        assert np.array_equal(rsr.rsr_matvec_fused(a, vf), orc.fused_matvec(ref, vf))
+
+
+def test_torch_inputs_stay_on_device(rsr):
+    import torch
+    p = orc.random_matrix(64, 512, "ternary", 3)
+    a = rsr.preprocess(rsr.PackedMatrix(64, 512, "ternary", p.data), 4)
+    ref = orc.preprocess(p, 4)
+    v = orc.random_vector(512, 3)
+    vb = torch.from_numpy(v).cuda().to(torch.bfloat16)
+    y = rsr.rsr_matvec(a, vb)
+    assert y.is_cuda and y.dtype == torch.float32
+    vr = vb.float().cpu().numpy()
+    assert float_ok(y.cpu().numpy(), orc.matvec_f64(ref, vr), orc.decode(p), vr).all()
+    yq = rsr.rsr_matvec_fused(a, vb)
+    assert np.array_equal(yq.cpu().numpy(), orc.fused_matvec(ref, vr))
+    vi = torch.randint(-128, 128, (512,), dtype=torch.int8, device="cuda")
+    assert np.array_equal(rsr.rsr_matvec(a, vi).cpu().numpy(),
+                          orc.matvec_i8(ref, vi.cpu().numpy()))
+
+
+def test_c2_full_size_bit_exact_vs_reference(rsr):
+    """Ternary 16384^2 (BASELINE config 1) at k=6: GPU artifact digests equal
+    the reference's; the int path equals the reference output; the float
+    path meets the stated tolerance; fused equals the reference exactly."""
+    import torch
+    name = "C2_ternary_16384_k6"
+    rec = gd.meta()["large"][name]
+    p = orc.random_matrix(16384, 16384, "ternary", 0)
+    assert gd.sha(p.data) == rec["data_sha"]
+    a = rsr.preprocess(rsr.PackedMatrix(16384, 16384, "ternary", p.data), 6)
+    assert gd.sha(a.words) == rec["words_sha"]
+    assert gd.sha(a.perm) == rec["perm_sha"]
+    assert gd.sha(a.group_offsets) == rec["go_sha"]
+    assert gd.sha(a.perm_offsets) == rec["po_sha"]
+    assert gd.sha(a.sort_steps) == rec["steps_sha"]
+    assert a.file_bytes() == rec["file_bytes"]
+    assert list(a.op_totals()) == rec["op_totals"]
+    vi = gd.int_vector(16384, 0)
+    assert np.array_equal(rsr.rsr_matvec(a, vi), gd.large_output(name + "_y_i8"))
+    vf = orc.random_vector(16384, 0)
+    vb = torch.from_numpy(vf).cuda().to(torch.bfloat16)
+    y = rsr.rsr_matvec(a, vb).cpu().numpy()
+    vr = gd.bf16_round(vf)
+    ref = orc.preprocess(p, 6)
+    yr = orc.matvec_f64(ref, vr, threads=8)
+    assert float_ok(y, yr, orc.decode(p), vr).all()
+    assert np.array_equal(rsr.rsr_matvec_fused(a, vb).cpu().numpy(),
+                          gd.large_output(name + "_fused_bf16v"))
