@@ -231,16 +231,11 @@ def main():
     views, keep = [], []
     for c in range(ncopies):
         if c == 0:
-            ent, gs, eo, go = a.entries_d, a.gsigns_d, a.e_off_d, a.g_off_d
+            ent, eo = a.entries_d, a.e_off_d
         else:
-            ent, gs, eo, go = (a.entries_d.clone(), a.gsigns_d.clone(), a.e_off_d.clone(),
-                               a.g_off_d.clone())
-        keep.append((ent, gs, eo, go))
-        v = a.view(b0, nb)
-        v.entries, v.gsigns = _lib.ptr(ent), _lib.ptr(gs)
-        v.e_off = _lib.ptr(eo) + 8 * b0 * a.plan.tile_count
-        v.g_off = _lib.ptr(go) + 8 * b0 * a.plan.tile_count
-        views.append(v)
+            ent, eo = a.entries_d.clone(), a.e_off_d.clone()
+        keep.append((ent, eo))
+        views.append(a.view(b0, nb, entries=ent, e_off=eo))
 
     vf = random_vector(cfg["n"], 0)
     vt = torch.from_numpy(vf).to(dev)

@@ -18,11 +18,14 @@
  *                   (_native.py:4-9, preproc.py:31-41)
  *   cells         : tile-major, cell = t * block_count + b (preproc.py:120-122)
  *
- * The multiply kernels consume a device-only "stream" layout derived from the
- * reference arrays once per artifact (rsr_stream_build): block-major cells,
- * u16 entries = tile-local column | head-of-group<<15 (u32 entries with bit
- * 31 for tiles wider than 32768 columns), a u32 sign word per group
- * (pos | neg<<16), every cell padded to 32 bytes of entries.  See DESIGN.md.
+ * The multiply kernels consume a device-only "chunk stream" derived from the
+ * reference arrays once per artifact (rsr_stream_build): cells in block-major
+ * order, each a run of fixed-size chunks (16 or 32 entries).  An entry is a
+ * u16 (u32 for tiles wider than 32768 columns or pattern spaces above 2^15):
+ * top bit clear -> a tile-local column to gather; top bit set -> the pattern
+ * KEY of the group whose columns follow (binary: pos mask; ternary: base-3
+ * digits, 0 = pad).  Every chunk starts with a key entry, so any warp can
+ * process any chunk without knowing what came before it.  See DESIGN.md.
  */
 #ifndef RSR_B200_H
 #define RSR_B200_H
@@ -57,17 +60,15 @@ typedef enum {
     RSR_I32 = 4
 } rsr_dtype;
 
-/* Device view of a matrix's stream layout (built by rsr_stream_build). */
+/* Device view of a matrix's chunk stream (built by rsr_stream_build). */
 typedef struct {
     int64_t m, n;              /* rows, cols */
     int32_t k, bitwidth;       /* block height, rsr_bitwidth */
     int64_t tile_width, block_count, tile_count;
-    int32_t entry_bytes;       /* 2 (u16 entries) or 4 (u32 entries, tile_width > 32768) */
-    int32_t reserved;
+    int32_t entry_bytes;       /* 2 (u16 entries) or 4 (u32 entries) */
+    int32_t chunk;             /* entries per chunk: 16 or 32 */
     const void *entries;       /* device, entry_bytes each */
-    const uint32_t *gsigns;    /* device, one sign word per group (incl. padding groups) */
     const int64_t *e_off;      /* device, cells+1 entry offsets, block-major cell order */
-    const int64_t *g_off;      /* device, cells+1 group offsets, block-major cell order */
     int64_t row_begin_block;   /* first block this view covers (row-block sharding) */
     int64_t n_blocks;          /* blocks covered (== block_count unless sharded) */
 } rsr_stream_view;
@@ -100,17 +101,21 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
                           const int64_t *go, const int64_t *po, uint64_t *words, uint16_t *perm,
                           void *workspace, size_t workspace_bytes, rsr_stream_t stream);
 
-/* ---- stream layout (device-only multiply format) ----------------------------
- * rsr_stream_count fills e_off/g_off (cells+1, block-major); the caller reads
- * e_off[cells], g_off[cells] to size entries/gsigns, then rsr_stream_build
- * fills them from the reference arrays.                                      */
-rsr_status rsr_stream_count(const int64_t *go, const int64_t *po, int64_t block_count,
-                            int64_t tile_count, int32_t entry_bytes, int64_t *e_off,
-                            int64_t *g_off, rsr_stream_t stream);
+/* ---- chunk stream (device-only multiply format) ------------------------------
+ * rsr_stream_count: per-cell entry counts exclusive-scanned into e_off
+ * (cells+1, block-major) and each group's first slot inside its cell into
+ * gslot (int32, one per reference word).  The caller reads e_off[cells] to
+ * size the entries, then rsr_stream_build writes them.  entry_bytes 0 asks
+ * the library to choose (rsr_stream_entry_bytes).                           */
+int32_t rsr_stream_entry_bytes(int32_t bitwidth, int32_t k, int64_t tile_width);
+rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, int64_t block_count,
+                            int64_t tile_count, int32_t chunk, int64_t *e_off, int32_t *gslot,
+                            rsr_stream_t stream);
 rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,
-                            int32_t entry_bytes, const int64_t *e_off, const int64_t *g_off,
-                            void *entries, uint32_t *gsigns, rsr_stream_t stream);
+                            int32_t bitwidth, int32_t entry_bytes, int32_t chunk,
+                            const int64_t *e_off, const int32_t *gslot, void *entries,
+                            rsr_stream_t stream);
 
 /* ---- online multiply --------------------------------------------------------
  * rsr_matvec: y (+)= A . v  over the view's row blocks.

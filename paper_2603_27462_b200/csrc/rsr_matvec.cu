@@ -1,23 +1,27 @@
 // rsr_matvec.cu -- online RSR multiply for sm_100a.
 //
 // Replaces the reference's matvec cores (pkg/src/rsrmv/_native.py:167-285)
-// and the fused quantize/multiply/dequantize path (_native.py:313-353).
+// and its fused quantize/multiply/dequantize path (_native.py:313-353).
+//
+// Input: the chunk stream (include/rsr_b200.h): per cell, 32-byte chunks of
+// entries; an entry is a column to gather or (top bit set) the pattern key of
+// the group whose columns follow; every chunk starts with a key.
 //
 // Work decomposition:
-//   * grid.y = column tile; each CTA stages its tile of v in shared memory
+//   * grid.y = column tile.  Each CTA stages its tile of v in shared memory
 //     once (fp32 for the float path, int8 for the integer/fused paths; the
-//     fused path quantizes while staging after a CTA-local absmax over the
-//     whole vector, so no separate quantization pass exists);
-//   * one warp owns one (block, tile) cell at a time and streams the cell's
-//     entries (u16 column | head<<15) with 2 x 16-byte loads per lane per
-//     round (1 KiB per warp-round), prefetching the next round;
-//   * each lane owns 16 consecutive entries: it gathers v from shared memory,
-//     keeps a running partial group sum, and at every group head flushes the
-//     partial sum into its k row accumulators with the group's signs
-//     (linearity: y_i = sum_g sgn_i(g) * S_g = sum over partial segments);
-//     the group index of a lane's first entry comes from a warp scan of the
-//     head counts;
-//   * at the end of the cell the k accumulators are warp-reduced and written.
+//     fused path quantizes while staging, after a CTA-local absmax over the
+//     whole vector -- no separate quantization launch);
+//   * one warp owns one (block, tile) cell at a time; lane L of a round owns
+//     chunk L: one 32-byte load, then a gather from shared memory per column
+//     entry and a running partial group sum;
+//   * at every key entry the partial sum is flushed into the warp's PATTERN
+//     BUCKET for that key (3^k ternary / 2^k binary buckets in shared memory);
+//   * when the cell is done, the pattern-table reduction y_i = sum_key
+//     sgn_i(key) * bucket[key] (sign table in shared memory) produces the k
+//     rows, warp-reduced and written once.
+// For pattern spaces too large for shared-memory buckets the "register"
+// variant flushes straight into k row accumulators instead.
 // Integer accumulation is exact, so the int8 and fused paths are
 // bit-identical to the reference.  The float path accumulates in fp32.
 
@@ -25,29 +29,30 @@
 
 namespace rsr {
 
-constexpr int MV_WARPS = 8;
-constexpr int MV_EPL = 16;  // u16 entries per lane per round (32 bytes)
-
 enum MvMode { MODE_FLOAT = 0, MODE_INT = 1, MODE_FUSED = 2 };
 
+constexpr int MV_MAX_WARPS = 32;
+constexpr int64_t BUCKET_MAX_KEYS = 2187;  // 3^7: buckets live in smem up to here
+
 struct MvParams {
-    const uint16_t *entries;
-    const uint32_t *gsigns;
+    const void *entries;
     const int64_t *e_off;
-    const int64_t *g_off;
     int64_t m_rows;      // rows of the full matrix
     int64_t n;           // columns
     int64_t tw, tc;      // tile width / count
     int64_t blk0;        // first global block of this view
     int64_t nblk;        // blocks in this view
     int k;
+    int bitwidth;
+    int nkeys;           // pattern buckets: 3^k or 2^k
     const void *v;
     int vdtype;
+    const void *vstaged; // u32-entry variant: v converted/quantized in global memory
     void *y;             // output slice (view rows)
     int accumulate;
     void *part;          // tc > 1: [tc][nblk*k] partials (float or int32)
     double beta;         // fused
-    double *scale_out;   // fused (may be null)
+    double *scale_dev;   // fused: device scale slot (may be null when tc == 1)
 };
 
 __device__ __forceinline__ float load_as_f32(const void *v, int dtype, int64_t i) {
@@ -67,8 +72,8 @@ __device__ __forceinline__ int8_t quantize_one(float x, double scale) {
     return (int8_t)(int)r;
 }
 
-// CTA-wide max of |v| over the whole vector, in float64 (exact: max is
-// order-independent).  Result broadcast to every thread.
+// CTA-wide max of |v| over the whole vector in float64 (order-independent,
+// hence exact and identical in every CTA).
 __device__ double cta_absmax(const void *v, int dtype, int64_t n) {
     __shared__ double red[32];
     double a = 0.0;
@@ -99,110 +104,158 @@ __device__ double cta_absmax(const void *v, int dtype, int64_t n) {
     return r;
 }
 
+// Sign of row i in the pattern with dense key `key`.
+__device__ __forceinline__ int key_sign(uint32_t key, int i, int bitwidth) {
+    if (bitwidth == RSR_BINARY) return (int)((key >> i) & 1u);
+    for (int j = 0; j < i; ++j) key /= 3u;
+    const uint32_t d = key % 3u;
+    return d == 1u ? 1 : (d == 2u ? -1 : 0);
+}
+
+template <int K>
+struct KPad {
+    static constexpr int value = (K + 3) & ~3;
+};
+
 template <typename Acc>
-__device__ __forceinline__ Acc sign_of(uint32_t m, int i) {
-    return (Acc)((int)((m >> i) & 1u) - (int)((m >> (16 + i)) & 1u));
+__device__ __forceinline__ void bucket_add_atomic(Acc *b, Acc s) {
+    atomicAdd(b, s);
 }
 
-// Flush a partial group sum into the k row accumulators (FMA with the
-// group's sign, so a non-finite partial poisons every row of the block
-// exactly as the reference's `y += sgn * s` does).
-template <int K, typename Acc>
-__device__ __forceinline__ void flush(Acc (&acc)[K], Acc s, uint32_t m) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) acc[i] += sign_of<Acc>(m, i) * s;
-}
-
-template <int K, int MODE>
-__global__ void __launch_bounds__(MV_WARPS * 32)
+template <int K, int MODE, typename E, bool BUCKET>
+__global__ void __launch_bounds__(MV_MAX_WARPS * 32)
 rsr_mv_kernel(MvParams p) {
     using Acc = typename std::conditional<MODE == MODE_FLOAT, float, int32_t>::type;
     using VS = typename std::conditional<MODE == MODE_FLOAT, float, int8_t>::type;
-    extern __shared__ __align__(16) unsigned char mv_smem[];
-    VS *vs = reinterpret_cast<VS *>(mv_smem);
+    constexpr bool SMEM_V = sizeof(E) == 2;
+    constexpr int CH = 32 / (int)sizeof(E);           // entries per chunk (32 bytes)
+    constexpr E KEYFLAG = (E)1 << (8 * sizeof(E) - 1);
+    constexpr int KP = KPad<K>::value;
 
+    extern __shared__ __align__(16) unsigned char mv_smem[];
+    const int nwarps = blockDim.x >> 5;
     const int64_t t = blockIdx.y;
     const int64_t c0 = t * p.tw;
     const int64_t tn = min(p.tw, p.n - c0);
 
-    // ---- prologue: stage this tile of v (quantizing on the fused path) ----
+    // smem carve-up: [v tile][sign table NB x KP][buckets nwarps x NB]
+    size_t off = 0;
+    VS *vs = reinterpret_cast<VS *>(mv_smem);
+    if (SMEM_V) off += ((size_t)tn * sizeof(VS) + 15) & ~(size_t)15;
+    Acc *stab = reinterpret_cast<Acc *>(mv_smem + off);
+    if (BUCKET) off += (size_t)p.nkeys * KP * sizeof(Acc);
+    Acc *buckets = reinterpret_cast<Acc *>(mv_smem + off);
+
+    // ---- prologue -------------------------------------------------------
     double scale = 1.0;
     if (MODE == MODE_FUSED) {
-        const double amax = cta_absmax(p.v, p.vdtype, p.n);
-        scale = amax == 0.0 ? 1.0 : 127.0 / amax;
-        if (p.scale_out && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-            *p.scale_out = scale;
-    }
-    for (int64_t i = threadIdx.x; i < tn; i += blockDim.x) {
-        if (MODE == MODE_FLOAT) {
-            vs[i] = (VS)load_as_f32(p.v, p.vdtype, c0 + i);
-        } else if (MODE == MODE_INT) {
-            vs[i] = __ldg((const int8_t *)p.v + c0 + i);
+        if (SMEM_V) {
+            const double amax = cta_absmax(p.v, p.vdtype, p.n);
+            scale = amax == 0.0 ? 1.0 : 127.0 / amax;
+            if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+                *p.scale_dev = scale;
         } else {
-            vs[i] = quantize_one(load_as_f32(p.v, p.vdtype, c0 + i), scale);
+            scale = *p.scale_dev;  // written by the staging kernel
         }
+    }
+    if (SMEM_V) {
+        for (int64_t i = threadIdx.x; i < tn; i += blockDim.x) {
+            if (MODE == MODE_FLOAT)
+                vs[i] = (VS)load_as_f32(p.v, p.vdtype, c0 + i);
+            else if (MODE == MODE_INT)
+                vs[i] = __ldg((const int8_t *)p.v + c0 + i);
+            else
+                vs[i] = quantize_one(load_as_f32(p.v, p.vdtype, c0 + i), scale);
+        }
+    }
+    if (BUCKET) {
+        for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
+#pragma unroll
+            for (int i = 0; i < KP; ++i)
+                stab[key * KP + i] = (Acc)(i < K ? key_sign((uint32_t)key, i, p.bitwidth) : 0);
+        }
+        for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
     }
     __syncthreads();
 
+    const VS *vg = SMEM_V ? vs : reinterpret_cast<const VS *>(p.vstaged) + c0;
     const uint32_t lane = lane_id();
     const int warp = threadIdx.x >> 5;
+    Acc *bk = buckets + (size_t)warp * p.nkeys;
     const uint4 *ent4 = reinterpret_cast<const uint4 *>(p.entries);
 
-    for (int64_t b = (int64_t)blockIdx.x * MV_WARPS + warp; b < p.nblk;
-         b += (int64_t)gridDim.x * MV_WARPS) {
+    for (int64_t b = (int64_t)blockIdx.x * nwarps + warp; b < p.nblk;
+         b += (int64_t)gridDim.x * nwarps) {
         const int64_t dc = b * p.tc + t;
-        const int64_t e0 = p.e_off[dc], e1 = p.e_off[dc + 1];
-        int64_t g = p.g_off[dc] - 1;  // index of the group before the cell's first entry
+        const int64_t ch0 = p.e_off[dc] / CH, ch1 = p.e_off[dc + 1] / CH;  // chunk range
         Acc acc[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
 
-        // 16 entries (two uint4) per lane per round; prefetch one round ahead.
-        int64_t idx = e0 + (int64_t)lane * MV_EPL;
+        int64_t ch = ch0 + lane;
         uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-        if (idx < e1) {
-            q0 = __ldg(ent4 + (idx >> 3));
-            q1 = __ldg(ent4 + (idx >> 3) + 1);
+        if (ch < ch1) {
+            q0 = __ldg(ent4 + 2 * ch);
+            q1 = __ldg(ent4 + 2 * ch + 1);
         }
-        for (int64_t base = e0; base < e1; base += 32 * MV_EPL) {
-            const bool valid = idx < e1;
-            const uint4 c0q = q0, c1q = q1;
-            const int64_t nidx = idx + 32 * MV_EPL;
-            if (nidx < e1) {
-                q0 = __ldg(ent4 + (nidx >> 3));
-                q1 = __ldg(ent4 + (nidx >> 3) + 1);
+        for (int64_t base = ch0; base < ch1; base += 32) {
+            const bool valid = ch < ch1;
+            const uint4 a0 = q0, a1 = q1;
+            const int64_t nch = ch + 32;
+            if (nch < ch1) {  // prefetch the next round
+                q0 = __ldg(ent4 + 2 * nch);
+                q1 = __ldg(ent4 + 2 * nch + 1);
             }
-            const uint32_t w[8] = {c0q.x, c0q.y, c0q.z, c0q.w, c1q.x, c1q.y, c1q.z, c1q.w};
-            // head bits of the 16 entries, packed: bit e = head of entry e
-            uint32_t hm = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                hm |= ((w[j] >> 15) & 1u) << (2 * j) | ((w[j] >> 31) & 1u) << (2 * j + 1);
-            const uint32_t cnt = valid ? __popc(hm) : 0u;
-            const uint32_t incl = warp_inclusive_scan(cnt, lane);
-            const uint32_t total = __shfl_sync(RSR_FULL_MASK, incl, 31);
             if (valid) {
-                int64_t gg = g + (int64_t)(incl - cnt);
-                uint32_t msk = gg >= 0 ? __ldg(p.gsigns + gg) : 0u;
+                const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                uint32_t cur = 0;
                 Acc s = (Acc)0;
 #pragma unroll
-                for (int e = 0; e < MV_EPL; ++e) {
-                    const uint32_t x = (e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xFFFFu);
-                    if ((hm >> e) & 1u) {
-                        if (e > 0) flush<K, Acc>(acc, s, msk);
+                for (int e = 0; e < CH; ++e) {
+                    uint32_t x;
+                    if (sizeof(E) == 2)
+                        x = (e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xFFFFu);
+                    else
+                        x = w[e];
+                    if (x & (uint32_t)KEYFLAG) {
+                        if (e > 0) {
+                            if (BUCKET) {
+                                if (MODE == MODE_FLOAT) bk[cur] += s;  // distinct keys per instruction
+                                else atomicAdd(bk + cur, s);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+                                    acc[i] += (Acc)key_sign(cur, i, p.bitwidth) * s;
+                            }
+                        }
+                        cur = x & ~(uint32_t)KEYFLAG;
                         s = (Acc)0;
-                        ++gg;
-                        msk = __ldg(p.gsigns + gg);
+                    } else {
+                        s += (Acc)vg[x];
                     }
-                    s += (Acc)vs[x & 0x7FFFu];
                 }
-                flush<K, Acc>(acc, s, msk);
+                if (BUCKET) {
+                    bucket_add_atomic(bk + cur, s);  // tails of one group may coincide
+                } else {
+#pragma unroll
+                    for (int i = 0; i < K; ++i) acc[i] += (Acc)key_sign(cur, i, p.bitwidth) * s;
+                }
             }
-            g += total;
-            idx = nidx;
+            __syncwarp();
+            ch = nch;
         }
 
-        // ---- epilogue: warp-reduce the k rows, write ----
+        // ---- pattern-table reduction: y_i = sum_key sgn_i(key) * bucket[key] ----
+        if (BUCKET) {
+            for (int key = lane; key < p.nkeys; key += 32) {
+                const Acc bv = bk[key];
+                bk[key] = (Acc)0;
+                const Acc *row = stab + key * KP;
+#pragma unroll
+                for (int i = 0; i < K; ++i) acc[i] += row[i] * bv;
+            }
+            __syncwarp();
+        }
         const int64_t row0 = b * p.k;  // row within the view
         const int64_t grow0 = (p.blk0 + b) * p.k;
         Acc mine = (Acc)0;
@@ -230,14 +283,14 @@ rsr_mv_kernel(MvParams p) {
     }
 }
 
-// tc > 1: sum tile partials in ascending tile order (the reference's order).
+// tc > 1: sum the tile partials in ascending tile order (the reference order).
 template <int MODE>
-__global__ void tile_finalize_kernel(MvParams p, int64_t rows_view, const double *scale_dev) {
+__global__ void tile_finalize_kernel(MvParams p, int64_t rows_view) {
     using Acc = typename std::conditional<MODE == MODE_FLOAT, float, int32_t>::type;
     const Acc *part = reinterpret_cast<const Acc *>(p.part);
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows_view;
          r += (int64_t)gridDim.x * blockDim.x) {
-        if ((p.blk0 * p.k) + r >= p.m_rows) continue;
+        if (p.blk0 * p.k + r >= p.m_rows) continue;
         Acc s = (Acc)0;
         for (int64_t t = 0; t < p.tc; ++t) s += part[t * rows_view + r];
         if (MODE == MODE_FLOAT) {
@@ -247,8 +300,26 @@ __global__ void tile_finalize_kernel(MvParams p, int64_t rows_view, const double
             int32_t *y = reinterpret_cast<int32_t *>(p.y);
             y[r] = p.accumulate ? y[r] + s : s;
         } else {
-            reinterpret_cast<float *>(p.y)[r] = (float)((double)s * (p.beta / *scale_dev));
+            reinterpret_cast<float *>(p.y)[r] = (float)((double)s * (p.beta / *p.scale_dev));
         }
+    }
+}
+
+// u32-entry variant (tiles wider than 32768 columns): v converted/quantized
+// once into global scratch; the multiply gathers it through L1/L2.
+__global__ void stage_global_kernel(const void *v, int dtype, int64_t n, int mode, void *out,
+                                    double *scale_dev) {
+    double scale = 1.0;
+    if (mode == MODE_FUSED) {
+        const double amax = cta_absmax(v, dtype, n);
+        scale = amax == 0.0 ? 1.0 : 127.0 / amax;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *scale_dev = scale;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (mode == MODE_FLOAT) ((float *)out)[i] = load_as_f32(v, dtype, i);
+        else if (mode == MODE_INT) ((int8_t *)out)[i] = ((const int8_t *)v)[i];
+        else ((int8_t *)out)[i] = quantize_one(load_as_f32(v, dtype, i), scale);
     }
 }
 
@@ -267,11 +338,11 @@ __global__ void absmax_quantize_kernel(const void *v, int dtype, int64_t n, int8
 
 using KernelFn = void (*)(MvParams);
 
-template <int MODE>
-static KernelFn pick_kernel(int k) {
+template <int MODE, typename E, bool BUCKET>
+static KernelFn pick_k(int k) {
     switch (k) {
 #define RSR_K_CASE(KK) \
-    case KK: return rsr_mv_kernel<KK, MODE>;
+    case KK: return rsr_mv_kernel<KK, MODE, E, BUCKET>;
         RSR_K_CASE(1) RSR_K_CASE(2) RSR_K_CASE(3) RSR_K_CASE(4) RSR_K_CASE(5) RSR_K_CASE(6)
         RSR_K_CASE(7) RSR_K_CASE(8) RSR_K_CASE(9) RSR_K_CASE(10) RSR_K_CASE(11) RSR_K_CASE(12)
         RSR_K_CASE(13) RSR_K_CASE(14) RSR_K_CASE(15) RSR_K_CASE(16)
@@ -280,19 +351,35 @@ static KernelFn pick_kernel(int k) {
     }
 }
 
+template <int MODE>
+static KernelFn pick_kernel(int k, int entry_bytes, bool bucket) {
+    if (entry_bytes == 4) return pick_k<MODE, uint32_t, false>(k);
+    return bucket ? pick_k<MODE, uint16_t, true>(k) : pick_k<MODE, uint16_t, false>(k);
+}
+
 static rsr_status check_view(const rsr_stream_view *vw) {
-    if (!vw || !vw->entries || !vw->gsigns || !vw->e_off || !vw->g_off) return RSR_ERR_INVALID;
+    if (!vw || !vw->entries || !vw->e_off) return RSR_ERR_INVALID;
     if (vw->k < 1 || vw->k > 16 || vw->m < 1 || vw->n < 1 || vw->tile_count < 1 ||
-        vw->n_blocks < 0)
+        vw->n_blocks < 0 || vw->tile_width < 1)
         return RSR_ERR_INVALID;
-    if (vw->entry_bytes != 2) return RSR_ERR_INVALID;  // u32 entries: see DESIGN.md
-    if (vw->tile_width > 32768) return RSR_ERR_INVALID;
+    if (vw->bitwidth != RSR_BINARY && vw->bitwidth != RSR_TERNARY) return RSR_ERR_INVALID;
+    if (vw->entry_bytes != 2 && vw->entry_bytes != 4) return RSR_ERR_INVALID;
+    if (vw->chunk != 32 / vw->entry_bytes) return RSR_ERR_INVALID;
+    if (vw->entry_bytes == 2 &&
+        (vw->tile_width > 32768 || bucket_count(vw->bitwidth, vw->k) > 32768))
+        return RSR_ERR_INVALID;
     return RSR_OK;
 }
 
+// workspace: [tile partials][16B: fused scale][staged v (u32 entries)]
 static size_t part_bytes(const rsr_stream_view *vw) {
-    if (vw->tile_count <= 1) return 0;
-    return (size_t)vw->tile_count * (size_t)vw->n_blocks * (size_t)vw->k * 4 + 16;
+    return vw->tile_count <= 1 ? 0
+                               : (((size_t)vw->tile_count * vw->n_blocks * vw->k * 4 + 15) & ~15);
+}
+static size_t ws_bytes_for(const rsr_stream_view *vw) {
+    size_t b = part_bytes(vw) + 16;
+    if (vw->entry_bytes == 4) b += (size_t)vw->n * 4;
+    return b;
 }
 
 template <int MODE>
@@ -303,13 +390,12 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     if (st != RSR_OK) return st;
     if (!v || !y) return RSR_ERR_INVALID;
     if (vw->n_blocks == 0) return RSR_OK;
-    const size_t need = part_bytes(vw);
-    if (need && (ws_bytes < need || !ws)) return RSR_ERR_WORKSPACE;
+    const bool need_ws = vw->tile_count > 1 || vw->entry_bytes == 4 ||
+                         (MODE == MODE_FUSED && !scale_out && vw->tile_count > 1);
+    if (need_ws && (ws_bytes < ws_bytes_for(vw) || !ws)) return RSR_ERR_WORKSPACE;
     MvParams p;
-    p.entries = (const uint16_t *)vw->entries;
-    p.gsigns = vw->gsigns;
+    p.entries = vw->entries;
     p.e_off = vw->e_off;
-    p.g_off = vw->g_off;
     p.m_rows = vw->m;
     p.n = vw->n;
     p.tw = vw->tile_width;
@@ -317,36 +403,57 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     p.blk0 = vw->row_begin_block;
     p.nblk = vw->n_blocks;
     p.k = vw->k;
+    p.bitwidth = vw->bitwidth;
+    p.nkeys = (int)bucket_count(vw->bitwidth, vw->k);
     p.v = v;
     p.vdtype = vdtype;
     p.y = y;
     p.accumulate = accumulate;
     p.part = ws;
     p.beta = beta;
-    double *scale_dev = nullptr;
-    if (MODE == MODE_FUSED) {
-        // with tiles, the finalize pass needs the scale: keep it in the workspace tail
-        scale_dev = scale_out;
-        if (!scale_dev && need) scale_dev = (double *)((char *)ws + need - 16);
+    p.scale_dev = scale_out;
+    if (MODE == MODE_FUSED && !p.scale_dev && need_ws)
+        p.scale_dev = (double *)((char *)ws + part_bytes(vw));
+    p.vstaged = nullptr;
+    if (vw->entry_bytes == 4) {
+        void *stg = (char *)ws + part_bytes(vw) + 16;
+        p.vstaged = stg;
+        stage_global_kernel<<<MODE == MODE_FUSED ? 1 : 256, 1024, 0, s>>>(v, vdtype, vw->n, MODE,
+                                                                          stg, p.scale_dev);
+        if (MODE == MODE_FUSED) {
+            // one CTA computed the scale; re-stage in parallel is unnecessary (n small)
+        }
     }
-    p.scale_out = scale_dev;
-    KernelFn fn = pick_kernel<MODE>(vw->k);
+    const bool bucket = vw->entry_bytes == 2 && p.nkeys <= BUCKET_MAX_KEYS;
+    KernelFn fn = pick_kernel<MODE>(vw->k, vw->entry_bytes, bucket);
     if (!fn) return RSR_ERR_INVALID;
+
+    // size: one persistent CTA per SM, as many warps as fit (<= 32) and needed
+    const int sms = sm_count();
     const size_t vsz = MODE == MODE_FLOAT ? 4 : 1;
-    const size_t smem = (size_t)std::min(vw->tile_width, vw->n) * vsz;
+    const int64_t tn = std::min(vw->tile_width, vw->n);
+    const size_t kp = (size_t)((vw->k + 3) & ~3);
+    size_t fixed = 0;
+    if (vw->entry_bytes == 2) fixed += ((size_t)tn * vsz + 15) & ~(size_t)15;
+    if (bucket) fixed += (size_t)p.nkeys * kp * 4;
+    const size_t per_warp = bucket ? (size_t)p.nkeys * 4 : 0;
+    const size_t smem_cap = 227 * 1024;
+    int64_t cells_per_tile = vw->n_blocks;
+    int64_t ctas_per_tile = std::max<int64_t>(1, sms / vw->tile_count);
+    int64_t warps = (cells_per_tile + ctas_per_tile - 1) / ctas_per_tile;
+    warps = std::max<int64_t>(1, std::min<int64_t>(warps, MV_MAX_WARPS));
+    while (warps > 1 && fixed + warps * per_warp > smem_cap) --warps;
+    if (fixed + warps * per_warp > smem_cap) return RSR_ERR_INVALID;
+    const size_t smem = fixed + warps * per_warp;
+    ctas_per_tile = std::min<int64_t>(ctas_per_tile, (cells_per_tile + warps - 1) / warps);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MV_WARPS * 32, smem);
-    if (occ < 1) occ = 1;
-    const int64_t want = (vw->n_blocks + MV_WARPS - 1) / MV_WARPS;
-    const int64_t cap = std::max<int64_t>(1, ((int64_t)sm_count() * occ) / vw->tile_count);
-    dim3 grid((unsigned)std::min(want, cap), (unsigned)vw->tile_count);
-    fn<<<grid, MV_WARPS * 32, smem, s>>>(p);
+    dim3 grid((unsigned)ctas_per_tile, (unsigned)vw->tile_count);
+    fn<<<grid, (unsigned)(warps * 32), smem, s>>>(p);
     if (vw->tile_count > 1) {
         const int64_t rows_view = vw->n_blocks * vw->k;
         const int g2 = (int)std::min<int64_t>((rows_view + 255) / 256, 4096);
-        tile_finalize_kernel<MODE><<<g2, 256, 0, s>>>(p, rows_view, scale_dev);
+        tile_finalize_kernel<MODE><<<g2, 256, 0, s>>>(p, rows_view);
     }
     return launch_status();
 }
@@ -358,7 +465,9 @@ using namespace rsr;
 extern "C" {
 
 size_t rsr_matvec_workspace_bytes(const rsr_stream_view *view) {
-    return view ? part_bytes(view) : 0;
+    if (!view) return 0;
+    if (view->tile_count <= 1 && view->entry_bytes != 4) return 0;
+    return ws_bytes_for(view);
 }
 
 rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtype, void *y,

@@ -247,22 +247,54 @@ scan2_kernel(int64_t *a, int64_t *b, int64_t cells) {
 }
 
 // ---------------------------------------------------------------------------
-// stream layout: block-major cells, entries padded to 32 bytes per cell.
+// chunk stream: block-major cells; each cell is a run of CH-entry chunks and
+// every chunk starts with a key entry (see include/rsr_b200.h).
 
-__global__ void stream_count_kernel(const int64_t *__restrict__ go, const int64_t *__restrict__ po,
-                                    int64_t bc, int64_t tc, int entry_bytes, int64_t *e_off,
-                                    int64_t *g_off) {
+// Slot placement of one group of L columns whose key would go at slot p (the
+// next free slot of its cell).  Returns the key slot; p becomes the next free
+// slot.  A key never takes the last slot of a chunk (it would own nothing),
+// and a group crossing a chunk boundary repeats its key at the new chunk.
+__host__ __device__ __forceinline__ int64_t place_group(int64_t &p, int64_t L, int64_t CH) {
+    if (p % CH == CH - 1) ++p;
+    const int64_t key_slot = p++;
+    int64_t rem = L;
+    while (rem > 0) {
+        if (p % CH == 0) ++p;
+        const int64_t take = min(rem, CH - p % CH);
+        p += take;
+        rem -= take;
+    }
+    return key_slot;
+}
+
+// Dense pattern key of a group from its masks: binary -> pos mask; ternary
+// -> base-3 digits (1 = +1, 2 = -1).  Key 0 never occurs (zero patterns are
+// dropped) and marks padding.
+__device__ __forceinline__ uint32_t dense_key(uint64_t w, int bitwidth) {
+    const uint32_t pos = (uint32_t)((w >> 32) & 0xFFFFu), neg = (uint32_t)(w >> 48);
+    if (bitwidth == RSR_BINARY) return pos;
+    uint32_t key = 0, p3 = 1;
+    for (int i = 0; i < 16; ++i) {
+        key += (((pos >> i) & 1u) + 2u * ((neg >> i) & 1u)) * p3;
+        p3 *= 3u;
+    }
+    return key;
+}
+
+__global__ void stream_count_kernel(const uint64_t *__restrict__ words,
+                                    const int64_t *__restrict__ go, int64_t bc, int64_t tc,
+                                    int64_t CH, int64_t *e_off, int32_t *gslot) {
     const int64_t cells = bc * tc;
-    const int64_t per_chunk = 32 / entry_bytes;
     for (int64_t dc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; dc < cells;
          dc += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = dc / tc, t = dc - b * tc;
         const int64_t src = t * bc + b;
-        const int64_t nret = po[src + 1] - po[src];
-        const int64_t ng = go[src + 1] - go[src];
-        const int64_t elen = (nret + per_chunk - 1) / per_chunk * per_chunk;
-        e_off[dc + 1] = elen;
-        g_off[dc + 1] = ng + (elen != nret ? 1 : 0);
+        int64_t p = 0;
+        for (int64_t g = go[src]; g < go[src + 1]; ++g) {
+            const int64_t L = (int64_t)((words[g] >> 16) & 0xFFFFu);
+            gslot[g] = (int32_t)place_group(p, L, CH);
+        }
+        e_off[dc + 1] = (p + CH - 1) / CH * CH;
     }
 }
 
@@ -270,29 +302,32 @@ template <typename E>
 __global__ void __launch_bounds__(256)
 stream_build_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                     const uint16_t *__restrict__ perm, const int64_t *__restrict__ po, int64_t bc,
-                    int64_t tc, const int64_t *__restrict__ e_off,
-                    const int64_t *__restrict__ g_off, E *__restrict__ entries,
-                    uint32_t *__restrict__ gsigns) {
-    constexpr E HEAD = (E)1 << (8 * sizeof(E) - 1);
+                    int64_t tc, int bitwidth, int64_t CH, const int64_t *__restrict__ e_off,
+                    const int32_t *__restrict__ gslot, E *__restrict__ entries) {
+    constexpr E KEYFLAG = (E)1 << (8 * sizeof(E) - 1);
     const uint32_t lane = lane_id();
     const int64_t cells = bc * tc;
     for (int64_t dc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; dc < cells;
          dc += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t b = dc / tc, t = dc - b * tc;
         const int64_t src = t * bc + b;
-        const int64_t p0 = po[src], nret = po[src + 1] - p0;
-        const int64_t w0 = go[src], ng = go[src + 1] - w0;
         const int64_t e0 = e_off[dc], elen = e_off[dc + 1] - e0;
-        const int64_t g0 = g_off[dc];
-        for (int64_t i = lane; i < elen; i += 32)
-            entries[e0 + i] = i < nret ? (E)perm[p0 + i] : (i == nret ? HEAD : (E)0);
+        E *out = entries + e0;
+        for (int64_t i = lane; i < elen; i += 32) out[i] = KEYFLAG;  // key 0 = pad
         __syncwarp();
-        for (int64_t gi = lane; gi < ng; gi += 32) {
-            const uint64_t w = words[w0 + gi];
-            entries[e0 + (int64_t)(w & 0xFFFFu)] |= HEAD;
-            gsigns[g0 + gi] = (uint32_t)(w >> 32);
+        const int64_t p0 = po[src];
+        for (int64_t g = go[src] + lane; g < go[src + 1]; g += 32) {
+            const uint64_t w = words[g];
+            const int64_t ps = (int64_t)(w & 0xFFFFu), L = (int64_t)((w >> 16) & 0xFFFFu);
+            const E key = KEYFLAG | (E)dense_key(w, bitwidth);
+            int64_t p = gslot[g];
+            out[p++] = key;
+            const uint16_t *cols = perm + p0 + ps;
+            for (int64_t j = 0; j < L; ++j) {
+                if (p % CH == 0) out[p++] = key;
+                out[p++] = (E)cols[j];
+            }
         }
-        if (lane == 0 && elen != nret) gsigns[g0 + ng] = 0u;
     }
 }
 
@@ -420,36 +455,44 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
     return launch_status();
 }
 
-rsr_status rsr_stream_count(const int64_t *go, const int64_t *po, int64_t block_count,
-                            int64_t tile_count, int32_t entry_bytes, int64_t *e_off,
-                            int64_t *g_off, rsr_stream_t stream) {
-    if (!go || !po || !e_off || !g_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
-    if (entry_bytes != 2 && entry_bytes != 4) return RSR_ERR_INVALID;
+int32_t rsr_stream_entry_bytes(int32_t bitwidth, int32_t k, int64_t tile_width) {
+    const int64_t keys = bucket_count(bitwidth, k);
+    return (tile_width <= 32768 && keys <= 32768) ? 2 : 4;
+}
+
+rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, int64_t block_count,
+                            int64_t tile_count, int32_t chunk, int64_t *e_off, int32_t *gslot,
+                            rsr_stream_t stream) {
+    if (!go || !e_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
+    if (chunk != 8 && chunk != 16 && chunk != 32) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cells = block_count * tile_count;
-    const int grid = (int)std::min<int64_t>((cells + 255) / 256, 4096);
-    stream_count_kernel<<<grid, 256, 0, s>>>(go, po, block_count, tile_count, entry_bytes, e_off,
-                                             g_off);
-    scan2_kernel<<<1, 1024, 0, s>>>(e_off, g_off, cells);
+    const int grid = (int)std::min<int64_t>((cells + 127) / 128, 8192);
+    stream_count_kernel<<<grid, 128, 0, s>>>(words, go, block_count, tile_count, chunk, e_off,
+                                             gslot);
+    scan2_kernel<<<1, 1024, 0, s>>>(e_off, nullptr, cells);
     return launch_status();
 }
 
 rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,
-                            int32_t entry_bytes, const int64_t *e_off, const int64_t *g_off,
-                            void *entries, uint32_t *gsigns, rsr_stream_t stream) {
-    if (!go || !po || !e_off || !g_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
+                            int32_t bitwidth, int32_t entry_bytes, int32_t chunk,
+                            const int64_t *e_off, const int32_t *gslot, void *entries,
+                            rsr_stream_t stream) {
+    if (!go || !po || !e_off || !entries || block_count < 1 || tile_count < 1)
+        return RSR_ERR_INVALID;
+    if (chunk != 8 && chunk != 16 && chunk != 32) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 32);
     if (entry_bytes == 2)
         stream_build_kernel<uint16_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
-                                                           tile_count, e_off, g_off,
-                                                           (uint16_t *)entries, gsigns);
+                                                           tile_count, bitwidth, chunk, e_off,
+                                                           gslot, (uint16_t *)entries);
     else if (entry_bytes == 4)
         stream_build_kernel<uint32_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
-                                                           tile_count, e_off, g_off,
-                                                           (uint32_t *)entries, gsigns);
+                                                           tile_count, bitwidth, chunk, e_off,
+                                                           gslot, (uint32_t *)entries);
     else
         return RSR_ERR_INVALID;
     return launch_status();

@@ -10,9 +10,9 @@ reference attribute names return host numpy copies on first access so code
 written against the reference (validate_artifact, reconstruct, .rsra I/O)
 works unchanged.
 
-On top of the reference arrays every artifact carries the device-only stream
-layout the multiply kernels read (block-major cells, u16 column|head entries,
-u32 group sign words); see DESIGN.md.
+On top of the reference arrays every artifact carries the device-only chunk
+stream the multiply kernels read (block-major cells of 32-byte chunks of
+column / pattern-key entries, every chunk led by a key); see DESIGN.md.
 """
 
 from __future__ import annotations
@@ -28,7 +28,6 @@ from .matcore import BINARY, TERNARY, PackedMatrix, _is_torch, encode
 MAX_TILE_WIDTH = 65536          # reference preproc.py:26
 DEFAULT_WIDE_TILE = 32768       # reference preproc.py:27
 K_CAP = {BINARY: 16, TERNARY: 10}   # reference preproc.py:28
-STREAM_MAX_TILE = 32768         # widest tile the u16 stream entries address
 
 
 def pack_group(perm_start: int, perm_len: int, pos_mask: int, neg_mask: int) -> int:
@@ -114,7 +113,7 @@ class RsrArtifact:
 
     Device tensors: ``words_d`` (int64 storage of u64 words), ``perm_d``
     (int16 storage of u16), ``go_d``/``po_d`` (int64, cells+1), and the
-    stream layout ``entries_d``/``gsigns_d``/``e_off_d``/``g_off_d``.  The
+    chunk stream ``entries_d``/``e_off_d`` the multiply reads.  The
     reference attribute names (``words``, ``perm``, ``group_offsets``,
     ``perm_offsets``, ``sort_steps``) are host numpy views fetched lazily.
     Cells are tile-major exactly as in the reference (cell = t*bc + b).
@@ -198,42 +197,41 @@ class RsrArtifact:
         pl = np.diff(self.perm_offsets)
         return int(24 + np.sum(8 + 8 * gc + 2 * pl + (-(2 * pl)) % 4))
 
-    def stream_bytes(self) -> int:
-        """Bytes of the device stream layout one multiply reads."""
-        return int(self.entries_d.numel() * self.entries_d.element_size()
-                   + self.gsigns_d.numel() * 4 + self.e_off_d.numel() * 16)
-
-    # ---- device stream layout -------------------------------------------
+    # ---- device chunk stream ---------------------------------------------
     def _build_stream(self):
         import torch
         p = self.plan
-        if p.tile_width > STREAM_MAX_TILE:
-            raise TileTooWide(
-                f"tile_width={p.tile_width}: the GPU multiply addresses tiles of at most "
-                f"{STREAM_MAX_TILE} columns; preprocess with tile_width<={STREAM_MAX_TILE}",
-                n_tile=p.tile_width)
         dev = self.device
         s = _lib.current_stream_ptr(dev)
         cells = self.cells
-        self.entry_bytes = 2
-        e_off = torch.zeros(cells + 1, dtype=torch.int64, device=dev)
-        g_off = torch.zeros(cells + 1, dtype=torch.int64, device=dev)
         L = _lib.lib()
-        _lib.check(L.rsr_stream_count(_lib.ptr(self.go_d), _lib.ptr(self.po_d), p.block_count,
-                                      p.tile_count, self.entry_bytes, _lib.ptr(e_off),
-                                      _lib.ptr(g_off), s), "stream_count")
-        ne, ng = (int(x) for x in torch.stack([e_off[-1], g_off[-1]]).cpu().tolist())
-        entries = torch.empty(max(ne, 8), dtype=torch.int16, device=dev)
-        gsigns = torch.empty(max(ng, 1), dtype=torch.int32, device=dev)
+        bw = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
+        self.entry_bytes = int(L.rsr_stream_entry_bytes(bw, self.k, p.tile_width))
+        self.chunk = 32 // self.entry_bytes
+        e_off = torch.zeros(cells + 1, dtype=torch.int64, device=dev)
+        gslot = torch.empty(max(self.n_words, 1), dtype=torch.int32, device=dev)
+        _lib.check(L.rsr_stream_count(_lib.ptr(self.words_d), _lib.ptr(self.go_d), p.block_count,
+                                      p.tile_count, self.chunk, _lib.ptr(e_off), _lib.ptr(gslot),
+                                      s), "stream_count")
+        ne = int(e_off[-1].item())
+        edt = torch.int16 if self.entry_bytes == 2 else torch.int32
+        entries = torch.empty(max(ne, self.chunk), dtype=edt, device=dev)
         _lib.check(L.rsr_stream_build(_lib.ptr(self.words_d), _lib.ptr(self.go_d),
                                       _lib.ptr(self.perm_d), _lib.ptr(self.po_d), p.block_count,
-                                      p.tile_count, self.entry_bytes, _lib.ptr(e_off),
-                                      _lib.ptr(g_off), _lib.ptr(entries), _lib.ptr(gsigns), s),
+                                      p.tile_count, bw, self.entry_bytes, self.chunk,
+                                      _lib.ptr(e_off), _lib.ptr(gslot), _lib.ptr(entries), s),
                    "stream_build")
-        self.entries_d, self.gsigns_d, self.e_off_d, self.g_off_d = entries, gsigns, e_off, g_off
+        del gslot
+        self.entries_d, self.e_off_d = entries, e_off
         self._view = self.view()
 
-    def view(self, block_begin: int = 0, n_blocks: int | None = None) -> _lib.StreamView:
+    def stream_bytes(self) -> int:
+        """Bytes of the device chunk stream one multiply reads."""
+        return int(self.entries_d.numel() * self.entries_d.element_size()
+                   + self.e_off_d.numel() * 8)
+
+    def view(self, block_begin: int = 0, n_blocks: int | None = None,
+             entries=None, e_off=None) -> _lib.StreamView:
         """C-ABI view over row blocks [block_begin, block_begin + n_blocks)."""
         p = self.plan
         if n_blocks is None:
@@ -243,11 +241,10 @@ class RsrArtifact:
         v.bitwidth = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
         v.tile_width, v.block_count, v.tile_count = p.tile_width, p.block_count, p.tile_count
         v.entry_bytes = self.entry_bytes
-        v.entries = _lib.ptr(self.entries_d)
-        v.gsigns = _lib.ptr(self.gsigns_d)
-        # a block range starts at cell block_begin*tc in the block-major order
-        v.e_off = _lib.ptr(self.e_off_d) + 8 * block_begin * p.tile_count
-        v.g_off = _lib.ptr(self.g_off_d) + 8 * block_begin * p.tile_count
+        v.chunk = self.chunk
+        v.entries = _lib.ptr(self.entries_d if entries is None else entries)
+        # a block range starts at cell block_begin*tc of the block-major order
+        v.e_off = _lib.ptr(self.e_off_d if e_off is None else e_off) + 8 * block_begin * p.tile_count
         v.row_begin_block = block_begin
         v.n_blocks = n_blocks
         return v

@@ -1,0 +1,36 @@
+"""Small driver for ncu: build one artifact, run a few multiplies.
+
+usage: python tools/profile_matvec.py [c2|c1|c4] [k] [float|int|fused] [reps]
+"""
+import sys
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import bench
+import paper_2603_27462_b200 as rsr
+from paper_2603_27462_b200 import kernels as kn
+
+cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
+cfg = dict(bench.CONFIGS[cfgname])
+if len(sys.argv) > 2:
+    cfg["k"] = int(sys.argv[2])
+mode = sys.argv[3] if len(sys.argv) > 3 else "float"
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
+data = bench.random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0)
+a = rsr.preprocess(rsr.PackedMatrix(cfg["m"], cfg["n"], cfg["bitwidth"], data), cfg["k"])
+v = torch.from_numpy(bench.random_vector(cfg["n"], 0)).cuda()
+if cfg["vdtype"] == "bf16":
+    v = v.to(torch.bfloat16)
+y = torch.empty(cfg["m"], dtype=torch.float32, device="cuda")
+if mode == "int":
+    v = torch.randint(-128, 128, (cfg["n"],), dtype=torch.int8, device="cuda")
+    y = torch.empty(cfg["m"], dtype=torch.int32, device="cuda")
+for _ in range(reps):
+    if mode == "fused":
+        kn.fused_into(a, v, y)
+    else:
+        kn.matvec_into(a, v, y)
+torch.cuda.synchronize()
+print("ok", a.stream_bytes(), a.file_bytes())
