@@ -20,12 +20,11 @@
  *
  * The multiply kernels consume a device-only "chunk stream" derived from the
  * reference arrays once per artifact (rsr_stream_build): cells in block-major
- * order, each a run of fixed-size chunks (16 or 32 entries).  An entry is a
- * u16 (u32 for tiles wider than 32768 columns or pattern spaces above 2^15):
- * top bit clear -> a tile-local column to gather; top bit set -> the pattern
- * KEY of the group whose columns follow (binary: pos mask; ternary: base-3
- * digits, 0 = pad).  Every chunk starts with a key entry, so any warp can
- * process any chunk without knowing what came before it.  See DESIGN.md.
+ * order, each a run of 32-byte chunks.  An entry is either a tile-local
+ * column to gather or the pattern KEY of the group whose columns follow
+ * (binary: pos mask; ternary: base-3 digits; key 0 = padding).  Every chunk
+ * starts with a key entry, so any warp can process any chunk without knowing
+ * what came before it, and keys only occupy even slots.  See DESIGN.md.
  */
 #ifndef RSR_B200_H
 #define RSR_B200_H
@@ -65,9 +64,9 @@ typedef struct {
     int64_t m, n;              /* rows, cols */
     int32_t k, bitwidth;       /* block height, rsr_bitwidth */
     int64_t tile_width, block_count, tile_count;
-    int32_t entry_bytes;       /* 2 (u16 entries) or 4 (u32 entries) */
-    int32_t chunk;             /* entries per chunk: 16 or 32 */
-    const void *entries;       /* device, entry_bytes each */
+    int32_t format;            /* rsr_stream_format(): 0 u16, 1 u16 scaled, 2 u32 */
+    int32_t chunk;             /* entries per 32-byte chunk: 16 (u16) or 8 (u32) */
+    const void *entries;       /* device chunk stream */
     const int64_t *e_off;      /* device, cells+1 entry offsets, block-major cell order */
     int64_t row_begin_block;   /* first block this view covers (row-block sharding) */
     int64_t n_blocks;          /* blocks covered (== block_count unless sharded) */
@@ -105,15 +104,21 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
  * rsr_stream_count: per-cell entry counts exclusive-scanned into e_off
  * (cells+1, block-major) and each group's first slot inside its cell into
  * gslot (int32, one per reference word).  The caller reads e_off[cells] to
- * size the entries, then rsr_stream_build writes them.  entry_bytes 0 asks
- * the library to choose (rsr_stream_entry_bytes).                           */
-int32_t rsr_stream_entry_bytes(int32_t bitwidth, int32_t k, int64_t tile_width);
+ * size the entries, then rsr_stream_build writes them.
+ * Formats (rsr_stream_format picks one per plan):
+ *   0  u16, flag bit 15: column, or KEY|0x8000          (tiles <= 32768)
+ *   1  u16, "scaled": column*4, or KEY*4|1 -- byte offsets straight into
+ *      4-byte shared-memory elements           (tiles <= 16384, keys <= 16384)
+ *   2  u32, flag bit 31                          (anything wider / larger)
+ * 32-byte chunks (16 u16 / 8 u32 entries); within a cell each group of 32
+ * chunks is stored as [their first 16-byte halves][their second halves].     */
+int32_t rsr_stream_format(int32_t bitwidth, int32_t k, int64_t tile_width);
 rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, int64_t block_count,
                             int64_t tile_count, int32_t chunk, int64_t *e_off, int32_t *gslot,
                             rsr_stream_t stream);
 rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,
-                            int32_t bitwidth, int32_t entry_bytes, int32_t chunk,
+                            int32_t bitwidth, int32_t format, int32_t chunk,
                             const int64_t *e_off, const int32_t *gslot, void *entries,
                             rsr_stream_t stream);
 

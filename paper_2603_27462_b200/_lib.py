@@ -43,7 +43,7 @@ class StreamView(ctypes.Structure):
         ("m", I64), ("n", I64),
         ("k", I32), ("bitwidth", I32),
         ("tile_width", I64), ("block_count", I64), ("tile_count", I64),
-        ("entry_bytes", I32), ("chunk", I32),
+        ("format", I32), ("chunk", I32),
         ("entries", P), ("e_off", P),
         ("row_begin_block", I64), ("n_blocks", I64),
     ]
@@ -58,7 +58,7 @@ SIGNATURES = {
     "rsr_group_workspace_bytes": (SZ, [I64, I64, I32, I32, I64]),
     "rsr_group_count": (I32, [P, I64, I64, I64, I32, I32, I64, P, P, P, P, P, SZ, P]),
     "rsr_group_fill": (I32, [P, I64, I64, I64, I32, I32, I64, P, P, P, P, P, SZ, P]),
-    "rsr_stream_entry_bytes": (I32, [I32, I32, I64]),
+    "rsr_stream_format": (I32, [I32, I32, I64]),
     "rsr_stream_count": (I32, [P, P, I64, I64, I32, P, P, P]),
     "rsr_stream_build": (I32, [P, P, P, P, I64, I64, I32, I32, I32, P, P, P, P]),
     "rsr_matvec_workspace_bytes": (SZ, [ctypes.POINTER(StreamView)]),

@@ -1,0 +1,424 @@
+// rsr_mv_impl.cuh -- the sm_100a RSR multiply kernel (templates).
+//
+// Replaces the reference's matvec cores (pkg/src/rsrmv/_native.py:167-285)
+// and its fused quantize/multiply/dequantize path (_native.py:313-353).
+//
+// Input: the chunk stream (include/rsr_b200.h): per cell, 32-byte chunks of
+// entries; an entry is a column to gather or the pattern key of the group
+// whose columns follow; every chunk starts with a key and keys only sit at
+// even slots (place_group in rsr_preprocess.cu).
+//
+// Work decomposition:
+//   * grid.y = column tile.  Each CTA stages its tile of v in shared memory
+//     once (the fused path quantizes while staging, after a CTA-local absmax
+//     over the whole vector -- no separate quantization launch);
+//   * one warp owns one (block, tile) cell at a time; in each round lane L
+//     owns chunk L (two coalesced 16-byte loads per lane, the next round
+//     prefetched), gathers v from shared memory per column slot and keeps a
+//     running partial group sum;
+//   * at a key slot the partial sum is flushed into the warp's PATTERN BUCKET
+//     for that key (3^k ternary / 2^k binary buckets in shared memory) --
+//     branch-free, predicated;
+//   * when the cell is done, the pattern-table reduction y_i = sum_key
+//     sgn_i(key) * bucket[key] (sign table in shared memory) produces the k
+//     rows, warp-reduced and written once.
+// For pattern spaces too large for shared-memory buckets the register
+// variant flushes straight into k row accumulators instead.
+// Integer accumulation is exact, so the int8 and fused paths are
+// bit-identical to the reference.  The float path accumulates in fp32.
+#pragma once
+
+#include "rsr_common.cuh"
+
+namespace rsr {
+
+enum MvMode { MODE_FLOAT = 0, MODE_INT = 1, MODE_FUSED = 2 };
+
+// chunk-stream entry formats (rsr_stream_view.format)
+enum StreamFormat {
+    FMT_U16 = 0,         // u16: column | key<<..., flag bit 15, tiles <= 32768
+    FMT_U16_SCALED = 1,  // u16: column*4, or key*4|1; tiles <= 16384, <= 16384 keys
+    FMT_U32 = 2          // u32: column, or key | 1<<31
+};
+
+constexpr int MV_MAX_WARPS = 32;
+constexpr int64_t BUCKET_MAX_KEYS = 2187;  // 3^7: buckets live in smem up to here
+
+struct MvParams {
+    const void *entries;
+    const int64_t *e_off;
+    int64_t m_rows;      // rows of the full matrix
+    int64_t n;           // columns
+    int64_t tw, tc;      // tile width / count
+    int64_t blk0;        // first global block of this view
+    int64_t nblk;        // blocks in this view
+    int k;
+    int bitwidth;
+    int nkeys;           // pattern buckets: 3^k or 2^k
+    const void *v;
+    int vdtype;
+    const void *vstaged; // FMT_U32: v converted/quantized in global memory
+    void *y;             // output slice (view rows)
+    int accumulate;
+    void *part;          // tc > 1: [tc][nblk*k] partials (float or int32)
+    double beta;         // fused
+    double *scale_dev;   // fused: device scale slot (may be null when tc == 1)
+};
+
+__device__ __forceinline__ float load_as_f32(const void *v, int dtype, int64_t i) {
+    switch (dtype) {
+        case RSR_F32: return __ldg((const float *)v + i);
+        case RSR_BF16: return bf16_bits_to_f32(__ldg((const uint16_t *)v + i));
+        case RSR_F16: return __half2float(__ldg((const __half *)v + i));
+        default: return 0.f;
+    }
+}
+
+// Reference absmax quantization of one element (_native.py:326-335).
+__device__ __forceinline__ int8_t quantize_one(float x, double scale) {
+    const double xs = (double)x * scale;
+    double r = xs >= 0.0 ? floor(xs + 0.5) : -floor(-xs + 0.5);
+    r = r > 127.0 ? 127.0 : (r < -127.0 ? -127.0 : r);
+    return (int8_t)(int)r;
+}
+
+// CTA-wide max of |v| over the whole vector in float64 (order-independent,
+// hence exact and identical in every CTA).
+__device__ __forceinline__ double cta_absmax(const void *v, int dtype, int64_t n) {
+    __shared__ double red[32];
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = fabs((double)load_as_f32(v, dtype, i));
+        a = x > a ? x : a;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+        a = o > a ? o : a;
+    }
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red[warp] = a;
+    __syncthreads();
+    if (warp == 0) {
+        a = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+            a = o > a ? o : a;
+        }
+        if (threadIdx.x == 0) red[0] = a;
+    }
+    __syncthreads();
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// Sign of row i in the pattern with dense key `key`.
+__device__ __forceinline__ int key_sign(uint32_t key, int i, int bitwidth) {
+    if (bitwidth == RSR_BINARY) return (int)((key >> i) & 1u);
+    for (int j = 0; j < i; ++j) key /= 3u;
+    const uint32_t d = key % 3u;
+    return d == 1u ? 1 : (d == 2u ? -1 : 0);
+}
+
+template <int K>
+struct KPad {
+    static constexpr int value = (K + 3) & ~3;
+};
+
+// ---- shared-memory primitives on 32-bit shared addresses -----------------
+// Gathers are plain (non-volatile) asm: v is read-only while they run, so the
+// compiler may schedule them freely.  Bucket updates are volatile asm and keep
+// their program order with respect to each other.
+template <typename Acc, int VSZ>
+__device__ __forceinline__ Acc lds_v(uint32_t addr) {
+    if constexpr (VSZ == 4) {
+        if constexpr (std::is_same<Acc, float>::value) {
+            float r;
+            asm("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(addr));
+            return r;
+        } else {
+            int r;
+            asm("ld.shared.s32 %0, [%1];" : "=r"(r) : "r"(addr));
+            return r;
+        }
+    } else {
+        int r;
+        asm("ld.shared.s8 %0, [%1];" : "=r"(r) : "r"(addr));
+        return (Acc)r;
+    }
+}
+
+// v[addr] unless `skip` (then 0): the load is predicated off for key slots.
+template <typename Acc, int VSZ>
+__device__ __forceinline__ Acc lds_v_unless(uint32_t skip, uint32_t addr) {
+    if constexpr (VSZ == 4 && std::is_same<Acc, float>::value) {
+        float r;
+        asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\tmov.f32 %0, 0f00000000;\n\t"
+            "@p ld.shared.f32 %0, [%2];\n\t}"
+            : "=f"(r) : "r"(skip), "r"(addr));
+        return r;
+    } else if constexpr (VSZ == 4) {
+        int r;
+        asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\tmov.u32 %0, 0;\n\t"
+            "@p ld.shared.s32 %0, [%2];\n\t}"
+            : "=r"(r) : "r"(skip), "r"(addr));
+        return r;
+    } else {
+        int r;
+        asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\tmov.u32 %0, 0;\n\t"
+            "@p ld.shared.s8 %0, [%2];\n\t}"
+            : "=r"(r) : "r"(skip), "r"(addr));
+        return (Acc)r;
+    }
+}
+
+// if (pred) bucket += s.  In-loop flushes of one warp instruction never share
+// a key (a group's in-chunk segment ends at exactly one slot), so the float
+// path can use a plain read-modify-write.
+__device__ __forceinline__ void bucket_flush_pred(uint32_t pred, uint32_t addr, float s) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .f32 t;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+        "@p ld.shared.f32 t, [%1];\n\t@p add.f32 t, t, %2;\n\t@p st.shared.f32 [%1], t;\n\t}" ::"r"(pred),
+        "r"(addr), "f"(s));
+}
+__device__ __forceinline__ void bucket_flush_pred(uint32_t pred, uint32_t addr, int32_t s) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p red.shared.add.s32 [%1], %2;\n\t}" ::"r"(pred),
+        "r"(addr), "r"(s));
+}
+// A chunk's last segment may continue in the next lane's chunk: atomic.
+__device__ __forceinline__ void bucket_flush_final(uint32_t addr, float s) {
+    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(addr), "f"(s));
+}
+__device__ __forceinline__ void bucket_flush_final(uint32_t addr, int32_t s) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(s));
+}
+
+template <int K, typename Acc>
+__device__ __forceinline__ void reg_flush(Acc (&acc)[K], uint32_t key, Acc s, int bitwidth) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc[i] += (Acc)key_sign(key, i, bitwidth) * s;
+}
+
+template <int MODE, int FMT>
+struct MvTypes {
+    using Acc = typename std::conditional<MODE == MODE_FLOAT, float, int32_t>::type;
+    // staged element of v: 4 bytes for the scaled format (column*4 addressing),
+    // else f32 (float) / int8 (integer paths)
+    static constexpr int VSZ = (FMT == FMT_U16_SCALED || MODE == MODE_FLOAT) ? 4 : 1;
+    static constexpr bool SMEM_V = FMT != FMT_U32;
+};
+
+template <int K, int MODE, int FMT, bool BUCKET>
+__global__ void __launch_bounds__(MV_MAX_WARPS * 32)
+rsr_mv_kernel(MvParams p) {
+    using T = MvTypes<MODE, FMT>;
+    using Acc = typename T::Acc;
+    constexpr int VSZ = T::VSZ;
+    constexpr bool SMEM_V = T::SMEM_V;
+    constexpr int CH = FMT == FMT_U32 ? 8 : 16;  // entries per 32-byte chunk
+    constexpr int KP = KPad<K>::value;
+
+    extern __shared__ __align__(16) unsigned char mv_smem[];
+    const int nwarps = blockDim.x >> 5;
+    const int64_t t = blockIdx.y;
+    const int64_t c0 = t * p.tw;
+    const int64_t tn = min(p.tw, p.n - c0);
+
+    // smem carve-up: [v tile][sign table NB x KP][buckets nwarps x NB]
+    size_t off = 0;
+    unsigned char *vsm = mv_smem;
+    if constexpr (SMEM_V) off += ((size_t)tn * VSZ + 15) & ~(size_t)15;
+    Acc *__restrict__ stab = reinterpret_cast<Acc *>(mv_smem + off);
+    if constexpr (BUCKET) off += (size_t)p.nkeys * KP * sizeof(Acc);
+    Acc *__restrict__ buckets = reinterpret_cast<Acc *>(mv_smem + off);
+
+    // ---- prologue -------------------------------------------------------
+    double scale = 1.0;
+    if constexpr (MODE == MODE_FUSED) {
+        if constexpr (SMEM_V) {
+            const double amax = cta_absmax(p.v, p.vdtype, p.n);
+            scale = amax == 0.0 ? 1.0 : 127.0 / amax;
+            if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+                *p.scale_dev = scale;
+        } else {
+            scale = *p.scale_dev;  // written by the staging kernel
+        }
+    }
+    if constexpr (SMEM_V) {
+        for (int64_t i = threadIdx.x; i < tn; i += blockDim.x) {
+            if constexpr (MODE == MODE_FLOAT) {
+                reinterpret_cast<float *>(vsm)[i] = load_as_f32(p.v, p.vdtype, c0 + i);
+            } else {
+                const int8_t q = MODE == MODE_INT ? __ldg((const int8_t *)p.v + c0 + i)
+                                                  : quantize_one(load_as_f32(p.v, p.vdtype, c0 + i), scale);
+                if constexpr (VSZ == 4) reinterpret_cast<int32_t *>(vsm)[i] = q;
+                else reinterpret_cast<int8_t *>(vsm)[i] = q;
+            }
+        }
+    }
+    if constexpr (BUCKET) {
+        for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
+#pragma unroll
+            for (int i = 0; i < KP; ++i)
+                stab[key * KP + i] = (Acc)(i < K ? key_sign((uint32_t)key, i, p.bitwidth) : 0);
+        }
+        for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
+    }
+    __syncthreads();
+
+    using VG = typename std::conditional<MODE == MODE_FLOAT, float, int8_t>::type;
+    const VG *__restrict__ vglob = reinterpret_cast<const VG *>(p.vstaged) + c0;
+    const uint32_t lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    Acc *__restrict__ bk = buckets + (size_t)warp * p.nkeys;
+    const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
+    const uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
+    const uint4 *__restrict__ ent4 = reinterpret_cast<const uint4 *>(p.entries);
+
+    for (int64_t b = (int64_t)blockIdx.x * nwarps + warp; b < p.nblk;
+         b += (int64_t)gridDim.x * nwarps) {
+        const int64_t dc = b * p.tc + t;
+        const int64_t ch0 = p.e_off[dc] / CH, ch1 = p.e_off[dc + 1] / CH;  // chunk range
+        Acc acc[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
+
+        // round = 32 chunks stored as [first 16B halves][second 16B halves]
+        int64_t nr = min((int64_t)32, ch1 - ch0);
+        uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+        if ((int64_t)lane < nr) {
+            q0 = __ldg(ent4 + 2 * ch0 + lane);
+            q1 = __ldg(ent4 + 2 * ch0 + nr + lane);
+        }
+        for (int64_t base = ch0; base < ch1; base += 32) {
+            const bool valid = (int64_t)lane < nr;
+            const uint4 a0 = q0, a1 = q1;
+            const int64_t nbase = base + 32;
+            const int64_t nnr = min((int64_t)32, ch1 - nbase);
+            if ((int64_t)lane < nnr) {  // prefetch the next round
+                q0 = __ldg(ent4 + 2 * nbase + lane);
+                q1 = __ldg(ent4 + 2 * nbase + nnr + lane);
+            }
+            if (valid) {
+                const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                if constexpr (FMT == FMT_U16_SCALED && BUCKET) {
+                    // slot 2i = low half of w[i]: column*4, or key*4|1;
+                    // slot 2i+1 = high half: always column*4.  Byte offsets
+                    // straight into v (4-byte elements) and the buckets.
+                    uint32_t cur = w[0] & 0xFFFCu;
+                    Acc s = lds_v<Acc, 4>(vbase + (w[0] >> 16));
+#pragma unroll
+                    for (int i = 1; i < 8; ++i) {
+                        const uint32_t lo = w[i] & 0xFFFCu;
+                        const uint32_t isk = w[i] & 1u;
+                        const Acc g = lds_v_unless<Acc, 4>(isk, vbase + lo);
+                        const Acc h = lds_v<Acc, 4>(vbase + (w[i] >> 16));
+                        bucket_flush_pred(isk, bkbase + cur, s);
+                        cur = isk ? lo : cur;
+                        s = (isk ? (Acc)0 : s) + g + h;
+                    }
+                    bucket_flush_final(bkbase + cur, s);
+                } else if constexpr (FMT == FMT_U16) {
+                    uint32_t cur = w[0] & 0x7FFFu;
+                    Acc s = lds_v<Acc, VSZ>(vbase + (w[0] >> 16) * VSZ);
+#pragma unroll
+                    for (int i = 1; i < 8; ++i) {
+                        const uint32_t lo = w[i] & 0xFFFFu;
+                        const uint32_t isk = lo & 0x8000u;
+                        const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (lo & 0x7FFFu) * VSZ);
+                        const Acc h = lds_v<Acc, VSZ>(vbase + (w[i] >> 16) * VSZ);
+                        if constexpr (BUCKET) {
+                            bucket_flush_pred(isk, bkbase + cur * 4u, s);
+                        } else if (isk) {
+                            reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                        }
+                        cur = isk ? (lo & 0x7FFFu) : cur;
+                        s = (isk ? (Acc)0 : s) + g + h;
+                    }
+                    if constexpr (BUCKET) bucket_flush_final(bkbase + cur * 4u, s);
+                    else reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                } else {  // FMT_U32, register flush, v gathered from global scratch
+                    constexpr uint32_t KF = 1u << 31;
+                    uint32_t cur = w[0] & ~KF;
+                    Acc s = (Acc)__ldg(vglob + w[1]);
+#pragma unroll
+                    for (int i = 2; i < 8; i += 2) {
+                        const Acc h = (Acc)__ldg(vglob + w[i + 1]);
+                        if (w[i] & KF) {
+                            reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                            cur = w[i] & ~KF;
+                            s = (Acc)0;
+                        } else {
+                            s += (Acc)__ldg(vglob + w[i]);
+                        }
+                        s += h;
+                    }
+                    reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                }
+            }
+            __syncwarp();
+            nr = nnr;
+        }
+        asm volatile("" ::: "memory");
+
+        // ---- pattern-table reduction: y_i = sum_key sgn_i(key) * bucket[key] ----
+        // (bucket 0 collects padding and is never reduced)
+        if constexpr (BUCKET) {
+            for (int key = lane; key < p.nkeys; key += 32) {
+                const Acc bv = key ? bk[key] : (Acc)0;
+                bk[key] = (Acc)0;
+                const Acc *row = stab + key * KP;
+#pragma unroll
+                for (int i = 0; i < K; ++i) acc[i] += row[i] * bv;
+            }
+            __syncwarp();
+        }
+        const int64_t row0 = b * p.k;  // row within the view
+        const int64_t grow0 = (p.blk0 + b) * p.k;
+        Acc mine = (Acc)0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const Acc r = warp_sum(acc[i]);
+            if (lane == (uint32_t)i) mine = r;
+        }
+        if (lane < (uint32_t)K && grow0 + lane < p.m_rows) {
+            const int64_t r = row0 + lane;
+            if (p.tc > 1) {
+                const int64_t rows_view = p.nblk * p.k;
+                reinterpret_cast<Acc *>(p.part)[t * rows_view + r] = mine;
+            } else if constexpr (MODE == MODE_FLOAT) {
+                float *y = reinterpret_cast<float *>(p.y);
+                y[r] = p.accumulate ? y[r] + (float)mine : (float)mine;
+            } else if constexpr (MODE == MODE_INT) {
+                int32_t *y = reinterpret_cast<int32_t *>(p.y);
+                y[r] = p.accumulate ? y[r] + (int32_t)mine : (int32_t)mine;
+            } else {
+                reinterpret_cast<float *>(p.y)[r] =
+                    (float)((double)(int32_t)mine * (p.beta / scale));
+            }
+        }
+    }
+}
+
+using KernelFn = void (*)(MvParams);
+
+// Kernel lookup, defined per format in rsr_mv_fmt*.cu (parallel compilation).
+KernelFn pick_fmt1(int mode, int k);             // FMT_U16_SCALED, buckets
+KernelFn pick_fmt0(int mode, int k, bool bucket);  // FMT_U16
+KernelFn pick_fmt2(int mode, int k);             // FMT_U32, register flush
+
+#define RSR_K_SWITCH(EXPR)                                                                   \
+    switch (k) {                                                                             \
+        case 1: return EXPR(1); case 2: return EXPR(2); case 3: return EXPR(3);              \
+        case 4: return EXPR(4); case 5: return EXPR(5); case 6: return EXPR(6);              \
+        case 7: return EXPR(7); case 8: return EXPR(8); case 9: return EXPR(9);              \
+        case 10: return EXPR(10); case 11: return EXPR(11); case 12: return EXPR(12);        \
+        case 13: return EXPR(13); case 14: return EXPR(14); case 15: return EXPR(15);        \
+        case 16: return EXPR(16);                                                            \
+        default: return nullptr;                                                             \
+    }
+
+}  // namespace rsr

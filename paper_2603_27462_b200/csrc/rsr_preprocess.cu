@@ -250,21 +250,48 @@ scan2_kernel(int64_t *a, int64_t *b, int64_t cells) {
 // chunk stream: block-major cells; each cell is a run of CH-entry chunks and
 // every chunk starts with a key entry (see include/rsr_b200.h).
 
-// Slot placement of one group of L columns whose key would go at slot p (the
-// next free slot of its cell).  Returns the key slot; p becomes the next free
-// slot.  A key never takes the last slot of a chunk (it would own nothing),
-// and a group crossing a chunk boundary repeats its key at the new chunk.
-__host__ __device__ __forceinline__ int64_t place_group(int64_t &p, int64_t L, int64_t CH) {
-    if (p % CH == CH - 1) ++p;
-    const int64_t key_slot = p++;
-    int64_t rem = L;
-    while (rem > 0) {
-        if (p % CH == 0) ++p;
-        const int64_t take = min(rem, CH - p % CH);
-        p += take;
-        rem -= take;
+// Slot placement of one group of L columns (the reference word's perm_len)
+// starting at slot p (always even).  Keys only ever sit at EVEN slots: every
+// segment that ends inside a chunk has odd length (an even remainder is split
+// 1 + (R-1) with one repeated key), and a segment running to the chunk end
+// has odd length automatically.  A group crossing a chunk boundary repeats its
+// key at slot 0 of the next chunk.  emit_key(slot) / emit_col(slot, j).
+template <typename KeyFn, typename ColFn>
+__host__ __device__ __forceinline__ void place_group(int64_t &p, int64_t L, int64_t CH,
+                                                    KeyFn emit_key, ColFn emit_col) {
+    emit_key(p++);
+    int64_t R = L, j = 0;
+    while (true) {
+        const int64_t room = CH - p % CH;  // odd
+        if (R >= room) {
+            for (int64_t i = 0; i < room; ++i) emit_col(p++, j++);
+            R -= room;
+            if (R == 0) break;
+            emit_key(p++);
+            continue;
+        }
+        if (R & 1) {
+            for (int64_t i = 0; i < R; ++i) emit_col(p++, j++);
+            break;
+        }
+        for (int64_t i = 0; i < R - 1; ++i) emit_col(p++, j++);
+        emit_key(p++);
+        emit_col(p++, j++);
+        break;
     }
-    return key_slot;
+}
+
+// Physical index of logical slot p inside a cell of nch chunks: chunks are
+// taken 32 at a time (one warp round) and stored as [first halves][second
+// halves] so each of the round's two 16-byte loads is one coalesced 512-byte
+// access.
+__host__ __device__ __forceinline__ int64_t phys_slot(int64_t p, int64_t CH, int64_t nch) {
+    const int64_t c = p / CH, js = p - c * CH;
+    const int64_t r = c >> 5, lanec = c & 31;
+    const int64_t nr = min((int64_t)32, nch - (r << 5));
+    const int64_t half = CH >> 1;
+    const int64_t h = js / half, within = js - h * half;
+    return r * 32 * CH + h * nr * half + lanec * half + within;
 }
 
 // Dense pattern key of a group from its masks: binary -> pos mask; ternary
@@ -292,19 +319,24 @@ __global__ void stream_count_kernel(const uint64_t *__restrict__ words,
         int64_t p = 0;
         for (int64_t g = go[src]; g < go[src + 1]; ++g) {
             const int64_t L = (int64_t)((words[g] >> 16) & 0xFFFFu);
-            gslot[g] = (int32_t)place_group(p, L, CH);
+            gslot[g] = (int32_t)p;
+            place_group(p, L, CH, [](int64_t) {}, [](int64_t, int64_t) {});
         }
         e_off[dc + 1] = (p + CH - 1) / CH * CH;
     }
 }
 
-template <typename E>
+template <typename E, bool SCALED>
 __global__ void __launch_bounds__(256)
 stream_build_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                     const uint16_t *__restrict__ perm, const int64_t *__restrict__ po, int64_t bc,
                     int64_t tc, int bitwidth, int64_t CH, const int64_t *__restrict__ e_off,
                     const int32_t *__restrict__ gslot, E *__restrict__ entries) {
+    // scaled: column*4 / key*4|1 (byte offsets into 4-byte smem elements);
+    // otherwise column / key with the top bit as the key flag
     constexpr E KEYFLAG = (E)1 << (8 * sizeof(E) - 1);
+    auto enc_key = [](uint32_t k) -> E { return SCALED ? (E)((k << 2) | 1u) : (E)(KEYFLAG | k); };
+    auto enc_col = [](uint32_t c) -> E { return SCALED ? (E)(c << 2) : (E)c; };
     const uint32_t lane = lane_id();
     const int64_t cells = bc * tc;
     for (int64_t dc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; dc < cells;
@@ -312,21 +344,22 @@ stream_build_kernel(const uint64_t *__restrict__ words, const int64_t *__restric
         const int64_t b = dc / tc, t = dc - b * tc;
         const int64_t src = t * bc + b;
         const int64_t e0 = e_off[dc], elen = e_off[dc + 1] - e0;
+        const int64_t nch = elen / CH;
         E *out = entries + e0;
-        for (int64_t i = lane; i < elen; i += 32) out[i] = KEYFLAG;  // key 0 = pad
+        // padding: key 0 at even slots, column 0 at odd slots (both land in the
+        // never-reduced bucket 0)
+        for (int64_t i = lane; i < elen; i += 32) out[phys_slot(i, CH, nch)] = (i & 1) ? enc_col(0) : enc_key(0);
         __syncwarp();
         const int64_t p0 = po[src];
         for (int64_t g = go[src] + lane; g < go[src + 1]; g += 32) {
             const uint64_t w = words[g];
             const int64_t ps = (int64_t)(w & 0xFFFFu), L = (int64_t)((w >> 16) & 0xFFFFu);
-            const E key = KEYFLAG | (E)dense_key(w, bitwidth);
-            int64_t p = gslot[g];
-            out[p++] = key;
+            const E key = enc_key(dense_key(w, bitwidth));
             const uint16_t *cols = perm + p0 + ps;
-            for (int64_t j = 0; j < L; ++j) {
-                if (p % CH == 0) out[p++] = key;
-                out[p++] = (E)cols[j];
-            }
+            int64_t p = gslot[g];
+            place_group(
+                p, L, CH, [&](int64_t q) { out[phys_slot(q, CH, nch)] = key; },
+                [&](int64_t q, int64_t j) { out[phys_slot(q, CH, nch)] = enc_col(cols[j]); });
         }
     }
 }
@@ -455,9 +488,11 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
     return launch_status();
 }
 
-int32_t rsr_stream_entry_bytes(int32_t bitwidth, int32_t k, int64_t tile_width) {
+int32_t rsr_stream_format(int32_t bitwidth, int32_t k, int64_t tile_width) {
     const int64_t keys = bucket_count(bitwidth, k);
-    return (tile_width <= 32768 && keys <= 32768) ? 2 : 4;
+    if (tile_width <= 16384 && keys <= 16384) return 1;  // scaled u16
+    if (tile_width <= 32768 && keys <= 32768) return 0;  // u16
+    return 2;                                            // u32
 }
 
 rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, int64_t block_count,
@@ -476,7 +511,7 @@ rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, int64_t bl
 
 rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,
-                            int32_t bitwidth, int32_t entry_bytes, int32_t chunk,
+                            int32_t bitwidth, int32_t format, int32_t chunk,
                             const int64_t *e_off, const int32_t *gslot, void *entries,
                             rsr_stream_t stream) {
     if (!go || !po || !e_off || !entries || block_count < 1 || tile_count < 1)
@@ -485,12 +520,16 @@ rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 32);
-    if (entry_bytes == 2)
-        stream_build_kernel<uint16_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
+    if (format == 1)
+        stream_build_kernel<uint16_t, true><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
+                                                                 tile_count, bitwidth, chunk, e_off,
+                                                                 gslot, (uint16_t *)entries);
+    else if (format == 0)
+        stream_build_kernel<uint16_t, false><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
                                                            tile_count, bitwidth, chunk, e_off,
                                                            gslot, (uint16_t *)entries);
-    else if (entry_bytes == 4)
-        stream_build_kernel<uint32_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
+    else if (format == 2)
+        stream_build_kernel<uint32_t, false><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
                                                            tile_count, bitwidth, chunk, e_off,
                                                            gslot, (uint32_t *)entries);
     else

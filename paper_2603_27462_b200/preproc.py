@@ -206,7 +206,8 @@ class RsrArtifact:
         cells = self.cells
         L = _lib.lib()
         bw = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
-        self.entry_bytes = int(L.rsr_stream_entry_bytes(bw, self.k, p.tile_width))
+        self.format = int(L.rsr_stream_format(bw, self.k, p.tile_width))
+        self.entry_bytes = 4 if self.format == 2 else 2
         self.chunk = 32 // self.entry_bytes
         e_off = torch.zeros(cells + 1, dtype=torch.int64, device=dev)
         gslot = torch.empty(max(self.n_words, 1), dtype=torch.int32, device=dev)
@@ -218,7 +219,7 @@ class RsrArtifact:
         entries = torch.empty(max(ne, self.chunk), dtype=edt, device=dev)
         _lib.check(L.rsr_stream_build(_lib.ptr(self.words_d), _lib.ptr(self.go_d),
                                       _lib.ptr(self.perm_d), _lib.ptr(self.po_d), p.block_count,
-                                      p.tile_count, bw, self.entry_bytes, self.chunk,
+                                      p.tile_count, bw, self.format, self.chunk,
                                       _lib.ptr(e_off), _lib.ptr(gslot), _lib.ptr(entries), s),
                    "stream_build")
         del gslot
@@ -240,7 +241,7 @@ class RsrArtifact:
         v.m, v.n, v.k = self.m, self.n, self.k
         v.bitwidth = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
         v.tile_width, v.block_count, v.tile_count = p.tile_width, p.block_count, p.tile_count
-        v.entry_bytes = self.entry_bytes
+        v.format = self.format
         v.chunk = self.chunk
         v.entries = _lib.ptr(self.entries_d if entries is None else entries)
         # a block range starts at cell block_begin*tc of the block-major order
