@@ -188,6 +188,15 @@ __device__ __forceinline__ void bucket_flush_pred(uint32_t pred, uint32_t addr, 
         "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p red.shared.add.s32 [%1], %2;\n\t}" ::"r"(pred),
         "r"(addr), "r"(s));
 }
+// Batched float flush halves (volatile: ordered against every other bucket op).
+__device__ __forceinline__ float lds_bucket(uint32_t addr) {
+    float r;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(addr));
+    return r;
+}
+__device__ __forceinline__ void sts_bucket(uint32_t addr, float x) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(x));
+}
 // A chunk's last segment may continue in the next lane's chunk: atomic.
 __device__ __forceinline__ void bucket_flush_final(uint32_t addr, float s) {
     asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(addr), "f"(s));
@@ -304,21 +313,55 @@ rsr_mv_kernel(MvParams p) {
             }
             if (valid) {
                 const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                if constexpr (FMT == FMT_U16_SCALED && BUCKET) {
-                    // slot 2i = low half of w[i]: column*4, or key*4|1;
-                    // slot 2i+1 = high half: always column*4.  Byte offsets
-                    // straight into v (4-byte elements) and the buckets.
-                    uint32_t cur = w[0] & 0xFFFCu;
-                    Acc s = lds_v<Acc, 4>(vbase + (w[0] >> 16));
+                if constexpr (FMT != FMT_U32 && BUCKET) {
+                    // slot 2i = low half of w[i] (column or key), slot 2i+1 =
+                    // high half (always a column).  Scaled format: entries are
+                    // byte offsets (column*4; key*4|1) straight into v and the
+                    // buckets.
+                    constexpr bool SC = FMT == FMT_U16_SCALED;
+                    auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
+                    auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
+                    auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
+                    auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
+                    uint32_t cur = key_off(w[0]);
+                    Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
+                    if constexpr (MODE == MODE_FLOAT) {
+                        // Completed segments are recorded in registers and
+                        // flushed as one batch (all bucket loads, then all
+                        // adds/stores) so the read-modify-write latency is paid
+                        // once per chunk.  A repeated key equal to the current
+                        // one continues the segment.  Bucket 0 absorbs no-ops.
+                        uint32_t fk[7];
+                        float fs[7];
 #pragma unroll
-                    for (int i = 1; i < 8; ++i) {
-                        const uint32_t lo = w[i] & 0xFFFCu;
-                        const uint32_t isk = w[i] & 1u;
-                        const Acc g = lds_v_unless<Acc, 4>(isk, vbase + lo);
-                        const Acc h = lds_v<Acc, 4>(vbase + (w[i] >> 16));
-                        bucket_flush_pred(isk, bkbase + cur, s);
-                        cur = isk ? lo : cur;
-                        s = (isk ? (Acc)0 : s) + g + h;
+                        for (int i = 1; i < 8; ++i) {
+                            const uint32_t x = w[i];
+                            const uint32_t isk = is_key(x);
+                            const uint32_t ko = key_off(x);
+                            const bool newseg = isk && ko != cur;
+                            const float g = lds_v_unless<float, VSZ>(isk, vbase + lo_off(x));
+                            const float h = lds_v<float, VSZ>(vbase + hi_off(x));
+                            fk[i - 1] = newseg ? cur : 0u;
+                            fs[i - 1] = s;
+                            cur = newseg ? ko : cur;
+                            s = (newseg ? 0.f : s) + g + h;
+                        }
+                        float tb[7];
+#pragma unroll
+                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
+#pragma unroll
+                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                    } else {
+#pragma unroll
+                        for (int i = 1; i < 8; ++i) {
+                            const uint32_t x = w[i];
+                            const uint32_t isk = is_key(x);
+                            const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
+                            const Acc h = lds_v<Acc, VSZ>(vbase + hi_off(x));
+                            bucket_flush_pred(isk, bkbase + cur, s);
+                            cur = isk ? key_off(x) : cur;
+                            s = (isk ? (Acc)0 : s) + g + h;
+                        }
                     }
                     bucket_flush_final(bkbase + cur, s);
                 } else if constexpr (FMT == FMT_U16) {

@@ -490,7 +490,7 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
 
 int32_t rsr_stream_format(int32_t bitwidth, int32_t k, int64_t tile_width) {
     const int64_t keys = bucket_count(bitwidth, k);
-    if (tile_width <= 16384 && keys <= 16384) return 1;  // scaled u16
+    if (tile_width <= 16384 && keys <= 2187) return 1;   // scaled u16 (bucket kernel)
     if (tile_width <= 32768 && keys <= 32768) return 0;  // u16
     return 2;                                            // u32
 }
