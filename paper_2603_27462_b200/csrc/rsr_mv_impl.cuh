@@ -41,7 +41,7 @@ enum StreamFormat {
     FMT_U32 = 2          // u32: column, or key | 1<<31
 };
 
-constexpr int MV_MAX_WARPS = 32;
+constexpr int MV_MAX_WARPS = 24;  // 768 threads: up to 85 registers per thread
 constexpr int64_t BUCKET_MAX_KEYS = 2187;  // 3^7: buckets live in smem up to here
 
 struct MvParams {
@@ -295,6 +295,94 @@ rsr_mv_kernel(MvParams p) {
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
 
+        if constexpr (FMT != FMT_U32 && BUCKET) {
+            // Bucket path.  A round is NCH groups of 32 chunks; lane L owns
+            // chunk L of each group (independent dependency chains for ILP).
+            // Each group of 32 chunks is stored as [first 16B halves][second
+            // 16B halves], so every load below is one coalesced 512B access.
+            // Chunks past the cell end read as zeros, which decode to column-0
+            // gathers flushed into bucket 0 (never reduced): no divergence.
+            constexpr int NCH = 2;
+            constexpr bool SC = FMT == FMT_U16_SCALED;
+            auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
+            auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
+            auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
+            auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
+            auto load_round = [&](int64_t rb, uint4 (&q)[NCH][2]) {
+#pragma unroll
+                for (int j = 0; j < NCH; ++j) {
+                    const int64_t gb = rb + 32 * j;
+                    const int64_t nr = min((int64_t)32, ch1 - gb);
+                    q[j][0] = make_uint4(0, 0, 0, 0);
+                    q[j][1] = q[j][0];
+                    if ((int64_t)lane < nr) {
+                        q[j][0] = __ldg(ent4 + 2 * gb + lane);
+                        q[j][1] = __ldg(ent4 + 2 * gb + nr + lane);
+                    }
+                }
+            };
+            uint4 q[NCH][2];
+            load_round(ch0, q);
+            for (int64_t base = ch0; base < ch1; base += 32 * NCH) {
+                uint4 a[NCH][2];
+#pragma unroll
+                for (int j = 0; j < NCH; ++j) {
+                    a[j][0] = q[j][0];
+                    a[j][1] = q[j][1];
+                }
+                if (base + 32 * NCH < ch1) load_round(base + 32 * NCH, q);  // prefetch
+                uint32_t cur[NCH];
+                Acc s[NCH];
+                uint32_t fk[NCH][7];
+                float fs[NCH][7];
+#pragma unroll
+                for (int j = 0; j < NCH; ++j) {
+                    const uint32_t w[8] = {a[j][0].x, a[j][0].y, a[j][0].z, a[j][0].w,
+                                           a[j][1].x, a[j][1].y, a[j][1].z, a[j][1].w};
+                    cur[j] = key_off(w[0]);
+                    s[j] = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
+#pragma unroll
+                    for (int i = 1; i < 8; ++i) {
+                        const uint32_t x = w[i];
+                        const uint32_t isk = is_key(x);
+                        const uint32_t ko = key_off(x);
+                        const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
+                        const Acc h = lds_v<Acc, VSZ>(vbase + hi_off(x));
+                        if constexpr (MODE == MODE_FLOAT) {
+                            // record completed segments; flushed below as one batch
+                            const bool newseg = isk && ko != cur[j];
+                            fk[j][i - 1] = newseg ? cur[j] : 0u;
+                            fs[j][i - 1] = s[j];
+                            cur[j] = newseg ? ko : cur[j];
+                            s[j] = (newseg ? (Acc)0 : s[j]) + g + h;
+                        } else {
+                            bucket_flush_pred(isk, bkbase + cur[j], s[j]);  // native red
+                            cur[j] = isk ? ko : cur[j];
+                            s[j] = (isk ? (Acc)0 : s[j]) + g + h;
+                        }
+                    }
+                }
+                if constexpr (MODE == MODE_FLOAT) {
+                    // all bucket loads, then all adds/stores: one latency per round.
+                    // Keys of completed segments are distinct across the whole
+                    // round (a group completes inside a chunk at most once; a
+                    // repeated equal key continues the segment), bucket 0 aside.
+                    float tb[NCH][7];
+#pragma unroll
+                    for (int j = 0; j < NCH; ++j)
+#pragma unroll
+                        for (int i = 0; i < 7; ++i) tb[j][i] = lds_bucket(bkbase + fk[j][i]);
+#pragma unroll
+                    for (int j = 0; j < NCH; ++j)
+#pragma unroll
+                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[j][i], tb[j][i] + fs[j][i]);
+                }
+                // a chunk's last segment may continue in the next lane's chunk
+#pragma unroll
+                for (int j = 0; j < NCH; ++j) bucket_flush_final(bkbase + cur[j], s[j]);
+                __syncwarp();
+            }
+        } else {
         // round = 32 chunks stored as [first 16B halves][second 16B halves]
         int64_t nr = min((int64_t)32, ch1 - ch0);
         uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
@@ -405,6 +493,7 @@ rsr_mv_kernel(MvParams p) {
             __syncwarp();
             nr = nnr;
         }
+        }  // generic path
         asm volatile("" ::: "memory");
 
         // ---- pattern-table reduction: y_i = sum_key sgn_i(key) * bucket[key] ----
