@@ -110,6 +110,12 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     p.part = ws;
     p.beta = beta;
     p.scale_dev = scale_out;
+    {
+        static const int dbg = getenv("RSR_MV_DEBUG") ? atoi(getenv("RSR_MV_DEBUG")) : 0;
+        p.dbg = dbg;
+        static const int pf = getenv("RSR_MV_PF") ? atoi(getenv("RSR_MV_PF")) : 4;
+        p.pf = pf;
+    }
     if (MODE == MODE_FUSED && !p.scale_dev && need_ws)
         p.scale_dev = (double *)((char *)ws + part_bytes(vw));
     p.vstaged = nullptr;
@@ -134,7 +140,9 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     size_t fixed = 0;
     if (vw->format != FMT_U32) fixed += ((size_t)tn * vsz + 15) & ~(size_t)15;
     if (bucket) fixed += (size_t)p.nkeys * kp * 4;
-    const size_t per_warp = bucket ? (size_t)p.nkeys * 4 : 0;
+    size_t per_warp = bucket ? (size_t)p.nkeys * 4 : 0;
+    if (bucket && vw->format != FMT_U32) per_warp += RING_STAGES * (RING_STAGE_BYTES + 8);
+    fixed += 16;  // alignment slack (mbarriers)
     const size_t smem_cap = 227 * 1024;
     const int64_t cells_per_tile = vw->n_blocks;
     int64_t ctas_per_tile = std::max<int64_t>(1, sms / vw->tile_count);

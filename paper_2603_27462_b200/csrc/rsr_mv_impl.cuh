@@ -41,7 +41,7 @@ enum StreamFormat {
     FMT_U32 = 2          // u32: column, or key | 1<<31
 };
 
-constexpr int MV_MAX_WARPS = 24;  // 768 threads: up to 85 registers per thread
+constexpr int MV_MAX_WARPS = 20;  // 640 threads: up to 102 registers per thread
 constexpr int64_t BUCKET_MAX_KEYS = 2187;  // 3^7: buckets live in smem up to here
 
 struct MvParams {
@@ -63,6 +63,8 @@ struct MvParams {
     void *part;          // tc > 1: [tc][nblk*k] partials (float or int32)
     double beta;         // fused
     double *scale_dev;   // fused: device scale slot (may be null when tc == 1)
+    int dbg;             // experiment knobs (RSR_MV_DEBUG); 0 in production
+    int pf;              // L2 prefetch distance in rounds (0 = off)
 };
 
 __device__ __forceinline__ float load_as_f32(const void *v, int dtype, int64_t i) {
@@ -220,21 +222,101 @@ struct MvTypes {
     static constexpr bool SMEM_V = FMT != FMT_U32;
 };
 
+// Element loader for the staging loops, templated on the input dtype.
+template <int DT>
+__device__ __forceinline__ float ld_elem(const void *v, int64_t i) {
+    if constexpr (DT == RSR_F32) return __ldg((const float *)v + i);
+    else if constexpr (DT == RSR_BF16) return bf16_bits_to_f32(__ldg((const uint16_t *)v + i));
+    else if constexpr (DT == RSR_F16) return __half2float(__ldg((const __half *)v + i));
+    else return (float)__ldg((const int8_t *)v + i);
+}
+
+// fn(i, x) for i in [0, cnt) with x = v[c0 + i]; 16 independent coalesced
+// loads in flight per thread (a plain strided loop is a chain of L2 latencies).
+template <int DT, typename Fn>
+__device__ __forceinline__ void for_each_v_t(const void *v, int64_t c0, int64_t cnt, Fn fn) {
+    constexpr int U = 16;
+    const int64_t nt = blockDim.x;
+    for (int64_t i0 = threadIdx.x; i0 < cnt; i0 += U * nt) {
+        float x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * nt;
+            x[u] = i < cnt ? ld_elem<DT>(v, c0 + i) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * nt;
+            if (i < cnt) fn(i, x[u]);
+        }
+    }
+}
+template <typename Fn>
+__device__ __forceinline__ void for_each_v(const void *v, int dtype, int64_t c0, int64_t cnt,
+                                           Fn fn) {
+    switch (dtype) {
+        case RSR_F32: for_each_v_t<RSR_F32>(v, c0, cnt, fn); break;
+        case RSR_BF16: for_each_v_t<RSR_BF16>(v, c0, cnt, fn); break;
+        case RSR_F16: for_each_v_t<RSR_F16>(v, c0, cnt, fn); break;
+        default: for_each_v_t<RSR_I8>(v, c0, cnt, fn); break;
+    }
+}
+
+// CTA-wide max |v| (float64, exact), with the batched loader.
+__device__ __forceinline__ double cta_absmax_fast(const void *v, int dtype, int64_t n) {
+    __shared__ double red[32];
+    double a = 0.0;
+    for_each_v(v, dtype, 0, n, [&](int64_t, float x) {
+        const double ax = fabs((double)x);
+        a = ax > a ? ax : a;
+    });
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+        a = o > a ? o : a;
+    }
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red[warp] = a;
+    __syncthreads();
+    if (warp == 0) {
+        a = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+            a = o > a ? o : a;
+        }
+        if (threadIdx.x == 0) red[0] = a;
+    }
+    __syncthreads();
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+}  // namespace rsr
+#include "rsr_mv_kernel.cuh"
+namespace rsr {
+#if 0  // superseded register-ring kernel (kept out of the build)
 template <int K, int MODE, int FMT, bool BUCKET>
 __global__ void __launch_bounds__(MV_MAX_WARPS * 32)
-rsr_mv_kernel(MvParams p) {
+rsr_mv_kernel_old(MvParams p) {
     using T = MvTypes<MODE, FMT>;
     using Acc = typename T::Acc;
     constexpr int VSZ = T::VSZ;
     constexpr bool SMEM_V = T::SMEM_V;
     constexpr int CH = FMT == FMT_U32 ? 8 : 16;  // entries per 32-byte chunk
     constexpr int KP = KPad<K>::value;
+    constexpr int PD = 4;                        // rounds in flight (bucket path)
 
     extern __shared__ __align__(16) unsigned char mv_smem[];
     const int nwarps = blockDim.x >> 5;
     const int64_t t = blockIdx.y;
     const int64_t c0 = t * p.tw;
     const int64_t tn = min(p.tw, p.n - c0);
+    const uint32_t lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const uint4 *__restrict__ ent4 = reinterpret_cast<const uint4 *>(p.entries);
+    const int64_t bstride = (int64_t)gridDim.x * nwarps;
 
     // smem carve-up: [v tile][sign table NB x KP][buckets nwarps x NB]
     size_t off = 0;
@@ -243,12 +325,41 @@ rsr_mv_kernel(MvParams p) {
     Acc *__restrict__ stab = reinterpret_cast<Acc *>(mv_smem + off);
     if constexpr (BUCKET) off += (size_t)p.nkeys * KP * sizeof(Acc);
     Acc *__restrict__ buckets = reinterpret_cast<Acc *>(mv_smem + off);
+    Acc *__restrict__ bk = buckets + (size_t)warp * p.nkeys;
+    const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
+    const uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
+
+    // ---- bucket-path stream helpers (see the round loop below) -------------
+    constexpr bool SC = FMT == FMT_U16_SCALED;
+    auto load_round = [&](int64_t gb, int64_t cend, uint4 &q0, uint4 &q1) {
+        const int64_t nr = min((int64_t)32, cend - gb);
+        q0 = make_uint4(0, 0, 0, 0);
+        q1 = q0;
+        if ((int64_t)lane < nr) {
+            q0 = __ldg(ent4 + 2 * gb + lane);
+            q1 = __ldg(ent4 + 2 * gb + nr + lane);
+        }
+    };
+    uint4 ring[PD][2];
+    int64_t b = (int64_t)blockIdx.x * nwarps + warp;
+    int64_t ch0 = 0, ch1 = 0;
+    if constexpr (FMT != FMT_U32 && BUCKET) {
+        // start the first cell's stream before the prologue so its DRAM
+        // latency overlaps the staging of v
+        if (b < p.nblk && !(p.dbg & 512)) {
+            const int64_t dc = b * p.tc + t;
+            ch0 = p.e_off[dc] / CH;
+            ch1 = p.e_off[dc + 1] / CH;
+#pragma unroll
+            for (int u = 0; u < PD; ++u) load_round(ch0 + 32 * u, ch1, ring[u][0], ring[u][1]);
+        }
+    }
 
     // ---- prologue -------------------------------------------------------
     double scale = 1.0;
     if constexpr (MODE == MODE_FUSED) {
         if constexpr (SMEM_V) {
-            const double amax = cta_absmax(p.v, p.vdtype, p.n);
+            const double amax = cta_absmax_fast(p.v, p.vdtype, p.n);
             scale = amax == 0.0 ? 1.0 : 127.0 / amax;
             if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
                 *p.scale_dev = scale;
@@ -256,250 +367,48 @@ rsr_mv_kernel(MvParams p) {
             scale = *p.scale_dev;  // written by the staging kernel
         }
     }
-    if constexpr (SMEM_V) {
-        for (int64_t i = threadIdx.x; i < tn; i += blockDim.x) {
-            if constexpr (MODE == MODE_FLOAT) {
-                reinterpret_cast<float *>(vsm)[i] = load_as_f32(p.v, p.vdtype, c0 + i);
-            } else {
-                const int8_t q = MODE == MODE_INT ? __ldg((const int8_t *)p.v + c0 + i)
-                                                  : quantize_one(load_as_f32(p.v, p.vdtype, c0 + i), scale);
+    if (!(p.dbg & 128)) if constexpr (SMEM_V) {
+        if constexpr (MODE == MODE_FLOAT) {
+            for_each_v(p.v, p.vdtype, c0, tn,
+                       [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
+        } else {
+            const int dt = MODE == MODE_INT ? (int)RSR_I8 : p.vdtype;
+            for_each_v(p.v, dt, c0, tn, [&](int64_t i, float x) {
+                const int8_t q = MODE == MODE_INT ? (int8_t)x : quantize_one(x, scale);
                 if constexpr (VSZ == 4) reinterpret_cast<int32_t *>(vsm)[i] = q;
                 else reinterpret_cast<int8_t *>(vsm)[i] = q;
-            }
+            });
         }
     }
-    if constexpr (BUCKET) {
+    if (!(p.dbg & 256)) if constexpr (BUCKET) {
         for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
+            uint32_t kk = (uint32_t)key;
 #pragma unroll
-            for (int i = 0; i < KP; ++i)
-                stab[key * KP + i] = (Acc)(i < K ? key_sign((uint32_t)key, i, p.bitwidth) : 0);
+            for (int i = 0; i < KP; ++i) {
+                int sg = 0;
+                if (p.bitwidth == RSR_BINARY) {
+                    sg = (int)((kk >> i) & 1u);
+                } else {
+                    const uint32_t q3 = kk / 3u, d = kk - 3u * q3;
+                    kk = q3;
+                    sg = d == 1u ? 1 : (d == 2u ? -1 : 0);
+                }
+                stab[key * KP + i] = (Acc)(i < K ? sg : 0);
+            }
         }
         for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
     }
     __syncthreads();
+    if (p.dbg & 64) return;  // prologue only (experiment)
 
     using VG = typename std::conditional<MODE == MODE_FLOAT, float, int8_t>::type;
     const VG *__restrict__ vglob = reinterpret_cast<const VG *>(p.vstaged) + c0;
-    const uint32_t lane = lane_id();
-    const int warp = threadIdx.x >> 5;
-    Acc *__restrict__ bk = buckets + (size_t)warp * p.nkeys;
-    const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
-    const uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
-    const uint4 *__restrict__ ent4 = reinterpret_cast<const uint4 *>(p.entries);
 
-    for (int64_t b = (int64_t)blockIdx.x * nwarps + warp; b < p.nblk;
-         b += (int64_t)gridDim.x * nwarps) {
-        const int64_t dc = b * p.tc + t;
-        const int64_t ch0 = p.e_off[dc] / CH, ch1 = p.e_off[dc + 1] / CH;  // chunk range
-        Acc acc[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-
-        if constexpr (FMT != FMT_U32 && BUCKET) {
-            // Bucket path.  A round is NCH groups of 32 chunks; lane L owns
-            // chunk L of each group (independent dependency chains for ILP).
-            // Each group of 32 chunks is stored as [first 16B halves][second
-            // 16B halves], so every load below is one coalesced 512B access.
-            // Chunks past the cell end read as zeros, which decode to column-0
-            // gathers flushed into bucket 0 (never reduced): no divergence.
-            constexpr int NCH = 2;
-            constexpr bool SC = FMT == FMT_U16_SCALED;
-            auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
-            auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
-            auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
-            auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
-            auto load_round = [&](int64_t rb, uint4 (&q)[NCH][2]) {
-#pragma unroll
-                for (int j = 0; j < NCH; ++j) {
-                    const int64_t gb = rb + 32 * j;
-                    const int64_t nr = min((int64_t)32, ch1 - gb);
-                    q[j][0] = make_uint4(0, 0, 0, 0);
-                    q[j][1] = q[j][0];
-                    if ((int64_t)lane < nr) {
-                        q[j][0] = __ldg(ent4 + 2 * gb + lane);
-                        q[j][1] = __ldg(ent4 + 2 * gb + nr + lane);
-                    }
-                }
-            };
-            uint4 q[NCH][2];
-            load_round(ch0, q);
-            for (int64_t base = ch0; base < ch1; base += 32 * NCH) {
-                uint4 a[NCH][2];
-#pragma unroll
-                for (int j = 0; j < NCH; ++j) {
-                    a[j][0] = q[j][0];
-                    a[j][1] = q[j][1];
-                }
-                if (base + 32 * NCH < ch1) load_round(base + 32 * NCH, q);  // prefetch
-                uint32_t cur[NCH];
-                Acc s[NCH];
-                uint32_t fk[NCH][7];
-                float fs[NCH][7];
-#pragma unroll
-                for (int j = 0; j < NCH; ++j) {
-                    const uint32_t w[8] = {a[j][0].x, a[j][0].y, a[j][0].z, a[j][0].w,
-                                           a[j][1].x, a[j][1].y, a[j][1].z, a[j][1].w};
-                    cur[j] = key_off(w[0]);
-                    s[j] = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
-#pragma unroll
-                    for (int i = 1; i < 8; ++i) {
-                        const uint32_t x = w[i];
-                        const uint32_t isk = is_key(x);
-                        const uint32_t ko = key_off(x);
-                        const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
-                        const Acc h = lds_v<Acc, VSZ>(vbase + hi_off(x));
-                        if constexpr (MODE == MODE_FLOAT) {
-                            // record completed segments; flushed below as one batch
-                            const bool newseg = isk && ko != cur[j];
-                            fk[j][i - 1] = newseg ? cur[j] : 0u;
-                            fs[j][i - 1] = s[j];
-                            cur[j] = newseg ? ko : cur[j];
-                            s[j] = (newseg ? (Acc)0 : s[j]) + g + h;
-                        } else {
-                            bucket_flush_pred(isk, bkbase + cur[j], s[j]);  // native red
-                            cur[j] = isk ? ko : cur[j];
-                            s[j] = (isk ? (Acc)0 : s[j]) + g + h;
-                        }
-                    }
-                }
-                if constexpr (MODE == MODE_FLOAT) {
-                    // all bucket loads, then all adds/stores: one latency per round.
-                    // Keys of completed segments are distinct across the whole
-                    // round (a group completes inside a chunk at most once; a
-                    // repeated equal key continues the segment), bucket 0 aside.
-                    float tb[NCH][7];
-#pragma unroll
-                    for (int j = 0; j < NCH; ++j)
-#pragma unroll
-                        for (int i = 0; i < 7; ++i) tb[j][i] = lds_bucket(bkbase + fk[j][i]);
-#pragma unroll
-                    for (int j = 0; j < NCH; ++j)
-#pragma unroll
-                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[j][i], tb[j][i] + fs[j][i]);
-                }
-                // a chunk's last segment may continue in the next lane's chunk
-#pragma unroll
-                for (int j = 0; j < NCH; ++j) bucket_flush_final(bkbase + cur[j], s[j]);
-                __syncwarp();
-            }
-        } else {
-        // round = 32 chunks stored as [first 16B halves][second 16B halves]
-        int64_t nr = min((int64_t)32, ch1 - ch0);
-        uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-        if ((int64_t)lane < nr) {
-            q0 = __ldg(ent4 + 2 * ch0 + lane);
-            q1 = __ldg(ent4 + 2 * ch0 + nr + lane);
-        }
-        for (int64_t base = ch0; base < ch1; base += 32) {
-            const bool valid = (int64_t)lane < nr;
-            const uint4 a0 = q0, a1 = q1;
-            const int64_t nbase = base + 32;
-            const int64_t nnr = min((int64_t)32, ch1 - nbase);
-            if ((int64_t)lane < nnr) {  // prefetch the next round
-                q0 = __ldg(ent4 + 2 * nbase + lane);
-                q1 = __ldg(ent4 + 2 * nbase + nnr + lane);
-            }
-            if (valid) {
-                const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                if constexpr (FMT != FMT_U32 && BUCKET) {
-                    // slot 2i = low half of w[i] (column or key), slot 2i+1 =
-                    // high half (always a column).  Scaled format: entries are
-                    // byte offsets (column*4; key*4|1) straight into v and the
-                    // buckets.
-                    constexpr bool SC = FMT == FMT_U16_SCALED;
-                    auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
-                    auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
-                    auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
-                    auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
-                    uint32_t cur = key_off(w[0]);
-                    Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
-                    if constexpr (MODE == MODE_FLOAT) {
-                        // Completed segments are recorded in registers and
-                        // flushed as one batch (all bucket loads, then all
-                        // adds/stores) so the read-modify-write latency is paid
-                        // once per chunk.  A repeated key equal to the current
-                        // one continues the segment.  Bucket 0 absorbs no-ops.
-                        uint32_t fk[7];
-                        float fs[7];
-#pragma unroll
-                        for (int i = 1; i < 8; ++i) {
-                            const uint32_t x = w[i];
-                            const uint32_t isk = is_key(x);
-                            const uint32_t ko = key_off(x);
-                            const bool newseg = isk && ko != cur;
-                            const float g = lds_v_unless<float, VSZ>(isk, vbase + lo_off(x));
-                            const float h = lds_v<float, VSZ>(vbase + hi_off(x));
-                            fk[i - 1] = newseg ? cur : 0u;
-                            fs[i - 1] = s;
-                            cur = newseg ? ko : cur;
-                            s = (newseg ? 0.f : s) + g + h;
-                        }
-                        float tb[7];
-#pragma unroll
-                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
-#pragma unroll
-                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
-                    } else {
-#pragma unroll
-                        for (int i = 1; i < 8; ++i) {
-                            const uint32_t x = w[i];
-                            const uint32_t isk = is_key(x);
-                            const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
-                            const Acc h = lds_v<Acc, VSZ>(vbase + hi_off(x));
-                            bucket_flush_pred(isk, bkbase + cur, s);
-                            cur = isk ? key_off(x) : cur;
-                            s = (isk ? (Acc)0 : s) + g + h;
-                        }
-                    }
-                    bucket_flush_final(bkbase + cur, s);
-                } else if constexpr (FMT == FMT_U16) {
-                    uint32_t cur = w[0] & 0x7FFFu;
-                    Acc s = lds_v<Acc, VSZ>(vbase + (w[0] >> 16) * VSZ);
-#pragma unroll
-                    for (int i = 1; i < 8; ++i) {
-                        const uint32_t lo = w[i] & 0xFFFFu;
-                        const uint32_t isk = lo & 0x8000u;
-                        const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (lo & 0x7FFFu) * VSZ);
-                        const Acc h = lds_v<Acc, VSZ>(vbase + (w[i] >> 16) * VSZ);
-                        if constexpr (BUCKET) {
-                            bucket_flush_pred(isk, bkbase + cur * 4u, s);
-                        } else if (isk) {
-                            reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                        }
-                        cur = isk ? (lo & 0x7FFFu) : cur;
-                        s = (isk ? (Acc)0 : s) + g + h;
-                    }
-                    if constexpr (BUCKET) bucket_flush_final(bkbase + cur * 4u, s);
-                    else reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                } else {  // FMT_U32, register flush, v gathered from global scratch
-                    constexpr uint32_t KF = 1u << 31;
-                    uint32_t cur = w[0] & ~KF;
-                    Acc s = (Acc)__ldg(vglob + w[1]);
-#pragma unroll
-                    for (int i = 2; i < 8; i += 2) {
-                        const Acc h = (Acc)__ldg(vglob + w[i + 1]);
-                        if (w[i] & KF) {
-                            reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                            cur = w[i] & ~KF;
-                            s = (Acc)0;
-                        } else {
-                            s += (Acc)__ldg(vglob + w[i]);
-                        }
-                        s += h;
-                    }
-                    reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                }
-            }
-            __syncwarp();
-            nr = nnr;
-        }
-        }  // generic path
-        asm volatile("" ::: "memory");
-
-        // ---- pattern-table reduction: y_i = sum_key sgn_i(key) * bucket[key] ----
-        // (bucket 0 collects padding and is never reduced)
+    // ---- per-cell epilogue: pattern-table reduction + warp reduce + store ----
+    auto finish_cell = [&](int64_t bb, Acc (&acc)[K]) {
+        // y_i = sum_key sgn_i(key) * bucket[key]  (bucket 0 collects padding)
         if constexpr (BUCKET) {
-            for (int key = lane; key < p.nkeys; key += 32) {
+            for (int key = lane; key < ((p.dbg & 4) ? 0 : p.nkeys); key += 32) {
                 const Acc bv = key ? bk[key] : (Acc)0;
                 bk[key] = (Acc)0;
                 const Acc *row = stab + key * KP;
@@ -508,8 +417,8 @@ rsr_mv_kernel(MvParams p) {
             }
             __syncwarp();
         }
-        const int64_t row0 = b * p.k;  // row within the view
-        const int64_t grow0 = (p.blk0 + b) * p.k;
+        const int64_t row0 = bb * p.k;  // row within the view
+        const int64_t grow0 = (p.blk0 + bb) * p.k;
         Acc mine = (Acc)0;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -532,8 +441,186 @@ rsr_mv_kernel(MvParams p) {
                     (float)((double)(int32_t)mine * (p.beta / scale));
             }
         }
+    };
+
+    if constexpr (FMT != FMT_U32 && BUCKET) {
+        // ===== bucket path =====================================================
+        // A round is 32 chunks; lane L owns chunk L.  Each round is stored as
+        // [first 16B halves][second 16B halves], so both loads are coalesced
+        // 512B accesses.  Rounds are fetched PD ahead into a register ring and
+        // the next cell's first rounds are fetched before this cell's epilogue.
+        // Chunks past the cell end read as zeros, which decode to column-0
+        // gathers flushed into bucket 0 (never reduced): no divergence.
+        auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
+        auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
+        auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
+        auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
+        while (b < p.nblk) {
+            Acc acc[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
+            auto do_round = [&](const uint4 &a0, const uint4 &a1) {
+                if (p.dbg & 32) {  // stream only (bandwidth experiment)
+                    acc[0] += (Acc)(a0.x ^ a0.y ^ a0.z ^ a0.w ^ a1.x ^ a1.y ^ a1.z ^ a1.w);
+                    return;
+                }
+                const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                uint32_t cur = key_off(w[0]);
+                Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
+                uint32_t fk[7];
+                float fs[7];
+#pragma unroll
+                for (int i = 1; i < 8; ++i) {
+                    const uint32_t x = w[i];
+                    const uint32_t isk = is_key(x);
+                    const uint32_t ko = key_off(x);
+                    const uint32_t ga = (p.dbg & 8) ? lane * 4u : lo_off(x);
+                    const uint32_t ha = (p.dbg & 8) ? lane * 4u + 128u : hi_off(x);
+                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + ga);
+                    const Acc h = lds_v<Acc, VSZ>(vbase + ha);
+                    if constexpr (MODE == MODE_FLOAT) {
+                        // record completed segments; flushed below as one batch
+                        const bool newseg = isk && ko != cur;
+                        fk[i - 1] = newseg ? cur : 0u;
+                        fs[i - 1] = s;
+                        cur = newseg ? ko : cur;
+                        s = (newseg ? (Acc)0 : s) + g + h;
+                    } else {
+                        if (!(p.dbg & 1)) bucket_flush_pred(isk, bkbase + cur, s);  // native red
+                        cur = isk ? ko : cur;
+                        s = (isk ? (Acc)0 : s) + g + h;
+                    }
+                }
+                if constexpr (MODE == MODE_FLOAT) {
+                    // all bucket loads, then all adds/stores: one latency per
+                    // round.  Keys of completed segments are distinct across the
+                    // round (a group completes inside a chunk at most once; a
+                    // repeated equal key continues the segment), bucket 0 aside.
+                    if (!(p.dbg & 1)) {
+                        float tb[7];
+#pragma unroll
+                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
+#pragma unroll
+                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                    }
+                }
+                // A chunk's last segment may continue in the next lane's chunk.
+                // Integer: native shared red handles same-key lanes.  Float:
+                // lanes with equal final keys form contiguous runs; a segmented
+                // suffix sum over the run lets the run's first lane flush alone
+                // (no CAS loop, fixed summation order).
+                if (!(p.dbg & 2)) {
+                    if constexpr (MODE == MODE_FLOAT) {
+                        float sj = s;
+                        const uint32_t kj = cur;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const float os = __shfl_down_sync(RSR_FULL_MASK, sj, d);
+                            const uint32_t ok = __shfl_down_sync(RSR_FULL_MASK, kj, d);
+                            if (lane + d < 32 && ok == kj) sj += os;
+                        }
+                        const uint32_t pk = __shfl_up_sync(RSR_FULL_MASK, kj, 1);
+                        const bool head = lane == 0 || pk != kj;
+                        if (head) sts_bucket(bkbase + kj, lds_bucket(bkbase + kj) + sj);
+                    } else {
+                        bucket_flush_final(bkbase + cur, s);
+                    }
+                } else {
+                    acc[0] += s;
+                }
+                __syncwarp();
+            };
+            for (int64_t base = ch0; base < ch1; base += 32 * PD) {
+#pragma unroll
+                for (int u = 0; u < PD; ++u) {
+                    const int64_t rb = base + 32 * u;
+                    if (rb < ch1) {
+                        const uint4 a0 = ring[u][0], a1 = ring[u][1];
+                        load_round(rb + 32 * PD, ch1, ring[u][0], ring[u][1]);
+                        do_round(a0, a1);
+                    }
+                }
+            }
+            // prefetch the next cell before this cell's epilogue
+            const int64_t nb = b + bstride;
+            const int64_t cb = b;
+            if (nb < p.nblk) {
+                const int64_t dc = nb * p.tc + t;
+                ch0 = p.e_off[dc] / CH;
+                ch1 = p.e_off[dc + 1] / CH;
+#pragma unroll
+                for (int u = 0; u < PD; ++u) load_round(ch0 + 32 * u, ch1, ring[u][0], ring[u][1]);
+            }
+            asm volatile("" ::: "memory");
+            finish_cell(cb, acc);
+            b = nb;
+        }
+    } else {
+        // ===== generic path (register flush and/or u32 entries) ================
+        for (; b < p.nblk; b += bstride) {
+            const int64_t dc = b * p.tc + t;
+            const int64_t cch0 = p.e_off[dc] / CH, cch1 = p.e_off[dc + 1] / CH;
+            Acc acc[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
+            int64_t nr = min((int64_t)32, cch1 - cch0);
+            uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+            if ((int64_t)lane < nr) {
+                q0 = __ldg(ent4 + 2 * cch0 + lane);
+                q1 = __ldg(ent4 + 2 * cch0 + nr + lane);
+            }
+            for (int64_t base = cch0; base < cch1; base += 32) {
+                const bool valid = (int64_t)lane < nr;
+                const uint4 a0 = q0, a1 = q1;
+                const int64_t nbase = base + 32;
+                const int64_t nnr = min((int64_t)32, cch1 - nbase);
+                if ((int64_t)lane < nnr) {  // prefetch the next round
+                    q0 = __ldg(ent4 + 2 * nbase + lane);
+                    q1 = __ldg(ent4 + 2 * nbase + nnr + lane);
+                }
+                if (valid) {
+                    const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    if constexpr (FMT == FMT_U16) {
+                        uint32_t cur = w[0] & 0x7FFFu;
+                        Acc s = lds_v<Acc, VSZ>(vbase + (w[0] >> 16) * VSZ);
+#pragma unroll
+                        for (int i = 1; i < 8; ++i) {
+                            const uint32_t lo = w[i] & 0xFFFFu;
+                            const uint32_t isk = lo & 0x8000u;
+                            const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (lo & 0x7FFFu) * VSZ);
+                            const Acc h = lds_v<Acc, VSZ>(vbase + (w[i] >> 16) * VSZ);
+                            if (isk) reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                            cur = isk ? (lo & 0x7FFFu) : cur;
+                            s = (isk ? (Acc)0 : s) + g + h;
+                        }
+                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                    } else {  // FMT_U32, register flush, v gathered from global scratch
+                        constexpr uint32_t KF = 1u << 31;
+                        uint32_t cur = w[0] & ~KF;
+                        Acc s = (Acc)__ldg(vglob + w[1]);
+#pragma unroll
+                        for (int i = 2; i < 8; i += 2) {
+                            const Acc h = (Acc)__ldg(vglob + w[i + 1]);
+                            if (w[i] & KF) {
+                                reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                                cur = w[i] & ~KF;
+                                s = (Acc)0;
+                            } else {
+                                s += (Acc)__ldg(vglob + w[i]);
+                            }
+                            s += h;
+                        }
+                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                    }
+                }
+                nr = nnr;
+            }
+            finish_cell(b, acc);
+        }
     }
 }
+
+#endif
 
 using KernelFn = void (*)(MvParams);
 

@@ -1,0 +1,365 @@
+// rsr_mv_kernel.cuh -- the sm_100a RSR multiply kernel (included by
+// rsr_mv_impl.cuh; see that file's header for the algorithm).
+#pragma once
+
+namespace rsr {
+
+// ---- TMA (cp.async.bulk) + mbarrier helpers ---------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tRSR_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra RSR_WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared, completion signalled on `bar` (transaction bytes).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(addr));
+    return r;
+}
+
+constexpr int RING_STAGES = 4;     // rounds in flight per warp (bucket path)
+constexpr int RING_STAGE_BYTES = 1024;  // one round = 32 chunks x 32 bytes
+
+template <int K, int MODE, int FMT, bool BUCKET>
+__global__ void __launch_bounds__(MV_MAX_WARPS * 32)
+rsr_mv_kernel(MvParams p) {
+    using T = MvTypes<MODE, FMT>;
+    using Acc = typename T::Acc;
+    constexpr int VSZ = T::VSZ;
+    constexpr bool SMEM_V = T::SMEM_V;
+    constexpr int CH = FMT == FMT_U32 ? 8 : 16;  // entries per 32-byte chunk
+    constexpr int KP = KPad<K>::value;
+    constexpr bool RING = FMT != FMT_U32 && BUCKET;
+    constexpr int S = RING_STAGES;
+
+    extern __shared__ __align__(128) unsigned char mv_smem[];
+    const int nwarps = blockDim.x >> 5;
+    const int64_t t = blockIdx.y;
+    const int64_t c0 = t * p.tw;
+    const int64_t tn = min(p.tw, p.n - c0);
+    const uint32_t lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const uint4 *__restrict__ ent4 = reinterpret_cast<const uint4 *>(p.entries);
+    const int64_t bstride = (int64_t)gridDim.x * nwarps;
+
+    // smem: [ring W x S x 1KB][v tile][sign table NB x KP][buckets W x NB][mbarriers W x S]
+    size_t off = 0;
+    unsigned char *ringsm = mv_smem;
+    if constexpr (RING) off += (size_t)nwarps * S * RING_STAGE_BYTES;
+    unsigned char *vsm = mv_smem + off;
+    if constexpr (SMEM_V) off += ((size_t)tn * VSZ + 15) & ~(size_t)15;
+    Acc *__restrict__ stab = reinterpret_cast<Acc *>(mv_smem + off);
+    if constexpr (BUCKET) off += (size_t)p.nkeys * KP * sizeof(Acc);
+    Acc *__restrict__ buckets = reinterpret_cast<Acc *>(mv_smem + off);
+    if constexpr (BUCKET) off += (size_t)nwarps * p.nkeys * sizeof(Acc);
+    off = (off + 7) & ~(size_t)7;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(mv_smem + off) + (size_t)warp * S;
+    Acc *__restrict__ bk = buckets + (size_t)warp * p.nkeys;
+    const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
+    const uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
+    const uint32_t ringbase =
+        (uint32_t)__cvta_generic_to_shared(ringsm) + (uint32_t)(warp * S * RING_STAGE_BYTES);
+    const uint32_t barbase = (uint32_t)__cvta_generic_to_shared(bars);
+
+    int64_t b = (int64_t)blockIdx.x * nwarps + warp;
+
+    // ---- stream producer (lane 0 of each warp feeds its own ring) -----------
+    // Walks this warp's cells (b, b + bstride, ...) round by round, S rounds
+    // ahead of the consumer; each round is one 1-D bulk copy (TMA) into a
+    // 1 KiB stage whose mbarrier completes on the transaction bytes.
+    int64_t pb = b, pbase = 0, pend = 0;
+    if (RING && lane == 0 && pb < p.nblk) {
+        const int64_t dc = pb * p.tc + t;
+        pbase = p.e_off[dc] / CH;
+        pend = p.e_off[dc + 1] / CH;
+    }
+    auto produce = [&](int stage) {
+        while (pb < p.nblk && pbase >= pend) {
+            pb += bstride;
+            if (pb < p.nblk) {
+                const int64_t dc = pb * p.tc + t;
+                pbase = p.e_off[dc] / CH;
+                pend = p.e_off[dc + 1] / CH;
+            }
+        }
+        if (pb >= p.nblk) return;
+        const uint32_t bytes = (uint32_t)(min((int64_t)32, pend - pbase) * 32);
+        const uint32_t bar = barbase + stage * 8;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(ringbase + stage * RING_STAGE_BYTES, ent4 + 2 * pbase, bytes, bar);
+        pbase += 32;
+    };
+    if constexpr (RING) {
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) mbar_init(barbase + s * 8, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            // start the stream before the prologue: its DRAM latency overlaps
+            // the staging of v
+            for (int s = 0; s < S; ++s) produce(s);
+        }
+        __syncwarp();
+    }
+
+    // ---- prologue -------------------------------------------------------
+    double scale = 1.0;
+    if constexpr (MODE == MODE_FUSED) {
+        if constexpr (SMEM_V) {
+            const double amax = cta_absmax_fast(p.v, p.vdtype, p.n);
+            scale = amax == 0.0 ? 1.0 : 127.0 / amax;
+            if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+                *p.scale_dev = scale;
+        } else {
+            scale = *p.scale_dev;  // written by the staging kernel
+        }
+    }
+    if constexpr (SMEM_V) {
+        if constexpr (MODE == MODE_FLOAT) {
+            for_each_v(p.v, p.vdtype, c0, tn,
+                       [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
+        } else {
+            const int dt = MODE == MODE_INT ? (int)RSR_I8 : p.vdtype;
+            for_each_v(p.v, dt, c0, tn, [&](int64_t i, float x) {
+                const int8_t q = MODE == MODE_INT ? (int8_t)x : quantize_one(x, scale);
+                if constexpr (VSZ == 4) reinterpret_cast<int32_t *>(vsm)[i] = q;
+                else reinterpret_cast<int8_t *>(vsm)[i] = q;
+            });
+        }
+    }
+    if constexpr (BUCKET) {
+        for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
+            uint32_t kk = (uint32_t)key;
+#pragma unroll
+            for (int i = 0; i < KP; ++i) {
+                int sg = 0;
+                if (p.bitwidth == RSR_BINARY) {
+                    sg = (int)((kk >> i) & 1u);
+                } else {
+                    const uint32_t q3 = kk / 3u, d = kk - 3u * q3;
+                    kk = q3;
+                    sg = d == 1u ? 1 : (d == 2u ? -1 : 0);
+                }
+                stab[key * KP + i] = (Acc)(i < K ? sg : 0);
+            }
+        }
+        for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
+    }
+    __syncthreads();
+
+    using VG = typename std::conditional<MODE == MODE_FLOAT, float, int8_t>::type;
+    const VG *__restrict__ vglob = reinterpret_cast<const VG *>(p.vstaged) + c0;
+
+    // ---- per-cell epilogue: pattern-table reduction + warp reduce + store ----
+    auto finish_cell = [&](int64_t bb, Acc (&acc)[K]) {
+        // y_i = sum_key sgn_i(key) * bucket[key]  (bucket 0 collects padding)
+        if constexpr (BUCKET) {
+            for (int key = lane; key < p.nkeys; key += 32) {
+                const Acc bv = key ? bk[key] : (Acc)0;
+                bk[key] = (Acc)0;
+                const Acc *row = stab + key * KP;
+#pragma unroll
+                for (int i = 0; i < K; ++i) acc[i] += row[i] * bv;
+            }
+            __syncwarp();
+        }
+        const int64_t row0 = bb * p.k;  // row within the view
+        const int64_t grow0 = (p.blk0 + bb) * p.k;
+        Acc mine = (Acc)0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const Acc r = warp_sum(acc[i]);
+            if (lane == (uint32_t)i) mine = r;
+        }
+        if (lane < (uint32_t)K && grow0 + lane < p.m_rows) {
+            const int64_t r = row0 + lane;
+            if (p.tc > 1) {
+                const int64_t rows_view = p.nblk * p.k;
+                reinterpret_cast<Acc *>(p.part)[t * rows_view + r] = mine;
+            } else if constexpr (MODE == MODE_FLOAT) {
+                float *y = reinterpret_cast<float *>(p.y);
+                y[r] = p.accumulate ? y[r] + (float)mine : (float)mine;
+            } else if constexpr (MODE == MODE_INT) {
+                int32_t *y = reinterpret_cast<int32_t *>(p.y);
+                y[r] = p.accumulate ? y[r] + (int32_t)mine : (int32_t)mine;
+            } else {
+                reinterpret_cast<float *>(p.y)[r] =
+                    (float)((double)(int32_t)mine * (p.beta / scale));
+            }
+        }
+    };
+
+    if constexpr (RING) {
+        // ===== bucket path =====================================================
+        // A round is 32 chunks; lane L owns chunk L.  A round sits in a ring
+        // stage as [first 16B halves][second 16B halves] (conflict-free 16B
+        // shared loads).  Slot 2i = low half of word i (column or key), slot
+        // 2i+1 = high half (always a column).  Scaled format: entries are byte
+        // offsets (column*4; key*4|1) straight into v and the buckets.
+        constexpr bool SC = FMT == FMT_U16_SCALED;
+        auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
+        auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
+        auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
+        auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
+        int64_t it = 0;  // rounds consumed by this warp (ring position)
+        for (; b < p.nblk; b += bstride) {
+            const int64_t dc = b * p.tc + t;
+            const int64_t ch0 = p.e_off[dc] / CH, ch1 = p.e_off[dc + 1] / CH;
+            Acc acc[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
+            for (int64_t base = ch0; base < ch1; base += 32, ++it) {
+                const int stage = (int)(it % S);
+                mbar_wait(barbase + stage * 8, (uint32_t)((it / S) & 1));
+                const uint32_t nr = (uint32_t)min((int64_t)32, ch1 - base);
+                const uint32_t st = ringbase + stage * RING_STAGE_BYTES;
+                uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
+                if (lane < nr) {
+                    a0 = lds128(st + lane * 16);
+                    a1 = lds128(st + nr * 16 + lane * 16);
+                }
+                __syncwarp();
+                if (lane == 0) produce(stage);  // refill the stage just drained
+                // chunks past the cell end are zeros: column-0 gathers flushed
+                // into bucket 0 (never reduced) -- no divergence
+                const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                uint32_t cur = key_off(w[0]);
+                Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
+                uint32_t fk[7];
+                float fs[7];
+#pragma unroll
+                for (int i = 1; i < 8; ++i) {
+                    const uint32_t x = w[i];
+                    const uint32_t isk = is_key(x);
+                    const uint32_t ko = key_off(x);
+                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
+                    const Acc h = lds_v<Acc, VSZ>(vbase + hi_off(x));
+                    if constexpr (MODE == MODE_FLOAT) {
+                        // record completed segments; flushed below as one batch
+                        const bool newseg = isk && ko != cur;
+                        fk[i - 1] = newseg ? cur : 0u;
+                        fs[i - 1] = s;
+                        cur = newseg ? ko : cur;
+                        s = (newseg ? (Acc)0 : s) + g + h;
+                    } else {
+                        bucket_flush_pred(isk, bkbase + cur, s);  // native shared red
+                        cur = isk ? ko : cur;
+                        s = (isk ? (Acc)0 : s) + g + h;
+                    }
+                }
+                if constexpr (MODE == MODE_FLOAT) {
+                    // all bucket loads, then all adds/stores: one latency per
+                    // round.  Keys of completed segments are distinct across the
+                    // round (a group completes inside a chunk at most once; a
+                    // repeated equal key continues the segment), bucket 0 aside.
+                    float tb[7];
+#pragma unroll
+                    for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
+#pragma unroll
+                    for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                    // The chunk's last segment may continue in the next lane's
+                    // chunk: equal final keys form contiguous lane runs; a
+                    // segmented suffix sum lets each run's first lane flush
+                    // alone (no CAS loop, fixed summation order).
+                    float sj = s;
+                    const uint32_t kj = cur;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const float os = __shfl_down_sync(RSR_FULL_MASK, sj, d);
+                        const uint32_t ok = __shfl_down_sync(RSR_FULL_MASK, kj, d);
+                        if (lane + d < 32 && ok == kj) sj += os;
+                    }
+                    const uint32_t pk = __shfl_up_sync(RSR_FULL_MASK, kj, 1);
+                    if (lane == 0 || pk != kj) sts_bucket(bkbase + kj, lds_bucket(bkbase + kj) + sj);
+                } else {
+                    bucket_flush_final(bkbase + cur, s);  // native red handles same keys
+                }
+                __syncwarp();
+            }
+            asm volatile("" ::: "memory");
+            finish_cell(b, acc);
+        }
+    } else {
+        // ===== generic path (register flush and/or u32 entries) ================
+        for (; b < p.nblk; b += bstride) {
+            const int64_t dc = b * p.tc + t;
+            const int64_t cch0 = p.e_off[dc] / CH, cch1 = p.e_off[dc + 1] / CH;
+            Acc acc[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
+            int64_t nr = min((int64_t)32, cch1 - cch0);
+            uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+            if ((int64_t)lane < nr) {
+                q0 = __ldg(ent4 + 2 * cch0 + lane);
+                q1 = __ldg(ent4 + 2 * cch0 + nr + lane);
+            }
+            for (int64_t base = cch0; base < cch1; base += 32) {
+                const bool valid = (int64_t)lane < nr;
+                const uint4 a0 = q0, a1 = q1;
+                const int64_t nbase = base + 32;
+                const int64_t nnr = min((int64_t)32, cch1 - nbase);
+                if ((int64_t)lane < nnr) {  // prefetch the next round
+                    q0 = __ldg(ent4 + 2 * nbase + lane);
+                    q1 = __ldg(ent4 + 2 * nbase + nnr + lane);
+                }
+                if (valid) {
+                    const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    if constexpr (FMT == FMT_U16) {
+                        uint32_t cur = w[0] & 0x7FFFu;
+                        Acc s = lds_v<Acc, VSZ>(vbase + (w[0] >> 16) * VSZ);
+#pragma unroll
+                        for (int i = 1; i < 8; ++i) {
+                            const uint32_t lo = w[i] & 0xFFFFu;
+                            const uint32_t isk = lo & 0x8000u;
+                            const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (lo & 0x7FFFu) * VSZ);
+                            const Acc h = lds_v<Acc, VSZ>(vbase + (w[i] >> 16) * VSZ);
+                            if (isk) reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                            cur = isk ? (lo & 0x7FFFu) : cur;
+                            s = (isk ? (Acc)0 : s) + g + h;
+                        }
+                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                    } else {  // FMT_U32, register flush, v gathered from global scratch
+                        constexpr uint32_t KF = 1u << 31;
+                        uint32_t cur = w[0] & ~KF;
+                        Acc s = (Acc)__ldg(vglob + w[1]);
+#pragma unroll
+                        for (int i = 2; i < 8; i += 2) {
+                            const Acc h = (Acc)__ldg(vglob + w[i + 1]);
+                            if (w[i] & KF) {
+                                reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                                cur = w[i] & ~KF;
+                                s = (Acc)0;
+                            } else {
+                                s += (Acc)__ldg(vglob + w[i]);
+                            }
+                            s += h;
+                        }
+                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                    }
+                }
+                nr = nnr;
+            }
+            finish_cell(b, acc);
+        }
+    }
+}
+
+}  // namespace rsr
