@@ -141,10 +141,27 @@ rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtyp
  * +-127), exact int32 multiply, out[i] = f32(f64(y_i) * (beta / scale)).
  * Bit-identical to _native.fused_matvec (_native.py:339-353).  The
  * quantization is fused into every CTA's prologue (no separate pass).
- * scale_out (device f64, may be NULL) receives the activation scale.       */
+ * row_beta (device f64[m], may be NULL): per-row beta for stacked siblings
+ * (kernels.batched_preprocess, kernels.py:128-160) -- each sibling's rows get
+ * exactly its own f32(f64(y_i) * (beta_j / scale)).  out_dtype RSR_F32 or
+ * RSR_BF16 (bf16 = round-to-nearest-even of that f32).  scale_out (device
+ * f64, may be NULL) receives the activation scale.                         */
 rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtype,
-                            double beta, float *out, double *scale_out, void *workspace,
-                            size_t workspace_bytes, rsr_stream_t stream);
+                            double beta, const double *row_beta, void *out, int32_t out_dtype,
+                            double *scale_out, void *workspace, size_t workspace_bytes,
+                            rsr_stream_t stream);
+
+/* ---- device weight conversion ------------------------------------------------
+ * matcore.ternarize_weights + encode (matcore.py:151-173, :114-125) for a
+ * weight matrix already on the device (f32/bf16/f16, row-major rows x cols):
+ * *beta_out (device f64) = mean|w| (1.0 if zero); packed (device u8,
+ * rows x ceil(cols/4)) = 2-bit codes of clamp(round_half_away(w/beta), -1, 1).
+ * The |w| sum is a fixed-shape two-level reduction (deterministic; its
+ * rounding may differ from numpy's pairwise sum in the last bits).          */
+size_t rsr_ternarize_workspace_bytes(void);
+rsr_status rsr_ternarize_pack(const void *w, int32_t w_dtype, int64_t rows, int64_t cols,
+                              uint8_t *packed, double *beta_out, void *workspace,
+                              size_t workspace_bytes, rsr_stream_t stream);
 
 /* ---- helpers ---------------------------------------------------------------- */
 /* _native.count_ops (_native.py:288-307): out3 (device int64[3]) =

@@ -63,7 +63,9 @@ SIGNATURES = {
     "rsr_stream_build": (I32, [P, P, P, P, I64, I64, I32, I32, I32, P, P, P, P]),
     "rsr_matvec_workspace_bytes": (SZ, [ctypes.POINTER(StreamView)]),
     "rsr_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, P, I32, P, SZ, P]),
-    "rsr_fused_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, F64, P, P, P, SZ, P]),
+    "rsr_fused_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, F64, P, P, I32, P, P, SZ, P]),
+    "rsr_ternarize_workspace_bytes": (SZ, []),
+    "rsr_ternarize_pack": (I32, [P, I32, I64, I64, P, P, P, SZ, P]),
     "rsr_count_ops": (I32, [P, I64, P, P]),
     "rsr_absmax_quantize": (I32, [P, I32, I64, P, P, P]),
 }

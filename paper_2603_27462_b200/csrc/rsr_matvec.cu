@@ -22,7 +22,10 @@ __global__ void tile_finalize_kernel(MvParams p, int64_t rows_view) {
             int32_t *y = reinterpret_cast<int32_t *>(p.y);
             y[r] = p.accumulate ? y[r] + s : s;
         } else {
-            reinterpret_cast<float *>(p.y)[r] = (float)((double)s * (p.beta / *p.scale_dev));
+            const double beta = p.row_beta ? p.row_beta[p.blk0 * p.k + r] : p.beta;
+            const float o = (float)((double)s * (beta / *p.scale_dev));
+            if (p.out_bf16) reinterpret_cast<__nv_bfloat16 *>(p.y)[r] = __float2bfloat16_rn(o);
+            else reinterpret_cast<float *>(p.y)[r] = o;
         }
     }
 }
@@ -84,7 +87,8 @@ static size_t ws_bytes_for(const rsr_stream_view *vw) {
 template <int MODE>
 static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype, void *y,
                             int accumulate, double beta, double *scale_out, void *ws,
-                            size_t ws_bytes, cudaStream_t s) {
+                            size_t ws_bytes, cudaStream_t s, const double *row_beta = nullptr,
+                            int out_bf16 = 0) {
     rsr_status st = check_view(vw);
     if (st != RSR_OK) return st;
     if (!v || !y) return RSR_ERR_INVALID;
@@ -109,6 +113,8 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     p.accumulate = accumulate;
     p.part = ws;
     p.beta = beta;
+    p.row_beta = row_beta;
+    p.out_bf16 = out_bf16;
     p.scale_dev = scale_out;
     {
         static const int dbg = getenv("RSR_MV_DEBUG") ? atoi(getenv("RSR_MV_DEBUG")) : 0;
@@ -132,28 +138,51 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
                                                : pick_fmt2(MODE, vw->k);
     if (!fn) return RSR_ERR_INVALID;
 
-    // one persistent CTA per SM (per tile), as many warps as fit (<= 32) and needed
-    const int sms = sm_count();
+    // One persistent CTA per SM (per tile) with as many warps as fit and are
+    // needed.  Small matrices (few cells per SM) put a team of 2-8 warps on
+    // each cell so the whole grid stays busy.
+    static const int sms = sm_count();
     const int64_t tn = std::min(vw->tile_width, vw->n);
+    const bool ring = bucket && vw->format != FMT_U32;
     const size_t vsz = (vw->format == FMT_U16_SCALED || MODE == MODE_FLOAT) ? 4 : 1;
     const size_t kp = (size_t)((vw->k + 3) & ~3);
     size_t fixed = 0;
     if (vw->format != FMT_U32) fixed += ((size_t)tn * vsz + 15) & ~(size_t)15;
     if (bucket) fixed += (size_t)p.nkeys * kp * 4;
     size_t per_warp = bucket ? (size_t)p.nkeys * 4 : 0;
-    if (bucket && vw->format != FMT_U32) per_warp += RING_STAGES * (RING_STAGE_BYTES + 8);
+    if (ring) per_warp += RING_STAGES * (RING_STAGE_BYTES + 8) + 16 * 4;
     fixed += 16;  // alignment slack (mbarriers)
     const size_t smem_cap = 227 * 1024;
     const int64_t cells_per_tile = vw->n_blocks;
-    int64_t ctas_per_tile = std::max<int64_t>(1, sms / vw->tile_count);
-    int64_t warps = (cells_per_tile + ctas_per_tile - 1) / ctas_per_tile;
-    warps = std::max<int64_t>(1, std::min<int64_t>(warps, MV_MAX_WARPS));
-    while (warps > 1 && fixed + warps * per_warp > smem_cap) --warps;
+    const int64_t cta_cap = std::max<int64_t>(1, sms / vw->tile_count);
+    int team = 1;
+    if (ring) {
+        const int64_t est_rounds = std::max<int64_t>(1, (tn * 9 / 8 + 511) / 512);
+        while (team < 8 && cells_per_tile * team * 2 <= cta_cap * MV_MAX_WARPS &&
+               est_rounds >= 2 * team)
+            team *= 2;
+    }
+    int64_t warps = (cells_per_tile * team + cta_cap - 1) / cta_cap;
+    warps = (warps + team - 1) / team * team;
+    warps = std::max<int64_t>(team, std::min<int64_t>(warps, MV_MAX_WARPS / team * team));
+    while (warps > team && fixed + warps * per_warp > smem_cap) warps -= team;
     if (fixed + warps * per_warp > smem_cap) return RSR_ERR_INVALID;
     const size_t smem = fixed + warps * per_warp;
-    ctas_per_tile = std::min<int64_t>(ctas_per_tile, (cells_per_tile + warps - 1) / warps);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t teams_per_cta = warps / team;
+    const int64_t ctas_per_tile =
+        std::min<int64_t>(cta_cap, (cells_per_tile + teams_per_cta - 1) / teams_per_cta);
+    p.team = team;
+    {
+        // raise the dynamic-smem limit once per kernel (not on every launch)
+        static thread_local KernelFn last_fn[64];
+        static thread_local size_t last_smem[64];
+        const size_t slot = ((uintptr_t)fn >> 4) & 63;
+        if (smem > 48 * 1024 && (last_fn[slot] != fn || last_smem[slot] < smem)) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            last_fn[slot] = fn;
+            last_smem[slot] = smem;
+        }
+    }
     dim3 grid((unsigned)ctas_per_tile, (unsigned)vw->tile_count);
     fn<<<grid, (unsigned)(warps * 32), smem, s>>>(p);
     if (vw->tile_count > 1) {
@@ -190,12 +219,15 @@ rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtyp
 }
 
 rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtype,
-                            double beta, float *out, double *scale_out, void *workspace,
-                            size_t workspace_bytes, rsr_stream_t stream) {
+                            double beta, const double *row_beta, void *out, int32_t out_dtype,
+                            double *scale_out, void *workspace, size_t workspace_bytes,
+                            rsr_stream_t stream) {
     if (v_dtype != RSR_F32 && v_dtype != RSR_BF16 && v_dtype != RSR_F16) return RSR_ERR_INVALID;
+    if (out_dtype != RSR_F32 && out_dtype != RSR_BF16) return RSR_ERR_INVALID;
     if (view && view->bitwidth != RSR_TERNARY) return RSR_ERR_INVALID;
     return launch_mv<MODE_FUSED>(view, v, v_dtype, out, 0, beta, scale_out, workspace,
-                                 workspace_bytes, (cudaStream_t)stream);
+                                 workspace_bytes, (cudaStream_t)stream, row_beta,
+                                 out_dtype == RSR_BF16);
 }
 
 rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t *q,

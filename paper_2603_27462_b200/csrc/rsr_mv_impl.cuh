@@ -65,6 +65,9 @@ struct MvParams {
     double *scale_dev;   // fused: device scale slot (may be null when tc == 1)
     int dbg;             // experiment knobs (RSR_MV_DEBUG); 0 in production
     int pf;              // L2 prefetch distance in rounds (0 = off)
+    int team;            // warps per cell (ring path): 1, 2, 4 or 8
+    const double *row_beta;  // fused: per-row beta (sibling stacks), or null
+    int out_bf16;        // fused: write bf16 instead of f32
 };
 
 __device__ __forceinline__ float load_as_f32(const void *v, int dtype, int64_t i) {

@@ -37,6 +37,32 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return r;
 }
 
+// CTA-wide max of a per-thread double (result broadcast to every thread).
+__device__ __forceinline__ double cta_reduce_max(double a) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+        a = o > a ? o : a;
+    }
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red[warp] = a;
+    __syncthreads();
+    if (warp == 0) {
+        a = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+            a = o > a ? o : a;
+        }
+        if (threadIdx.x == 0) red[0] = a;
+    }
+    __syncthreads();
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
 constexpr int RING_STAGES = 4;     // rounds in flight per warp (bucket path)
 constexpr int RING_STAGE_BYTES = 1024;  // one round = 32 chunks x 32 bytes
 
@@ -72,33 +98,50 @@ rsr_mv_kernel(MvParams p) {
     if constexpr (BUCKET) off += (size_t)p.nkeys * KP * sizeof(Acc);
     Acc *__restrict__ buckets = reinterpret_cast<Acc *>(mv_smem + off);
     if constexpr (BUCKET) off += (size_t)nwarps * p.nkeys * sizeof(Acc);
+    Acc *__restrict__ xch = reinterpret_cast<Acc *>(mv_smem + off);  // team exchange [W][16]
+    if constexpr (RING) off += (size_t)nwarps * 16 * sizeof(Acc);
     off = (off + 7) & ~(size_t)7;
     uint64_t *bars = reinterpret_cast<uint64_t *>(mv_smem + off) + (size_t)warp * S;
-    Acc *__restrict__ bk = buckets + (size_t)warp * p.nkeys;
+    Acc *bk = buckets + (size_t)warp * p.nkeys;
     const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
-    const uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
+    uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
     const uint32_t ringbase =
         (uint32_t)__cvta_generic_to_shared(ringsm) + (uint32_t)(warp * S * RING_STAGE_BYTES);
     const uint32_t barbase = (uint32_t)__cvta_generic_to_shared(bars);
 
-    int64_t b = (int64_t)blockIdx.x * nwarps + warp;
+    // Teams (ring path): `team` consecutive warps share one cell; warp `sub`
+    // of the team takes rounds sub, sub+team, ... with its own buckets, and
+    // the team's k-row partials are combined in a fixed order at the end.
+    const int team = RING ? p.team : 1;
+    const int tpc = nwarps / team;               // teams per CTA
+    const int tid_team = warp / team, sub = warp % team;
+    int64_t b = RING ? (int64_t)blockIdx.x * tpc + tid_team : (int64_t)blockIdx.x * nwarps + warp;
+    const int64_t cstride = RING ? (int64_t)gridDim.x * tpc : bstride;
+    // Integer paths flush with native shared atomics, so a team shares one set
+    // of buckets and splits the pattern-table reduction; the float path keeps
+    // per-warp buckets (plain read-modify-write flushes).
+    const bool shbk = RING && MODE != MODE_FLOAT && team > 1;
+    if (shbk) {
+        bk = buckets + (size_t)(tid_team * team) * p.nkeys;
+        bkbase = (uint32_t)__cvta_generic_to_shared(bk);
+    }
 
     // ---- stream producer (lane 0 of each warp feeds its own ring) -----------
-    // Walks this warp's cells (b, b + bstride, ...) round by round, S rounds
+    // Walks this warp's rounds of its cells (b, b + cstride, ...), S rounds
     // ahead of the consumer; each round is one 1-D bulk copy (TMA) into a
     // 1 KiB stage whose mbarrier completes on the transaction bytes.
     int64_t pb = b, pbase = 0, pend = 0;
     if (RING && lane == 0 && pb < p.nblk) {
         const int64_t dc = pb * p.tc + t;
-        pbase = p.e_off[dc] / CH;
+        pbase = p.e_off[dc] / CH + 32 * sub;
         pend = p.e_off[dc + 1] / CH;
     }
     auto produce = [&](int stage) {
         while (pb < p.nblk && pbase >= pend) {
-            pb += bstride;
+            pb += cstride;
             if (pb < p.nblk) {
                 const int64_t dc = pb * p.tc + t;
-                pbase = p.e_off[dc] / CH;
+                pbase = p.e_off[dc] / CH + 32 * sub;
                 pend = p.e_off[dc + 1] / CH;
             }
         }
@@ -107,7 +150,7 @@ rsr_mv_kernel(MvParams p) {
         const uint32_t bar = barbase + stage * 8;
         mbar_expect_tx(bar, bytes);
         bulk_g2s(ringbase + stage * RING_STAGE_BYTES, ent4 + 2 * pbase, bytes, bar);
-        pbase += 32;
+        pbase += 32 * team;
     };
     if constexpr (RING) {
         if (lane == 0) {
@@ -122,17 +165,40 @@ rsr_mv_kernel(MvParams p) {
 
     // ---- prologue -------------------------------------------------------
     double scale = 1.0;
-    if constexpr (MODE == MODE_FUSED) {
-        if constexpr (SMEM_V) {
-            const double amax = cta_absmax_fast(p.v, p.vdtype, p.n);
+    // Fused path with one tile and 4-byte staging: a single pass over v stages
+    // it as f32 while tracking |v|max, then quantizes in place.
+    bool staged = false;
+    if constexpr (MODE == MODE_FUSED && SMEM_V && VSZ == 4) {
+        if (p.tc == 1) {
+            double a = 0.0;
+            for_each_v(p.v, p.vdtype, 0, tn, [&](int64_t i, float x) {
+                reinterpret_cast<float *>(vsm)[i] = x;
+                const double ax = fabs((double)x);
+                a = ax > a ? ax : a;
+            });
+            const double amax = cta_reduce_max(a);
             scale = amax == 0.0 ? 1.0 : 127.0 / amax;
+            for (int64_t i = threadIdx.x; i < tn; i += blockDim.x)  // same thread wrote i
+                reinterpret_cast<int32_t *>(vsm)[i] =
+                    quantize_one(reinterpret_cast<float *>(vsm)[i], scale);
             if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
                 *p.scale_dev = scale;
-        } else {
-            scale = *p.scale_dev;  // written by the staging kernel
+            staged = true;
         }
     }
-    if constexpr (SMEM_V) {
+    if constexpr (MODE == MODE_FUSED) {
+        if (!staged) {
+            if constexpr (SMEM_V) {
+                const double amax = cta_absmax_fast(p.v, p.vdtype, p.n);
+                scale = amax == 0.0 ? 1.0 : 127.0 / amax;
+                if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+                    *p.scale_dev = scale;
+            } else {
+                scale = *p.scale_dev;  // written by the staging kernel
+            }
+        }
+    }
+    if (!staged) if constexpr (SMEM_V) {
         if constexpr (MODE == MODE_FLOAT) {
             for_each_v(p.v, p.vdtype, c0, tn,
                        [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
@@ -172,7 +238,13 @@ rsr_mv_kernel(MvParams p) {
     auto finish_cell = [&](int64_t bb, Acc (&acc)[K]) {
         // y_i = sum_key sgn_i(key) * bucket[key]  (bucket 0 collects padding)
         if constexpr (BUCKET) {
-            for (int key = lane; key < p.nkeys; key += 32) {
+            int kfirst = (int)lane, kstep = 32;
+            if (shbk) {  // whole team has flushed; split the keys across it
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + tid_team), "r"(team * 32) : "memory");
+                kfirst += 32 * sub;
+                kstep *= team;
+            }
+            for (int key = kfirst; key < p.nkeys; key += kstep) {
                 const Acc bv = key ? bk[key] : (Acc)0;
                 bk[key] = (Acc)0;
                 const Acc *row = stab + key * KP;
@@ -189,6 +261,17 @@ rsr_mv_kernel(MvParams p) {
             const Acc r = warp_sum(acc[i]);
             if (lane == (uint32_t)i) mine = r;
         }
+        if (team > 1) {
+            // combine the team's partials in warp order (deterministic)
+            if (lane < (uint32_t)K) xch[warp * 16 + lane] = mine;
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + tid_team), "r"(team * 32) : "memory");
+            if (sub == 0 && lane < (uint32_t)K) {
+                mine = (Acc)0;
+                for (int j = 0; j < team; ++j) mine += xch[(tid_team * team + j) * 16 + lane];
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + tid_team), "r"(team * 32) : "memory");
+            if (sub != 0) return;
+        }
         if (lane < (uint32_t)K && grow0 + lane < p.m_rows) {
             const int64_t r = row0 + lane;
             if (p.tc > 1) {
@@ -201,8 +284,10 @@ rsr_mv_kernel(MvParams p) {
                 int32_t *y = reinterpret_cast<int32_t *>(p.y);
                 y[r] = p.accumulate ? y[r] + (int32_t)mine : (int32_t)mine;
             } else {
-                reinterpret_cast<float *>(p.y)[r] =
-                    (float)((double)(int32_t)mine * (p.beta / scale));
+                const double beta = p.row_beta ? p.row_beta[grow0 + lane] : p.beta;
+                const float o = (float)((double)(int32_t)mine * (beta / scale));
+                if (p.out_bf16) reinterpret_cast<__nv_bfloat16 *>(p.y)[r] = __float2bfloat16_rn(o);
+                else reinterpret_cast<float *>(p.y)[r] = o;
             }
         }
     };
@@ -220,13 +305,13 @@ rsr_mv_kernel(MvParams p) {
         auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
         auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
         int64_t it = 0;  // rounds consumed by this warp (ring position)
-        for (; b < p.nblk; b += bstride) {
+        for (; b < p.nblk; b += cstride) {
             const int64_t dc = b * p.tc + t;
             const int64_t ch0 = p.e_off[dc] / CH, ch1 = p.e_off[dc + 1] / CH;
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            for (int64_t base = ch0; base < ch1; base += 32, ++it) {
+            for (int64_t base = ch0 + 32 * sub; base < ch1; base += 32 * team, ++it) {
                 const int stage = (int)(it % S);
                 mbar_wait(barbase + stage * 8, (uint32_t)((it / S) & 1));
                 const uint32_t nr = (uint32_t)min((int64_t)32, ch1 - base);

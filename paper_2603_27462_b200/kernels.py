@@ -59,8 +59,11 @@ def _count(a: RsrArtifact, counter: OpCounter | None):
 
 
 class _Workspace:
-    """Per-device scratch for tile partials (grown on demand, reused)."""
+    """Per-device scratch for tile partials (grown on demand, reused).
+
+    Superseded buffers are kept alive: launch states cache raw pointers."""
     _bufs: dict = {}
+    _retired: list = []
 
     @classmethod
     def get(cls, device, nbytes: int):
@@ -70,7 +73,9 @@ class _Workspace:
         key = str(device)
         b = cls._bufs.get(key)
         if b is None or b.numel() < nbytes:
-            b = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            if b is not None:
+                cls._retired.append(b)
+            b = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
             cls._bufs[key] = b
         return b, nbytes
 
@@ -103,36 +108,56 @@ def _prepare_vec(a: RsrArtifact, v):
     return t.contiguous(), False
 
 
+class _ViewLaunch:
+    """Per-view launch state cached on first use (ctypes byref + workspace)."""
+    __slots__ = ("ref", "ws", "wsb")
+
+    def __init__(self, a: RsrArtifact, vw):
+        import ctypes
+        self.ref = ctypes.byref(vw)
+        wsb = int(_lib.lib().rsr_matvec_workspace_bytes(self.ref))
+        ws, self.wsb = _Workspace.get(a.device, wsb)
+        self.ws = _lib.ptr(ws)
+
+
+def _launch_state(a: RsrArtifact, view) -> _ViewLaunch:
+    vw = a._view if view is None else view
+    cache = a.__dict__.setdefault("_launch_cache", {})
+    st = cache.get(id(vw))
+    if st is None or st.ref._obj is not vw:
+        st = _ViewLaunch(a, vw)
+        cache[id(vw)] = st
+    return st
+
+
 def matvec_into(a: RsrArtifact, vt, y, accumulate: bool = False, view=None, stream=None):
     """Launch the multiply on device tensors: y (+)= A.v (no checks, no sync).
 
     vt: int8 -> y int32; float32/bfloat16/float16 -> y float32.
     """
     from .matcore import _dtype_code
-    vw = a._view if view is None else view
-    L = _lib.lib()
-    import ctypes
-    wsb = int(L.rsr_matvec_workspace_bytes(ctypes.byref(vw)))
-    ws, wsb = _Workspace.get(a.device, wsb)
+    st = _launch_state(a, view)
     s = _lib.current_stream_ptr(a.device) if stream is None else stream
-    _lib.check(L.rsr_matvec(ctypes.byref(vw), _lib.ptr(vt), _dtype_code(vt), _lib.ptr(y),
-                            int(accumulate), _lib.ptr(ws), wsb, s), "rsr_matvec")
+    _lib.check(_lib.lib().rsr_matvec(st.ref, vt.data_ptr(), _dtype_code(vt), y.data_ptr(),
+                                     int(accumulate), st.ws, st.wsb, s), "rsr_matvec")
     return y
 
 
 def fused_into(a: RsrArtifact, vt, out, beta: float | None = None, view=None, stream=None,
-               scale_out=None):
-    """Launch the fused quantize/multiply/dequantize kernel on device tensors."""
+               scale_out=None, row_beta=None):
+    """Launch the fused quantize/multiply/dequantize kernel on device tensors.
+
+    out: float32 or bfloat16.  row_beta: optional float64 device tensor of
+    per-row betas (stacked siblings)."""
+    import torch
     from .matcore import _dtype_code
-    import ctypes
-    vw = a._view if view is None else view
-    L = _lib.lib()
-    wsb = int(L.rsr_matvec_workspace_bytes(ctypes.byref(vw)))
-    ws, wsb = _Workspace.get(a.device, wsb)
+    st = _launch_state(a, view)
     s = _lib.current_stream_ptr(a.device) if stream is None else stream
     b = float(a.weight_scale) if beta is None else float(beta)
-    _lib.check(L.rsr_fused_matvec(ctypes.byref(vw), _lib.ptr(vt), _dtype_code(vt), b,
-                                  _lib.ptr(out), _lib.ptr(scale_out), _lib.ptr(ws), wsb, s),
+    odt = _lib.RSR_BF16 if out.dtype == torch.bfloat16 else _lib.RSR_F32
+    _lib.check(_lib.lib().rsr_fused_matvec(st.ref, vt.data_ptr(), _dtype_code(vt), b,
+                                           _lib.ptr(row_beta), out.data_ptr(), odt,
+                                           _lib.ptr(scale_out), st.ws, st.wsb, s),
                "rsr_matvec_fused")
     return out
 

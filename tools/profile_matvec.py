@@ -13,7 +13,11 @@ import paper_2603_27462_b200 as rsr
 from paper_2603_27462_b200 import kernels as kn
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
-cfg = dict(bench.CONFIGS[cfgname])
+if cfgname.startswith("mn"):  # e.g. mn2560x2560 -> ternary m x n, bf16 v
+    mm, nn = (int(x) for x in cfgname[2:].split("x"))
+    cfg = dict(workload="custom", m=mm, n=nn, bitwidth="ternary", k=5, vdtype="bf16")
+else:
+    cfg = dict(bench.CONFIGS[cfgname])
 if len(sys.argv) > 2:
     cfg["k"] = int(sys.argv[2])
 mode = sys.argv[3] if len(sys.argv) > 3 else "float"
