@@ -161,6 +161,7 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
         while (team < 8 && cells_per_tile * team * 2 <= cta_cap * MV_MAX_WARPS &&
                est_rounds >= 2 * team)
             team *= 2;
+        while (team > 1 && fixed + team * per_warp > smem_cap) team /= 2;
     }
     int64_t warps = (cells_per_tile * team + cta_cap - 1) / cta_cap;
     warps = (warps + team - 1) / team * team;

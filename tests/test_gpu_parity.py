@@ -27,17 +27,12 @@ def float_ok(y, ref_f64, dense, v):
     return np.abs(y.astype(np.float64) - ref_f64) <= FLOAT_RTOL * cond + FLOAT_RTOL * np.abs(ref_f64)
 
 
-def _golden_usable(md):
-    tw = md["tile_width"] or (md["n"] if md["n"] <= 65536 else 32768)
-    return tw <= 32768
 
 
 @pytest.mark.parametrize("i", range(19))
 def test_preprocess_bit_exact_vs_reference(rsr, i):
     case = gd.small_case(i)
     md = case["meta"]
-    if not _golden_usable(md):
-        pytest.skip("tile wider than 32768 columns (see DESIGN.md)")
     m = rsr.PackedMatrix(md["m"], md["n"], md["bitwidth"], case["data"], md["weight_scale"])
     a = rsr.preprocess(m, md["k"], md["tile_width"])
     assert np.array_equal(a.words, case["words"])
@@ -54,8 +49,6 @@ def test_preprocess_bit_exact_vs_reference(rsr, i):
 def test_multiply_vs_reference(rsr, i):
     case = gd.small_case(i)
     md = case["meta"]
-    if not _golden_usable(md):
-        pytest.skip("tile wider than 32768 columns (see DESIGN.md)")
     m = rsr.PackedMatrix(md["m"], md["n"], md["bitwidth"], case["data"], md["weight_scale"])
     a = rsr.preprocess(m, md["k"], md["tile_width"])
     y = rsr.rsr_matvec(a, case["vi"])
@@ -103,6 +96,8 @@ def test_zero_matrix(rsr):
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("bw", ["binary", "ternary"])
 def test_random_shapes_vs_oracle(rsr, seed, bw):
+    """Random shapes/k/tile widths: every stream format (scaled u16, u16,
+    u32) and both flush variants (pattern buckets, register flush)."""
     rng = np.random.default_rng(100 + seed)
     m_, n_ = int(rng.integers(1, 300)), int(rng.integers(1, 3000))
     k = int(rng.integers(1, (16 if bw == "binary" else 10) + 1))
@@ -170,3 +165,25 @@ def test_c2_full_size_bit_exact_vs_reference(rsr):
     assert float_ok(y, yr, orc.decode(p), vr).all()
     assert np.array_equal(rsr.rsr_matvec_fused(a, vb).cpu().numpy(),
                           gd.large_output(name + "_fused_bf16v"))
+
+
+@pytest.mark.parametrize("n,tw,k,bw", [(40000, None, 5, "ternary"), (65536, None, 4, "binary"),
+                                       (70000, None, 6, "ternary"), (30000, 20000, 7, "ternary"),
+                                       (3000, None, 9, "ternary"), (2000, None, 13, "binary"),
+                                       (5000, 2500, 10, "ternary"), (1000, None, 16, "binary")])
+def test_wide_tiles_and_large_k(rsr, n, tw, k, bw):
+    """Tiles wider than 32768 columns (u32 stream) and pattern spaces too big
+    for shared-memory buckets (register flush), bit-exact on the int paths."""
+    rng = np.random.default_rng(n + k)
+    m_ = 3 * k + 1
+    p = orc.random_matrix(m_, n, bw, k)
+    ref = orc.preprocess(p, k, tw)
+    a = rsr.preprocess(rsr.PackedMatrix(m_, n, bw, p.data, 0.7), k, tw)
+    assert np.array_equal(a.words, ref.words) and np.array_equal(a.perm, ref.perm)
+    vi = rng.integers(-128, 128, n).astype(np.int8)
+    assert np.array_equal(rsr.rsr_matvec(a, vi), orc.matvec_i8(ref, vi))
+    vf = rng.standard_normal(n).astype(np.float32)
+    assert float_ok(rsr.rsr_matvec(a, vf), orc.matvec_f64(ref, vf), orc.decode(p), vf).all()
+    if bw == "ternary":
+        ref.weight_scale = 0.7
+        assert np.array_equal(rsr.rsr_matvec_fused(a, vf), orc.fused_matvec(ref, vf))
