@@ -163,6 +163,13 @@ rsr_status rsr_ternarize_pack(const void *w, int32_t w_dtype, int64_t rows, int6
                               uint8_t *packed, double *beta_out, void *workspace,
                               size_t workspace_bytes, rsr_stream_t stream);
 
+/* Synthetic ternary rows [row0, row0+rows) of a cols-wide matrix, packed, for
+ * configs too large for the reference's numpy generator (C5, 131072^2):
+ * entry (r, c) = +1/-1/0 with p = density/2, density/2, 1-density from
+ * splitmix64(seed, r, c).  Restated in oracle/rsr_oracle.c for CPU checks.  */
+rsr_status rsr_random_ternary(int64_t row0, int64_t rows, int64_t cols, uint64_t seed,
+                              double density, uint8_t *packed, rsr_stream_t stream);
+
 /* ---- helpers ---------------------------------------------------------------- */
 /* _native.count_ops (_native.py:288-307): out3 (device int64[3]) =
  * gather adds, scatter adds, groups.                                         */

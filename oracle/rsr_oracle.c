@@ -335,3 +335,37 @@ int oracle_max_threads(void)
     return 1;
 #endif
 }
+
+/* Counter-based synthetic ternary rows (the device generator of
+ * paper_2603_27462_b200/csrc/rsr_pack.cu, restated for sampled-strip checks
+ * of the C5 config; not a reference function). */
+static inline uint64_t splitmix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+void oracle_random_ternary_rows(int64_t row0, int64_t rows, int64_t cols, uint64_t seed,
+                                double density, uint8_t *out)
+{
+    const int64_t row_bytes = (cols + 3) / 4;
+    const uint64_t thr_half = (uint64_t)(density / 2.0 * 9007199254740992.0);
+    const uint64_t base = splitmix64(seed);
+    for (int64_t r = 0; r < rows; ++r) {
+        const uint64_t rowkey = splitmix64(base ^ (uint64_t)(row0 + r));
+        for (int64_t b = 0; b < row_bytes; ++b) {
+            uint32_t byte = 0;
+            for (int j = 0; j < 4; ++j) {
+                const int64_t c = b * 4 + j;
+                if (c < cols) {
+                    const uint64_t h = splitmix64(rowkey + (uint64_t)c) >> 11;
+                    const uint32_t code = h < thr_half ? 1u : (h >= (1ull << 53) - thr_half ? 2u : 0u);
+                    byte |= code << (2 * j);
+                }
+            }
+            out[r * row_bytes + b] = (uint8_t)byte;
+        }
+    }
+}

@@ -94,3 +94,52 @@ rsr_status rsr_ternarize_pack(const void *w, int32_t w_dtype, int64_t rows, int6
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Counter-based synthetic ternary generator for matrices too large for the
+// reference's numpy generator (C5: 131072^2).  Entry (r, c) is +1 / -1 / 0
+// with probabilities density/2, density/2, 1-density, decided by
+// splitmix64(seed, r, c) -- restated bit-for-bit in oracle/rsr_oracle.c
+// (oracle_random_ternary_rows) so sampled row strips can be checked on CPU.
+namespace rsr {
+__device__ __host__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__global__ void random_ternary_kernel(int64_t row0, int64_t rows, int64_t cols, int64_t row_bytes,
+                                      uint64_t seed, uint64_t thr_half, uint8_t *out) {
+    const int64_t total = rows * row_bytes;
+    const uint64_t base = splitmix64(seed);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / row_bytes, cb = (i - r * row_bytes) * 4;
+        const uint64_t rowkey = splitmix64(base ^ (uint64_t)(row0 + r));
+        uint32_t byte = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t c = cb + j;
+            if (c < cols) {
+                const uint64_t h = splitmix64(rowkey + (uint64_t)c) >> 11;  // 53-bit uniform
+                const uint32_t code = h < thr_half ? 1u : (h >= (1ull << 53) - thr_half ? 2u : 0u);
+                byte |= code << (2 * j);
+            }
+        }
+        out[i] = (uint8_t)byte;
+    }
+}
+}  // namespace rsr
+
+extern "C" rsr_status rsr_random_ternary(int64_t row0, int64_t rows, int64_t cols, uint64_t seed,
+                                         double density, uint8_t *packed, rsr_stream_t stream) {
+    if (!packed || rows < 1 || cols < 1 || !(density >= 0.0 && density <= 1.0))
+        return RSR_ERR_INVALID;
+    const int64_t row_bytes = (cols + 3) / 4;
+    const uint64_t thr_half = (uint64_t)(density / 2.0 * 9007199254740992.0);  // * 2^53
+    const int64_t total = rows * row_bytes;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)rsr::sm_count() * 32);
+    rsr::random_ternary_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(row0, rows, cols, row_bytes,
+                                                                        seed, thr_half, packed);
+    return rsr::launch_status();
+}

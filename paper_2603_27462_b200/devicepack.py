@@ -14,6 +14,20 @@ from .errors import DimensionMismatch, NonFinite
 from .matcore import TERNARY, PackedMatrix, _dtype_code
 
 
+def random_ternary_device(rows: int, cols: int, seed: int, density: float = 0.5, row0: int = 0,
+                          device=None) -> PackedMatrix:
+    """Rows [row0, row0+rows) of the counter-based synthetic ternary matrix,
+    generated and packed on the device (C5-scale inputs; see
+    rsr_random_ternary in include/rsr_b200.h)."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+        else torch.device(device)
+    packed = torch.empty(rows, (cols + 3) // 4, dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib().rsr_random_ternary(row0, rows, cols, seed, density, packed.data_ptr(),
+                                             _lib.current_stream_ptr(dev)), "random_ternary")
+    return PackedMatrix(rows, cols, TERNARY, packed)
+
+
 def ternarize_pack_device(w, check_finite: bool = True) -> PackedMatrix:
     import torch
     if w.dim() != 2:
