@@ -1,16 +1,22 @@
 """Benchmark of the RSR hot path on B200 (driver contract: one JSON line).
 
-Default workload (N=1): BASELINE config 1 -- ternary 16384x16384 RSR matvec,
-bf16 vector, k=6 (the k with the fewest artifact bytes), seed 0, matrix from
-the reference generator (bench.py:102-113 of rsrmv).  A "step" is one
-single-vector multiply.  ``value`` is matvecs/s with the artifact resident
-in HBM; L2 is defeated by rotating >= 3 artifact copies (each ~92 MB, L2 is
-126 MB).  ``e2e`` is the same metric through the public API with a host
-(numpy float32) vector and a host result.
+Workloads (BASELINE.json configs):
+  c2  (default at N=1) ternary 16384x16384 single-vector RSR matvec, bf16
+      vector, k=6 (fewest artifact bytes); matrix = reference generator
+      (rsrmv bench.py:102-113), seed 0.  A step is one matvec.
+  c5  (default at N>1) ternary 131072x131072, k=6, row-block sharded across
+      the ranks (each rank generates and preprocesses only its strip with the
+      device generator) + NCCL all-gather of the output slices.  Strong
+      scaling: every step is one full 131072^2 matvec for the whole job.
+  c1, c4 (binary 4096^2 k=8 f32 vector; ternary 8192^2 k=5) on request.
 
---gpus N > 1 (torchrun): the same matrix is row-block sharded (balanced by
-stream bytes) and each step ends with an NCCL all-gather of the output
-slices (strong scaling).  --impl reference times the CPU restatement of the
+`value` = matvec/s with the stream resident in HBM; L2 is defeated by
+rotating >= 3 copies of the stream (inputs larger than L2 per step).  `e2e` =
+the same metric through the public API with a host (numpy float32) vector
+and a host result (rank 0, unsharded configs).  `decode` (N=1) = greedy
+decode tok/s of BitNetForCausalLM(BitNetConfig()) with the HF linear
+replacement vs the same model with dense bf16 nn.Linear (cuBLAS), identical
+graph-captured loop.  --impl reference times the CPU restatement of the
 reference float path (oracle/, all host cores) on the same config.
 """
 
@@ -31,13 +37,16 @@ if ROOT not in sys.path:
 
 CONFIGS = {
     "c2": dict(workload="ternary 16384x16384 RSR matvec, bf16 vector, single vector",
-               m=16384, n=16384, bitwidth="ternary", k=6, vdtype="bf16"),
+               m=16384, n=16384, bitwidth="ternary", k=6, vdtype="bf16", gen="numpy"),
     "c1": dict(workload="binary 4096x4096 RSR matvec, fp32 vector, k=8",
-               m=4096, n=4096, bitwidth="binary", k=8, vdtype="f32"),
+               m=4096, n=4096, bitwidth="binary", k=8, vdtype="f32", gen="numpy"),
     "c4": dict(workload="ternary 8192x8192 RSR matvec, bf16 vector, single vector",
-               m=8192, n=8192, bitwidth="ternary", k=5, vdtype="bf16"),
+               m=8192, n=8192, bitwidth="ternary", k=5, vdtype="bf16", gen="numpy"),
+    "c5": dict(workload="ternary 131072x131072 RSR matvec, bf16 vector, row-block sharded "
+                        "+ NCCL all-gather of outputs",
+               m=131072, n=131072, bitwidth="ternary", k=6, vdtype="bf16", gen="hash"),
 }
-METRIC = "ternary matvec/s & %HBM roofline at 16384^2"
+METRIC = "ternary matvec/s & %HBM roofline at 16384^2; BitNet-2B-shape decode tok/s"
 UNIT = "matvec/s"
 
 
@@ -63,6 +72,11 @@ def random_vector(n, seed):
     return np.random.default_rng(seed ^ 0x5EED).standard_normal(n).astype(np.float32)
 
 
+def bf16_round(v):
+    b = v.view(np.uint32).astype(np.uint64)
+    return ((((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16).astype(np.uint32)).view(np.float32)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -82,6 +96,7 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index = index
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -94,7 +109,6 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
@@ -108,12 +122,12 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             try:
                 sm.append(float(f[0]))
                 mx = max(mx, float(f[1]))
-            except ValueError:
+            except (ValueError, IndexError):
                 continue
             for nm, val in zip(names, f[2:]):
                 if val.lower().startswith("active"):
@@ -122,17 +136,26 @@ class ClockSampler:
                 "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle/ = C restatement of the reference float path)
+
 def cpu_reference_run(cfg, steps, warmup, seconds=None):
-    """Time the CPU restatement of the reference float path (oracle/, all
-    host threads; float64 accumulation exactly as rsrmv matvec_f32)."""
+    """Matvec/s of the reference float path (float64 accumulation, exactly
+    rsrmv matvec_f32) on all host threads.  For c5 the sample is one row
+    strip (the whole matrix does not fit the host); the rate is scaled to the
+    full matrix by rows."""
     from oracle import rsr_oracle as orc
-    data = random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0)
-    p = orc.Packed(cfg["m"], cfg["n"], cfg["bitwidth"], data)
+    rows = cfg["m"]
+    if cfg["gen"] == "hash":
+        rows = 1200
+        p = orc.random_ternary_rows(0, rows, cfg["n"], 0, 0.5)
+    else:
+        p = orc.Packed(cfg["m"], cfg["n"], cfg["bitwidth"],
+                       random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0))
     a = orc.preprocess(p, cfg["k"])
     v = random_vector(cfg["n"], 0)
     if cfg["vdtype"] == "bf16":
-        b = v.view(np.uint32).astype(np.uint64)
-        v = ((((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16).astype(np.uint32)).view(np.float32)
+        v = bf16_round(v)
     threads = orc.max_threads()
     for _ in range(max(warmup, 1)):
         orc.matvec_f32(a, v, threads=threads)
@@ -144,8 +167,49 @@ def cpu_reference_run(cfg, steps, warmup, seconds=None):
         el = time.perf_counter() - t0
         if (seconds is None and n >= steps) or (seconds is not None and el >= seconds):
             break
-    return n / el, threads, n, el
+    frac = rows / cfg["m"]
+    rate = n / el * frac
+    sample = (f"{n} {'strip (' + str(rows) + ' rows) ' if frac < 1 else ''}"
+              f"{rows}x{cfg['n']} float-path matvecs in {el:.1f}s on {threads} threads "
+              f"(C restatement of rsrmv matvec_f32, block-parallel, float64 accumulation)"
+              + (f"; rate scaled by rows to the full {cfg['m']}x{cfg['n']}" if frac < 1 else ""))
+    return rate, threads, n, el, sample
 
+
+# ---------------------------------------------------------------------------
+# decode sub-benchmark (C3)
+
+def decode_bench(steps=64, k=5):
+    import torch
+    from transformers import BitNetConfig, BitNetForCausalLM
+    from paper_2603_27462_b200.decode import GraphDecoder
+    from paper_2603_27462_b200.hf import replace_linear_with_rsr
+    torch.manual_seed(0)
+    cfg = BitNetConfig()
+    cfg._attn_implementation = "sdpa"
+    with torch.device("cuda"):
+        model = BitNetForCausalLM(cfg).to(torch.bfloat16).eval()
+    prompt = torch.randint(0, cfg.vocab_size, (1, 16), device="cuda")
+    res = {}
+    for name in ("dense_bf16_cublas", "rsr"):
+        if name == "rsr":
+            replace_linear_with_rsr(model, k=k)
+        dec = GraphDecoder(model, max_len=16 + steps + 8)
+        dec.prefill(prompt)
+        dec.capture()
+        dec.time_steps(prompt, 8)
+        res[name] = steps / dec.time_steps(prompt, steps)
+        del dec
+        torch.cuda.empty_cache()
+    return {"model": "BitNetForCausalLM(BitNetConfig()) random init, bf16, 30 layers, "
+                     "hidden 2560, FFN 6912",
+            "loop": "greedy, HF StaticCache, one CUDA graph per step, batch 1",
+            "k": k, "steps": steps, "rsr_tok_s": res["rsr"],
+            "dense_tok_s": res["dense_bf16_cublas"],
+            "speedup": res["rsr"] / res["dense_bf16_cublas"]}
+
+
+# ---------------------------------------------------------------------------
 
 def main():
     ap = argparse.ArgumentParser()
@@ -153,37 +217,38 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
     args = ap.parse_args()
-    cfg = dict(CONFIGS[args.config])
-    if args.k:
-        cfg["k"] = args.k
-    warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-
-    config = {"workload": cfg["workload"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
-              "bitwidth": cfg["bitwidth"], "vector_dtype": cfg["vdtype"], "seed": 0,
-              "density": 0.5}
+    cname = args.config or ("c2" if world == 1 else "c5")
+    cfg = dict(CONFIGS[cname])
+    if args.k:
+        cfg["k"] = args.k
+    warmup = max(args.warmup, 3)
+    config = {"workload": cfg["workload"], "name": cname, "m": cfg["m"], "n": cfg["n"],
+              "k": cfg["k"], "bitwidth": cfg["bitwidth"], "vector_dtype": cfg["vdtype"],
+              "seed": 0, "density": 0.5,
+              "generator": "rsrmv random_matrix (numpy)" if cfg["gen"] == "numpy"
+              else "counter-based splitmix64 (device; CPU restatement in oracle/)"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        val, threads, n, el = cpu_reference_run(cfg, args.steps, warmup)
+        val, threads, n, el, sample = cpu_reference_run(cfg, args.steps, warmup)
         line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": n, "warmup": warmup, "ms_per_step": 1e3 * el / n,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic (rsrmv random_matrix seed 0)",
+                "steps": n, "warmup": warmup, "ms_per_step": 1e3 / val,
+                "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config, "impl": "reference",
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-                                 "sample": f"{n} full {cfg['m']}x{cfg['n']} float-path "
-                                           f"matvecs (C restatement of rsrmv matvec_f32, "
-                                           f"block-parallel, float64 accumulation)"},
+                                 "sample": sample},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -192,7 +257,8 @@ def main():
     import torch
     import paper_2603_27462_b200 as rsr
     from paper_2603_27462_b200 import kernels as kn
-    from paper_2603_27462_b200 import _lib
+    from paper_2603_27462_b200 import shard
+    from paper_2603_27462_b200.devicepack import random_ternary_device
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -201,53 +267,39 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    data = random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0)
-    mat = rsr.PackedMatrix(cfg["m"], cfg["n"], cfg["bitwidth"], data)
+    m, n, k = cfg["m"], cfg["n"], cfg["k"]
+    if cfg["gen"] == "numpy":
+        full = random_packed(m, n, cfg["bitwidth"], 0)
+        strip = lambda r0, r1: rsr.PackedMatrix(r1 - r0, n, cfg["bitwidth"], full[r0:r1])
+    else:
+        strip = lambda r0, r1: random_ternary_device(r1 - r0, n, 0, 0.5, row0=r0, device=dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    a = rsr.preprocess(mat, cfg["k"])
+    sm = shard.ShardedMatrix(m, n, cfg["bitwidth"], k, strip, rank, world, device=dev)
     torch.cuda.synchronize()
     preprocess_ms = 1e3 * (time.perf_counter() - t0)
-    del data
+    a = sm.local
+    nb = a.plan.block_count
 
-    # ---- shard by stream bytes (row blocks), one contiguous range per rank
-    bc = a.plan.block_count
-    if world > 1:
-        e_off = a.e_off_d.cpu().numpy()
-        tc = a.plan.tile_count
-        cum = e_off[::tc]  # entry offset at the start of each block
-        bounds = [0] + [int(np.searchsorted(cum, cum[-1] * r / world)) for r in range(1, world)] + [bc]
-        b0, b1 = bounds[rank], bounds[rank + 1]
-    else:
-        b0, b1 = 0, bc
-    nb = b1 - b0
-    k = cfg["k"]
-    rows_per_rank = -(-bc // world) * k  # padded slice for the all-gather
-
-    # ---- L2 defeat: rotate copies of the stream arrays
+    # L2 defeat: rotate copies of the local stream
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    sb = a.stream_bytes() * nb // max(bc, 1)
+    sb = a.stream_bytes()
     ncopies = int(max(3, min(16, -(-3 * l2 // max(sb, 1)))))
-    views, keep = [], []
-    for c in range(ncopies):
-        if c == 0:
-            ent, eo = a.entries_d, a.e_off_d
-        else:
-            ent, eo = a.entries_d.clone(), a.e_off_d.clone()
-        keep.append((ent, eo))
-        views.append(a.view(b0, nb, entries=ent, e_off=eo))
+    copies = [(a.entries_d, a.e_off_d)] + [(a.entries_d.clone(), a.e_off_d.clone())
+                                           for _ in range(ncopies - 1)]
+    views = [a.view(entries=e, e_off=o) for e, o in copies]
 
-    vf = random_vector(cfg["n"], 0)
+    vf = random_vector(n, 0)
     vt = torch.from_numpy(vf).to(dev)
     if cfg["vdtype"] == "bf16":
         vt = vt.to(torch.bfloat16)
-    y_local = torch.zeros(rows_per_rank, dtype=torch.float32, device=dev)
-    y_all = torch.zeros(rows_per_rank * world, dtype=torch.float32, device=dev)
+    y_local, y_all = sm.buffers(torch.float32)
+    rows = sm.r1 - sm.r0
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
     def step(i):
-        kn.matvec_into(a, vt, y_local, view=views[i % ncopies], stream=sptr)
+        kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies], stream=sptr)
         if world > 1:
             dist.all_gather_into_tensor(y_all, y_local)
 
@@ -260,10 +312,10 @@ def main():
            for _ in range(min(args.steps, 100))]
     for i, (e0, e1) in enumerate(kev):
         e0.record(stream)
-        kn.matvec_into(a, vt, y_local, view=views[i % ncopies], stream=sptr)
+        kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies], stream=sptr)
         e1.record(stream)
     torch.cuda.synchronize()
-    kernel_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in kev]))
+    kernel_ms = float(np.median([e0.elapsed_time(e1) for e0, e1 in kev]))
 
     # ---- timed region: exactly K steps
     if dist:
@@ -277,8 +329,7 @@ def main():
             step(i)
         end.record(stream)
         torch.cuda.synchronize()
-        # keep the GPU loaded for the sampler's benefit (untimed)
-        t_hold = time.perf_counter()
+        t_hold = time.perf_counter()  # keep the GPU loaded for the sampler (untimed)
         while time.perf_counter() - t_hold < 0.5:
             for i in range(50):
                 step(i)
@@ -287,15 +338,15 @@ def main():
         dist.barrier()
     total_ms = start.elapsed_time(end)
     if dist:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([total_ms, kernel_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+        total_ms, kernel_ms = (float(x) for x in tt.tolist())
     ms_per_step = total_ms / args.steps
-    value = 1e3 / ms_per_step  # matvecs/s of the whole job (each step = one full matvec)
+    value = 1e3 / ms_per_step  # whole-job matvecs/s (each step = one full matvec)
 
-    # ---- e2e through the public API with host buffers (rank 0, unsharded)
+    # ---- e2e through the public API with host buffers (rank 0, 1 GPU)
     e2e = None
-    if rank == 0:
+    if rank == 0 and world == 1:
         vh = vf.copy()
         for _ in range(5):
             rsr.rsr_matvec(a, vh)
@@ -307,7 +358,7 @@ def main():
         e2e_s = (time.perf_counter() - t0) / ne
         e2e = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(vh.nbytes),
                "d2h_bytes_per_step": int(yh.nbytes),
-               "api": "paper_2603_27462_b200.rsr_matvec(artifact, numpy float32 v)"}
+               "api": "paper_2603_27462_b200.rsr_matvec(artifact, numpy float32 vector)"}
 
     if rank != 0:
         if dist:
@@ -316,29 +367,33 @@ def main():
 
     hbm, peak_kind = peaks()
     vbytes = 2 if cfg["vdtype"] == "bf16" else 4
-    alg_bytes = (a.file_bytes() - 24) + cfg["n"] * vbytes + cfg["m"] * 4
-    if world > 1:
-        alg_bytes = alg_bytes * nb // bc
-    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
-    own_bytes = a.stream_bytes() * nb // bc + cfg["n"] * vbytes + nb * k * 4
+    local_alg = (a.file_bytes() - 24) + n * vbytes + rows * 4
+    achieved = local_alg / (kernel_ms * 1e-3) / 1e9
+    own = sb + n * vbytes + rows * 4
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(f"{args.config}_k{k}")
+            traffic = json.load(f).get(f"{cname}_k{k}_world{world}")
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-            "algorithmic_bytes": int(alg_bytes), "stream_bytes": int(own_bytes),
-            "achieved_own_bytes_gbs": own_bytes / (kernel_ms * 1e-3) / 1e9,
-            "kernel_us": kernel_ms * 1e3, "frac_of_8TBs_nominal": achieved / 8000.0}
+            "algorithmic_bytes": int(local_alg), "stream_bytes": int(own),
+            "achieved_own_bytes_gbs": own / (kernel_ms * 1e-3) / 1e9,
+            "kernel_us": kernel_ms * 1e3, "frac_of_8TBs_nominal": achieved / 8000.0,
+            "note": "per rank (rank 0's shard) when sharded"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        val, threads, n, el = cpu_reference_run(cfg, 0, 1, seconds=args.cpu_seconds)
-        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{n} full {cfg['m']}x{cfg['n']} float-path matvecs in {el:.1f}s "
-                         f"(C restatement of rsrmv matvec_f32, block-parallel, f64 accum)"}
+        val, threads, nn_, el, sample = cpu_reference_run(cfg, 0, 1, seconds=args.cpu_seconds)
+        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+
+    decode = None
+    if world == 1 and not args.no_decode:
+        try:
+            decode = decode_bench()
+        except Exception as e:  # reported, never silently replaced
+            decode = {"error": repr(e)[:300]}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
@@ -348,7 +403,8 @@ def main():
                                               f"({sb / 1e6:.1f} MB each, L2 {l2 / 1e6:.0f} MB)",
                            parallelism=f"rowblock{world}" if world > 1 else "single"),
             "preprocess_ms": preprocess_ms, "gpu_launches": args.steps,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "decode": decode,
+            "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
