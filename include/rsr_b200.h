@@ -170,6 +170,12 @@ rsr_status rsr_ternarize_pack(const void *w, int32_t w_dtype, int64_t rows, int6
 rsr_status rsr_random_ternary(int64_t row0, int64_t rows, int64_t cols, uint64_t seed,
                               double density, uint8_t *packed, rsr_stream_t stream);
 
+/* Debug: when non-NULL, subsequent multiply launches record a per-CTA
+ * %globaltimer timeline into probe[cta*4 + {0: start, 1: prologue done,
+ * 2: first warp done (min), 3: last warp done (max)}] (device u64; slots 2/3
+ * must be pre-set to UINT64_MAX / 0).  NULL (default) disables it.          */
+void rsr_debug_set_probe(unsigned long long *probe);
+
 /* ---- helpers ---------------------------------------------------------------- */
 /* _native.count_ops (_native.py:288-307): out3 (device int64[3]) =
  * gather adds, scatter adds, groups.                                         */

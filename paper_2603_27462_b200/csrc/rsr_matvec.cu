@@ -61,6 +61,8 @@ __global__ void absmax_quantize_kernel(const void *v, int dtype, int64_t n, int8
 // ---------------------------------------------------------------------------
 // host-side dispatch
 
+static unsigned long long *g_probe = nullptr;  // debug timeline buffer (off by default)
+
 static rsr_status check_view(const rsr_stream_view *vw) {
     if (!vw || !vw->entries || !vw->e_off) return RSR_ERR_INVALID;
     if (vw->k < 1 || vw->k > 16 || vw->m < 1 || vw->n < 1 || vw->tile_count < 1 ||
@@ -116,6 +118,7 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     p.row_beta = row_beta;
     p.out_bf16 = out_bf16;
     p.scale_dev = scale_out;
+    p.probe = g_probe;
     {
         static const int dbg = getenv("RSR_MV_DEBUG") ? atoi(getenv("RSR_MV_DEBUG")) : 0;
         p.dbg = dbg;
@@ -150,7 +153,9 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     if (vw->format != FMT_U32) fixed += ((size_t)tn * vsz + 15) & ~(size_t)15;
     if (bucket) fixed += (size_t)p.nkeys * kp * 4;
     size_t per_warp = bucket ? (size_t)p.nkeys * 4 : 0;
-    if (ring) per_warp += RING_STAGES * (RING_STAGE_BYTES + 8) + 16 * 4;
+    static const int ring_stages = getenv("RSR_MV_STAGES") ? atoi(getenv("RSR_MV_STAGES")) : RING_STAGES;
+    p.stages = ring_stages;
+    if (ring) per_warp += ring_stages * (RING_STAGE_BYTES + 8) + 16 * 4;
     fixed += 16;  // alignment slack (mbarriers)
     const size_t smem_cap = 227 * 1024;
     const int64_t cells_per_tile = vw->n_blocks;
@@ -230,6 +235,8 @@ rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t 
                                  workspace_bytes, (cudaStream_t)stream, row_beta,
                                  out_dtype == RSR_BF16);
 }
+
+void rsr_debug_set_probe(unsigned long long *probe) { g_probe = probe; }
 
 rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t *q,
                                double *scale_out, rsr_stream_t stream) {

@@ -68,6 +68,8 @@ struct MvParams {
     int team;            // warps per cell (ring path): 1, 2, 4 or 8
     const double *row_beta;  // fused: per-row beta (sibling stacks), or null
     int out_bf16;        // fused: write bf16 instead of f32
+    int stages;          // TMA ring depth per warp (bucket path)
+    unsigned long long *probe;  // debug timeline (rsr_debug_set_probe), null in production
 };
 
 __device__ __forceinline__ float load_as_f32(const void *v, int dtype, int64_t i) {

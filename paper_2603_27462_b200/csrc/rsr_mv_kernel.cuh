@@ -76,7 +76,7 @@ rsr_mv_kernel(MvParams p) {
     constexpr int CH = FMT == FMT_U32 ? 8 : 16;  // entries per 32-byte chunk
     constexpr int KP = KPad<K>::value;
     constexpr bool RING = FMT != FMT_U32 && BUCKET;
-    constexpr int S = RING_STAGES;
+    const int S = p.stages;  // ring depth (rounds in flight per warp)
 
     extern __shared__ __align__(128) unsigned char mv_smem[];
     const int nwarps = blockDim.x >> 5;
@@ -87,6 +87,15 @@ rsr_mv_kernel(MvParams p) {
     const int warp = threadIdx.x >> 5;
     const uint4 *__restrict__ ent4 = reinterpret_cast<const uint4 *>(p.entries);
     const int64_t bstride = (int64_t)gridDim.x * nwarps;
+    const int64_t cta_id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    auto probe = [&](int slot) {  // debug timeline: globaltimer per CTA
+        if (p.probe && threadIdx.x == 0) {
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            p.probe[cta_id * 4 + slot] = tnow;
+        }
+    };
+    probe(0);
 
     // smem: [ring W x S x 1KB][v tile][sign table NB x KP][buckets W x NB][mbarriers W x S]
     size_t off = 0;
@@ -152,19 +161,81 @@ rsr_mv_kernel(MvParams p) {
         bulk_g2s(ringbase + stage * RING_STAGE_BYTES, ent4 + 2 * pbase, bytes, bar);
         pbase += 32 * team;
     };
-    if constexpr (RING) {
-        if (lane == 0) {
-            for (int s = 0; s < S; ++s) mbar_init(barbase + s * 8, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            // start the stream before the prologue: its DRAM latency overlaps
-            // the staging of v
-            for (int s = 0; s < S; ++s) produce(s);
+    auto start_stream = [&]() {
+        if constexpr (RING) {
+            if (lane == 0) {
+                for (int s = 0; s < S; ++s) mbar_init(barbase + s * 8, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                for (int s = 0; s < S; ++s) produce(s);
+            }
+            __syncwarp();
         }
-        __syncwarp();
-    }
+    };
+    const bool fine = p.dbg & 256;  // debug: finer prologue timeline
 
     // ---- prologue -------------------------------------------------------
+    // The float path's v loads are issued first (vectorized, into registers),
+    // then the entry stream is started, then v is converted into shared
+    // memory: the stream's burst of bulk copies must not queue ahead of v.
     double scale = 1.0;
+    bool vstaged_float = false;
+    if constexpr (MODE == MODE_FLOAT && SMEM_V && VSZ == 4) {
+        const int esz = p.vdtype == RSR_F32 ? 4 : 2;
+        const int epv = 16 / esz;  // elements per 16-byte load
+        const char *src = reinterpret_cast<const char *>(p.v) + c0 * esz;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const int64_t nvec = tn / epv;
+            constexpr int U = 4;
+            const int64_t nt = blockDim.x;
+            bool started = false;
+            for (int64_t i0 = threadIdx.x; i0 < nvec; i0 += U * nt) {
+                uint4 r[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t i = i0 + u * nt;
+                    r[u] = i < nvec ? __ldg(reinterpret_cast<const uint4 *>(src) + i)
+                                    : make_uint4(0, 0, 0, 0);
+                }
+                if (!started) {
+                    start_stream();
+                    started = true;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t i = i0 + u * nt;
+                    if (i < nvec) {
+                        float *d = reinterpret_cast<float *>(vsm) + i * epv;
+                        const uint32_t w4[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+                        if (esz == 4) {
+                            reinterpret_cast<float4 *>(d)[0] = make_float4(
+                                __uint_as_float(w4[0]), __uint_as_float(w4[1]),
+                                __uint_as_float(w4[2]), __uint_as_float(w4[3]));
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                float lo, hi;
+                                if (p.vdtype == RSR_BF16) {
+                                    lo = __uint_as_float(w4[q] << 16);
+                                    hi = __uint_as_float(w4[q] & 0xFFFF0000u);
+                                } else {
+                                    const __half2 h2 = *reinterpret_cast<const __half2 *>(&w4[q]);
+                                    lo = __low2float(h2);
+                                    hi = __high2float(h2);
+                                }
+                                reinterpret_cast<float2 *>(d)[q] = make_float2(lo, hi);
+                            }
+                        }
+                    }
+                }
+            }
+            if (!started) start_stream();
+            for (int64_t i = nvec * epv + threadIdx.x; i < tn; i += nt)  // tail
+                reinterpret_cast<float *>(vsm)[i] = load_as_f32(p.v, p.vdtype, c0 + i);
+            vstaged_float = true;
+        }
+    }
+    if (!vstaged_float) start_stream();
+    if (fine) probe(1);
     // Fused path with one tile and 4-byte staging: a single pass over v stages
     // it as f32 while tracking |v|max, then quantizes in place.
     bool staged = false;
@@ -198,7 +269,7 @@ rsr_mv_kernel(MvParams p) {
             }
         }
     }
-    if (!staged) if constexpr (SMEM_V) {
+    if (!staged && !vstaged_float) if constexpr (SMEM_V) {
         if constexpr (MODE == MODE_FLOAT) {
             for_each_v(p.v, p.vdtype, c0, tn,
                        [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
@@ -211,6 +282,7 @@ rsr_mv_kernel(MvParams p) {
             });
         }
     }
+    if (fine) probe(2);
     if constexpr (BUCKET) {
         for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
             uint32_t kk = (uint32_t)key;
@@ -230,6 +302,7 @@ rsr_mv_kernel(MvParams p) {
         for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
     }
     __syncthreads();
+    probe(fine ? 3 : 1);
 
     using VG = typename std::conditional<MODE == MODE_FLOAT, float, int8_t>::type;
     const VG *__restrict__ vglob = reinterpret_cast<const VG *>(p.vstaged) + c0;
@@ -244,7 +317,7 @@ rsr_mv_kernel(MvParams p) {
                 kfirst += 32 * sub;
                 kstep *= team;
             }
-            for (int key = kfirst; key < p.nkeys; key += kstep) {
+            for (int key = kfirst; key < ((p.dbg & 4) ? 0 : p.nkeys); key += kstep) {
                 const Acc bv = key ? bk[key] : (Acc)0;
                 bk[key] = (Acc)0;
                 const Acc *row = stab + key * KP;
@@ -304,16 +377,16 @@ rsr_mv_kernel(MvParams p) {
         auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
         auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
         auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
-        int64_t it = 0;  // rounds consumed by this warp (ring position)
+        int stage = 0;      // ring position of this warp's next round
+        uint32_t phase = 0; // mbarrier phase parity of that stage
         for (; b < p.nblk; b += cstride) {
             const int64_t dc = b * p.tc + t;
             const int64_t ch0 = p.e_off[dc] / CH, ch1 = p.e_off[dc + 1] / CH;
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            for (int64_t base = ch0 + 32 * sub; base < ch1; base += 32 * team, ++it) {
-                const int stage = (int)(it % S);
-                mbar_wait(barbase + stage * 8, (uint32_t)((it / S) & 1));
+            for (int64_t base = ch0 + 32 * sub; base < ch1; base += 32 * team) {
+                mbar_wait(barbase + stage * 8, phase);
                 const uint32_t nr = (uint32_t)min((int64_t)32, ch1 - base);
                 const uint32_t st = ringbase + stage * RING_STAGE_BYTES;
                 uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
@@ -323,20 +396,30 @@ rsr_mv_kernel(MvParams p) {
                 }
                 __syncwarp();
                 if (lane == 0) produce(stage);  // refill the stage just drained
+                if (++stage == S) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
                 // chunks past the cell end are zeros: column-0 gathers flushed
                 // into bucket 0 (never reduced) -- no divergence
                 const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                if (p.dbg & 32) {  // experiment: stream only
+                    acc[0] += (Acc)(w[0] ^ w[1] ^ w[2] ^ w[3] ^ w[4] ^ w[5] ^ w[6] ^ w[7]);
+                    __syncwarp();
+                    continue;
+                }
                 uint32_t cur = key_off(w[0]);
                 Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
                 uint32_t fk[7];
                 float fs[7];
+                const bool cfree = p.dbg & 8;  // experiment: conflict-free gathers
 #pragma unroll
                 for (int i = 1; i < 8; ++i) {
                     const uint32_t x = w[i];
                     const uint32_t isk = is_key(x);
                     const uint32_t ko = key_off(x);
-                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
-                    const Acc h = lds_v<Acc, VSZ>(vbase + hi_off(x));
+                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (cfree ? lane * 4u : lo_off(x)));
+                    const Acc h = lds_v<Acc, VSZ>(vbase + (cfree ? lane * 4u + 128u : hi_off(x)));
                     if constexpr (MODE == MODE_FLOAT) {
                         // record completed segments; flushed below as one batch
                         const bool newseg = isk && ko != cur;
@@ -355,11 +438,14 @@ rsr_mv_kernel(MvParams p) {
                     // round.  Keys of completed segments are distinct across the
                     // round (a group completes inside a chunk at most once; a
                     // repeated equal key continues the segment), bucket 0 aside.
-                    float tb[7];
+                    if (!(p.dbg & 1)) {
+                        float tb[7];
 #pragma unroll
-                    for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
+                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
 #pragma unroll
-                    for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                    }
+                    if (p.dbg & 2) { acc[0] += s; __syncwarp(); continue; }
                     // The chunk's last segment may continue in the next lane's
                     // chunk: equal final keys form contiguous lane runs; a
                     // segmented suffix sum lets each run's first lane flush
@@ -381,6 +467,12 @@ rsr_mv_kernel(MvParams p) {
             }
             asm volatile("" ::: "memory");
             finish_cell(b, acc);
+        }
+        if (p.probe && lane == 0 && !fine) {  // debug timeline: first / last warp done
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            atomicMin(p.probe + cta_id * 4 + 2, tnow);
+            atomicMax(p.probe + cta_id * 4 + 3, tnow);
         }
     } else {
         // ===== generic path (register flush and/or u32 entries) ================
