@@ -162,7 +162,7 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     const int64_t cta_cap = std::max<int64_t>(1, sms / vw->tile_count);
     int team = 1;
     if (ring) {
-        const int64_t est_rounds = std::max<int64_t>(1, (tn * 9 / 8 + 511) / 512);
+        const int64_t est_rounds = std::max<int64_t>(1, (tn * 9 / 8 + 1023) / 1024);
         while (team < 8 && cells_per_tile * team * 2 <= cta_cap * MV_MAX_WARPS &&
                est_rounds >= 2 * team)
             team *= 2;

@@ -63,8 +63,8 @@ __device__ __forceinline__ double cta_reduce_max(double a) {
     return r;
 }
 
-constexpr int RING_STAGES = 4;     // rounds in flight per warp (bucket path)
-constexpr int RING_STAGE_BYTES = 1024;  // one round = 32 chunks x 32 bytes
+constexpr int RING_STAGES = 2;     // rounds in flight per warp (bucket path)
+constexpr int RING_STAGE_BYTES = 2048;  // one round = 64 chunks x 32 bytes
 
 template <int K, int MODE, int FMT, bool BUCKET>
 __global__ void __launch_bounds__(MV_MAX_WARPS * 32)
@@ -137,12 +137,12 @@ rsr_mv_kernel(MvParams p) {
 
     // ---- stream producer (lane 0 of each warp feeds its own ring) -----------
     // Walks this warp's rounds of its cells (b, b + cstride, ...), S rounds
-    // ahead of the consumer; each round is one 1-D bulk copy (TMA) into a
-    // 1 KiB stage whose mbarrier completes on the transaction bytes.
+    // ahead of the consumer; each round (64 chunks) is one 1-D bulk copy (TMA)
+    // into a 2 KiB stage whose mbarrier completes on the transaction bytes.
     int64_t pb = b, pbase = 0, pend = 0;
     if (RING && lane == 0 && pb < p.nblk) {
         const int64_t dc = pb * p.tc + t;
-        pbase = p.e_off[dc] / CH + 32 * sub;
+        pbase = p.e_off[dc] / CH + 64 * sub;
         pend = p.e_off[dc + 1] / CH;
     }
     auto produce = [&](int stage) {
@@ -150,16 +150,16 @@ rsr_mv_kernel(MvParams p) {
             pb += cstride;
             if (pb < p.nblk) {
                 const int64_t dc = pb * p.tc + t;
-                pbase = p.e_off[dc] / CH + 32 * sub;
+                pbase = p.e_off[dc] / CH + 64 * sub;
                 pend = p.e_off[dc + 1] / CH;
             }
         }
         if (pb >= p.nblk) return;
-        const uint32_t bytes = (uint32_t)(min((int64_t)32, pend - pbase) * 32);
+        const uint32_t bytes = (uint32_t)(min((int64_t)64, pend - pbase) * 32);
         const uint32_t bar = barbase + stage * 8;
         mbar_expect_tx(bar, bytes);
         bulk_g2s(ringbase + stage * RING_STAGE_BYTES, ent4 + 2 * pbase, bytes, bar);
-        pbase += 32 * team;
+        pbase += 64 * team;
     };
     auto start_stream = [&]() {
         if constexpr (RING) {
@@ -385,14 +385,16 @@ rsr_mv_kernel(MvParams p) {
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            for (int64_t base = ch0 + 32 * sub; base < ch1; base += 32 * team) {
+            for (int64_t base = ch0 + 64 * sub; base < ch1; base += 64 * team) {
                 mbar_wait(barbase + stage * 8, phase);
-                const uint32_t nr = (uint32_t)min((int64_t)32, ch1 - base);
-                const uint32_t st = ringbase + stage * RING_STAGE_BYTES;
-                uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
-                if (lane < nr) {
-                    a0 = lds128(st + lane * 16);
-                    a1 = lds128(st + nr * 16 + lane * 16);
+                const uint32_t np = (uint32_t)min((int64_t)64, ch1 - base) >> 1;  // chunk pairs
+                const uint32_t st = ringbase + stage * RING_STAGE_BYTES + lane * 16;
+                uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, a2 = a0, a3 = a0;
+                if (lane < np) {
+                    a0 = lds128(st);
+                    a1 = lds128(st + np * 16);
+                    a2 = lds128(st + np * 32);
+                    a3 = lds128(st + np * 48);
                 }
                 __syncwarp();
                 if (lane == 0) produce(stage);  // refill the stage just drained
@@ -400,21 +402,27 @@ rsr_mv_kernel(MvParams p) {
                     stage = 0;
                     phase ^= 1u;
                 }
-                // chunks past the cell end are zeros: column-0 gathers flushed
-                // into bucket 0 (never reduced) -- no divergence
-                const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                // lane L owns chunks 2L, 2L+1 (32 slots).  Pairs past the cell
+                // end are zeros: column-0 gathers flushed into bucket 0 (never
+                // reduced) -- no divergence.  The second chunk's leading key is
+                // an ordinary key slot (a repeated key continues the segment).
+                const uint32_t w[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
+                                        a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
                 if (p.dbg & 32) {  // experiment: stream only
-                    acc[0] += (Acc)(w[0] ^ w[1] ^ w[2] ^ w[3] ^ w[4] ^ w[5] ^ w[6] ^ w[7]);
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) x ^= w[i];
+                    acc[0] += (Acc)x;
                     __syncwarp();
                     continue;
                 }
                 uint32_t cur = key_off(w[0]);
                 Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
-                uint32_t fk[7];
-                float fs[7];
+                uint32_t fk[15];
+                float fs[15];
                 const bool cfree = p.dbg & 8;  // experiment: conflict-free gathers
 #pragma unroll
-                for (int i = 1; i < 8; ++i) {
+                for (int i = 1; i < 16; ++i) {
                     const uint32_t x = w[i];
                     const uint32_t isk = is_key(x);
                     const uint32_t ko = key_off(x);
@@ -439,11 +447,11 @@ rsr_mv_kernel(MvParams p) {
                     // round (a group completes inside a chunk at most once; a
                     // repeated equal key continues the segment), bucket 0 aside.
                     if (!(p.dbg & 1)) {
-                        float tb[7];
+                        float tb[15];
 #pragma unroll
-                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
+                        for (int i = 0; i < 15; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
 #pragma unroll
-                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                        for (int i = 0; i < 15; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
                     }
                     if (p.dbg & 2) { acc[0] += s; __syncwarp(); continue; }
                     // The chunk's last segment may continue in the next lane's
@@ -482,22 +490,29 @@ rsr_mv_kernel(MvParams p) {
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            int64_t nr = min((int64_t)32, cch1 - cch0);
-            uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-            if ((int64_t)lane < nr) {
-                q0 = __ldg(ent4 + 2 * cch0 + lane);
-                q1 = __ldg(ent4 + 2 * cch0 + nr + lane);
-            }
-            for (int64_t base = cch0; base < cch1; base += 32) {
-                const bool valid = (int64_t)lane < nr;
-                const uint4 a0 = q0, a1 = q1;
-                const int64_t nbase = base + 32;
-                const int64_t nnr = min((int64_t)32, cch1 - nbase);
-                if ((int64_t)lane < nnr) {  // prefetch the next round
-                    q0 = __ldg(ent4 + 2 * nbase + lane);
-                    q1 = __ldg(ent4 + 2 * nbase + nnr + lane);
+            // rounds of 64 chunks, lane L owns the chunk pair (2L, 2L+1): four
+            // coalesced 16-byte quarters (see phys_slot in rsr_preprocess.cu)
+            auto load_pair = [&](int64_t base, uint4 (&q)[4]) {
+                const int64_t np = min((int64_t)64, cch1 - base) >> 1;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) q[j] = make_uint4(0, 0, 0, 0);
+                if ((int64_t)lane < np) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) q[j] = __ldg(ent4 + 2 * base + j * np + lane);
                 }
-                if (valid) {
+            };
+            uint4 q[4];
+            load_pair(cch0, q);
+            for (int64_t base = cch0; base < cch1; base += 64) {
+                const bool valid_pair = (int64_t)lane < (min((int64_t)64, cch1 - base) >> 1);
+                uint4 a[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a[j] = q[j];
+                if (base + 64 < cch1) load_pair(base + 64, q);  // prefetch the next round
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    if (!valid_pair) break;
+                    const uint4 a0 = a[2 * half], a1 = a[2 * half + 1];
                     const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                     if constexpr (FMT == FMT_U16) {
                         uint32_t cur = w[0] & 0x7FFFu;
@@ -532,7 +547,6 @@ rsr_mv_kernel(MvParams p) {
                         reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
                     }
                 }
-                nr = nnr;
             }
             finish_cell(b, acc);
         }

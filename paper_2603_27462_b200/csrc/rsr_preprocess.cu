@@ -281,17 +281,21 @@ __host__ __device__ __forceinline__ void place_group(int64_t &p, int64_t L, int6
     }
 }
 
-// Physical index of logical slot p inside a cell of nch chunks: chunks are
-// taken 32 at a time (one warp round) and stored as [first halves][second
-// halves] so each of the round's two 16-byte loads is one coalesced 512-byte
-// access.
+// Physical index of logical slot p inside a cell of nch chunks (nch even).
+// A warp round is 64 chunks: lane L owns the consecutive chunk pair (2L,
+// 2L+1), i.e. 64 bytes in four 16-byte quarters; the round is stored as
+// [quarter 0 of every pair][quarter 1]...[quarter 3], so each of a lane's four
+// 16-byte loads is one coalesced 512-byte access, and the round is one
+// contiguous 2 KiB bulk copy.
 __host__ __device__ __forceinline__ int64_t phys_slot(int64_t p, int64_t CH, int64_t nch) {
     const int64_t c = p / CH, js = p - c * CH;
-    const int64_t r = c >> 5, lanec = c & 31;
-    const int64_t nr = min((int64_t)32, nch - (r << 5));
-    const int64_t half = CH >> 1;
-    const int64_t h = js / half, within = js - h * half;
-    return r * 32 * CH + h * nr * half + lanec * half + within;
+    const int64_t pair = c >> 1, cin = c & 1;
+    const int64_t r = pair >> 5, lanep = pair & 31;
+    const int64_t npairs = nch >> 1;
+    const int64_t np = min((int64_t)32, npairs - (r << 5));
+    const int64_t qe = CH >> 1;  // entries per 16-byte quarter
+    const int64_t q = cin * 2 + js / qe, within = js % qe;
+    return r * 64 * CH + q * np * qe + lanep * qe + within;
 }
 
 // Dense pattern key of a group from its masks: binary -> pos mask; ternary
@@ -322,7 +326,7 @@ __global__ void stream_count_kernel(const uint64_t *__restrict__ words,
             gslot[g] = (int32_t)p;
             place_group(p, L, CH, [](int64_t) {}, [](int64_t, int64_t) {});
         }
-        e_off[dc + 1] = (p + CH - 1) / CH * CH;
+        e_off[dc + 1] = (p + 2 * CH - 1) / (2 * CH) * (2 * CH);  // whole chunk pairs
     }
 }
 
