@@ -2,6 +2,14 @@
 // rsr_mv_impl.cuh; see that file's header for the algorithm).
 #pragma once
 
+// Experiment knobs (RSR_MV_DEBUG bits) are compiled in only with
+// -DRSR_MV_EXPERIMENTS; production builds carry no extra instructions.
+#ifdef RSR_MV_EXPERIMENTS
+#define RSR_DBG(p, bit) ((p).dbg & (bit))
+#else
+#define RSR_DBG(p, bit) 0
+#endif
+
 namespace rsr {
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers ---------------------------------
@@ -171,7 +179,7 @@ rsr_mv_kernel(MvParams p) {
             __syncwarp();
         }
     };
-    const bool fine = p.dbg & 256;  // debug: finer prologue timeline
+    const bool fine = RSR_DBG(p, 256);  // debug: finer prologue timeline
 
     // ---- prologue -------------------------------------------------------
     // The float path's v loads are issued first (vectorized, into registers),
@@ -317,7 +325,7 @@ rsr_mv_kernel(MvParams p) {
                 kfirst += 32 * sub;
                 kstep *= team;
             }
-            for (int key = kfirst; key < ((p.dbg & 4) ? 0 : p.nkeys); key += kstep) {
+            for (int key = kfirst; key < (RSR_DBG(p, 4) ? 0 : p.nkeys); key += kstep) {
                 const Acc bv = key ? bk[key] : (Acc)0;
                 bk[key] = (Acc)0;
                 const Acc *row = stab + key * KP;
@@ -408,7 +416,7 @@ rsr_mv_kernel(MvParams p) {
                 // an ordinary key slot (a repeated key continues the segment).
                 const uint32_t w[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
                                         a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
-                if (p.dbg & 32) {  // experiment: stream only
+                if (RSR_DBG(p, 32)) {  // experiment: stream only
                     uint32_t x = 0;
 #pragma unroll
                     for (int i = 0; i < 16; ++i) x ^= w[i];
@@ -420,7 +428,7 @@ rsr_mv_kernel(MvParams p) {
                 Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
                 uint32_t fk[15];
                 float fs[15];
-                const bool cfree = p.dbg & 8;  // experiment: conflict-free gathers
+                const bool cfree = RSR_DBG(p, 8);  // experiment: conflict-free gathers
 #pragma unroll
                 for (int i = 1; i < 16; ++i) {
                     const uint32_t x = w[i];
@@ -446,14 +454,14 @@ rsr_mv_kernel(MvParams p) {
                     // round.  Keys of completed segments are distinct across the
                     // round (a group completes inside a chunk at most once; a
                     // repeated equal key continues the segment), bucket 0 aside.
-                    if (!(p.dbg & 1)) {
+                    if (!RSR_DBG(p, 1)) {
                         float tb[15];
 #pragma unroll
                         for (int i = 0; i < 15; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
 #pragma unroll
                         for (int i = 0; i < 15; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
                     }
-                    if (p.dbg & 2) { acc[0] += s; __syncwarp(); continue; }
+                    if (RSR_DBG(p, 2)) { acc[0] += s; __syncwarp(); continue; }
                     // The chunk's last segment may continue in the next lane's
                     // chunk: equal final keys form contiguous lane runs; a
                     // segmented suffix sum lets each run's first lane flush
