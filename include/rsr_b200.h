@@ -22,9 +22,9 @@
  * reference arrays once per artifact (rsr_stream_build): cells in block-major
  * order, each a run of 32-byte chunks.  An entry is either a tile-local
  * column to gather or the pattern KEY of the group whose columns follow
- * (binary: pos mask; ternary: base-3 digits; key 0 = padding).  Every chunk
- * starts with a key entry, so any warp can process any chunk without knowing
- * what came before it, and keys only occupy even slots.  See DESIGN.md.
+ * (binary: pos mask; ternary: base-3 digits).  A warp round is 64 chunks and
+ * lane L owns the chunk pair (2L, 2L+1), so any lane can start decoding at a
+ * pair boundary without knowing what came before it.  See DESIGN.md.
  */
 #ifndef RSR_B200_H
 #define RSR_B200_H
@@ -70,6 +70,8 @@ typedef struct {
     const int64_t *e_off;      /* device, cells+1 entry offsets, block-major cell order */
     int64_t row_begin_block;   /* first block this view covers (row-block sharding) */
     int64_t n_blocks;          /* blocks covered (== block_count unless sharded) */
+    const uint32_t *col0_key;  /* device, per cell (block-major): pattern key of the
+                                  tile's column 0 (u16 formats; NULL for format 2) */
 } rsr_stream_view;
 
 /* ---- library info ---------------------------------------------------- */
@@ -108,19 +110,28 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
  * Formats (rsr_stream_format picks one per plan):
  *   0  u16, flag bit 15: column, or KEY|0x8000          (tiles <= 32768)
  *   1  u16, "scaled": column*4, or KEY*4|1 -- byte offsets straight into
- *      4-byte shared-memory elements           (tiles <= 16384, keys <= 16384)
+ *      4-byte shared-memory elements           (tiles <= 16384, keys <= 2187)
  *   2  u32, flag bit 31                          (anything wider / larger)
- * 32-byte chunks (16 u16 / 8 u32 entries); within a cell each group of 32
- * chunks is stored as [their first 16-byte halves][their second halves].     */
+ * u16 formats use the QUAD layout: every chunk pair starts with a key, keys
+ * sit only at slots = 0 mod 4, inside a pair each key starts a new group,
+ * padding is column 0 (staged as zero; the tile's real column 0 is carried
+ * as col0_key[cell], 0 = none), and inside each group the columns are
+ * ordered to spread each round's shared-memory gathers over the 32 banks.
+ * Format 2 uses the EVEN layout: every chunk starts with a key, keys at even
+ * slots, padding key 0 / column 0.
+ * Each warp round (64 chunks) is stored as four 16-byte quarters per chunk
+ * pair, [quarter 0 of all pairs][quarter 1][quarter 2][quarter 3].           */
 int32_t rsr_stream_format(int32_t bitwidth, int32_t k, int64_t tile_width);
-rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, int64_t block_count,
-                            int64_t tile_count, int32_t chunk, int64_t *e_off, int32_t *gslot,
+rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                            const int64_t *po, int64_t block_count, int64_t tile_count,
+                            int32_t format, int32_t chunk, int64_t *e_off, int32_t *gslot,
                             rsr_stream_t stream);
+/* col0_key: device u32[cells] (u16 formats; may be NULL for format 2).       */
 rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,
                             int32_t bitwidth, int32_t format, int32_t chunk,
                             const int64_t *e_off, const int32_t *gslot, void *entries,
-                            rsr_stream_t stream);
+                            uint32_t *col0_key, rsr_stream_t stream);
 
 /* ---- online multiply --------------------------------------------------------
  * rsr_matvec: y (+)= A . v  over the view's row blocks.

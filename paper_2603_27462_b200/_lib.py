@@ -46,6 +46,7 @@ class StreamView(ctypes.Structure):
         ("format", I32), ("chunk", I32),
         ("entries", P), ("e_off", P),
         ("row_begin_block", I64), ("n_blocks", I64),
+        ("col0_key", P),
     ]
 
 
@@ -59,8 +60,8 @@ SIGNATURES = {
     "rsr_group_count": (I32, [P, I64, I64, I64, I32, I32, I64, P, P, P, P, P, SZ, P]),
     "rsr_group_fill": (I32, [P, I64, I64, I64, I32, I32, I64, P, P, P, P, P, SZ, P]),
     "rsr_stream_format": (I32, [I32, I32, I64]),
-    "rsr_stream_count": (I32, [P, P, I64, I64, I32, P, P, P]),
-    "rsr_stream_build": (I32, [P, P, P, P, I64, I64, I32, I32, I32, P, P, P, P]),
+    "rsr_stream_count": (I32, [P, P, P, P, I64, I64, I32, I32, P, P, P]),
+    "rsr_stream_build": (I32, [P, P, P, P, I64, I64, I32, I32, I32, P, P, P, P, P]),
     "rsr_matvec_workspace_bytes": (SZ, [ctypes.POINTER(StreamView)]),
     "rsr_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, P, I32, P, SZ, P]),
     "rsr_fused_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, F64, P, P, I32, P, P, SZ, P]),

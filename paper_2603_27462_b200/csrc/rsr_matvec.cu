@@ -72,6 +72,7 @@ static rsr_status check_view(const rsr_stream_view *vw) {
     if (vw->format != rsr_stream_format(vw->bitwidth, vw->k, vw->tile_width))
         return RSR_ERR_INVALID;
     if (vw->chunk != (vw->format == FMT_U32 ? 8 : 16)) return RSR_ERR_INVALID;
+    if (vw->format != FMT_U32 && !vw->col0_key) return RSR_ERR_INVALID;
     return RSR_OK;
 }
 
@@ -100,6 +101,7 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     MvParams p;
     p.entries = vw->entries;
     p.e_off = vw->e_off;
+    p.col0_key = vw->col0_key;
     p.m_rows = vw->m;
     p.n = vw->n;
     p.tw = vw->tile_width;

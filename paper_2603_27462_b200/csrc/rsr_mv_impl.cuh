@@ -5,17 +5,19 @@
 //
 // Input: the chunk stream (include/rsr_b200.h): per cell, 32-byte chunks of
 // entries; an entry is a column to gather or the pattern key of the group
-// whose columns follow; every chunk starts with a key and keys only sit at
-// even slots (place_group in rsr_preprocess.cu).
+// whose columns follow.  u16 formats use the quad layout (keys at slots = 0
+// mod 4, column 0 = zero padding, the tile's real column 0 added from
+// col0_key in the epilogue); u32 the even layout (place_group* in
+// rsr_preprocess.cu).
 //
 // Work decomposition:
 //   * grid.y = column tile.  Each CTA stages its tile of v in shared memory
 //     once (the fused path quantizes while staging, after a CTA-local absmax
 //     over the whole vector -- no separate quantization launch);
-//   * one warp owns one (block, tile) cell at a time; in each round lane L
-//     owns chunk L (two coalesced 16-byte loads per lane, the next round
-//     prefetched), gathers v from shared memory per column slot and keeps a
-//     running partial group sum;
+//   * one warp (or a team of warps) owns one (block, tile) cell at a time; a
+//     round is 64 chunks moved by one TMA bulk copy into the warp's ring, lane
+//     L owns the chunk pair (2L, 2L+1), gathers v from shared memory per
+//     column slot and keeps a running partial group sum;
 //   * at a key slot the partial sum is flushed into the warp's PATTERN BUCKET
 //     for that key (3^k ternary / 2^k binary buckets in shared memory) --
 //     branch-free, predicated;
@@ -47,6 +49,7 @@ constexpr int64_t BUCKET_MAX_KEYS = 2187;  // 3^7: buckets live in smem up to he
 struct MvParams {
     const void *entries;
     const int64_t *e_off;
+    const uint32_t *col0_key;  // u16 formats: per-cell key of the tile's column 0
     int64_t m_rows;      // rows of the full matrix
     int64_t n;           // columns
     int64_t tw, tc;      // tile width / count
@@ -301,332 +304,6 @@ __device__ __forceinline__ double cta_absmax_fast(const void *v, int dtype, int6
 }  // namespace rsr
 #include "rsr_mv_kernel.cuh"
 namespace rsr {
-#if 0  // superseded register-ring kernel (kept out of the build)
-template <int K, int MODE, int FMT, bool BUCKET>
-__global__ void __launch_bounds__(MV_MAX_WARPS * 32)
-rsr_mv_kernel_old(MvParams p) {
-    using T = MvTypes<MODE, FMT>;
-    using Acc = typename T::Acc;
-    constexpr int VSZ = T::VSZ;
-    constexpr bool SMEM_V = T::SMEM_V;
-    constexpr int CH = FMT == FMT_U32 ? 8 : 16;  // entries per 32-byte chunk
-    constexpr int KP = KPad<K>::value;
-    constexpr int PD = 4;                        // rounds in flight (bucket path)
-
-    extern __shared__ __align__(16) unsigned char mv_smem[];
-    const int nwarps = blockDim.x >> 5;
-    const int64_t t = blockIdx.y;
-    const int64_t c0 = t * p.tw;
-    const int64_t tn = min(p.tw, p.n - c0);
-    const uint32_t lane = lane_id();
-    const int warp = threadIdx.x >> 5;
-    const uint4 *__restrict__ ent4 = reinterpret_cast<const uint4 *>(p.entries);
-    const int64_t bstride = (int64_t)gridDim.x * nwarps;
-
-    // smem carve-up: [v tile][sign table NB x KP][buckets nwarps x NB]
-    size_t off = 0;
-    unsigned char *vsm = mv_smem;
-    if constexpr (SMEM_V) off += ((size_t)tn * VSZ + 15) & ~(size_t)15;
-    Acc *__restrict__ stab = reinterpret_cast<Acc *>(mv_smem + off);
-    if constexpr (BUCKET) off += (size_t)p.nkeys * KP * sizeof(Acc);
-    Acc *__restrict__ buckets = reinterpret_cast<Acc *>(mv_smem + off);
-    Acc *__restrict__ bk = buckets + (size_t)warp * p.nkeys;
-    const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
-    const uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
-
-    // ---- bucket-path stream helpers (see the round loop below) -------------
-    constexpr bool SC = FMT == FMT_U16_SCALED;
-    auto load_round = [&](int64_t gb, int64_t cend, uint4 &q0, uint4 &q1) {
-        const int64_t nr = min((int64_t)32, cend - gb);
-        q0 = make_uint4(0, 0, 0, 0);
-        q1 = q0;
-        if ((int64_t)lane < nr) {
-            q0 = __ldg(ent4 + 2 * gb + lane);
-            q1 = __ldg(ent4 + 2 * gb + nr + lane);
-        }
-    };
-    uint4 ring[PD][2];
-    int64_t b = (int64_t)blockIdx.x * nwarps + warp;
-    int64_t ch0 = 0, ch1 = 0;
-    if constexpr (FMT != FMT_U32 && BUCKET) {
-        // start the first cell's stream before the prologue so its DRAM
-        // latency overlaps the staging of v
-        if (b < p.nblk && !(p.dbg & 512)) {
-            const int64_t dc = b * p.tc + t;
-            ch0 = p.e_off[dc] / CH;
-            ch1 = p.e_off[dc + 1] / CH;
-#pragma unroll
-            for (int u = 0; u < PD; ++u) load_round(ch0 + 32 * u, ch1, ring[u][0], ring[u][1]);
-        }
-    }
-
-    // ---- prologue -------------------------------------------------------
-    double scale = 1.0;
-    if constexpr (MODE == MODE_FUSED) {
-        if constexpr (SMEM_V) {
-            const double amax = cta_absmax_fast(p.v, p.vdtype, p.n);
-            scale = amax == 0.0 ? 1.0 : 127.0 / amax;
-            if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-                *p.scale_dev = scale;
-        } else {
-            scale = *p.scale_dev;  // written by the staging kernel
-        }
-    }
-    if (!(p.dbg & 128)) if constexpr (SMEM_V) {
-        if constexpr (MODE == MODE_FLOAT) {
-            for_each_v(p.v, p.vdtype, c0, tn,
-                       [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
-        } else {
-            const int dt = MODE == MODE_INT ? (int)RSR_I8 : p.vdtype;
-            for_each_v(p.v, dt, c0, tn, [&](int64_t i, float x) {
-                const int8_t q = MODE == MODE_INT ? (int8_t)x : quantize_one(x, scale);
-                if constexpr (VSZ == 4) reinterpret_cast<int32_t *>(vsm)[i] = q;
-                else reinterpret_cast<int8_t *>(vsm)[i] = q;
-            });
-        }
-    }
-    if (!(p.dbg & 256)) if constexpr (BUCKET) {
-        for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
-            uint32_t kk = (uint32_t)key;
-#pragma unroll
-            for (int i = 0; i < KP; ++i) {
-                int sg = 0;
-                if (p.bitwidth == RSR_BINARY) {
-                    sg = (int)((kk >> i) & 1u);
-                } else {
-                    const uint32_t q3 = kk / 3u, d = kk - 3u * q3;
-                    kk = q3;
-                    sg = d == 1u ? 1 : (d == 2u ? -1 : 0);
-                }
-                stab[key * KP + i] = (Acc)(i < K ? sg : 0);
-            }
-        }
-        for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
-    }
-    __syncthreads();
-    if (p.dbg & 64) return;  // prologue only (experiment)
-
-    using VG = typename std::conditional<MODE == MODE_FLOAT, float, int8_t>::type;
-    const VG *__restrict__ vglob = reinterpret_cast<const VG *>(p.vstaged) + c0;
-
-    // ---- per-cell epilogue: pattern-table reduction + warp reduce + store ----
-    auto finish_cell = [&](int64_t bb, Acc (&acc)[K]) {
-        // y_i = sum_key sgn_i(key) * bucket[key]  (bucket 0 collects padding)
-        if constexpr (BUCKET) {
-            for (int key = lane; key < ((p.dbg & 4) ? 0 : p.nkeys); key += 32) {
-                const Acc bv = key ? bk[key] : (Acc)0;
-                bk[key] = (Acc)0;
-                const Acc *row = stab + key * KP;
-#pragma unroll
-                for (int i = 0; i < K; ++i) acc[i] += row[i] * bv;
-            }
-            __syncwarp();
-        }
-        const int64_t row0 = bb * p.k;  // row within the view
-        const int64_t grow0 = (p.blk0 + bb) * p.k;
-        Acc mine = (Acc)0;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            const Acc r = warp_sum(acc[i]);
-            if (lane == (uint32_t)i) mine = r;
-        }
-        if (lane < (uint32_t)K && grow0 + lane < p.m_rows) {
-            const int64_t r = row0 + lane;
-            if (p.tc > 1) {
-                const int64_t rows_view = p.nblk * p.k;
-                reinterpret_cast<Acc *>(p.part)[t * rows_view + r] = mine;
-            } else if constexpr (MODE == MODE_FLOAT) {
-                float *y = reinterpret_cast<float *>(p.y);
-                y[r] = p.accumulate ? y[r] + (float)mine : (float)mine;
-            } else if constexpr (MODE == MODE_INT) {
-                int32_t *y = reinterpret_cast<int32_t *>(p.y);
-                y[r] = p.accumulate ? y[r] + (int32_t)mine : (int32_t)mine;
-            } else {
-                reinterpret_cast<float *>(p.y)[r] =
-                    (float)((double)(int32_t)mine * (p.beta / scale));
-            }
-        }
-    };
-
-    if constexpr (FMT != FMT_U32 && BUCKET) {
-        // ===== bucket path =====================================================
-        // A round is 32 chunks; lane L owns chunk L.  Each round is stored as
-        // [first 16B halves][second 16B halves], so both loads are coalesced
-        // 512B accesses.  Rounds are fetched PD ahead into a register ring and
-        // the next cell's first rounds are fetched before this cell's epilogue.
-        // Chunks past the cell end read as zeros, which decode to column-0
-        // gathers flushed into bucket 0 (never reduced): no divergence.
-        auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
-        auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
-        auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
-        auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
-        while (b < p.nblk) {
-            Acc acc[K];
-#pragma unroll
-            for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            auto do_round = [&](const uint4 &a0, const uint4 &a1) {
-                if (p.dbg & 32) {  // stream only (bandwidth experiment)
-                    acc[0] += (Acc)(a0.x ^ a0.y ^ a0.z ^ a0.w ^ a1.x ^ a1.y ^ a1.z ^ a1.w);
-                    return;
-                }
-                const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                uint32_t cur = key_off(w[0]);
-                Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
-                uint32_t fk[7];
-                float fs[7];
-#pragma unroll
-                for (int i = 1; i < 8; ++i) {
-                    const uint32_t x = w[i];
-                    const uint32_t isk = is_key(x);
-                    const uint32_t ko = key_off(x);
-                    const uint32_t ga = (p.dbg & 8) ? lane * 4u : lo_off(x);
-                    const uint32_t ha = (p.dbg & 8) ? lane * 4u + 128u : hi_off(x);
-                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + ga);
-                    const Acc h = lds_v<Acc, VSZ>(vbase + ha);
-                    if constexpr (MODE == MODE_FLOAT) {
-                        // record completed segments; flushed below as one batch
-                        const bool newseg = isk && ko != cur;
-                        fk[i - 1] = newseg ? cur : 0u;
-                        fs[i - 1] = s;
-                        cur = newseg ? ko : cur;
-                        s = (newseg ? (Acc)0 : s) + g + h;
-                    } else {
-                        if (!(p.dbg & 1)) bucket_flush_pred(isk, bkbase + cur, s);  // native red
-                        cur = isk ? ko : cur;
-                        s = (isk ? (Acc)0 : s) + g + h;
-                    }
-                }
-                if constexpr (MODE == MODE_FLOAT) {
-                    // all bucket loads, then all adds/stores: one latency per
-                    // round.  Keys of completed segments are distinct across the
-                    // round (a group completes inside a chunk at most once; a
-                    // repeated equal key continues the segment), bucket 0 aside.
-                    if (!(p.dbg & 1)) {
-                        float tb[7];
-#pragma unroll
-                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
-#pragma unroll
-                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
-                    }
-                }
-                // A chunk's last segment may continue in the next lane's chunk.
-                // Integer: native shared red handles same-key lanes.  Float:
-                // lanes with equal final keys form contiguous runs; a segmented
-                // suffix sum over the run lets the run's first lane flush alone
-                // (no CAS loop, fixed summation order).
-                if (!(p.dbg & 2)) {
-                    if constexpr (MODE == MODE_FLOAT) {
-                        float sj = s;
-                        const uint32_t kj = cur;
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const float os = __shfl_down_sync(RSR_FULL_MASK, sj, d);
-                            const uint32_t ok = __shfl_down_sync(RSR_FULL_MASK, kj, d);
-                            if (lane + d < 32 && ok == kj) sj += os;
-                        }
-                        const uint32_t pk = __shfl_up_sync(RSR_FULL_MASK, kj, 1);
-                        const bool head = lane == 0 || pk != kj;
-                        if (head) sts_bucket(bkbase + kj, lds_bucket(bkbase + kj) + sj);
-                    } else {
-                        bucket_flush_final(bkbase + cur, s);
-                    }
-                } else {
-                    acc[0] += s;
-                }
-                __syncwarp();
-            };
-            for (int64_t base = ch0; base < ch1; base += 32 * PD) {
-#pragma unroll
-                for (int u = 0; u < PD; ++u) {
-                    const int64_t rb = base + 32 * u;
-                    if (rb < ch1) {
-                        const uint4 a0 = ring[u][0], a1 = ring[u][1];
-                        load_round(rb + 32 * PD, ch1, ring[u][0], ring[u][1]);
-                        do_round(a0, a1);
-                    }
-                }
-            }
-            // prefetch the next cell before this cell's epilogue
-            const int64_t nb = b + bstride;
-            const int64_t cb = b;
-            if (nb < p.nblk) {
-                const int64_t dc = nb * p.tc + t;
-                ch0 = p.e_off[dc] / CH;
-                ch1 = p.e_off[dc + 1] / CH;
-#pragma unroll
-                for (int u = 0; u < PD; ++u) load_round(ch0 + 32 * u, ch1, ring[u][0], ring[u][1]);
-            }
-            asm volatile("" ::: "memory");
-            finish_cell(cb, acc);
-            b = nb;
-        }
-    } else {
-        // ===== generic path (register flush and/or u32 entries) ================
-        for (; b < p.nblk; b += bstride) {
-            const int64_t dc = b * p.tc + t;
-            const int64_t cch0 = p.e_off[dc] / CH, cch1 = p.e_off[dc + 1] / CH;
-            Acc acc[K];
-#pragma unroll
-            for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            int64_t nr = min((int64_t)32, cch1 - cch0);
-            uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-            if ((int64_t)lane < nr) {
-                q0 = __ldg(ent4 + 2 * cch0 + lane);
-                q1 = __ldg(ent4 + 2 * cch0 + nr + lane);
-            }
-            for (int64_t base = cch0; base < cch1; base += 32) {
-                const bool valid = (int64_t)lane < nr;
-                const uint4 a0 = q0, a1 = q1;
-                const int64_t nbase = base + 32;
-                const int64_t nnr = min((int64_t)32, cch1 - nbase);
-                if ((int64_t)lane < nnr) {  // prefetch the next round
-                    q0 = __ldg(ent4 + 2 * nbase + lane);
-                    q1 = __ldg(ent4 + 2 * nbase + nnr + lane);
-                }
-                if (valid) {
-                    const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                    if constexpr (FMT == FMT_U16) {
-                        uint32_t cur = w[0] & 0x7FFFu;
-                        Acc s = lds_v<Acc, VSZ>(vbase + (w[0] >> 16) * VSZ);
-#pragma unroll
-                        for (int i = 1; i < 8; ++i) {
-                            const uint32_t lo = w[i] & 0xFFFFu;
-                            const uint32_t isk = lo & 0x8000u;
-                            const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (lo & 0x7FFFu) * VSZ);
-                            const Acc h = lds_v<Acc, VSZ>(vbase + (w[i] >> 16) * VSZ);
-                            if (isk) reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                            cur = isk ? (lo & 0x7FFFu) : cur;
-                            s = (isk ? (Acc)0 : s) + g + h;
-                        }
-                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                    } else {  // FMT_U32, register flush, v gathered from global scratch
-                        constexpr uint32_t KF = 1u << 31;
-                        uint32_t cur = w[0] & ~KF;
-                        Acc s = (Acc)__ldg(vglob + w[1]);
-#pragma unroll
-                        for (int i = 2; i < 8; i += 2) {
-                            const Acc h = (Acc)__ldg(vglob + w[i + 1]);
-                            if (w[i] & KF) {
-                                reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                                cur = w[i] & ~KF;
-                                s = (Acc)0;
-                            } else {
-                                s += (Acc)__ldg(vglob + w[i]);
-                            }
-                            s += h;
-                        }
-                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                    }
-                }
-                nr = nnr;
-            }
-            finish_cell(b, acc);
-        }
-    }
-}
-
-#endif
-
 using KernelFn = void (*)(MvParams);
 
 // Kernel lookup, defined per format in rsr_mv_fmt*.cu (parallel compilation).

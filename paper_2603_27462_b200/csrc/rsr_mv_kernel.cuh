@@ -309,6 +309,19 @@ rsr_mv_kernel(MvParams p) {
         }
         for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
     }
+    // Quad layout: column 0 is the zero padding entry.  The tile's real
+    // column-0 value (as staged: f32 / int8 / quantized) is added in the
+    // epilogue to the bucket of col0_key[cell].  Thread 0 staged element 0.
+    Acc v0 = (Acc)0;
+    if constexpr (SMEM_V) {
+        if constexpr (MODE == MODE_FLOAT) v0 = load_as_f32(p.v, p.vdtype, c0);
+        else if constexpr (MODE == MODE_INT) v0 = (Acc)__ldg(reinterpret_cast<const int8_t *>(p.v) + c0);
+        else v0 = (Acc)quantize_one(load_as_f32(p.v, p.vdtype, c0), scale);
+        if (threadIdx.x == 0) {
+            if constexpr (VSZ == 4) reinterpret_cast<uint32_t *>(vsm)[0] = 0u;
+            else vsm[0] = 0;
+        }
+    }
     __syncthreads();
     probe(fine ? 3 : 1);
 
@@ -317,8 +330,16 @@ rsr_mv_kernel(MvParams p) {
 
     // ---- per-cell epilogue: pattern-table reduction + warp reduce + store ----
     auto finish_cell = [&](int64_t bb, Acc (&acc)[K]) {
-        // y_i = sum_key sgn_i(key) * bucket[key]  (bucket 0 collects padding)
+        // the tile's column 0 (not in the u16 stream)
+        uint32_t key0 = 0;
+        if constexpr (SMEM_V) key0 = p.col0_key[bb * p.tc + t];
+        // y_i = sum_key sgn_i(key) * bucket[key]  (bucket 0 is never reduced)
         if constexpr (BUCKET) {
+            if (key0 && sub == 0 && lane == 0) {
+                if (shbk) bucket_flush_final(bkbase + key0 * 4u, v0);  // native red
+                else bk[key0] += v0;
+            }
+            __syncwarp();
             int kfirst = (int)lane, kstep = 32;
             if (shbk) {  // whole team has flushed; split the keys across it
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + tid_team), "r"(team * 32) : "memory");
@@ -333,6 +354,8 @@ rsr_mv_kernel(MvParams p) {
                 for (int i = 0; i < K; ++i) acc[i] += row[i] * bv;
             }
             __syncwarp();
+        } else if constexpr (SMEM_V) {
+            if (key0 && lane == 0) reg_flush<K, Acc>(acc, key0, v0, p.bitwidth);
         }
         const int64_t row0 = bb * p.k;  // row within the view
         const int64_t grow0 = (p.blk0 + bb) * p.k;
@@ -375,16 +398,18 @@ rsr_mv_kernel(MvParams p) {
 
     if constexpr (RING) {
         // ===== bucket path =====================================================
-        // A round is 32 chunks; lane L owns chunk L.  A round sits in a ring
-        // stage as [first 16B halves][second 16B halves] (conflict-free 16B
-        // shared loads).  Slot 2i = low half of word i (column or key), slot
-        // 2i+1 = high half (always a column).  Scaled format: entries are byte
-        // offsets (column*4; key*4|1) straight into v and the buckets.
+        // A round is 64 chunks; lane L owns the chunk pair (2L, 2L+1) = 32
+        // slots, stored as four 16-byte quarters (conflict-free 16B shared
+        // loads).  Quad layout: slot 4q (low half of word 2q) is a key or a
+        // column, slots 4q+1..4q+3 are columns; slot 0 is always a key and,
+        // inside a pair, every key starts a new group.  Scaled format: entries
+        // are byte offsets (column*4; key*4|1) straight into v and the buckets.
         constexpr bool SC = FMT == FMT_U16_SCALED;
         auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
         auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
         auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
         auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
+        auto gat = [&](uint32_t off) -> Acc { return lds_v<Acc, VSZ>(vbase + off); };
         int stage = 0;      // ring position of this warp's next round
         uint32_t phase = 0; // mbarrier phase parity of that stage
         for (; b < p.nblk; b += cstride) {
@@ -410,10 +435,8 @@ rsr_mv_kernel(MvParams p) {
                     stage = 0;
                     phase ^= 1u;
                 }
-                // lane L owns chunks 2L, 2L+1 (32 slots).  Pairs past the cell
-                // end are zeros: column-0 gathers flushed into bucket 0 (never
-                // reduced) -- no divergence.  The second chunk's leading key is
-                // an ordinary key slot (a repeated key continues the segment).
+                // Pairs past the cell end are zeros: key 0 with column-0 (zero)
+                // gathers, flushed into bucket 0 (never reduced) -- no divergence.
                 const uint32_t w[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
                                         a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
                 if (RSR_DBG(p, 32)) {  // experiment: stream only
@@ -425,45 +448,41 @@ rsr_mv_kernel(MvParams p) {
                     continue;
                 }
                 uint32_t cur = key_off(w[0]);
-                Acc s = lds_v<Acc, VSZ>(vbase + hi_off(w[0]));
-                uint32_t fk[15];
-                float fs[15];
-                const bool cfree = RSR_DBG(p, 8);  // experiment: conflict-free gathers
+                Acc s = gat(hi_off(w[0])) + (gat(lo_off(w[1])) + gat(hi_off(w[1])));
+                uint32_t fk[7];
+                float fs[7];
 #pragma unroll
-                for (int i = 1; i < 16; ++i) {
-                    const uint32_t x = w[i];
+                for (int q = 1; q < 8; ++q) {
+                    const uint32_t x = w[2 * q], y = w[2 * q + 1];
                     const uint32_t isk = is_key(x);
                     const uint32_t ko = key_off(x);
-                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (cfree ? lane * 4u : lo_off(x)));
-                    const Acc h = lds_v<Acc, VSZ>(vbase + (cfree ? lane * 4u + 128u : hi_off(x)));
+                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
+                    const Acc t3 = gat(hi_off(x)) + (gat(lo_off(y)) + gat(hi_off(y)));
                     if constexpr (MODE == MODE_FLOAT) {
                         // record completed segments; flushed below as one batch
-                        const bool newseg = isk && ko != cur;
-                        fk[i - 1] = newseg ? cur : 0u;
-                        fs[i - 1] = s;
-                        cur = newseg ? ko : cur;
-                        s = (newseg ? (Acc)0 : s) + g + h;
+                        fk[q - 1] = isk ? cur : 0u;
+                        fs[q - 1] = s;
                     } else {
                         bucket_flush_pred(isk, bkbase + cur, s);  // native shared red
-                        cur = isk ? ko : cur;
-                        s = (isk ? (Acc)0 : s) + g + h;
                     }
+                    cur = isk ? ko : cur;
+                    s = (isk ? (Acc)0 : s) + g + t3;
                 }
                 if constexpr (MODE == MODE_FLOAT) {
                     // all bucket loads, then all adds/stores: one latency per
                     // round.  Keys of completed segments are distinct across the
-                    // round (a group completes inside a chunk at most once; a
-                    // repeated equal key continues the segment), bucket 0 aside.
+                    // round (a group's segment ends inside a pair at most once
+                    // per round), bucket 0 aside.
                     if (!RSR_DBG(p, 1)) {
-                        float tb[15];
+                        float tb[7];
 #pragma unroll
-                        for (int i = 0; i < 15; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
+                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
 #pragma unroll
-                        for (int i = 0; i < 15; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
                     }
                     if (RSR_DBG(p, 2)) { acc[0] += s; __syncwarp(); continue; }
-                    // The chunk's last segment may continue in the next lane's
-                    // chunk: equal final keys form contiguous lane runs; a
+                    // The pair's last segment may continue in the next lane's
+                    // pair: equal final keys form contiguous lane runs; a
                     // segmented suffix sum lets each run's first lane flush
                     // alone (no CAS loop, fixed summation order).
                     float sj = s;
@@ -517,26 +536,31 @@ rsr_mv_kernel(MvParams p) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) a[j] = q[j];
                 if (base + 64 < cch1) load_pair(base + 64, q);  // prefetch the next round
+                if (!valid_pair) continue;
+                if constexpr (FMT == FMT_U16) {  // quad layout, register flush
+                    const uint32_t w[16] = {a[0].x, a[0].y, a[0].z, a[0].w, a[1].x, a[1].y,
+                                            a[1].z, a[1].w, a[2].x, a[2].y, a[2].z, a[2].w,
+                                            a[3].x, a[3].y, a[3].z, a[3].w};
+                    auto gat = [&](uint32_t c) -> Acc { return lds_v<Acc, VSZ>(vbase + c * VSZ); };
+                    uint32_t cur = w[0] & 0x7FFFu;
+                    Acc s = gat(w[0] >> 16) + (gat(w[1] & 0xFFFFu) + gat(w[1] >> 16));
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    if (!valid_pair) break;
-                    const uint4 a0 = a[2 * half], a1 = a[2 * half + 1];
-                    const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                    if constexpr (FMT == FMT_U16) {
-                        uint32_t cur = w[0] & 0x7FFFu;
-                        Acc s = lds_v<Acc, VSZ>(vbase + (w[0] >> 16) * VSZ);
+                    for (int qd = 1; qd < 8; ++qd) {
+                        const uint32_t x = w[2 * qd], y = w[2 * qd + 1];
+                        const uint32_t lo = x & 0xFFFFu;
+                        const uint32_t isk = lo & 0x8000u;
+                        const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (lo & 0x7FFFu) * VSZ);
+                        const Acc t3 = gat(x >> 16) + (gat(y & 0xFFFFu) + gat(y >> 16));
+                        if (isk) reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                        cur = isk ? (lo & 0x7FFFu) : cur;
+                        s = (isk ? (Acc)0 : s) + g + t3;
+                    }
+                    reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                } else {  // FMT_U32 (even layout), v gathered from global scratch
 #pragma unroll
-                        for (int i = 1; i < 8; ++i) {
-                            const uint32_t lo = w[i] & 0xFFFFu;
-                            const uint32_t isk = lo & 0x8000u;
-                            const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + (lo & 0x7FFFu) * VSZ);
-                            const Acc h = lds_v<Acc, VSZ>(vbase + (w[i] >> 16) * VSZ);
-                            if (isk) reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                            cur = isk ? (lo & 0x7FFFu) : cur;
-                            s = (isk ? (Acc)0 : s) + g + h;
-                        }
-                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                    } else {  // FMT_U32, register flush, v gathered from global scratch
+                    for (int half = 0; half < 2; ++half) {
+                        const uint4 a0 = a[2 * half], a1 = a[2 * half + 1];
+                        const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                         constexpr uint32_t KF = 1u << 31;
                         uint32_t cur = w[0] & ~KF;
                         Acc s = (Acc)__ldg(vglob + w[1]);

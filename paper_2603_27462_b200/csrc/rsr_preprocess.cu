@@ -247,11 +247,33 @@ scan2_kernel(int64_t *a, int64_t *b, int64_t cells) {
 }
 
 // ---------------------------------------------------------------------------
-// chunk stream: block-major cells; each cell is a run of CH-entry chunks and
-// every chunk starts with a key entry (see include/rsr_b200.h).
+// chunk stream: block-major cells, each a run of 32-byte chunks (see
+// include/rsr_b200.h).  Two layouts:
+//   u16 formats (0, 1) -- "quad" layout, rounds of 64 chunks, lane = chunk pair:
+//     every pair (32 entries) starts with a key; keys only at slots = 0 mod 4;
+//     inside a pair every key starts a new group (a group crossing a pair
+//     boundary repeats its key at slot 0 of the next pair); padding is
+//     column 0, whose staged v element is 0 -- the cell's real column 0 is not
+//     in the stream, its pattern key is stored in col0_key[cell] instead.
+//   u32 format (2) -- "even" layout: every chunk starts with a key, keys only at
+//     even slots, padding key 0 / column 0 (bucket 0 is never reduced).
 
-// Slot placement of one group of L columns (the reference word's perm_len)
-// starting at slot p (always even).  Keys only ever sit at EVEN slots: every
+// Quad layout: slots of one group of R stream columns starting at slot p
+// (p = 0 mod 4).  emit_key(slot) / emit_col(slot, j) / emit_pad(slot).
+template <typename KeyFn, typename ColFn, typename PadFn>
+__host__ __device__ __forceinline__ void place_group_quad(int64_t &p, int64_t R, KeyFn emit_key,
+                                                         ColFn emit_col, PadFn emit_pad) {
+    if (R == 0) return;
+    emit_key(p++);
+    for (int64_t j = 0; j < R; ++j) {
+        if ((p & 31) == 0) emit_key(p++);  // pair start: the group continues
+        emit_col(p++, j);
+    }
+    while (p & 3) emit_pad(p++);
+}
+
+// Even layout: slot placement of one group of L columns (the reference word's
+// perm_len) starting at slot p (always even).  Keys only ever sit at EVEN slots: every
 // segment that ends inside a chunk has odd length (an even remainder is split
 // 1 + (R-1) with one repeated key), and a segment running to the chunk end
 // has odd length automatically.  A group crossing a chunk boundary repeats its
@@ -313,8 +335,10 @@ __device__ __forceinline__ uint32_t dense_key(uint64_t w, int bitwidth) {
 }
 
 __global__ void stream_count_kernel(const uint64_t *__restrict__ words,
-                                    const int64_t *__restrict__ go, int64_t bc, int64_t tc,
-                                    int64_t CH, int64_t *e_off, int32_t *gslot) {
+                                    const int64_t *__restrict__ go,
+                                    const uint16_t *__restrict__ perm,
+                                    const int64_t *__restrict__ po, int64_t bc, int64_t tc,
+                                    int64_t CH, bool quad, int64_t *e_off, int32_t *gslot) {
     const int64_t cells = bc * tc;
     for (int64_t dc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; dc < cells;
          dc += (int64_t)gridDim.x * blockDim.x) {
@@ -322,9 +346,17 @@ __global__ void stream_count_kernel(const uint64_t *__restrict__ words,
         const int64_t src = t * bc + b;
         int64_t p = 0;
         for (int64_t g = go[src]; g < go[src + 1]; ++g) {
-            const int64_t L = (int64_t)((words[g] >> 16) & 0xFFFFu);
+            const uint64_t w = words[g];
+            const int64_t L = (int64_t)((w >> 16) & 0xFFFFu);
             gslot[g] = (int32_t)p;
-            place_group(p, L, CH, [](int64_t) {}, [](int64_t, int64_t) {});
+            if (quad) {
+                // column 0 leads its group (columns ascend inside a group)
+                const bool has0 = perm[po[src] + (int64_t)(w & 0xFFFFu)] == 0;
+                place_group_quad(p, L - has0, [](int64_t) {}, [](int64_t, int64_t) {},
+                                 [](int64_t) {});
+            } else {
+                place_group(p, L, CH, [](int64_t) {}, [](int64_t, int64_t) {});
+            }
         }
         e_off[dc + 1] = (p + 2 * CH - 1) / (2 * CH) * (2 * CH);  // whole chunk pairs
     }
@@ -365,6 +397,118 @@ stream_build_kernel(const uint64_t *__restrict__ words, const int64_t *__restric
                 p, L, CH, [&](int64_t q) { out[phys_slot(q, CH, nch)] = key; },
                 [&](int64_t q, int64_t j) { out[phys_slot(q, CH, nch)] = enc_col(cols[j]); });
         }
+    }
+}
+
+// Bank-aware build of the u16 formats (quad layout).  The multiply gathers v
+// from shared memory (4-byte elements, bank = column % 32); at slot j of a
+// round the 32 lanes gather the columns at round positions 32L + j, and a
+// key-sorted column order costs ~3.3 shared-memory wavefronts per gather
+// instruction.  Columns of a group may be stored in any order (their sum is
+// order-free up to float rounding), so one warp walks its cell's groups in key
+// order and fills each column position with the window column (lane i holds
+// one of the group's unplaced columns) whose bank is least used so far at that
+// (round, slot): ~1.9 wavefronts per gather on random ternary cells
+// (tools/bank_sim.py).  Also records the pattern key of the cell's column 0.
+constexpr int BB_WARPS = 8;
+
+template <bool SCALED>
+__global__ void __launch_bounds__(BB_WARPS * 32)
+stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
+                           const uint16_t *__restrict__ perm, const int64_t *__restrict__ po,
+                           int64_t bc, int64_t tc, int bitwidth,
+                           const int64_t *__restrict__ e_off, const int32_t *__restrict__ gslot,
+                           uint16_t *__restrict__ entries, uint32_t *__restrict__ col0_key) {
+    constexpr int64_t CH = 16;        // u16 entries per 32-byte chunk (constant: no divisions)
+    constexpr int64_t SLOTS = 2 * CH; // entries per lane per round
+    __shared__ uint8_t cnt_all[BB_WARPS][32 * 32];  // [slot][bank] uses in the current round
+    constexpr uint16_t KEYFLAG = 0x8000u;
+    auto enc_key = [](uint32_t k) -> uint16_t {
+        return SCALED ? (uint16_t)((k << 2) | 1u) : (uint16_t)(KEYFLAG | k);
+    };
+    auto enc_col = [](uint32_t c) -> uint16_t { return SCALED ? (uint16_t)(c << 2) : (uint16_t)c; };
+    const uint32_t lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    uint8_t *cnt = cnt_all[warp];
+    const int64_t cells = bc * tc;
+    const uint32_t INVALID = 0xFFFFFFFFu;
+    for (int64_t dc = (int64_t)blockIdx.x * BB_WARPS + warp; dc < cells;
+         dc += (int64_t)gridDim.x * BB_WARPS) {
+        const int64_t b = dc / tc, t = dc - b * tc;
+        const int64_t src = t * bc + b;
+        const int64_t e0 = e_off[dc], elen = e_off[dc + 1] - e0;
+        const int64_t nch = elen / CH;
+        uint16_t *out = entries + e0;
+        for (int64_t i = lane; i < elen; i += 32) out[phys_slot(i, CH, nch)] = enc_col(0);  // pads
+        __syncwarp();
+        int64_t cur_round = -1;
+        uint32_t key0 = 0;
+        auto touch = [&](int64_t q, uint32_t bank) {  // lane 0: count one gather
+            uint8_t &u = cnt[(q % SLOTS) * 32 + bank];
+            u = u < 255 ? u + 1 : 255;
+        };
+        auto enter = [&](int64_t q) {  // new round: clear the bank counts
+            const int64_t r = q / (32 * SLOTS);
+            if (r != cur_round) {
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t *>(cnt)[lane * 8 + i] = 0;
+                cur_round = r;
+            }
+            __syncwarp();
+        };
+        const int64_t p0 = po[src];
+        for (int64_t g = go[src]; g < go[src + 1]; ++g) {
+            const uint64_t w = words[g];
+            const int64_t ps = (int64_t)(w & 0xFFFFu);
+            int64_t L = (int64_t)((w >> 16) & 0xFFFFu);
+            const uint32_t dk = dense_key(w, bitwidth);
+            const uint16_t key = enc_key(dk);
+            const uint16_t *cols = perm + p0 + ps;
+            if (cols[0] == 0) {  // column 0 leads its group; it travels as col0_key
+                key0 = dk;
+                ++cols;
+                --L;
+            }
+            // window: lane i holds one unplaced column; refills come from a
+            // register batch of the next 32 columns (one coalesced load per 32)
+            uint32_t cand = (int64_t)lane < L ? cols[lane] : INVALID;
+            int64_t nb = min(L, (int64_t)32);  // next batch start
+            uint32_t batch = nb + lane < L ? cols[nb + lane] : INVALID;
+            int bi = 0;
+            int64_t p = gslot[g];
+            place_group_quad(
+                p, L,
+                [&](int64_t q) {
+                    if (lane == 0) out[phys_slot(q, CH, nch)] = key;
+                },
+                [&](int64_t q, int64_t) {
+                    enter(q);
+                    const int slot = (int)(q % SLOTS);
+                    const uint32_t mine = cand != INVALID ? cnt[slot * 32 + (cand & 31u)] : 0x100u;
+                    const uint32_t m = __reduce_min_sync(RSR_FULL_MASK, mine);
+                    const int win = __ffs(__ballot_sync(RSR_FULL_MASK, mine == m)) - 1;
+                    const uint32_t c = __shfl_sync(RSR_FULL_MASK, cand, win);
+                    // refill the chosen lane from the batch
+                    const uint32_t nxt = __shfl_sync(RSR_FULL_MASK, batch, bi);
+                    if ((int)lane == win) cand = nxt;
+                    if (++bi == 32) {
+                        bi = 0;
+                        nb += 32;
+                        batch = nb + lane < L ? cols[nb + lane] : INVALID;
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        touch(q, c & 31u);
+                        out[phys_slot(q, CH, nch)] = enc_col(c);
+                    }
+                },
+                [&](int64_t q) {  // pad (column 0, pre-filled)
+                    enter(q);
+                    if (lane == 0) touch(q, 0);
+                });
+        }
+        if (lane == 0) col0_key[dc] = key0;
     }
 }
 
@@ -499,16 +643,17 @@ int32_t rsr_stream_format(int32_t bitwidth, int32_t k, int64_t tile_width) {
     return 2;                                            // u32
 }
 
-rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, int64_t block_count,
-                            int64_t tile_count, int32_t chunk, int64_t *e_off, int32_t *gslot,
+rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                            const int64_t *po, int64_t block_count, int64_t tile_count,
+                            int32_t format, int32_t chunk, int64_t *e_off, int32_t *gslot,
                             rsr_stream_t stream) {
-    if (!go || !e_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
-    if (chunk != 8 && chunk != 16 && chunk != 32) return RSR_ERR_INVALID;
+    if (!go || !po || !e_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
+    if (format < 0 || format > 2 || chunk != (format == 2 ? 8 : 16)) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells + 127) / 128, 8192);
-    stream_count_kernel<<<grid, 128, 0, s>>>(words, go, block_count, tile_count, chunk, e_off,
-                                             gslot);
+    stream_count_kernel<<<grid, 128, 0, s>>>(words, go, perm, po, block_count, tile_count, chunk,
+                                             format != 2, e_off, gslot);
     scan2_kernel<<<1, 1024, 0, s>>>(e_off, nullptr, cells);
     return launch_status();
 }
@@ -517,27 +662,28 @@ rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint
                             const int64_t *po, int64_t block_count, int64_t tile_count,
                             int32_t bitwidth, int32_t format, int32_t chunk,
                             const int64_t *e_off, const int32_t *gslot, void *entries,
-                            rsr_stream_t stream) {
+                            uint32_t *col0_key, rsr_stream_t stream) {
     if (!go || !po || !e_off || !entries || block_count < 1 || tile_count < 1)
         return RSR_ERR_INVALID;
-    if (chunk != 8 && chunk != 16 && chunk != 32) return RSR_ERR_INVALID;
+    if (format < 0 || format > 2 || chunk != (format == 2 ? 8 : 16)) return RSR_ERR_INVALID;
+    if (format != 2 && !col0_key) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 32);
+    const int bgrid =
+        (int)std::min<int64_t>((cells + BB_WARPS - 1) / BB_WARPS, (int64_t)sm_count() * 8);
     if (format == 1)
-        stream_build_kernel<uint16_t, true><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
-                                                                 tile_count, bitwidth, chunk, e_off,
-                                                                 gslot, (uint16_t *)entries);
+        stream_build_banked_kernel<true><<<bgrid, BB_WARPS * 32, 0, s>>>(
+            words, go, perm, po, block_count, tile_count, bitwidth, e_off, gslot,
+            (uint16_t *)entries, col0_key);
     else if (format == 0)
-        stream_build_kernel<uint16_t, false><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
-                                                           tile_count, bitwidth, chunk, e_off,
-                                                           gslot, (uint16_t *)entries);
-    else if (format == 2)
+        stream_build_banked_kernel<false><<<bgrid, BB_WARPS * 32, 0, s>>>(
+            words, go, perm, po, block_count, tile_count, bitwidth, e_off, gslot,
+            (uint16_t *)entries, col0_key);
+    else
         stream_build_kernel<uint32_t, false><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
                                                            tile_count, bitwidth, chunk, e_off,
                                                            gslot, (uint32_t *)entries);
-    else
-        return RSR_ERR_INVALID;
     return launch_status();
 }
 

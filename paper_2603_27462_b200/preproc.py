@@ -211,25 +211,31 @@ class RsrArtifact:
         self.chunk = 32 // self.entry_bytes
         e_off = torch.zeros(cells + 1, dtype=torch.int64, device=dev)
         gslot = torch.empty(max(self.n_words, 1), dtype=torch.int32, device=dev)
-        _lib.check(L.rsr_stream_count(_lib.ptr(self.words_d), _lib.ptr(self.go_d), p.block_count,
-                                      p.tile_count, self.chunk, _lib.ptr(e_off), _lib.ptr(gslot),
-                                      s), "stream_count")
+        _lib.check(L.rsr_stream_count(_lib.ptr(self.words_d), _lib.ptr(self.go_d),
+                                      _lib.ptr(self.perm_d), _lib.ptr(self.po_d), p.block_count,
+                                      p.tile_count, self.format, self.chunk, _lib.ptr(e_off),
+                                      _lib.ptr(gslot), s), "stream_count")
         ne = int(e_off[-1].item())
         edt = torch.int16 if self.entry_bytes == 2 else torch.int32
         entries = torch.empty(max(ne, self.chunk), dtype=edt, device=dev)
+        # u16 formats: pattern key of each cell's column 0 (quad layout)
+        col0 = torch.zeros(cells if self.format != 2 else 1, dtype=torch.int32, device=dev)
         _lib.check(L.rsr_stream_build(_lib.ptr(self.words_d), _lib.ptr(self.go_d),
                                       _lib.ptr(self.perm_d), _lib.ptr(self.po_d), p.block_count,
                                       p.tile_count, bw, self.format, self.chunk,
-                                      _lib.ptr(e_off), _lib.ptr(gslot), _lib.ptr(entries), s),
+                                      _lib.ptr(e_off), _lib.ptr(gslot), _lib.ptr(entries),
+                                      _lib.ptr(col0) if self.format != 2 else None, s),
                    "stream_build")
         del gslot
         self.entries_d, self.e_off_d = entries, e_off
+        self.col0_d = col0 if self.format != 2 else None
         self._view = self.view()
 
     def stream_bytes(self) -> int:
         """Bytes of the device chunk stream one multiply reads."""
         return int(self.entries_d.numel() * self.entries_d.element_size()
-                   + self.e_off_d.numel() * 8)
+                   + self.e_off_d.numel() * 8
+                   + (0 if self.col0_d is None else self.col0_d.numel() * 4))
 
     def view(self, block_begin: int = 0, n_blocks: int | None = None,
              entries=None, e_off=None) -> _lib.StreamView:
@@ -246,6 +252,8 @@ class RsrArtifact:
         v.entries = _lib.ptr(self.entries_d if entries is None else entries)
         # a block range starts at cell block_begin*tc of the block-major order
         v.e_off = _lib.ptr(self.e_off_d if e_off is None else e_off) + 8 * block_begin * p.tile_count
+        v.col0_key = (None if self.col0_d is None
+                      else _lib.ptr(self.col0_d) + 4 * block_begin * p.tile_count)
         v.row_begin_block = block_begin
         v.n_blocks = n_blocks
         return v

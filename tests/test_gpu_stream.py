@@ -1,0 +1,159 @@
+"""Structure of the device chunk stream (include/rsr_b200.h).
+
+The stream is ours (the reference has no device format), so these tests pin
+its invariants by decoding it on the host: every cell holds exactly the
+reference groups (key -> column set, paper's Step 1/2 output in
+pkg/src/rsrmv/preproc.py:239-289) and the layout rules hold -- u16 formats
+(quad layout): every chunk pair starts with a key, keys only at slots = 0 mod
+4, inside a pair each key starts a new group, column 0 is padding and the
+cell's real column 0 is in col0_key; u32 (even layout): every chunk starts
+with a key, keys at even slots, padding key 0 / column 0.  The bank-aware
+column order keeps the shared-memory gathers near conflict-free.
+"""
+import numpy as np
+import pytest
+
+from oracle import rsr_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rsr():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_27462_b200 as rsr
+    return rsr
+
+
+def phys_slots(nent, CH):
+    """numpy restatement of phys_slot() (csrc/rsr_preprocess.cu)."""
+    p = np.arange(nent, dtype=np.int64)
+    nch = nent // CH
+    c, js = p // CH, p % CH
+    pair, cin = c >> 1, c & 1
+    r, lanep = pair >> 5, pair & 31
+    np_ = np.minimum(32, (nch >> 1) - (r << 5))
+    qe = CH >> 1
+    q = cin * 2 + js // qe
+    return r * 64 * CH + q * np_ * qe + lanep * qe + js % qe
+
+
+def dense_key(w, bitwidth_binary):
+    pos, neg = (w >> 32) & 0xFFFF, w >> 48
+    if bitwidth_binary:
+        return int(pos)
+    key, p3 = 0, 1
+    for i in range(16):
+        key += (((pos >> i) & 1) + 2 * ((neg >> i) & 1)) * p3
+        p3 *= 3
+    return int(key)
+
+
+def decode_cell(ent, fmt):
+    """-> list of (is_key, value) in logical order."""
+    out = []
+    for x in ent:
+        x = int(x)
+        if fmt == 1:
+            out.append((True, x >> 2) if x & 1 else (False, x >> 2))
+        elif fmt == 0:
+            out.append((True, x & 0x7FFF) if x & 0x8000 else (False, x))
+        else:
+            out.append((True, x & 0x7FFFFFFF) if x & 0x80000000 else (False, x))
+    return out
+
+
+def wavefronts(seq, CH):
+    """Mean shared-memory wavefronts per gather instruction of one cell
+    (max over banks of distinct columns read at one slot across the lanes)."""
+    slots = 2 * CH
+    tot = n = 0
+    for r0 in range(0, len(seq), 32 * slots):
+        rnd = seq[r0:r0 + 32 * slots]
+        nl = len(rnd) // slots
+        for j in range(slots):
+            banks = {}
+            for L in range(nl):
+                isk, val = rnd[slots * L + j]
+                if not isk:
+                    banks.setdefault(val % 32, set()).add(val)
+            tot += max([1] + [len(v) for v in banks.values()])
+            n += 1
+    return tot / max(n, 1)
+
+
+def check_stream(a, binary):
+    fmt, CH = a.format, a.chunk
+    quad = fmt != 2
+    ent = a.entries_d.cpu().numpy().view(np.uint16 if a.entry_bytes == 2 else np.uint32)
+    e_off = a.e_off_d.cpu().numpy()
+    col0 = a.col0_d.cpu().numpy() if quad else None
+    go, po = a.group_offsets, a.perm_offsets
+    words, perm = a.words, a.perm
+    bc, tc = a.plan.block_count, a.plan.tile_count
+    wfs = []
+    for dc in range(bc * tc):
+        b, t = divmod(dc, tc)
+        src = t * bc + b
+        e0, e1 = int(e_off[dc]), int(e_off[dc + 1])
+        assert (e1 - e0) % (2 * CH) == 0
+        cell = ent[e0:e1]
+        seq = decode_cell(cell[phys_slots(e1 - e0, CH)], fmt)
+        exp, key0 = {}, 0
+        for g in range(go[src], go[src + 1]):
+            w = int(words[g])
+            ps, L = w & 0xFFFF, (w >> 16) & 0xFFFF
+            cols = sorted(int(c) for c in perm[po[src] + ps: po[src] + ps + L])
+            key = dense_key(w, binary)
+            if quad and cols[0] == 0:
+                key0, cols = key, cols[1:]
+            if cols:
+                exp[key] = cols
+        got, seen = {}, set()
+        cur = None
+        for i, (isk, val) in enumerate(seq):
+            if i % (2 * CH if quad else CH) == 0:
+                assert isk, f"cell {dc}: slot {i} must hold a key"
+            if isk:
+                assert i % (4 if quad else 2) == 0, f"cell {dc}: key at slot {i}"
+                if quad and i % 32:
+                    assert val not in seen, f"cell {dc}: repeated key inside a pair at {i}"
+                cur = val
+                seen.add(val)
+                continue
+            if (quad and val == 0) or cur == 0:
+                assert val == 0, "padding must be column 0"
+                continue
+            got.setdefault(cur, []).append(val)
+        got = {k: sorted(v) for k, v in got.items()}
+        assert got == exp, f"cell {dc}: groups differ"
+        if quad:
+            assert int(col0[dc]) == key0, f"cell {dc}: col0_key"
+        if quad and len(seq) >= 2048:
+            wfs.append(wavefronts(seq, CH))
+    return wfs
+
+
+@pytest.mark.parametrize("m,n,k,bw,tw", [
+    (96, 3000, 6, "ternary", None),
+    (64, 4096, 8, "binary", None),
+    (40, 20000, 5, "ternary", 20000),   # format 0 (tile > 16384)
+    (30, 5000, 12, "binary", None),      # format 0 (keys > 2187)
+    (24, 40000, 4, "ternary", 40000),    # format 2 (tile > 32768)
+])
+def test_stream_structure(rsr, m, n, k, bw, tw):
+    p = orc.random_matrix(m, n, bw, m * 7 + n)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k, tw)
+    check_stream(a, bw == "binary")
+
+
+def test_bank_aware_order(rsr):
+    """Random ternary 16384-wide cells: gathers average well under the ~3.3
+    wavefronts a key-sorted column order costs (tools/bank_sim.py)."""
+    p = orc.random_matrix(12, 16384, "ternary", 5)
+    a = rsr.preprocess(rsr.PackedMatrix(12, 16384, "ternary", p.data), 6)
+    assert a.format == 1
+    wfs = check_stream(a, False)
+    assert wfs and float(np.mean(wfs)) < 2.2, wfs
