@@ -124,8 +124,6 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     {
         static const int dbg = getenv("RSR_MV_DEBUG") ? atoi(getenv("RSR_MV_DEBUG")) : 0;
         p.dbg = dbg;
-        static const int pf = getenv("RSR_MV_PF") ? atoi(getenv("RSR_MV_PF")) : 4;
-        p.pf = pf;
     }
     if (MODE == MODE_FUSED && !p.scale_dev && need_ws)
         p.scale_dev = (double *)((char *)ws + part_bytes(vw));
@@ -150,15 +148,11 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     const int64_t tn = std::min(vw->tile_width, vw->n);
     const bool ring = bucket && vw->format != FMT_U32;
     const size_t vsz = (vw->format == FMT_U16_SCALED || MODE == MODE_FLOAT) ? 4 : 1;
-    const size_t kp = (size_t)((vw->k + 3) & ~3);
     size_t fixed = 0;
     if (vw->format != FMT_U32) fixed += ((size_t)tn * vsz + 15) & ~(size_t)15;
-    if (bucket) fixed += (size_t)p.nkeys * kp * 4;
+    if (bucket) fixed += ((size_t)p.nkeys * vw->k * 4 + 15) & ~(size_t)15;
     size_t per_warp = bucket ? (size_t)p.nkeys * 4 : 0;
-    static const int ring_stages = getenv("RSR_MV_STAGES") ? atoi(getenv("RSR_MV_STAGES")) : RING_STAGES;
-    p.stages = ring_stages;
-    if (ring) per_warp += ring_stages * (RING_STAGE_BYTES + 8) + 16 * 4;
-    fixed += 16;  // alignment slack (mbarriers)
+    if (ring) per_warp += 16 * 4;  // team exchange
     const size_t smem_cap = 227 * 1024;
     const int64_t cells_per_tile = vw->n_blocks;
     const int64_t cta_cap = std::max<int64_t>(1, sms / vw->tile_count);

@@ -12,36 +12,12 @@
 
 namespace rsr {
 
-// ---- TMA (cp.async.bulk) + mbarrier helpers ---------------------------------
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tRSR_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra RSR_WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-// 1-D bulk copy global -> shared, completion signalled on `bar` (transaction bytes).
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
-                                         uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+// Streaming 16-byte load of the chunk stream: read once, not kept in L1.
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
     uint4 r;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "r"(addr));
+                 : "l"(p));
     return r;
 }
 
@@ -71,8 +47,6 @@ __device__ __forceinline__ double cta_reduce_max(double a) {
     return r;
 }
 
-constexpr int RING_STAGES = 2;     // rounds in flight per warp (bucket path)
-constexpr int RING_STAGE_BYTES = 2048;  // one round = 64 chunks x 32 bytes
 
 template <int K, int MODE, int FMT, bool BUCKET>
 __global__ void __launch_bounds__(MV_MAX_WARPS * 32)
@@ -82,9 +56,7 @@ rsr_mv_kernel(MvParams p) {
     constexpr int VSZ = T::VSZ;
     constexpr bool SMEM_V = T::SMEM_V;
     constexpr int CH = FMT == FMT_U32 ? 8 : 16;  // entries per 32-byte chunk
-    constexpr int KP = KPad<K>::value;
     constexpr bool RING = FMT != FMT_U32 && BUCKET;
-    const int S = p.stages;  // ring depth (rounds in flight per warp)
 
     extern __shared__ __align__(128) unsigned char mv_smem[];
     const int nwarps = blockDim.x >> 5;
@@ -105,28 +77,20 @@ rsr_mv_kernel(MvParams p) {
     };
     probe(0);
 
-    // smem: [ring W x S x 1KB][v tile][sign table NB x KP][buckets W x NB][mbarriers W x S]
+    // smem: [v tile][sign table K x NB][buckets W x NB][team exchange W x 16]
     size_t off = 0;
-    unsigned char *ringsm = mv_smem;
-    if constexpr (RING) off += (size_t)nwarps * S * RING_STAGE_BYTES;
     unsigned char *vsm = mv_smem + off;
     if constexpr (SMEM_V) off += ((size_t)tn * VSZ + 15) & ~(size_t)15;
     Acc *__restrict__ stab = reinterpret_cast<Acc *>(mv_smem + off);
-    if constexpr (BUCKET) off += (size_t)p.nkeys * KP * sizeof(Acc);
+    if constexpr (BUCKET) off += ((size_t)p.nkeys * K * sizeof(Acc) + 15) & ~(size_t)15;
     Acc *__restrict__ buckets = reinterpret_cast<Acc *>(mv_smem + off);
     if constexpr (BUCKET) off += (size_t)nwarps * p.nkeys * sizeof(Acc);
     Acc *__restrict__ xch = reinterpret_cast<Acc *>(mv_smem + off);  // team exchange [W][16]
-    if constexpr (RING) off += (size_t)nwarps * 16 * sizeof(Acc);
-    off = (off + 7) & ~(size_t)7;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(mv_smem + off) + (size_t)warp * S;
     Acc *bk = buckets + (size_t)warp * p.nkeys;
     const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
     uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
-    const uint32_t ringbase =
-        (uint32_t)__cvta_generic_to_shared(ringsm) + (uint32_t)(warp * S * RING_STAGE_BYTES);
-    const uint32_t barbase = (uint32_t)__cvta_generic_to_shared(bars);
 
-    // Teams (ring path): `team` consecutive warps share one cell; warp `sub`
+    // Teams (bucket path): `team` consecutive warps share one cell; warp `sub`
     // of the team takes rounds sub, sub+team, ... with its own buckets, and
     // the team's k-row partials are combined in a fixed order at the end.
     const int team = RING ? p.team : 1;
@@ -143,40 +107,49 @@ rsr_mv_kernel(MvParams p) {
         bkbase = (uint32_t)__cvta_generic_to_shared(bk);
     }
 
-    // ---- stream producer (lane 0 of each warp feeds its own ring) -----------
-    // Walks this warp's rounds of its cells (b, b + cstride, ...), S rounds
-    // ahead of the consumer; each round (64 chunks) is one 1-D bulk copy (TMA)
-    // into a 2 KiB stage whose mbarrier completes on the transaction bytes.
-    int64_t pb = b, pbase = 0, pend = 0;
-    if (RING && lane == 0 && pb < p.nblk) {
-        const int64_t dc = pb * p.tc + t;
-        pbase = p.e_off[dc] / CH + 64 * sub;
-        pend = p.e_off[dc + 1] / CH;
-    }
-    auto produce = [&](int stage) {
-        while (pb < p.nblk && pbase >= pend) {
-            pb += cstride;
-            if (pb < p.nblk) {
-                const int64_t dc = pb * p.tc + t;
-                pbase = p.e_off[dc] / CH + 64 * sub;
-                pend = p.e_off[dc + 1] / CH;
+    // ---- stream fetch (bucket path) ------------------------------------------
+    // Each warp walks its rounds (cells b, b + cstride, ...; rounds sub, sub +
+    // team, ... of each) one round ahead: a round is 64 chunks, lane L loads
+    // its chunk pair as four coalesced 16-byte quarters straight into
+    // registers (no shared-memory staging: the L1 data pipe is the bottleneck
+    // resource of this kernel, and a TMA copy into shared memory costs it
+    // twice).  Pairs past the cell end read as zeros.
+    uint4 qa[4], qb[4];  // ping-pong round buffers (the prefetched round is in qa)
+    // chunk indices are 32-bit (a view's stream stays below 2^32 chunks = 128 GiB)
+    int64_t fb = b;                  // cell of the prefetched round
+    uint32_t fbase = 0, fend = 0;    // its first chunk / the cell's end chunk
+    constexpr int CSH = CH == 16 ? 4 : 3;  // log2(CH)
+    auto fetch = [&](int64_t cb) {  // first round of this warp in cells cb, cb + cstride, ...
+        fb = cb;
+        while (fb < p.nblk) {
+            const int64_t dc = fb * p.tc + t;
+            fbase = (uint32_t)(p.e_off[dc] >> CSH) + 64u * sub;
+            fend = (uint32_t)(p.e_off[dc + 1] >> CSH);
+            if (fbase < fend) break;
+            fb += cstride;
+        }
+    };
+    auto load_round = [&](uint4 (&nq)[4]) {
+        if (fb >= p.nblk) return;  // nothing left: the stale registers are never consumed
+        const uint4 *src = ent4 + 2 * (size_t)fbase + lane;
+        const uint32_t rem = fend - fbase;
+        if (rem >= 64u) {  // full round
+#pragma unroll
+            for (int j = 0; j < 4; ++j) nq[j] = ld_stream(src + 32 * j);
+        } else {           // the cell's last, partial round: pairs past the end read as zeros
+            const uint32_t np = rem >> 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) nq[j] = make_uint4(0, 0, 0, 0);
+            if (lane < np) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) nq[j] = ld_stream(src + j * np);
             }
         }
-        if (pb >= p.nblk) return;
-        const uint32_t bytes = (uint32_t)(min((int64_t)64, pend - pbase) * 32);
-        const uint32_t bar = barbase + stage * 8;
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(ringbase + stage * RING_STAGE_BYTES, ent4 + 2 * pbase, bytes, bar);
-        pbase += 64 * team;
     };
     auto start_stream = [&]() {
         if constexpr (RING) {
-            if (lane == 0) {
-                for (int s = 0; s < S; ++s) mbar_init(barbase + s * 8, 1);
-                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-                for (int s = 0; s < S; ++s) produce(s);
-            }
-            __syncwarp();
+            fetch(b);
+            load_round(qa);
         }
     };
     const bool fine = RSR_DBG(p, 256);  // debug: finer prologue timeline
@@ -295,7 +268,7 @@ rsr_mv_kernel(MvParams p) {
         for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
             uint32_t kk = (uint32_t)key;
 #pragma unroll
-            for (int i = 0; i < KP; ++i) {
+            for (int i = 0; i < K; ++i) {
                 int sg = 0;
                 if (p.bitwidth == RSR_BINARY) {
                     sg = (int)((kk >> i) & 1u);
@@ -304,7 +277,7 @@ rsr_mv_kernel(MvParams p) {
                     kk = q3;
                     sg = d == 1u ? 1 : (d == 2u ? -1 : 0);
                 }
-                stab[key * KP + i] = (Acc)(i < K ? sg : 0);
+                stab[i * p.nkeys + key] = (Acc)sg;  // row-major: lanes read consecutive keys
             }
         }
         for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
@@ -349,9 +322,8 @@ rsr_mv_kernel(MvParams p) {
             for (int key = kfirst; key < (RSR_DBG(p, 4) ? 0 : p.nkeys); key += kstep) {
                 const Acc bv = key ? bk[key] : (Acc)0;
                 bk[key] = (Acc)0;
-                const Acc *row = stab + key * KP;
 #pragma unroll
-                for (int i = 0; i < K; ++i) acc[i] += row[i] * bv;
+                for (int i = 0; i < K; ++i) acc[i] += stab[i * p.nkeys + key] * bv;
             }
             __syncwarp();
         } else if constexpr (SMEM_V) {
@@ -410,31 +382,16 @@ rsr_mv_kernel(MvParams p) {
         auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
         auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
         auto gat = [&](uint32_t off) -> Acc { return lds_v<Acc, VSZ>(vbase + off); };
-        int stage = 0;      // ring position of this warp's next round
-        uint32_t phase = 0; // mbarrier phase parity of that stage
         for (; b < p.nblk; b += cstride) {
             const int64_t dc = b * p.tc + t;
-            const int64_t ch0 = p.e_off[dc] / CH, ch1 = p.e_off[dc + 1] / CH;
+            const uint32_t ch0 = (uint32_t)(p.e_off[dc] >> CSH), ch1 = (uint32_t)(p.e_off[dc + 1] >> CSH);
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            for (int64_t base = ch0 + 64 * sub; base < ch1; base += 64 * team) {
-                mbar_wait(barbase + stage * 8, phase);
-                const uint32_t np = (uint32_t)min((int64_t)64, ch1 - base) >> 1;  // chunk pairs
-                const uint32_t st = ringbase + stage * RING_STAGE_BYTES + lane * 16;
-                uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, a2 = a0, a3 = a0;
-                if (lane < np) {
-                    a0 = lds128(st);
-                    a1 = lds128(st + np * 16);
-                    a2 = lds128(st + np * 32);
-                    a3 = lds128(st + np * 48);
-                }
-                __syncwarp();
-                if (lane == 0) produce(stage);  // refill the stage just drained
-                if (++stage == S) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
+            // two rounds per iteration with ping-pong buffers: no register
+            // copies between the prefetch and the round being processed
+            auto do_round = [&](const uint4 (&q)[4]) {
+                const uint4 a0 = q[0], a1 = q[1], a2 = q[2], a3 = q[3];
                 // Pairs past the cell end are zeros: key 0 with column-0 (zero)
                 // gathers, flushed into bucket 0 (never reduced) -- no divergence.
                 const uint32_t w[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
@@ -445,7 +402,7 @@ rsr_mv_kernel(MvParams p) {
                     for (int i = 0; i < 16; ++i) x ^= w[i];
                     acc[0] += (Acc)x;
                     __syncwarp();
-                    continue;
+                    return;
                 }
                 uint32_t cur = key_off(w[0]);
                 Acc s = gat(hi_off(w[0])) + (gat(lo_off(w[1])) + gat(hi_off(w[1])));
@@ -454,9 +411,12 @@ rsr_mv_kernel(MvParams p) {
 #pragma unroll
                 for (int q = 1; q < 8; ++q) {
                     const uint32_t x = w[2 * q], y = w[2 * q + 1];
-                    const uint32_t isk = is_key(x);
+                    const bool isk = is_key(x) != 0u;
                     const uint32_t ko = key_off(x);
-                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
+                    // scaled format: a key's offset (key*4 < the v + sign-table
+                    // span) is a harmless in-bounds read, so slot 4q is gathered
+                    // unconditionally and discarded by the select below
+                    const Acc g = SC ? gat(ko) : lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
                     const Acc t3 = gat(hi_off(x)) + (gat(lo_off(y)) + gat(hi_off(y)));
                     if constexpr (MODE == MODE_FLOAT) {
                         // record completed segments; flushed below as one batch
@@ -466,7 +426,7 @@ rsr_mv_kernel(MvParams p) {
                         bucket_flush_pred(isk, bkbase + cur, s);  // native shared red
                     }
                     cur = isk ? ko : cur;
-                    s = (isk ? (Acc)0 : s) + g + t3;
+                    s = (isk ? (Acc)0 : s + g) + t3;
                 }
                 if constexpr (MODE == MODE_FLOAT) {
                     // all bucket loads, then all adds/stores: one latency per
@@ -475,12 +435,14 @@ rsr_mv_kernel(MvParams p) {
                     // per round), bucket 0 aside.
                     if (!RSR_DBG(p, 1)) {
                         float tb[7];
+                        uint32_t ta[7];
 #pragma unroll
-                        for (int i = 0; i < 7; ++i) tb[i] = lds_bucket(bkbase + fk[i]);
+                        for (int i = 0; i < 7; ++i) ta[i] = bkbase + fk[i];
+                        lds_bucket7(ta, tb);
 #pragma unroll
                         for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
                     }
-                    if (RSR_DBG(p, 2)) { acc[0] += s; __syncwarp(); continue; }
+                    if (RSR_DBG(p, 2)) { acc[0] += s; __syncwarp(); return; }
                     // The pair's last segment may continue in the next lane's
                     // pair: equal final keys form contiguous lane runs; a
                     // segmented suffix sum lets each run's first lane flush
@@ -499,6 +461,25 @@ rsr_mv_kernel(MvParams p) {
                     bucket_flush_final(bkbase + cur, s);  // native red handles same keys
                 }
                 __syncwarp();
+            };
+            auto advance = [&](uint4 (&nq)[4]) {  // prefetch this warp's next round
+                fbase += 64u * team;
+                if (fbase >= fend) fetch(fb + cstride);
+                load_round(nq);
+            };
+            uint32_t base = ch0 + 64u * sub;
+            while (base < ch1) {
+                advance(qb);
+                do_round(qa);
+                base += 64u * team;
+                if (base >= ch1) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) qa[j] = qb[j];
+                    break;
+                }
+                advance(qa);
+                do_round(qb);
+                base += 64u * team;
             }
             asm volatile("" ::: "memory");
             finish_cell(b, acc);
