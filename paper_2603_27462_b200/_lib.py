@@ -15,7 +15,9 @@ import os
 from .errors import CorruptArtifact, DimensionMismatch, KTooLarge, RsrError, TileTooWide
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librsr_b200.so")
+# RSR_B200_LIB selects another build of the same library (tools/ experiments
+# use the knob-enabled librsr_b200_exp.so); the default is the in-tree build.
+LIB_PATH = os.environ.get("RSR_B200_LIB") or os.path.join(_HERE, "librsr_b200.so")
 
 RSR_OK = 0
 RSR_ERR_TILE_TOO_WIDE = 1

@@ -124,6 +124,8 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     {
         static const int dbg = getenv("RSR_MV_DEBUG") ? atoi(getenv("RSR_MV_DEBUG")) : 0;
         p.dbg = dbg;
+        static const int pf = getenv("RSR_MV_PF") ? atoi(getenv("RSR_MV_PF")) : 0;
+        p.pf = pf;
     }
     if (MODE == MODE_FUSED && !p.scale_dev && need_ws)
         p.scale_dev = (double *)((char *)ws + part_bytes(vw));

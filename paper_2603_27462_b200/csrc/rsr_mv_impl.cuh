@@ -67,7 +67,8 @@ struct MvParams {
     double beta;         // fused
     double *scale_dev;   // fused: device scale slot (may be null when tc == 1)
     int dbg;             // experiment knobs (RSR_MV_DEBUG); 0 in production
-    int team;            // warps per cell (ring path): 1, 2, 4 or 8
+    int team;            // warps per cell (bucket path): 1, 2, 4 or 8
+    int pf;              // L2 prefetch distance in rounds (0 = off)
     const double *row_beta;  // fused: per-row beta (sibling stacks), or null
     int out_bf16;        // fused: write bf16 instead of f32
     unsigned long long *probe;  // debug timeline (rsr_debug_set_probe), null in production
@@ -202,14 +203,15 @@ __device__ __forceinline__ float lds_bucket(uint32_t addr) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(addr));
     return r;
 }
-// Seven bucket loads issued back to back (one latency for the whole batch).
-__device__ __forceinline__ void lds_bucket7(const uint32_t (&a)[7], float (&r)[7]) {
+// Eight bucket loads issued back to back (one latency for the whole batch).
+__device__ __forceinline__ void lds_bucket8(const uint32_t (&a)[8], float (&r)[8]) {
     asm volatile(
-        "ld.shared.f32 %0, [%7];\n\tld.shared.f32 %1, [%8];\n\tld.shared.f32 %2, [%9];\n\t"
-        "ld.shared.f32 %3, [%10];\n\tld.shared.f32 %4, [%11];\n\tld.shared.f32 %5, [%12];\n\t"
-        "ld.shared.f32 %6, [%13];"
-        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]));
+        "ld.shared.f32 %0, [%8];\n\tld.shared.f32 %1, [%9];\n\tld.shared.f32 %2, [%10];\n\t"
+        "ld.shared.f32 %3, [%11];\n\tld.shared.f32 %4, [%12];\n\tld.shared.f32 %5, [%13];\n\t"
+        "ld.shared.f32 %6, [%14];\n\tld.shared.f32 %7, [%15];"
+        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+          "=f"(r[7])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
 }
 __device__ __forceinline__ void sts_bucket(uint32_t addr, float x) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(x));

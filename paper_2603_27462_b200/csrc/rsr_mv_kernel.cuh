@@ -108,36 +108,55 @@ rsr_mv_kernel(MvParams p) {
     }
 
     // ---- stream fetch (bucket path) ------------------------------------------
-    // Each warp walks its rounds (cells b, b + cstride, ...; rounds sub, sub +
-    // team, ... of each) one round ahead: a round is 64 chunks, lane L loads
-    // its chunk pair as four coalesced 16-byte quarters straight into
+    // Lane-run layout (run_slot in rsr_preprocess.cu): a cell of N chunk pairs
+    // takes P = ceil(N/32) rounds; lane L owns pairs [L*P, L*P + len_L), and
+    // round r holds np_r = Lf + (r < rem) pairs as four coalesced 16-byte
+    // quarters.  A team of warps splits a cell's rounds into contiguous
+    // ranges.  Each warp fetches its next round one round ahead straight into
     // registers (no shared-memory staging: the L1 data pipe is the bottleneck
-    // resource of this kernel, and a TMA copy into shared memory costs it
-    // twice).  Pairs past the cell end read as zeros.
+    // resource of this kernel).  Lanes past np_r read zeros (key 0 / column 0).
+    struct Cell {
+        int64_t b;          // cell (block index in the view)
+        uint32_t c0;        // first chunk
+        uint32_t P, Lf, rem;
+        uint32_t r0, r1;    // this warp's rounds
+    };
+    constexpr int CSH = CH == 16 ? 4 : 3;  // log2(CH); chunk indices are 32-bit
+    auto cell_at = [&](int64_t cb, int64_t e0, int64_t e1) {
+        Cell c;
+        c.b = cb;
+        c.c0 = (uint32_t)(e0 >> CSH);
+        const uint32_t N = ((uint32_t)(e1 >> CSH) - c.c0) >> 1;
+        c.P = (N + 31u) >> 5;
+        c.Lf = c.P ? N / c.P : 0u;
+        c.rem = N - c.Lf * c.P;
+        c.r0 = (uint32_t)(((uint64_t)c.P * sub) / team);
+        c.r1 = (uint32_t)(((uint64_t)c.P * (sub + 1)) / team);
+        return c;
+    };
+    Cell fc;          // cell of the prefetched round
+    uint32_t fr = 0;  // the prefetched round
     uint4 qa[4], qb[4];  // ping-pong round buffers (the prefetched round is in qa)
-    // chunk indices are 32-bit (a view's stream stays below 2^32 chunks = 128 GiB)
-    int64_t fb = b;                  // cell of the prefetched round
-    uint32_t fbase = 0, fend = 0;    // its first chunk / the cell's end chunk
-    constexpr int CSH = CH == 16 ? 4 : 3;  // log2(CH)
-    auto fetch = [&](int64_t cb) {  // first round of this warp in cells cb, cb + cstride, ...
-        fb = cb;
-        while (fb < p.nblk) {
-            const int64_t dc = fb * p.tc + t;
-            fbase = (uint32_t)(p.e_off[dc] >> CSH) + 64u * sub;
-            fend = (uint32_t)(p.e_off[dc + 1] >> CSH);
-            if (fbase < fend) break;
-            fb += cstride;
+    auto seek = [&](int64_t cb) {  // first round of this warp in cells cb, cb + cstride, ...
+        fc.b = cb;
+        while (cb < p.nblk) {
+            const int64_t dc = cb * p.tc + t;
+            fc = cell_at(cb, p.e_off[dc], p.e_off[dc + 1]);
+            if (fc.r0 < fc.r1) break;
+            cb += cstride;
+            fc.b = cb;
         }
+        fr = fc.r0;
     };
     auto load_round = [&](uint4 (&nq)[4]) {
-        if (fb >= p.nblk) return;  // nothing left: the stale registers are never consumed
-        const uint4 *src = ent4 + 2 * (size_t)fbase + lane;
-        const uint32_t rem = fend - fbase;
-        if (rem >= 64u) {  // full round
+        if (fc.b >= p.nblk) return;  // nothing left: the stale registers are never consumed
+        const uint32_t np = fc.Lf + (fr < fc.rem ? 1u : 0u);
+        const uint32_t R = fr * fc.Lf + min(fr, fc.rem);
+        const uint4 *src = ent4 + 2 * ((size_t)fc.c0 + 2 * (size_t)R) + lane;
+        if (np == 32u) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) nq[j] = ld_stream(src + 32 * j);
-        } else {           // the cell's last, partial round: pairs past the end read as zeros
-            const uint32_t np = rem >> 1;
+        } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j) nq[j] = make_uint4(0, 0, 0, 0);
             if (lane < np) {
@@ -146,18 +165,57 @@ rsr_mv_kernel(MvParams p) {
             }
         }
     };
+    // the first cell's offsets are requested up front (consumed by start_stream)
+    int64_t pre0 = 0, pre1 = 0;
+    if (RING && b < p.nblk) {
+        pre0 = __ldg(p.e_off + b * p.tc + t);
+        pre1 = __ldg(p.e_off + b * p.tc + t + 1);
+    }
+    bool stream_started = false;
     auto start_stream = [&]() {
+        if (stream_started) return;
+        stream_started = true;
         if constexpr (RING) {
-            fetch(b);
+            fc.b = p.nblk;
+            if (b < p.nblk) {
+                fc = cell_at(b, pre0, pre1);
+                fr = fc.r0;
+                if (fc.r0 >= fc.r1) seek(b + cstride);
+            }
             load_round(qa);
+        }
+    };
+    // sign table + zeroed buckets (no global loads: issued while v is in flight)
+    bool tables_done = false;
+    auto init_tables = [&]() {
+        if (tables_done) return;
+        tables_done = true;
+        if constexpr (BUCKET) {
+            for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
+                uint32_t kk = (uint32_t)key;
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    int sg = 0;
+                    if (p.bitwidth == RSR_BINARY) {
+                        sg = (int)((kk >> i) & 1u);
+                    } else {
+                        const uint32_t q3 = kk / 3u, d = kk - 3u * q3;
+                        kk = q3;
+                        sg = d == 1u ? 1 : (d == 2u ? -1 : 0);
+                    }
+                    stab[i * p.nkeys + key] = (Acc)sg;  // row-major: lanes read consecutive keys
+                }
+            }
+            for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
         }
     };
     const bool fine = RSR_DBG(p, 256);  // debug: finer prologue timeline
 
     // ---- prologue -------------------------------------------------------
-    // The float path's v loads are issued first (vectorized, into registers),
-    // then the entry stream is started, then v is converted into shared
-    // memory: the stream's burst of bulk copies must not queue ahead of v.
+    // The float path's v loads are issued first (vectorized, into registers);
+    // the sign table and buckets are initialised while they are in flight;
+    // v is converted into shared memory and only then is the first stream
+    // round requested.
     double scale = 1.0;
     bool vstaged_float = false;
     if constexpr (MODE == MODE_FLOAT && SMEM_V && VSZ == 4) {
@@ -177,10 +235,7 @@ rsr_mv_kernel(MvParams p) {
                     r[u] = i < nvec ? __ldg(reinterpret_cast<const uint4 *>(src) + i)
                                     : make_uint4(0, 0, 0, 0);
                 }
-                if (!started) {
-                    start_stream();
-                    started = true;
-                }
+                init_tables();  // ALU + shared stores while v is in flight
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int64_t i = i0 + u * nt;
@@ -208,14 +263,17 @@ rsr_mv_kernel(MvParams p) {
                         }
                     }
                 }
+                if (!started) {  // v has arrived: now request the stream
+                    start_stream();
+                    started = true;
+                }
             }
-            if (!started) start_stream();
             for (int64_t i = nvec * epv + threadIdx.x; i < tn; i += nt)  // tail
                 reinterpret_cast<float *>(vsm)[i] = load_as_f32(p.v, p.vdtype, c0 + i);
             vstaged_float = true;
         }
     }
-    if (!vstaged_float) start_stream();
+    init_tables();  // (no-op when the vectorized staging already did it)
     if (fine) probe(1);
     // Fused path with one tile and 4-byte staging: a single pass over v stages
     // it as f32 while tracking |v|max, then quantizes in place.
@@ -264,24 +322,9 @@ rsr_mv_kernel(MvParams p) {
         }
     }
     if (fine) probe(2);
-    if constexpr (BUCKET) {
-        for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
-            uint32_t kk = (uint32_t)key;
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-                int sg = 0;
-                if (p.bitwidth == RSR_BINARY) {
-                    sg = (int)((kk >> i) & 1u);
-                } else {
-                    const uint32_t q3 = kk / 3u, d = kk - 3u * q3;
-                    kk = q3;
-                    sg = d == 1u ? 1 : (d == 2u ? -1 : 0);
-                }
-                stab[i * p.nkeys + key] = (Acc)sg;  // row-major: lanes read consecutive keys
-            }
-        }
-        for (int i = threadIdx.x; i < nwarps * p.nkeys; i += blockDim.x) buckets[i] = (Acc)0;
-    }
+    // The stream is requested once v is in (its burst would otherwise queue
+    // ahead of the v loads); its first round's latency overlaps the rest.
+    start_stream();
     // Quad layout: column 0 is the zero padding entry.  The tile's real
     // column-0 value (as staged: f32 / int8 / quantized) is added in the
     // epilogue to the bucket of col0_key[cell].  Thread 0 staged element 0.
@@ -370,12 +413,13 @@ rsr_mv_kernel(MvParams p) {
 
     if constexpr (RING) {
         // ===== bucket path =====================================================
-        // A round is 64 chunks; lane L owns the chunk pair (2L, 2L+1) = 32
-        // slots, stored as four 16-byte quarters (conflict-free 16B shared
-        // loads).  Quad layout: slot 4q (low half of word 2q) is a key or a
-        // column, slots 4q+1..4q+3 are columns; slot 0 is always a key and,
-        // inside a pair, every key starts a new group.  Scaled format: entries
-        // are byte offsets (column*4; key*4|1) straight into v and the buckets.
+        // A round gives each lane the next chunk pair (32 slots) of its run, as
+        // four 16-byte quarters.  Quad layout: slot 4q (low half of word 2q) is
+        // a key or a column, slots 4q+1..4q+3 are columns; slot 0 is always a
+        // key (a repeat of the open group's key when the group continues), and
+        // inside a pair every other key starts a new group.  The open group
+        // (cur, s) is carried from round to round.  Scaled format: entries are
+        // byte offsets (column*4; key*4|1) straight into v and the buckets.
         constexpr bool SC = FMT == FMT_U16_SCALED;
         auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
         auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
@@ -384,16 +428,16 @@ rsr_mv_kernel(MvParams p) {
         auto gat = [&](uint32_t off) -> Acc { return lds_v<Acc, VSZ>(vbase + off); };
         for (; b < p.nblk; b += cstride) {
             const int64_t dc = b * p.tc + t;
-            const uint32_t ch0 = (uint32_t)(p.e_off[dc] >> CSH), ch1 = (uint32_t)(p.e_off[dc + 1] >> CSH);
+            const Cell c = cell_at(b, p.e_off[dc], p.e_off[dc + 1]);
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            // two rounds per iteration with ping-pong buffers: no register
-            // copies between the prefetch and the round being processed
+            uint32_t cur = 0;  // open group: bucket offset (0 = the never-reduced sink)
+            Acc s = (Acc)0;    //             and its partial sum
             auto do_round = [&](const uint4 (&q)[4]) {
                 const uint4 a0 = q[0], a1 = q[1], a2 = q[2], a3 = q[3];
-                // Pairs past the cell end are zeros: key 0 with column-0 (zero)
-                // gathers, flushed into bucket 0 (never reduced) -- no divergence.
+                // Pairs past a lane's run are zeros: key 0 (the sink) at slot 0,
+                // then column-0 (zero) gathers -- no divergence.
                 const uint32_t w[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
                                         a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
                 if (RSR_DBG(p, 32)) {  // experiment: stream only
@@ -401,16 +445,25 @@ rsr_mv_kernel(MvParams p) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) x ^= w[i];
                     acc[0] += (Acc)x;
-                    __syncwarp();
                     return;
                 }
-                uint32_t cur = key_off(w[0]);
-                Acc s = gat(hi_off(w[0])) + (gat(lo_off(w[1])) + gat(hi_off(w[1])));
-                uint32_t fk[7];
-                float fs[7];
+                uint32_t fk[8];
+                float fs[8];
+                {   // slot 0: always a key; a new one closes the open group
+                    const uint32_t k0 = key_off(w[0]);
+                    const bool ns = k0 != cur;
+                    if constexpr (MODE == MODE_FLOAT) {
+                        fk[0] = ns ? cur : 0u;
+                        fs[0] = s;
+                    } else {
+                        bucket_flush_pred(ns, bkbase + cur, s);  // native shared red
+                    }
+                    cur = k0;
+                    s = (ns ? (Acc)0 : s) + (gat(hi_off(w[0])) + (gat(lo_off(w[1])) + gat(hi_off(w[1]))));
+                }
 #pragma unroll
-                for (int q = 1; q < 8; ++q) {
-                    const uint32_t x = w[2 * q], y = w[2 * q + 1];
+                for (int qd = 1; qd < 8; ++qd) {
+                    const uint32_t x = w[2 * qd], y = w[2 * qd + 1];
                     const bool isk = is_key(x) != 0u;
                     const uint32_t ko = key_off(x);
                     // scaled format: a key's offset (key*4 < the v + sign-table
@@ -419,69 +472,67 @@ rsr_mv_kernel(MvParams p) {
                     const Acc g = SC ? gat(ko) : lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
                     const Acc t3 = gat(hi_off(x)) + (gat(lo_off(y)) + gat(hi_off(y)));
                     if constexpr (MODE == MODE_FLOAT) {
-                        // record completed segments; flushed below as one batch
-                        fk[q - 1] = isk ? cur : 0u;
-                        fs[q - 1] = s;
+                        // record completed groups; flushed below as one batch
+                        fk[qd] = isk ? cur : 0u;
+                        fs[qd] = s;
                     } else {
-                        bucket_flush_pred(isk, bkbase + cur, s);  // native shared red
+                        bucket_flush_pred(isk, bkbase + cur, s);
                     }
                     cur = isk ? ko : cur;
                     s = (isk ? (Acc)0 : s + g) + t3;
                 }
                 if constexpr (MODE == MODE_FLOAT) {
                     // all bucket loads, then all adds/stores: one latency per
-                    // round.  Keys of completed segments are distinct across the
-                    // round (a group's segment ends inside a pair at most once
-                    // per round), bucket 0 aside.
+                    // round.  The keys of one round's completed groups are
+                    // distinct (a group completes once, in the lane holding its
+                    // end), bucket 0 aside.
                     if (!RSR_DBG(p, 1)) {
-                        float tb[7];
-                        uint32_t ta[7];
+                        float tb[8];
+                        uint32_t ta[8];
 #pragma unroll
-                        for (int i = 0; i < 7; ++i) ta[i] = bkbase + fk[i];
-                        lds_bucket7(ta, tb);
+                        for (int i = 0; i < 8; ++i) ta[i] = bkbase + fk[i];
+                        lds_bucket8(ta, tb);
 #pragma unroll
-                        for (int i = 0; i < 7; ++i) sts_bucket(bkbase + fk[i], tb[i] + fs[i]);
+                        for (int i = 0; i < 8; ++i) sts_bucket(ta[i], tb[i] + fs[i]);
                     }
-                    if (RSR_DBG(p, 2)) { acc[0] += s; __syncwarp(); return; }
-                    // The pair's last segment may continue in the next lane's
-                    // pair: equal final keys form contiguous lane runs; a
-                    // segmented suffix sum lets each run's first lane flush
-                    // alone (no CAS loop, fixed summation order).
-                    float sj = s;
-                    const uint32_t kj = cur;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const float os = __shfl_down_sync(RSR_FULL_MASK, sj, d);
-                        const uint32_t ok = __shfl_down_sync(RSR_FULL_MASK, kj, d);
-                        if (lane + d < 32 && ok == kj) sj += os;
-                    }
-                    const uint32_t pk = __shfl_up_sync(RSR_FULL_MASK, kj, 1);
-                    if (lane == 0 || pk != kj) sts_bucket(bkbase + kj, lds_bucket(bkbase + kj) + sj);
-                } else {
-                    bucket_flush_final(bkbase + cur, s);  // native red handles same keys
                 }
-                __syncwarp();
             };
             auto advance = [&](uint4 (&nq)[4]) {  // prefetch this warp's next round
-                fbase += 64u * team;
-                if (fbase >= fend) fetch(fb + cstride);
+                if (++fr >= fc.r1) seek(fc.b + cstride);
                 load_round(nq);
             };
-            uint32_t base = ch0 + 64u * sub;
-            while (base < ch1) {
+            uint32_t r = c.r0;
+            while (r < c.r1) {
                 advance(qb);
                 do_round(qa);
-                base += 64u * team;
-                if (base >= ch1) {
+                if (++r >= c.r1) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) qa[j] = qb[j];
                     break;
                 }
                 advance(qa);
                 do_round(qb);
-                base += 64u * team;
+                ++r;
             }
-            asm volatile("" ::: "memory");
+            // Close every lane's open group.  A group spanning whole runs leaves
+            // equal open keys in consecutive lanes (contiguous lane runs): a
+            // segmented suffix sum lets each run's first lane flush alone (no
+            // CAS loop, fixed summation order).  Integer: native shared red.
+            if constexpr (MODE == MODE_FLOAT) {
+                float sj = s;
+                const uint32_t kj = cur;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const float os = __shfl_down_sync(RSR_FULL_MASK, sj, d);
+                    const uint32_t ok = __shfl_down_sync(RSR_FULL_MASK, kj, d);
+                    if (lane + d < 32 && ok == kj) sj += os;
+                }
+                const uint32_t pk = __shfl_up_sync(RSR_FULL_MASK, kj, 1);
+                if (lane == 0 || pk != kj) sts_bucket(bkbase + kj, lds_bucket(bkbase + kj) + sj);
+            } else {
+                bucket_flush_final(bkbase + cur, s);
+            }
+            __syncwarp();
             finish_cell(b, acc);
         }
         if (p.probe && lane == 0 && !fine) {  // debug timeline: first / last warp done
@@ -494,37 +545,36 @@ rsr_mv_kernel(MvParams p) {
         // ===== generic path (register flush and/or u32 entries) ================
         for (; b < p.nblk; b += bstride) {
             const int64_t dc = b * p.tc + t;
-            const int64_t cch0 = p.e_off[dc] / CH, cch1 = p.e_off[dc + 1] / CH;
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            // rounds of 64 chunks, lane L owns the chunk pair (2L, 2L+1): four
-            // coalesced 16-byte quarters (see phys_slot in rsr_preprocess.cu)
-            auto load_pair = [&](int64_t base, uint4 (&q)[4]) {
-                const int64_t np = min((int64_t)64, cch1 - base) >> 1;
+            if constexpr (FMT == FMT_U16) {
+                // quad layout in lane runs (see the bucket path), register flush
+                const Cell c = cell_at(b, p.e_off[dc], p.e_off[dc + 1]);
+                auto gat = [&](uint32_t col) -> Acc { return lds_v<Acc, VSZ>(vbase + col * VSZ); };
+                uint32_t cur = 0;
+                Acc s = (Acc)0;
+                for (uint32_t r = 0; r < c.P; ++r) {
+                    const uint32_t np = c.Lf + (r < c.rem ? 1u : 0u);
+                    const uint32_t R = r * c.Lf + min(r, c.rem);
+                    uint4 a[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) q[j] = make_uint4(0, 0, 0, 0);
-                if ((int64_t)lane < np) {
+                    for (int j = 0; j < 4; ++j) a[j] = make_uint4(0, 0, 0, 0);
+                    if (lane < np) {
+                        const uint4 *src = ent4 + 2 * ((size_t)c.c0 + 2 * (size_t)R) + lane;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) q[j] = __ldg(ent4 + 2 * base + j * np + lane);
-                }
-            };
-            uint4 q[4];
-            load_pair(cch0, q);
-            for (int64_t base = cch0; base < cch1; base += 64) {
-                const bool valid_pair = (int64_t)lane < (min((int64_t)64, cch1 - base) >> 1);
-                uint4 a[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) a[j] = q[j];
-                if (base + 64 < cch1) load_pair(base + 64, q);  // prefetch the next round
-                if (!valid_pair) continue;
-                if constexpr (FMT == FMT_U16) {  // quad layout, register flush
+                        for (int j = 0; j < 4; ++j) a[j] = ld_stream(src + j * np);
+                    }
                     const uint32_t w[16] = {a[0].x, a[0].y, a[0].z, a[0].w, a[1].x, a[1].y,
                                             a[1].z, a[1].w, a[2].x, a[2].y, a[2].z, a[2].w,
                                             a[3].x, a[3].y, a[3].z, a[3].w};
-                    auto gat = [&](uint32_t c) -> Acc { return lds_v<Acc, VSZ>(vbase + c * VSZ); };
-                    uint32_t cur = w[0] & 0x7FFFu;
-                    Acc s = gat(w[0] >> 16) + (gat(w[1] & 0xFFFFu) + gat(w[1] >> 16));
+                    const uint32_t k0 = w[0] & 0x7FFFu;
+                    if (k0 != cur) {
+                        reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+                        cur = k0;
+                        s = (Acc)0;
+                    }
+                    s += gat(w[0] >> 16) + (gat(w[1] & 0xFFFFu) + gat(w[1] >> 16));
 #pragma unroll
                     for (int qd = 1; qd < 8; ++qd) {
                         const uint32_t x = w[2 * qd], y = w[2 * qd + 1];
@@ -536,8 +586,30 @@ rsr_mv_kernel(MvParams p) {
                         cur = isk ? (lo & 0x7FFFu) : cur;
                         s = (isk ? (Acc)0 : s) + g + t3;
                     }
-                    reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
-                } else {  // FMT_U32 (even layout), v gathered from global scratch
+                }
+                reg_flush<K, Acc>(acc, cur, s, p.bitwidth);
+            } else {  // FMT_U32 (even layout, round-major), v gathered from global scratch
+                const int64_t cch0 = p.e_off[dc] / CH, cch1 = p.e_off[dc + 1] / CH;
+                // rounds of 64 chunks, lane L owns the chunk pair (2L, 2L+1): four
+                // coalesced 16-byte quarters (see phys_slot in rsr_preprocess.cu)
+                auto load_pair = [&](int64_t base, uint4 (&q)[4]) {
+                    const int64_t np = min((int64_t)64, cch1 - base) >> 1;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) q[j] = make_uint4(0, 0, 0, 0);
+                    if ((int64_t)lane < np) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) q[j] = __ldg(ent4 + 2 * base + j * np + lane);
+                    }
+                };
+                uint4 q[4];
+                load_pair(cch0, q);
+                for (int64_t base = cch0; base < cch1; base += 64) {
+                    const bool valid_pair = (int64_t)lane < (min((int64_t)64, cch1 - base) >> 1);
+                    uint4 a[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) a[j] = q[j];
+                    if (base + 64 < cch1) load_pair(base + 64, q);  // prefetch the next round
+                    if (!valid_pair) continue;
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
                         const uint4 a0 = a[2 * half], a1 = a[2 * half + 1];

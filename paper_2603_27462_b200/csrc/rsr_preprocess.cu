@@ -320,6 +320,33 @@ __host__ __device__ __forceinline__ int64_t phys_slot(int64_t p, int64_t CH, int
     return r * 64 * CH + q * np * qe + lanep * qe + within;
 }
 
+// Quad layout physical placement ("lane runs").  A cell of N chunk pairs is
+// processed in P = ceil(N / 32) rounds; lane L owns the CONTIGUOUS run of
+// pairs [L*P, L*P + len_L) (len_L = P for L < Lf = N / P, rem = N - Lf*P for
+// lane Lf, 0 beyond), so a lane carries its open group from round to round and
+// lanes only meet at run boundaries.  Round r holds the pairs L*P + r of its
+// np_r = Lf + (r < rem) active lanes, as four 16-byte quarters [q0 of the np_r
+// pairs][q1][q2][q3] (every lane load coalesced), starting at pair R(r) =
+// r*Lf + min(r, rem) of the cell.
+struct LaneRuns {
+    int64_t P, Lf, rem;
+};
+__host__ __device__ __forceinline__ LaneRuns lane_runs(int64_t npairs) {
+    LaneRuns lr;
+    lr.P = (npairs + 31) / 32;
+    lr.Lf = lr.P ? npairs / lr.P : 0;
+    lr.rem = npairs - lr.Lf * lr.P;
+    return lr;
+}
+// Physical u16 index (inside the cell) of logical slot p.
+__host__ __device__ __forceinline__ int64_t run_slot(int64_t p, const LaneRuns &lr) {
+    const int64_t j = p >> 5, slot = p & 31;
+    const int64_t L = j / lr.P, r = j - L * lr.P;
+    const int64_t np = lr.Lf + (r < lr.rem ? 1 : 0);
+    const int64_t R = r * lr.Lf + min(r, lr.rem);
+    return R * 32 + (slot >> 3) * np * 8 + L * 8 + (slot & 7);
+}
+
 // Dense pattern key of a group from its masks: binary -> pos mask; ternary
 // -> base-3 digits (1 = +1, 2 = -1).  Key 0 never occurs (zero patterns are
 // dropped) and marks padding.
@@ -410,7 +437,8 @@ stream_build_kernel(const uint64_t *__restrict__ words, const int64_t *__restric
 // one of the group's unplaced columns) whose bank is least used so far at that
 // (round, slot): ~1.9 wavefronts per gather on random ternary cells
 // (tools/bank_sim.py).  Also records the pattern key of the cell's column 0.
-constexpr int BB_WARPS = 8;
+constexpr int BB_WARPS = 4;
+constexpr int BB_PMAX = 32;  // rounds per cell tracked for bank use (beyond: no preference)
 
 template <bool SCALED>
 __global__ void __launch_bounds__(BB_WARPS * 32)
@@ -419,9 +447,8 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
                            int64_t bc, int64_t tc, int bitwidth,
                            const int64_t *__restrict__ e_off, const int32_t *__restrict__ gslot,
                            uint16_t *__restrict__ entries, uint32_t *__restrict__ col0_key) {
-    constexpr int64_t CH = 16;        // u16 entries per 32-byte chunk (constant: no divisions)
-    constexpr int64_t SLOTS = 2 * CH; // entries per lane per round
-    __shared__ uint8_t cnt_all[BB_WARPS][32 * 32];  // [slot][bank] uses in the current round
+    // per warp, per (round, slot): banks read once / at least twice so far
+    __shared__ uint32_t used_all[BB_WARPS][BB_PMAX][32][2];
     constexpr uint16_t KEYFLAG = 0x8000u;
     auto enc_key = [](uint32_t k) -> uint16_t {
         return SCALED ? (uint16_t)((k << 2) | 1u) : (uint16_t)(KEYFLAG | k);
@@ -429,7 +456,7 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
     auto enc_col = [](uint32_t c) -> uint16_t { return SCALED ? (uint16_t)(c << 2) : (uint16_t)c; };
     const uint32_t lane = lane_id();
     const int warp = threadIdx.x >> 5;
-    uint8_t *cnt = cnt_all[warp];
+    uint32_t (*used)[32][2] = used_all[warp];
     const int64_t cells = bc * tc;
     const uint32_t INVALID = 0xFFFFFFFFu;
     for (int64_t dc = (int64_t)blockIdx.x * BB_WARPS + warp; dc < cells;
@@ -437,25 +464,18 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
         const int64_t b = dc / tc, t = dc - b * tc;
         const int64_t src = t * bc + b;
         const int64_t e0 = e_off[dc], elen = e_off[dc + 1] - e0;
-        const int64_t nch = elen / CH;
+        const LaneRuns lr = lane_runs(elen >> 5);
         uint16_t *out = entries + e0;
-        for (int64_t i = lane; i < elen; i += 32) out[phys_slot(i, CH, nch)] = enc_col(0);  // pads
+        for (int64_t i = lane; i < elen; i += 32) out[i] = enc_col(0);  // pads everywhere
+        for (int64_t i = lane; i < min(lr.P, (int64_t)BB_PMAX) * 64; i += 32)
+            (&used[0][0][0])[i] = 0u;
         __syncwarp();
-        int64_t cur_round = -1;
         uint32_t key0 = 0;
-        auto touch = [&](int64_t q, uint32_t bank) {  // lane 0: count one gather
-            uint8_t &u = cnt[(q % SLOTS) * 32 + bank];
-            u = u < 255 ? u + 1 : 255;
-        };
-        auto enter = [&](int64_t q) {  // new round: clear the bank counts
-            const int64_t r = q / (32 * SLOTS);
-            if (r != cur_round) {
-                __syncwarp();
-#pragma unroll
-                for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t *>(cnt)[lane * 8 + i] = 0;
-                cur_round = r;
-            }
-            __syncwarp();
+        // (round, slot) of logical slot q; rounds past BB_PMAX are not tracked
+        auto rs = [&](int64_t q, int64_t &r, int &slot) {
+            const int64_t j = q >> 5;
+            r = j - (j / lr.P) * lr.P;
+            slot = (int)(q & 31);
         };
         const int64_t p0 = po[src];
         for (int64_t g = go[src]; g < go[src + 1]; ++g) {
@@ -480,12 +500,21 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
             place_group_quad(
                 p, L,
                 [&](int64_t q) {
-                    if (lane == 0) out[phys_slot(q, CH, nch)] = key;
+                    if (lane == 0) out[run_slot(q, lr)] = key;
                 },
                 [&](int64_t q, int64_t) {
-                    enter(q);
-                    const int slot = (int)(q % SLOTS);
-                    const uint32_t mine = cand != INVALID ? cnt[slot * 32 + (cand & 31u)] : 0x100u;
+                    int64_t r;
+                    int slot;
+                    rs(q, r, slot);
+                    const bool tracked = r < BB_PMAX;
+                    uint32_t u1 = 0, u2 = 0;
+                    if (tracked) {
+                        u1 = used[r][slot][0];
+                        u2 = used[r][slot][1];
+                    }
+                    const uint32_t bk = cand & 31u;
+                    const uint32_t mine =
+                        cand != INVALID ? ((u1 >> bk) & 1u) + ((u2 >> bk) & 1u) : 3u;
                     const uint32_t m = __reduce_min_sync(RSR_FULL_MASK, mine);
                     const int win = __ffs(__ballot_sync(RSR_FULL_MASK, mine == m)) - 1;
                     const uint32_t c = __shfl_sync(RSR_FULL_MASK, cand, win);
@@ -499,16 +528,25 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
                     }
                     __syncwarp();
                     if (lane == 0) {
-                        touch(q, c & 31u);
-                        out[phys_slot(q, CH, nch)] = enc_col(c);
+                        if (tracked) {
+                            const uint32_t bit = 1u << (c & 31u);
+                            used[r][slot][1] = u2 | (u1 & bit);
+                            used[r][slot][0] = u1 | bit;
+                        }
+                        out[run_slot(q, lr)] = enc_col(c);
                     }
+                    __syncwarp();
                 },
-                [&](int64_t q) {  // pad (column 0, pre-filled)
-                    enter(q);
-                    if (lane == 0) touch(q, 0);
+                [&](int64_t q) {  // pad (column 0, pre-filled): reads bank 0
+                    int64_t r;
+                    int slot;
+                    rs(q, r, slot);
+                    if (lane == 0 && r < BB_PMAX) used[r][slot][0] |= 1u;
+                    __syncwarp();
                 });
         }
         if (lane == 0) col0_key[dc] = key0;
+        __syncwarp();
     }
 }
 

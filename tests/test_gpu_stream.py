@@ -28,7 +28,8 @@ def rsr():
 
 
 def phys_slots(nent, CH):
-    """numpy restatement of phys_slot() (csrc/rsr_preprocess.cu)."""
+    """numpy restatement of phys_slot() (csrc/rsr_preprocess.cu): u32 format,
+    rounds of 64 chunks, lane L owns chunk pair L of the round."""
     p = np.arange(nent, dtype=np.int64)
     nch = nent // CH
     c, js = p // CH, p % CH
@@ -38,6 +39,21 @@ def phys_slots(nent, CH):
     qe = CH >> 1
     q = cin * 2 + js // qe
     return r * 64 * CH + q * np_ * qe + lanep * qe + js % qe
+
+
+def run_slots(nent):
+    """numpy restatement of run_slot() (csrc/rsr_preprocess.cu): u16 formats,
+    lane L owns the contiguous run of pairs [L*P, L*P + len_L)."""
+    p = np.arange(nent, dtype=np.int64)
+    N = nent // 32
+    P = (N + 31) // 32
+    Lf = N // P if P else 0
+    rem = N - Lf * P
+    j, slot = p >> 5, p & 31
+    L, r = j // P, j % P
+    npr = Lf + (r < rem)
+    R = r * Lf + np.minimum(r, rem)
+    return R * 32 + (slot >> 3) * npr * 8 + L * 8 + (slot & 7)
 
 
 def dense_key(w, bitwidth_binary):
@@ -65,18 +81,21 @@ def decode_cell(ent, fmt):
     return out
 
 
-def wavefronts(seq, CH):
-    """Mean shared-memory wavefronts per gather instruction of one cell
-    (max over banks of distinct columns read at one slot across the lanes)."""
-    slots = 2 * CH
+def wavefronts(seq):
+    """Mean shared-memory wavefronts per gather instruction of one u16 cell:
+    at round r, slot j, the active lanes L read sequence position
+    (L*P + r)*32 + j; cost = max over banks of the distinct columns read."""
+    N = len(seq) // 32
+    P = (N + 31) // 32
     tot = n = 0
-    for r0 in range(0, len(seq), 32 * slots):
-        rnd = seq[r0:r0 + 32 * slots]
-        nl = len(rnd) // slots
-        for j in range(slots):
+    for r in range(P):
+        for j in range(32):
             banks = {}
-            for L in range(nl):
-                isk, val = rnd[slots * L + j]
+            for L in range(32):
+                pair = L * P + r
+                if pair >= N or (pair // P) != L:
+                    continue
+                isk, val = seq[pair * 32 + j]
                 if not isk:
                     banks.setdefault(val % 32, set()).add(val)
             tot += max([1] + [len(v) for v in banks.values()])
@@ -100,7 +119,7 @@ def check_stream(a, binary):
         e0, e1 = int(e_off[dc]), int(e_off[dc + 1])
         assert (e1 - e0) % (2 * CH) == 0
         cell = ent[e0:e1]
-        seq = decode_cell(cell[phys_slots(e1 - e0, CH)], fmt)
+        seq = decode_cell(cell[run_slots(e1 - e0) if quad else phys_slots(e1 - e0, CH)], fmt)
         exp, key0 = {}, 0
         for g in range(go[src], go[src + 1]):
             w = int(words[g])
@@ -132,7 +151,7 @@ def check_stream(a, binary):
         if quad:
             assert int(col0[dc]) == key0, f"cell {dc}: col0_key"
         if quad and len(seq) >= 2048:
-            wfs.append(wavefronts(seq, CH))
+            wfs.append(wavefronts(seq))
     return wfs
 
 
