@@ -1,6 +1,8 @@
 // rsr_matvec.cu -- launch logic and C ABI of the online multiply.
 // The kernel itself is in rsr_mv_impl.cuh (instantiated in rsr_mv_fmt*.cu).
 
+#include <cstdio>
+
 #include "rsr_mv_impl.cuh"
 
 namespace rsr {
@@ -181,13 +183,28 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
         static thread_local KernelFn last_fn[64];
         static thread_local size_t last_smem[64];
         const size_t slot = ((uintptr_t)fn >> 4) & 63;
-        if (smem > 48 * 1024 && (last_fn[slot] != fn || last_smem[slot] < smem)) {
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // the default cap is 48 KiB minus the kernel's static shared memory
+        // (the fused kernels keep 512 B of reduction scratch): raise it early
+        if (smem > 46 * 1024 && (last_fn[slot] != fn || last_smem[slot] < smem)) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return launch_status();
             last_fn[slot] = fn;
             last_smem[slot] = smem;
         }
     }
     dim3 grid((unsigned)ctas_per_tile, (unsigned)vw->tile_count);
+    static const bool dbg_launch = getenv("RSR_DEBUG_LAUNCH") != nullptr;
+    if (dbg_launch) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, fn);
+        fprintf(stderr,
+                "rsr launch mode=%d fmt=%d k=%d grid=(%u,%u) block=%d smem=%zu team=%d | "
+                "maxThreads=%d static=%zu maxDyn=%d regs=%d local=%zu\n",
+                MODE, vw->format, vw->k, grid.x, grid.y, (int)(warps * 32), smem, team,
+                fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.numRegs,
+                fa.localSizeBytes);
+    }
     fn<<<grid, (unsigned)(warps * 32), smem, s>>>(p);
     if (vw->tile_count > 1) {
         const int64_t rows_view = vw->n_blocks * vw->k;

@@ -187,3 +187,16 @@ def test_wide_tiles_and_large_k(rsr, n, tw, k, bw):
     if bw == "ternary":
         ref.weight_scale = 0.7
         assert np.array_equal(rsr.rsr_matvec_fused(a, vf), orc.fused_matvec(ref, vf))
+
+
+def test_fused_smem_just_under_48k(rsr):
+    """BitNet down_proj shape (2560 x 6912, k=5): the team launch needs ~48 KiB
+    of dynamic shared memory, just above the default cap left by the fused
+    kernel's static reduction scratch -- the launch must raise the cap."""
+    m_, n_ = 2560, 6912
+    p = orc.random_matrix(m_, n_, "ternary", 7)
+    ref = orc.preprocess(p, 5)
+    ref.weight_scale = 0.5
+    a = rsr.preprocess(rsr.PackedMatrix(m_, n_, "ternary", p.data, 0.5), 5)
+    vf = np.random.default_rng(3).standard_normal(n_).astype(np.float32)
+    assert np.array_equal(rsr.rsr_matvec_fused(a, vf), orc.fused_matvec(ref, vf))
