@@ -162,6 +162,20 @@ rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t 
                             double *scale_out, void *workspace, size_t workspace_bytes,
                             rsr_stream_t stream);
 
+/* ---- batched multi-vector multiply (not in the reference) ----
+ * rsr_matmul: Y[b] = A . V[b] for b < B, over the view's row blocks.
+ *   V: B vectors, element (b, col) at V[b*ldv + col] (ldv >= n);
+ *   Y: element (b, row) at Y[b*ldy + row], rows of the view (ldy >= rows).
+ *   v_dtype RSR_I8 -> Y int32 (exact); F32/BF16/F16 -> Y float32 (fp32 sums,
+ *   the single-vector float tolerance).  u16 stream formats only (tiles <=
+ *   32768 columns, <= 2187 pattern keys); other views return
+ *   RSR_ERR_INVALID and the caller multiplies column by column.
+ * workspace: rsr_matmul_workspace_bytes(view, B) (only when tile_count > 1). */
+size_t rsr_matmul_workspace_bytes(const rsr_stream_view *view, int32_t B);
+rsr_status rsr_matmul(const rsr_stream_view *view, const void *V, int32_t v_dtype, int64_t ldv,
+                      int32_t B, void *Y, int64_t ldy, void *workspace, size_t workspace_bytes,
+                      rsr_stream_t stream);
+
 /* ---- device weight conversion ------------------------------------------------
  * matcore.ternarize_weights + encode (matcore.py:151-173, :114-125) for a
  * weight matrix already on the device (f32/bf16/f16, row-major rows x cols):

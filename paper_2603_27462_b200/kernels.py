@@ -196,6 +196,75 @@ def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
     return out.cpu().numpy() if host else out
 
 
+def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None):
+    """Batched multiply on device tensors: Y[b] = A . Vt[b].
+
+    Vt: [B, n] (int8 -> Y int32; float32/bfloat16/float16 -> Y float32), rows
+    contiguous; Y: [B, rows].  Streams without a batched kernel (u32 format,
+    > 2187 pattern keys, tiles above ~13k columns) run the single-vector
+    kernel column by column.
+    """
+    import ctypes
+    from .matcore import _dtype_code
+    vw = a._view if view is None else view
+    s = _lib.current_stream_ptr(a.device) if stream is None else stream
+    B = int(Vt.shape[0])
+    L = _lib.lib()
+    ref = ctypes.byref(vw)
+    wsb = int(L.rsr_matmul_workspace_bytes(ref, B))
+    ws, wsb = _Workspace.get(a.device, wsb)
+    st = L.rsr_matmul(ref, Vt.data_ptr(), _dtype_code(Vt), Vt.stride(0), B, Y.data_ptr(),
+                      Y.stride(0), _lib.ptr(ws), wsb, s)
+    if st == _lib.RSR_ERR_INVALID:
+        # no batched kernel for this stream (u32 format, > 2187 pattern keys,
+        # or a tile whose 4-vector shared-memory slab exceeds 227 KiB): the
+        # single-vector kernel per column (arguments were validated above)
+        for b in range(B):
+            matvec_into(a, Vt[b], Y[b], view=view, stream=stream)
+        return Y
+    _lib.check(st, "rsr_matmul")
+    return Y
+
+
+def rsr_matvec_batched(a: RsrArtifact, V, counter: OpCounter | None = None):
+    """Y = A . V for a batch of vectors V [B, n] (not in the reference, whose
+    kernels.py:196 takes one vector; the oracle is rsr_matvec per row of V).
+
+    int8 V -> int32 [B, m] (exact); real V -> float32 [B, m].  numpy in,
+    numpy out; torch in, torch (device) out.
+    """
+    import torch
+    host = not _is_torch(V)
+    if host:
+        Vn = np.asarray(V)
+        if Vn.ndim != 2 or Vn.shape[1] != a.n:
+            raise DimensionMismatch(f"batch of shape {Vn.shape} against {a.n} columns")
+        if np.issubdtype(Vn.dtype, np.integer):
+            if Vn.dtype != np.int8:
+                raise DimensionMismatch("integer vectors must be int8")
+            Vt = torch.from_numpy(np.ascontiguousarray(Vn)).to(a.device)
+        else:
+            Vt = torch.from_numpy(np.ascontiguousarray(Vn.astype(np.float32, copy=False))).to(a.device)
+    else:
+        Vt = V
+        if Vt.dim() != 2 or Vt.shape[1] != a.n:
+            raise DimensionMismatch(f"batch of shape {tuple(Vt.shape)} against {a.n} columns")
+        if not Vt.is_floating_point() and Vt.dtype != torch.int8:
+            raise DimensionMismatch("integer vectors must be int8")
+        if Vt.is_floating_point() and Vt.dtype not in (torch.float32, torch.bfloat16,
+                                                       torch.float16):
+            Vt = Vt.to(torch.float32)
+        Vt = Vt.to(a.device).contiguous()
+    B = int(Vt.shape[0])
+    for _ in range(B):
+        _count(a, counter)
+    ydt = torch.int32 if Vt.dtype == torch.int8 else torch.float32
+    Y = torch.empty(B, a.m, dtype=ydt, device=a.device)
+    if B:
+        matmul_into(a, Vt, Y)
+    return Y.cpu().numpy() if host else Y
+
+
 def batched_preprocess(mats: list, k: int, tile_width: int | None = None):
     """Stack sibling matrices sharing an input (reference kernels.py:128-160).
 

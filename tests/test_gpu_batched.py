@@ -1,0 +1,81 @@
+"""Batched multi-vector multiply.
+
+Not in the reference (kernels.py:196 takes one vector); the oracle is the
+single-vector path per column: int8 batches are bit-exact against the
+reference integer core, real batches are held to the float tolerance of
+test_gpu_parity.py per row, against the reference float64 path.
+"""
+import numpy as np
+import pytest
+
+from oracle import rsr_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rsr():
+    import torch
+    import paper_2603_27462_b200 as pkg
+    torch.cuda.set_device(0)
+    return pkg
+
+
+def float_ok(y, ref, dense, v):
+    bound = 1e-6 * (np.abs(dense.astype(np.float64)) @ np.abs(v.astype(np.float64)))
+    return np.abs(y.astype(np.float64) - ref) <= bound + 1e-6 * np.abs(ref)
+
+
+@pytest.mark.parametrize("m,n,k,bw,tw,B", [
+    (96, 3000, 5, "ternary", None, 5),
+    (64, 4096, 6, "ternary", None, 8),
+    (40, 2000, 8, "binary", None, 3),
+    (30, 20000, 4, "ternary", 20000, 7),   # u16 unscaled format
+    (33, 5000, 5, "ternary", 2048, 9),     # multi-tile (partials)
+    (50, 3000, 12, "binary", None, 4),     # > 2187 keys: column-by-column path
+    (24, 40000, 4, "ternary", 40000, 3),   # u32 format: column-by-column path
+])
+def test_batched_vs_single_vector_oracle(rsr, m, n, k, bw, tw, B):
+    rng = np.random.default_rng(m * 31 + B)
+    p = orc.random_matrix(m, n, bw, m + n)
+    ref = orc.preprocess(p, k, tw)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k, tw)
+    dense = orc.decode(p)
+    Vi = rng.integers(-128, 128, (B, n)).astype(np.int8)
+    Yi = rsr.rsr_matvec_batched(a, Vi)
+    assert Yi.shape == (B, m) and Yi.dtype == np.int32
+    for b in range(B):
+        assert np.array_equal(Yi[b], orc.matvec_i8(ref, Vi[b])), b
+    Vf = rng.standard_normal((B, n)).astype(np.float32)
+    Yf = rsr.rsr_matvec_batched(a, Vf)
+    assert Yf.shape == (B, m) and Yf.dtype == np.float32
+    for b in range(B):
+        assert float_ok(Yf[b], orc.matvec_f64(ref, Vf[b]), dense, Vf[b]).all(), b
+
+
+def test_batched_bf16_c4_shape(rsr):
+    """C4 (ternary 8192^2, k=5) with a bf16 batch of 16: every column against
+    the single-vector kernel's float tolerance vs the reference float path."""
+    import torch
+    m = n = 8192
+    p = orc.random_matrix(m, n, "ternary", 0)
+    ref = orc.preprocess(p, 5)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", p.data), 5)
+    V = torch.stack([torch.from_numpy(orc.random_vector(n, b)) for b in range(16)]).to(
+        torch.bfloat16).cuda()
+    Y = rsr.rsr_matvec_batched(a, V).cpu().numpy()
+    Vh = V.float().cpu().numpy()
+    dense = orc.decode(p)
+    for b in (0, 7, 15):
+        assert float_ok(Y[b], orc.matvec_f64(ref, Vh[b]), dense, Vh[b]).all(), b
+
+
+def test_batched_errors(rsr):
+    from paper_2603_27462_b200.errors import DimensionMismatch
+    p = orc.random_matrix(10, 100, "ternary", 1)
+    a = rsr.preprocess(rsr.PackedMatrix(10, 100, "ternary", p.data), 4)
+    with pytest.raises(DimensionMismatch):
+        rsr.rsr_matvec_batched(a, np.zeros((2, 99), np.float32))
+    with pytest.raises(DimensionMismatch):
+        rsr.rsr_matvec_batched(a, np.zeros((2, 100), np.int16))
+    assert rsr.rsr_matvec_batched(a, np.zeros((0, 100), np.float32)).shape == (0, 10)
