@@ -176,6 +176,26 @@ rsr_status rsr_matmul(const rsr_stream_view *view, const void *V, int32_t v_dtyp
                       int32_t B, void *Y, int64_t ldy, void *workspace, size_t workspace_bytes,
                       rsr_stream_t stream);
 
+/* ---- batched multiply on the tensor cores (tcgen05) ---------------------------
+ * For bf16 batches the pattern-table expansion runs on the tensor cores: the
+ * key matrix holds, per row block, the pattern key of every column (u8 when
+ * the pattern space has <= 256 keys, else u16; k <= 8), built once from the
+ * reference arrays (tile-major cells, as rsr_group_fill writes them).
+ * rsr_matmul_tc: Y[b] (f32, rows of blocks [block_begin, +n_blocks)) =
+ * A . V[b] for bf16 V[b*ldv + col], B <= 256; fp32 accumulation of exact +-1
+ * products (the float-path tolerance).                                      */
+size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k);
+rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                            const int64_t *po, int64_t block_count, int64_t tile_count,
+                            int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
+                            void *keymat, rsr_stream_t stream);
+size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t block_begin,
+                                     int64_t n_blocks, int32_t B);
+rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwidth, int32_t k,
+                         int64_t block_begin, int64_t n_blocks, const void *V, int32_t v_dtype,
+                         int64_t ldv, int32_t B, float *Y, int64_t ldy, void *workspace,
+                         size_t workspace_bytes, rsr_stream_t stream);
+
 /* ---- device weight conversion ------------------------------------------------
  * matcore.ternarize_weights + encode (matcore.py:151-173, :114-125) for a
  * weight matrix already on the device (f32/bf16/f16, row-major rows x cols):

@@ -59,22 +59,23 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
     const uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
 
     // ---- prologue: stage the vector chunk, sign table, zero buckets ---------
-    for (int64_t i = threadIdx.x; i < tn; i += blockDim.x) {
-        Acc x[BV];
+    // vector j of the chunk -> column j of the [tn][BV] tile (16-deep batched
+    // loads per thread; unused columns of a short last chunk are zero)
 #pragma unroll
-        for (int j = 0; j < BV; ++j) {
-            x[j] = (Acc)0;
-            if (j < nb) {
-                const int64_t src = (int64_t)(b0 + j) * p.ldv + c0 + i;
-                if constexpr (MODE == MODE_FLOAT) x[j] = load_as_f32(p.V, p.vdtype, src);
-                else x[j] = (Acc)reinterpret_cast<const int8_t *>(p.V)[src];
-            }
+    for (int j = 0; j < BV; ++j) {
+        if (j < nb) {
+            const int64_t base = (int64_t)(b0 + j) * p.ldv;
+            const char *vj = reinterpret_cast<const char *>(p.V) +
+                             base * (p.vdtype == RSR_F32 ? 4 : (p.vdtype == RSR_I8 ? 1 : 2));
+            for_each_v(vj, MODE == MODE_FLOAT ? p.vdtype : (int)RSR_I8, c0, tn,
+                       [&](int64_t i, float x) { vt[i * BV + j] = (Acc)x; });
+        } else {
+            for (int64_t i = threadIdx.x; i < tn; i += blockDim.x) vt[i * BV + j] = (Acc)0;
         }
-        if (i == 0) {  // column 0 is the zero padding entry (see col0_key)
-#pragma unroll
-            for (int j = 0; j < BV; ++j) x[j] = (Acc)0;
-        }
-        reinterpret_cast<Vec *>(vt)[i] = Vec{x[0], x[1], x[2], x[3]};
+    }
+    if (threadIdx.x == 0) {  // column 0 is the zero padding entry (see col0_key);
+#pragma unroll               // thread 0 staged element 0 of every column
+        for (int j = 0; j < BV; ++j) vt[j] = (Acc)0;
     }
     for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
         uint32_t kk = (uint32_t)key;

@@ -196,19 +196,41 @@ def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
     return out.cpu().numpy() if host else out
 
 
-def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None):
+TC_MIN_BATCH = 2  # bf16 batches of at least this many vectors use the tensor cores
+
+
+def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "auto"):
     """Batched multiply on device tensors: Y[b] = A . Vt[b].
 
     Vt: [B, n] (int8 -> Y int32; float32/bfloat16/float16 -> Y float32), rows
-    contiguous; Y: [B, rows].  Streams without a batched kernel (u32 format,
-    > 2187 pattern keys, tiles above ~13k columns) run the single-vector
-    kernel column by column.
+    contiguous; Y: [B, rows].  method: "tc" (bf16 batches on tcgen05 via the
+    key matrix), "stream" (CUDA-core kernel on the chunk stream) or "auto"
+    (tc for bf16 batches of >= TC_MIN_BATCH vectors).  Streams without a
+    batched kernel (u32 format, > 2187 pattern keys, tiles above ~13k
+    columns) run the single-vector kernel column by column.
     """
     import ctypes
+    import torch
     from .matcore import _dtype_code
+    B = int(Vt.shape[0])
+    use_tc = method == "tc" or (method == "auto" and Vt.dtype == torch.bfloat16 and
+                                B >= TC_MIN_BATCH and B <= 256)
+    if use_tc and Vt.dtype == torch.bfloat16 and a.keymat() is not None:
+        vw = a._view if view is None else view
+        s = _lib.current_stream_ptr(a.device) if stream is None else stream
+        L = _lib.lib()
+        wsb = int(L.rsr_matmul_tc_workspace_bytes(a.m, a.n, a.k, vw.row_begin_block,
+                                                  vw.n_blocks, B))
+        ws, wsb = _Workspace.get(a.device, wsb)
+        _lib.check(L.rsr_matmul_tc(_lib.ptr(a.keymat()), a.m, a.n, vw.bitwidth, a.k,
+                                   vw.row_begin_block, vw.n_blocks, Vt.data_ptr(),
+                                   _lib.RSR_BF16, Vt.stride(0), B, Y.data_ptr(), Y.stride(0),
+                                   _lib.ptr(ws), wsb, s), "rsr_matmul_tc")
+        return Y
+    if method == "tc":
+        raise ValueError("the tensor-core path needs a bf16 batch and k <= 8")
     vw = a._view if view is None else view
     s = _lib.current_stream_ptr(a.device) if stream is None else stream
-    B = int(Vt.shape[0])
     L = _lib.lib()
     ref = ctypes.byref(vw)
     wsb = int(L.rsr_matmul_workspace_bytes(ref, B))
@@ -226,7 +248,8 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None):
     return Y
 
 
-def rsr_matvec_batched(a: RsrArtifact, V, counter: OpCounter | None = None):
+def rsr_matvec_batched(a: RsrArtifact, V, counter: OpCounter | None = None,
+                       method: str = "auto"):
     """Y = A . V for a batch of vectors V [B, n] (not in the reference, whose
     kernels.py:196 takes one vector; the oracle is rsr_matvec per row of V).
 
@@ -261,7 +284,7 @@ def rsr_matvec_batched(a: RsrArtifact, V, counter: OpCounter | None = None):
     ydt = torch.int32 if Vt.dtype == torch.int8 else torch.float32
     Y = torch.empty(B, a.m, dtype=ydt, device=a.device)
     if B:
-        matmul_into(a, Vt, Y)
+        matmul_into(a, Vt, Y, method=method)
     return Y.cpu().numpy() if host else Y
 
 

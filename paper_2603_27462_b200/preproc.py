@@ -231,6 +231,27 @@ class RsrArtifact:
         self.col0_d = col0 if self.format != 2 else None
         self._view = self.view()
 
+    def keymat(self):
+        """Per-block pattern key of every column (device, u8 or u16 [bc][n]),
+        built on first use for the tensor-core batched multiply; None when the
+        pattern space is too large (k > 8)."""
+        if "_keymat" not in self.__dict__:
+            import torch
+            L = _lib.lib()
+            bw = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
+            p = self.plan
+            nb = int(L.rsr_keymat_bytes(p.block_count, self.n, bw, self.k))
+            km = None
+            if nb:
+                km = torch.empty(nb, dtype=torch.uint8, device=self.device)
+                _lib.check(L.rsr_keymat_build(
+                    _lib.ptr(self.words_d), _lib.ptr(self.go_d), _lib.ptr(self.perm_d),
+                    _lib.ptr(self.po_d), p.block_count, p.tile_count, p.tile_width, self.n,
+                    bw, self.k, _lib.ptr(km), _lib.current_stream_ptr(self.device)),
+                    "keymat_build")
+            self.__dict__["_keymat"] = km
+        return self.__dict__["_keymat"]
+
     def stream_bytes(self) -> int:
         """Bytes of the device chunk stream one multiply reads."""
         return int(self.entries_d.numel() * self.entries_d.element_size()

@@ -79,3 +79,25 @@ def test_batched_errors(rsr):
     with pytest.raises(DimensionMismatch):
         rsr.rsr_matvec_batched(a, np.zeros((2, 100), np.int16))
     assert rsr.rsr_matvec_batched(a, np.zeros((0, 100), np.float32)).shape == (0, 10)
+
+
+@pytest.mark.parametrize("m,n,k,bw,B", [
+    (96, 3000, 5, "ternary", 5),     # u8 keys, K tail, partial row tile
+    (200, 4096, 6, "ternary", 16),   # u16 keys
+    (64, 2048, 8, "binary", 33),     # N padded to 48
+    (2000, 1000, 4, "ternary", 2),   # several row tiles, split-K
+])
+def test_tensor_core_batched(rsr, m, n, k, bw, B):
+    """bf16 batches on tcgen05 (key matrix -> sign expansion -> MMA): each
+    column within the float tolerance of the reference float path."""
+    import torch
+    p = orc.random_matrix(m, n, bw, m + 3 * n)
+    ref = orc.preprocess(p, k)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k)
+    rng = np.random.default_rng(B)
+    V = torch.from_numpy(rng.standard_normal((B, n)).astype(np.float32)).to(torch.bfloat16).cuda()
+    Y = rsr.rsr_matvec_batched(a, V, method="tc").cpu().numpy()
+    Vh = V.float().cpu().numpy()
+    dense = orc.decode(p)
+    for b in range(B):
+        assert float_ok(Y[b], orc.matvec_f64(ref, Vh[b]), dense, Vh[b]).all(), b
