@@ -196,7 +196,12 @@ def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
     return out.cpu().numpy() if host else out
 
 
-TC_MIN_BATCH = 2  # bf16 batches of at least this many vectors use the tensor cores
+# auto policy (measured at C4, ternary 8192^2 k=5, tools/bench_batched.py):
+# up to SINGLE_MAX_BATCH vectors the single-vector kernel per column is
+# fastest; bf16 batches from TC_MIN_BATCH on go to the tensor cores; the
+# CUDA-core batched stream kernel covers the rest
+SINGLE_MAX_BATCH = 2
+TC_MIN_BATCH = 8
 
 
 def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "auto"):
@@ -205,7 +210,8 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
     Vt: [B, n] (int8 -> Y int32; float32/bfloat16/float16 -> Y float32), rows
     contiguous; Y: [B, rows].  method: "tc" (bf16 batches on tcgen05 via the
     key matrix), "stream" (CUDA-core kernel on the chunk stream) or "auto"
-    (tc for bf16 batches of >= TC_MIN_BATCH vectors).  Streams without a
+    (single-vector kernel per column up to SINGLE_MAX_BATCH, tc for bf16
+    batches of >= TC_MIN_BATCH vectors, else stream).  Streams without a
     batched kernel (u32 format, > 2187 pattern keys, tiles above ~13k
     columns) run the single-vector kernel column by column.
     """
@@ -216,6 +222,11 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
     use_tc = method == "tc" or (method == "auto" and Vt.dtype == torch.bfloat16 and
                                 B >= TC_MIN_BATCH and B <= 256)
     if use_tc and Vt.dtype == torch.bfloat16 and a.keymat() is not None:
+        if Vt.stride(0) % 8 or Vt.data_ptr() % 16:  # cp.async needs 16-byte rows
+            ld = (a.n + 7) // 8 * 8
+            Vp = torch.zeros(B, ld, dtype=Vt.dtype, device=Vt.device)
+            Vp[:, :a.n] = Vt
+            Vt = Vp
         vw = a._view if view is None else view
         s = _lib.current_stream_ptr(a.device) if stream is None else stream
         L = _lib.lib()
@@ -229,6 +240,10 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
         return Y
     if method == "tc":
         raise ValueError("the tensor-core path needs a bf16 batch and k <= 8")
+    if method == "auto" and B <= SINGLE_MAX_BATCH:
+        for b in range(B):
+            matvec_into(a, Vt[b], Y[b], view=view, stream=stream)
+        return Y
     vw = a._view if view is None else view
     s = _lib.current_stream_ptr(a.device) if stream is None else stream
     L = _lib.lib()

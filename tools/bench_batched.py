@@ -45,6 +45,10 @@ for B in Bs:
         torch.bfloat16).cuda()
     Y = torch.empty(B, m, dtype=torch.float32, device="cuda")
     us_rsr = timeit(lambda i: kn.matmul_into(a, V, Y, view=views[i % 4], method="stream"))
+    def single(i):
+        for b in range(B):
+            kn.matvec_into(a, V[b], Y[b], view=views[i % 4])
+    us_single = timeit(single, iters=10 if B > 8 else 50)
     a.keymat()
     kms = [a.keymat()] + [a.keymat().clone() for _ in range(3)]
     def tc(i):
@@ -54,6 +58,6 @@ for B in Bs:
     a.__dict__["_keymat"] = kms[0]
     Yd = torch.empty(B, m, dtype=torch.bfloat16, device="cuda")
     us_cub = timeit(lambda i: torch.matmul(V, Wb[i % 2].t(), out=Yd))
-    print(f"B={B:3d}  stream {us_rsr:8.2f} us   tcgen05 {us_tc:8.2f} us ({B/us_tc*1e6:10.0f} vec/s)   "
+    print(f"B={B:3d}  single-vector x B {us_single:8.2f} us   stream {us_rsr:8.2f} us   tcgen05 {us_tc:8.2f} us ({B/us_tc*1e6:10.0f} vec/s)   "
           f"cuBLAS bf16 {us_cub:8.2f} us ({B/us_cub*1e6:10.0f} vec/s)   tc/cuBLAS {us_cub/us_tc:5.2f}x",
           flush=True)
