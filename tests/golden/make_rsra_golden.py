@@ -1,4 +1,5 @@
-"""Add sha256 digests of REFERENCE-written .rsra files to golden.json.
+"""Add sha256 digests of REFERENCE-written .rsra files (and reference toy
+runtime decodes) to golden.json.
 
 Runs the reference package (rsrmv @ /root/reference) in the build container:
 for every small case of make_golden.SMALL and every LARGE config it saves the
@@ -18,7 +19,12 @@ import tempfile
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 import make_golden as mg  # noqa: E402  (puts the reference on sys.path)
-from rsrmv import artifact_io, bench, preproc  # noqa: E402
+from rsrmv import artifact_io, bench, preproc, toyrt  # noqa: E402
+
+TOY = [  # (seed, d, V, depth, k, prompt, steps)
+    (0, 64, 256, 2, 4, [1, 2, 3], 24),
+    (7, 96, 128, 3, 5, [5], 16),
+]
 
 
 def rsra_digest(a):
@@ -38,9 +44,16 @@ def main():
         p = bench.random_matrix(m, n, bw, seed)
         out["large"][name] = rsra_digest(preproc.preprocess(p, k))
         print(name, out["large"][name], flush=True)
+    toy = []
+    for seed, d, V, depth, k, prompt, steps in TOY:
+        model = toyrt.build_toy_model(seed, d, V, depth, k=k)
+        toks, _ = toyrt.greedy_decode(model, toyrt.RSR, prompt, steps)
+        toy.append(dict(seed=seed, d=d, V=V, depth=depth, k=k, prompt=prompt, steps=steps,
+                        tokens=toks, digest=model.digest()))
     path = os.path.join(HERE, "golden.json")
     g = json.load(open(path))
     g["rsra"] = out
+    g["toyrt"] = toy
     with open(path, "w") as f:
         json.dump(g, f, indent=1)
 
