@@ -148,6 +148,14 @@ rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtyp
                       int32_t accumulate, void *workspace, size_t workspace_bytes,
                       rsr_stream_t stream);
 
+/* rsr_matvec_host: the synchronous host-buffer form behind the Python API's
+ * numpy path -- copies v_host (n elements of v_dtype; pinned memory for full
+ * speed) to dev_v, multiplies into dev_y, copies the view's rows back to
+ * y_host and synchronizes the stream.                                       */
+rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
+                           void *y_host, void *dev_v, void *dev_y, void *workspace,
+                           size_t workspace_bytes, rsr_stream_t stream);
+
 /* rsr_fused_matvec: absmax-quantize v (float64 math, half away from zero,
  * +-127), exact int32 multiply, out[i] = f32(f64(y_i) * (beta / scale)).
  * Bit-identical to _native.fused_matvec (_native.py:339-353).  The

@@ -251,6 +251,27 @@ rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t 
                                  out_dtype == RSR_BF16);
 }
 
+// Host-buffer multiply for the synchronous API: H2D copy of v, the multiply,
+// D2H copy of y, stream sync -- one call instead of one per step.
+rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
+                           void *y_host, void *dev_v, void *dev_y, void *workspace,
+                           size_t workspace_bytes, rsr_stream_t stream) {
+    if (!view || !v_host || !y_host || !dev_v || !dev_y) return RSR_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t esz = v_dtype == RSR_F32 || v_dtype == RSR_I32 ? 4 : (v_dtype == RSR_I8 ? 1 : 2);
+    const int64_t rows =
+        std::min(view->n_blocks * view->k, view->m - view->row_begin_block * view->k);
+    if (cudaMemcpyAsync(dev_v, v_host, (size_t)view->n * esz, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+        return launch_status();
+    rsr_status st = rsr_matvec(view, dev_v, v_dtype, dev_y, 0, workspace, workspace_bytes, stream);
+    if (st != RSR_OK) return st;
+    if (cudaMemcpyAsync(y_host, dev_y, (size_t)rows * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return launch_status();
+    if (cudaStreamSynchronize(s) != cudaSuccess) return launch_status();
+    return RSR_OK;
+}
+
 void rsr_debug_set_probe(unsigned long long *probe) { g_probe = probe; }
 
 rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t *q,

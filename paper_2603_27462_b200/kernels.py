@@ -171,6 +171,11 @@ def rsr_matvec(a: RsrArtifact, v, counter: OpCounter | None = None,
     the stated tolerance).  ``threads`` is accepted for API compatibility.
     """
     import torch
+    if not _is_torch(v):
+        vn = np.asarray(v)
+        if vn.ndim == 1 and vn.shape[0] == a.n and vn.dtype in (np.int8, np.float32):
+            _count(a, counter)
+            return _matvec_host(a, np.ascontiguousarray(vn))
     vt, host = _prepare_vec(a, v)
     _count(a, counter)
     if vt.dtype == torch.int8:
@@ -179,6 +184,26 @@ def rsr_matvec(a: RsrArtifact, v, counter: OpCounter | None = None,
         y = torch.empty(a.m, dtype=torch.float32, device=a.device)
     matvec_into(a, vt, y)
     return y.cpu().numpy() if host else y
+
+
+def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
+    """numpy in, numpy out in one C call (H2D, multiply, D2H, sync) using
+    device buffers cached on the artifact."""
+    import torch
+    is_int = vn.dtype == np.int8
+    key = "_host_bufs_i8" if is_int else "_host_bufs_f32"
+    bufs = a.__dict__.get(key)
+    if bufs is None:
+        dv = torch.empty(a.n, dtype=torch.int8 if is_int else torch.float32, device=a.device)
+        dy = torch.empty(a.m, dtype=torch.int32 if is_int else torch.float32, device=a.device)
+        bufs = a.__dict__[key] = (dv, dy)
+    st = _launch_state(a, None)
+    y = np.empty(a.m, dtype=np.int32 if is_int else np.float32)
+    _lib.check(_lib.lib().rsr_matvec_host(
+        st.ref, vn.ctypes.data, _lib.RSR_I8 if is_int else _lib.RSR_F32, y.ctypes.data,
+        bufs[0].data_ptr(), bufs[1].data_ptr(), st.ws, st.wsb,
+        _lib.current_stream_ptr(a.device)), "rsr_matvec")
+    return y
 
 
 def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
