@@ -205,7 +205,25 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
                 fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.numRegs,
                 fa.localSizeBytes);
     }
-    fn<<<grid, (unsigned)(warps * 32), smem, s>>>(p);
+    static const bool use_pdl = !getenv("RSR_MV_PDL") || atoi(getenv("RSR_MV_PDL")) != 0;
+    p.pdl = use_pdl ? 1 : 0;
+    if (use_pdl) {
+        // programmatic dependent launch: overlaps this launch's pre-wait
+        // prologue with the tail of the previous multiply in the stream
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3((unsigned)(warps * 32));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, fn, p);
+    } else {
+        fn<<<grid, (unsigned)(warps * 32), smem, s>>>(p);
+    }
     if (vw->tile_count > 1) {
         const int64_t rows_view = vw->n_blocks * vw->k;
         const int g2 = (int)std::min<int64_t>((rows_view + 255) / 256, 4096);

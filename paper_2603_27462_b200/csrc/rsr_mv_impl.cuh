@@ -69,6 +69,7 @@ struct MvParams {
     int dbg;             // experiment knobs (RSR_MV_DEBUG); 0 in production
     int team;            // warps per cell (bucket path): 1, 2, 4 or 8
     int pf;              // L2 prefetch distance in rounds (0 = off)
+    int pdl;             // launched with programmatic stream serialization
     const double *row_beta;  // fused: per-row beta (sibling stacks), or null
     int out_bf16;        // fused: write bf16 instead of f32
     unsigned long long *probe;  // debug timeline (rsr_debug_set_probe), null in production

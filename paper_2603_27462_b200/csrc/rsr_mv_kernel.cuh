@@ -211,6 +211,19 @@ rsr_mv_kernel(MvParams p) {
     };
     const bool fine = RSR_DBG(p, 256);  // debug: finer prologue timeline
 
+    // ---- programmatic dependent launch ----------------------------------
+    // The next multiply in the stream may start its pre-wait prologue as soon
+    // as SMs free up.  Everything touched before griddepcontrol.wait (the
+    // chunk stream, e_off, the shared tables) is never written by a multiply;
+    // v, y and the workspace are touched only after it.  Without a PDL launch
+    // the wait returns at once and the stream is requested after v (below).
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (p.pdl) {
+        init_tables();
+        start_stream();
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
     // ---- prologue -------------------------------------------------------
     // The float path's v loads are issued first (vectorized, into registers);
     // the sign table and buckets are initialised while they are in flight;
