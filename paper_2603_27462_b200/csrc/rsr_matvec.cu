@@ -166,6 +166,8 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
         while (team < 8 && cells_per_tile * team * 2 <= cta_cap * MV_MAX_WARPS &&
                est_rounds >= 2 * team)
             team *= 2;
+        static const int force_team = getenv("RSR_MV_TEAM") ? atoi(getenv("RSR_MV_TEAM")) : 0;
+        if (force_team > 0) team = force_team;  // experiment knob
         while (team > 1 && fixed + team * per_warp > smem_cap) team /= 2;
     }
     int64_t warps = (cells_per_tile * team + cta_cap - 1) / cta_cap;
