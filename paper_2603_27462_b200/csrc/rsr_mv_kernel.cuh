@@ -445,8 +445,10 @@ rsr_mv_kernel(MvParams p) {
             Acc acc[K];
 #pragma unroll
             for (int i = 0; i < K; ++i) acc[i] = (Acc)0;
-            uint32_t cur = 0;  // open group: bucket offset (0 = the never-reduced sink)
-            Acc s = (Acc)0;    //             and its partial sum
+            // open group: its bucket's shared address (bkbase = bucket 0, the
+            // never-reduced sink) and its partial sum
+            uint32_t cur = bkbase;
+            Acc s = (Acc)0;
             auto do_round = [&](const uint4 (&q)[4]) {
                 const uint4 a0 = q[0], a1 = q[1], a2 = q[2], a3 = q[3];
                 // Pairs past a lane's run are zeros: key 0 (the sink) at slot 0,
@@ -463,13 +465,13 @@ rsr_mv_kernel(MvParams p) {
                 uint32_t fk[8];
                 float fs[8];
                 {   // slot 0: always a key; a new one closes the open group
-                    const uint32_t k0 = key_off(w[0]);
+                    const uint32_t k0 = bkbase + key_off(w[0]);
                     const bool ns = k0 != cur;
                     if constexpr (MODE == MODE_FLOAT) {
-                        fk[0] = ns ? cur : 0u;
+                        fk[0] = ns ? cur : bkbase;
                         fs[0] = s;
                     } else {
-                        bucket_flush_pred(ns, bkbase + cur, s);  // native shared red
+                        bucket_flush_pred(ns, cur, s);  // native shared red
                     }
                     cur = k0;
                     s = (ns ? (Acc)0 : s) + (gat(hi_off(w[0])) + (gat(lo_off(w[1])) + gat(hi_off(w[1]))));
@@ -486,12 +488,12 @@ rsr_mv_kernel(MvParams p) {
                     const Acc t3 = gat(hi_off(x)) + (gat(lo_off(y)) + gat(hi_off(y)));
                     if constexpr (MODE == MODE_FLOAT) {
                         // record completed groups; flushed below as one batch
-                        fk[qd] = isk ? cur : 0u;
+                        fk[qd] = isk ? cur : bkbase;
                         fs[qd] = s;
                     } else {
-                        bucket_flush_pred(isk, bkbase + cur, s);
+                        bucket_flush_pred(isk, cur, s);
                     }
-                    cur = isk ? ko : cur;
+                    cur = isk ? bkbase + ko : cur;
                     s = (isk ? (Acc)0 : s + g) + t3;
                 }
                 if constexpr (MODE == MODE_FLOAT) {
@@ -501,12 +503,9 @@ rsr_mv_kernel(MvParams p) {
                     // end), bucket 0 aside.
                     if (!RSR_DBG(p, 1)) {
                         float tb[8];
-                        uint32_t ta[8];
+                        lds_bucket8(fk, tb);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) ta[i] = bkbase + fk[i];
-                        lds_bucket8(ta, tb);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) sts_bucket(ta[i], tb[i] + fs[i]);
+                        for (int i = 0; i < 8; ++i) sts_bucket(fk[i], tb[i] + fs[i]);
                     }
                 }
             };
@@ -541,9 +540,9 @@ rsr_mv_kernel(MvParams p) {
                     if (lane + d < 32 && ok == kj) sj += os;
                 }
                 const uint32_t pk = __shfl_up_sync(RSR_FULL_MASK, kj, 1);
-                if (lane == 0 || pk != kj) sts_bucket(bkbase + kj, lds_bucket(bkbase + kj) + sj);
+                if (lane == 0 || pk != kj) sts_bucket(kj, lds_bucket(kj) + sj);
             } else {
-                bucket_flush_final(bkbase + cur, s);
+                bucket_flush_final(cur, s);
             }
             __syncwarp();
             finish_cell(b, acc);
