@@ -253,7 +253,7 @@ __device__ __forceinline__ float ld_elem(const void *v, int64_t i) {
 // loads in flight per thread (a plain strided loop is a chain of L2 latencies).
 template <int DT, typename Fn>
 __device__ __forceinline__ void for_each_v_t(const void *v, int64_t c0, int64_t cnt, Fn fn) {
-    constexpr int U = 16;
+    constexpr int U = 8;
     const int64_t nt = blockDim.x;
     for (int64_t i0 = threadIdx.x; i0 < cnt; i0 += U * nt) {
         float x[U];
@@ -267,6 +267,17 @@ __device__ __forceinline__ void for_each_v_t(const void *v, int64_t c0, int64_t 
             const int64_t i = i0 + u * nt;
             if (i < cnt) fn(i, x[u]);
         }
+    }
+}
+// Real vectors only (float / fused paths): three instantiations, not four --
+// the multiply kernels are i-cache sensitive when launched between other work.
+template <typename Fn>
+__device__ __forceinline__ void for_each_v_real(const void *v, int dtype, int64_t c0,
+                                                int64_t cnt, Fn fn) {
+    switch (dtype) {
+        case RSR_F32: for_each_v_t<RSR_F32>(v, c0, cnt, fn); break;
+        case RSR_BF16: for_each_v_t<RSR_BF16>(v, c0, cnt, fn); break;
+        default: for_each_v_t<RSR_F16>(v, c0, cnt, fn); break;
     }
 }
 template <typename Fn>
@@ -284,7 +295,7 @@ __device__ __forceinline__ void for_each_v(const void *v, int dtype, int64_t c0,
 __device__ __forceinline__ double cta_absmax_fast(const void *v, int dtype, int64_t n) {
     __shared__ double red[32];
     double a = 0.0;
-    for_each_v(v, dtype, 0, n, [&](int64_t, float x) {
+    for_each_v_real(v, dtype, 0, n, [&](int64_t, float x) {
         const double ax = fabs((double)x);
         a = ax > a ? ax : a;
     });

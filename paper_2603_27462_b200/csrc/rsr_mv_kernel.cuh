@@ -294,7 +294,7 @@ rsr_mv_kernel(MvParams p) {
     if constexpr (MODE == MODE_FUSED && SMEM_V && VSZ == 4) {
         if (p.tc == 1) {
             double a = 0.0;
-            for_each_v(p.v, p.vdtype, 0, tn, [&](int64_t i, float x) {
+            for_each_v_real(p.v, p.vdtype, 0, tn, [&](int64_t i, float x) {
                 reinterpret_cast<float *>(vsm)[i] = x;
                 const double ax = fabs((double)x);
                 a = ax > a ? ax : a;
@@ -323,15 +323,16 @@ rsr_mv_kernel(MvParams p) {
     }
     if (!staged && !vstaged_float) if constexpr (SMEM_V) {
         if constexpr (MODE == MODE_FLOAT) {
-            for_each_v(p.v, p.vdtype, c0, tn,
+            for_each_v_real(p.v, p.vdtype, c0, tn,
                        [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
         } else {
-            const int dt = MODE == MODE_INT ? (int)RSR_I8 : p.vdtype;
-            for_each_v(p.v, dt, c0, tn, [&](int64_t i, float x) {
+            auto put = [&](int64_t i, float x) {
                 const int8_t q = MODE == MODE_INT ? (int8_t)x : quantize_one(x, scale);
                 if constexpr (VSZ == 4) reinterpret_cast<int32_t *>(vsm)[i] = q;
                 else reinterpret_cast<int8_t *>(vsm)[i] = q;
-            });
+            };
+            if constexpr (MODE == MODE_INT) for_each_v_t<RSR_I8>(p.v, c0, tn, put);
+            else for_each_v_real(p.v, p.vdtype, c0, tn, put);
         }
     }
     if (fine) probe(2);
