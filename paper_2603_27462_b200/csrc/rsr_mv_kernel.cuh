@@ -514,18 +514,31 @@ rsr_mv_kernel(MvParams p) {
                 if (++fr >= fc.r1) seek(fc.b + cstride);
                 load_round(nq);
             };
-            uint32_t r = c.r0;
-            while (r < c.r1) {
-                advance(qb);
-                do_round(qa);
-                if (++r >= c.r1) {
+            if constexpr (MODE != MODE_FUSED) {
+                // two rounds per iteration (ping-pong: no register copies)
+                uint32_t r = c.r0;
+                while (r < c.r1) {
+                    advance(qb);
+                    do_round(qa);
+                    if (++r >= c.r1) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) qa[j] = qb[j];
+                        break;
+                    }
+                    advance(qa);
+                    do_round(qb);
+                    ++r;
+                }
+            } else {
+                // the fused kernel serves small decode-time matrices, launched
+                // between other kernels: one copy of the round body (smaller
+                // i-cache footprint) at the price of 16 register moves a round
+                for (uint32_t r = c.r0; r < c.r1; ++r) {
+                    advance(qb);
+                    do_round(qa);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) qa[j] = qb[j];
-                    break;
                 }
-                advance(qa);
-                do_round(qb);
-                ++r;
             }
             // Close every lane's open group.  A group spanning whole runs leaves
             // equal open keys in consecutive lanes (contiguous lane runs): a
