@@ -292,7 +292,50 @@ rsr_mv_kernel(MvParams p) {
     // it as f32 while tracking |v|max, then quantizes in place.
     bool staged = false;
     if constexpr (MODE == MODE_FUSED && SMEM_V && VSZ == 4) {
-        if (p.tc == 1) {
+        // Decode-sized bf16 vectors: the whole vector in registers (<= two
+        // 16-byte loads per thread), |v|max from registers, quantize straight
+        // from registers -- no f32 round trip through shared memory.
+        const int64_t nt = blockDim.x;
+        if (p.tc == 1 && p.vdtype == RSR_BF16 && (tn & 7) == 0 && tn <= nt * 16 &&
+            (reinterpret_cast<uintptr_t>(p.v) & 15) == 0) {
+            const int64_t nvec = tn >> 3;
+            uint4 r[2];
+            float mx = 0.f;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int64_t i = threadIdx.x + u * nt;
+                r[u] = i < nvec ? __ldg(reinterpret_cast<const uint4 *>(p.v) + i)
+                                : make_uint4(0, 0, 0, 0);
+                const uint32_t w4[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    mx = fmaxf(mx, fabsf(__uint_as_float(w4[q] << 16)));
+                    mx = fmaxf(mx, fabsf(__uint_as_float(w4[q] & 0xFFFF0000u)));
+                }
+            }
+            const double amax = cta_reduce_max((double)mx);  // exact: max of floats
+            scale = amax == 0.0 ? 1.0 : 127.0 / amax;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int64_t i = threadIdx.x + u * nt;
+                if (i < nvec) {
+                    const uint32_t w4[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+                    int32_t qv[8];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        qv[2 * q] = quantize_one(__uint_as_float(w4[q] << 16), scale);
+                        qv[2 * q + 1] = quantize_one(__uint_as_float(w4[q] & 0xFFFF0000u), scale);
+                    }
+                    int4 *d = reinterpret_cast<int4 *>(vsm) + 2 * i;
+                    d[0] = make_int4(qv[0], qv[1], qv[2], qv[3]);
+                    d[1] = make_int4(qv[4], qv[5], qv[6], qv[7]);
+                }
+            }
+            if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+                *p.scale_dev = scale;
+            staged = true;
+        }
+        if (!staged && p.tc == 1) {
             double a = 0.0;
             for_each_v_real(p.v, p.vdtype, 0, tn, [&](int64_t i, float x) {
                 reinterpret_cast<float *>(vsm)[i] = x;

@@ -200,3 +200,20 @@ def test_fused_smem_just_under_48k(rsr):
     a = rsr.preprocess(rsr.PackedMatrix(m_, n_, "ternary", p.data, 0.5), 5)
     vf = np.random.default_rng(3).standard_normal(n_).astype(np.float32)
     assert np.array_equal(rsr.rsr_matvec_fused(a, vf), orc.fused_matvec(ref, vf))
+
+
+@pytest.mark.parametrize("n", [2560, 1000, 3072, 6912, 8])
+def test_fused_bf16_vector_bit_exact(rsr, n):
+    """bf16 activations (the decode case; register-resident staging when the
+    vector fits two 16-byte loads per thread) against the reference fused path
+    on the same (bf16-valued) vector, bit for bit."""
+    import torch
+    m_ = 50
+    p = orc.random_matrix(m_, n, "ternary", n)
+    ref = orc.preprocess(p, 5)
+    ref.weight_scale = 0.37
+    a = rsr.preprocess(rsr.PackedMatrix(m_, n, "ternary", p.data, 0.37), 5)
+    vb = torch.from_numpy(np.random.default_rng(n).standard_normal(n).astype(np.float32)).to(
+        torch.bfloat16)
+    y = rsr.rsr_matvec_fused(a, vb.cuda()).cpu().numpy()
+    assert np.array_equal(y, orc.fused_matvec(ref, vb.float().numpy()))

@@ -16,6 +16,7 @@ else:
 if len(sys.argv) > 2:
     cfg["k"] = int(sys.argv[2])
 mode = sys.argv[3] if len(sys.argv) > 3 else "float"
+warm = len(sys.argv) > 4 and sys.argv[4] == "warm"  # keep L2 / i-cache warm
 data = bench.random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0)
 a = rsr.preprocess(rsr.PackedMatrix(cfg["m"], cfg["n"], cfg["bitwidth"], data), cfg["k"])
 v = torch.from_numpy(bench.random_vector(cfg["n"], 0)).cuda().to(torch.bfloat16)
@@ -28,8 +29,11 @@ probe = torch.zeros(4096 * 4, dtype=torch.int64, device="cuda")
 pv = probe.view(-1, 4)
 pv[:, 2] = torch.iinfo(torch.int64).max
 _lib.lib().rsr_debug_set_probe(probe.data_ptr())
-# evict: touch the copies
-for c in copies: c.add_(0)
+# evict: touch the copies (cold) or run the multiply right before (warm)
+if warm:
+    f()
+else:
+    for c in copies: c.add_(0)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); f(); e1.record()
 torch.cuda.synchronize()
