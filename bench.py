@@ -190,21 +190,29 @@ def decode_bench(steps=64, k=5):
     with torch.device("cuda"):
         model = BitNetForCausalLM(cfg).to(torch.bfloat16).eval()
     prompt = torch.randint(0, cfg.vocab_size, (1, 16), device="cuda")
-    res = {}
-    for name in ("dense_bf16_cublas", "rsr"):
-        if name == "rsr":
-            replace_linear_with_rsr(model, k=k)
-        dec = GraphDecoder(model, max_len=16 + steps + 8)
+    import copy
+    rsr_model = copy.deepcopy(model)
+    replace_linear_with_rsr(rsr_model, k=k)
+    decs = {}
+    for name, mdl in (("dense_bf16_cublas", model), ("rsr", rsr_model)):
+        dec = GraphDecoder(mdl, max_len=16 + steps + 8)
         dec.prefill(prompt)
         dec.capture()
         dec.time_steps(prompt, 8)
-        res[name] = steps / dec.time_steps(prompt, steps)
-        del dec
-        torch.cuda.empty_cache()
+        decs[name] = dec
+    # interleaved repetitions (clock / thermal drift hits both arms alike)
+    samples = {name: [] for name in decs}
+    for _ in range(5):
+        for name, dec in decs.items():
+            samples[name].append(steps / dec.time_steps(prompt, steps))
+    res = {name: float(np.median(v)) for name, v in samples.items()}
+    del decs
+    torch.cuda.empty_cache()
     return {"model": "BitNetForCausalLM(BitNetConfig()) random init, bf16, 30 layers, "
                      "hidden 2560, FFN 6912",
             "loop": "greedy, HF StaticCache, one CUDA graph per step, batch 1",
-            "k": k, "steps": steps, "rsr_tok_s": res["rsr"],
+            "k": k, "steps": steps, "reps": "median of 5 interleaved runs per arm",
+            "rsr_tok_s": res["rsr"],
             "dense_tok_s": res["dense_bf16_cublas"],
             "speedup": res["rsr"] / res["dense_bf16_cublas"]}
 
