@@ -208,7 +208,8 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
                 fa.localSizeBytes);
     }
     static const bool use_pdl = !getenv("RSR_MV_PDL") || atoi(getenv("RSR_MV_PDL")) != 0;
-    p.pdl = use_pdl ? 1 : 0;
+    static const int pdl_stream = getenv("RSR_MV_PDL_STREAM") ? atoi(getenv("RSR_MV_PDL_STREAM")) : -1;
+    p.pdl = !use_pdl ? 0 : (pdl_stream >= 0 ? (pdl_stream ? 2 : 1) : (tn > 8192 ? 2 : 1));
     if (use_pdl) {
         // programmatic dependent launch: overlaps this launch's pre-wait
         // prologue with the tail of the previous multiply in the stream

@@ -220,7 +220,9 @@ rsr_mv_kernel(MvParams p) {
     asm volatile("griddepcontrol.launch_dependents;");
     if (p.pdl) {
         init_tables();
-        start_stream();
+        // requesting the stream pre-wait pays off for long cells (its e_off
+        // round trip is exposed otherwise); short cells request it after v
+        if (p.pdl == 2) start_stream();
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
