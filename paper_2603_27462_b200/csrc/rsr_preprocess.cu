@@ -438,7 +438,12 @@ stream_build_kernel(const uint64_t *__restrict__ words, const int64_t *__restric
 // (round, slot): ~1.9 wavefronts per gather on random ternary cells
 // (tools/bank_sim.py).  Also records the pattern key of the cell's column 0.
 constexpr int BB_WARPS = 4;
-constexpr int BB_PMAX = 32;  // rounds per cell tracked for bank use (beyond: no preference)
+constexpr int BB_PMAX = 32;    // rounds per cell tracked for bank use (beyond: no preference)
+constexpr int BB_LSMAX = 256;  // groups up to this many stream columns get the local search
+#ifndef BB_LSPASSES
+#define BB_LSPASSES 1
+#endif
+constexpr size_t BB_WARP_SMEM = (size_t)BB_PMAX * 32 * 32 + BB_LSMAX * 8;
 
 template <bool SCALED>
 __global__ void __launch_bounds__(BB_WARPS * 32)
@@ -447,8 +452,9 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
                            int64_t bc, int64_t tc, int bitwidth,
                            const int64_t *__restrict__ e_off, const int32_t *__restrict__ gslot,
                            uint16_t *__restrict__ entries, uint32_t *__restrict__ col0_key) {
-    // per warp, per (round, slot): banks read once / at least twice so far
-    __shared__ uint32_t used_all[BB_WARPS][BB_PMAX][32][2];
+    // per warp: gathers per (round, slot, bank) so far (u8), and the local
+    // search's position / column lists of one group
+    extern __shared__ __align__(16) unsigned char bb_smem[];
     constexpr uint16_t KEYFLAG = 0x8000u;
     auto enc_key = [](uint32_t k) -> uint16_t {
         return SCALED ? (uint16_t)((k << 2) | 1u) : (uint16_t)(KEYFLAG | k);
@@ -456,7 +462,9 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
     auto enc_col = [](uint32_t c) -> uint16_t { return SCALED ? (uint16_t)(c << 2) : (uint16_t)c; };
     const uint32_t lane = lane_id();
     const int warp = threadIdx.x >> 5;
-    uint32_t (*used)[32][2] = used_all[warp];
+    uint8_t *cnt = bb_smem + (size_t)warp * BB_WARP_SMEM;            // [BB_PMAX][32][32]
+    uint32_t *lpos = reinterpret_cast<uint32_t *>(cnt + BB_PMAX * 32 * 32);  // [BB_LSMAX]
+    uint32_t *lcol = lpos + BB_LSMAX;                                 // [BB_LSMAX]
     const int64_t cells = bc * tc;
     const uint32_t INVALID = 0xFFFFFFFFu;
     for (int64_t dc = (int64_t)blockIdx.x * BB_WARPS + warp; dc < cells;
@@ -467,15 +475,16 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
         const LaneRuns lr = lane_runs(elen >> 5);
         uint16_t *out = entries + e0;
         for (int64_t i = lane; i < elen; i += 32) out[i] = enc_col(0);  // pads everywhere
-        for (int64_t i = lane; i < min(lr.P, (int64_t)BB_PMAX) * 64; i += 32)
-            (&used[0][0][0])[i] = 0u;
+        const int64_t tracked_bytes = min(lr.P, (int64_t)BB_PMAX) * 1024;
+        for (int64_t i = lane; i < tracked_bytes / 4; i += 32)
+            reinterpret_cast<uint32_t *>(cnt)[i] = 0u;
         __syncwarp();
         uint32_t key0 = 0;
-        // (round, slot) of logical slot q; rounds past BB_PMAX are not tracked
-        auto rs = [&](int64_t q, int64_t &r, int &slot) {
+        // counter of (round, slot, bank) of logical slot q, or -1 if untracked
+        auto cidx = [&](int64_t q, uint32_t bank) -> int {
             const int64_t j = q >> 5;
-            r = j - (j / lr.P) * lr.P;
-            slot = (int)(q & 31);
+            const int64_t r = j - (j / lr.P) * lr.P;
+            return r < BB_PMAX ? (int)((r * 32 + (q & 31)) * 32 + bank) : -1;
         };
         const int64_t p0 = po[src];
         for (int64_t g = go[src]; g < go[src + 1]; ++g) {
@@ -490,10 +499,11 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
                 ++cols;
                 --L;
             }
-            // window: lane i holds one unplaced column; refills come from a
-            // register batch of the next 32 columns (one coalesced load per 32)
+            // greedy: a window of 32 unplaced columns (one per lane, refilled
+            // from a register batch); each position takes the window column
+            // whose bank is least used at that (round, slot) so far
             uint32_t cand = (int64_t)lane < L ? cols[lane] : INVALID;
-            int64_t nb = min(L, (int64_t)32);  // next batch start
+            int64_t nb = min(L, (int64_t)32);
             uint32_t batch = nb + lane < L ? cols[nb + lane] : INVALID;
             int bi = 0;
             int64_t p = gslot[g];
@@ -503,22 +513,11 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
                     if (lane == 0) out[run_slot(q, lr)] = key;
                 },
                 [&](int64_t q, int64_t) {
-                    int64_t r;
-                    int slot;
-                    rs(q, r, slot);
-                    const bool tracked = r < BB_PMAX;
-                    uint32_t u1 = 0, u2 = 0;
-                    if (tracked) {
-                        u1 = used[r][slot][0];
-                        u2 = used[r][slot][1];
-                    }
-                    const uint32_t bk = cand & 31u;
-                    const uint32_t mine =
-                        cand != INVALID ? ((u1 >> bk) & 1u) + ((u2 >> bk) & 1u) : 3u;
+                    const int ci = cand != INVALID ? cidx(q, cand & 31u) : -1;
+                    const uint32_t mine = cand == INVALID ? 0x200u : (ci >= 0 ? cnt[ci] : 0u);
                     const uint32_t m = __reduce_min_sync(RSR_FULL_MASK, mine);
                     const int win = __ffs(__ballot_sync(RSR_FULL_MASK, mine == m)) - 1;
                     const uint32_t c = __shfl_sync(RSR_FULL_MASK, cand, win);
-                    // refill the chosen lane from the batch
                     const uint32_t nxt = __shfl_sync(RSR_FULL_MASK, batch, bi);
                     if ((int)lane == win) cand = nxt;
                     if (++bi == 32) {
@@ -528,22 +527,78 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
                     }
                     __syncwarp();
                     if (lane == 0) {
-                        if (tracked) {
-                            const uint32_t bit = 1u << (c & 31u);
-                            used[r][slot][1] = u2 | (u1 & bit);
-                            used[r][slot][0] = u1 | bit;
-                        }
+                        const int k = cidx(q, c & 31u);
+                        if (k >= 0 && cnt[k] < 255) ++cnt[k];
                         out[run_slot(q, lr)] = enc_col(c);
                     }
                     __syncwarp();
                 },
                 [&](int64_t q) {  // pad (column 0, pre-filled): reads bank 0
-                    int64_t r;
-                    int slot;
-                    rs(q, r, slot);
-                    if (lane == 0 && r < BB_PMAX) used[r][slot][0] |= 1u;
+                    if (lane == 0) {
+                        const int k = cidx(q, 0);
+                        if (k >= 0 && cnt[k] == 0) cnt[k] = 1;  // one address: counted once
+                    }
                     __syncwarp();
                 });
+        }
+        // local search: swap two columns of one group when that lowers the sum
+        // of squared bank loads over the (round, slot) sets they sit in
+        for (int pass = 0; pass < BB_LSPASSES; ++pass)
+        for (int64_t g = go[src]; g < go[src + 1]; ++g) {
+            const uint64_t w = words[g];
+            int64_t L = (int64_t)((w >> 16) & 0xFFFFu);
+            if (perm[p0 + (int64_t)(w & 0xFFFFu)] == 0) --L;
+            if (L < 2 || L > BB_LSMAX) continue;
+            int64_t p = gslot[g];
+            int n = 0;
+            place_group_quad(
+                p, L, [](int64_t) {},
+                [&](int64_t q, int64_t) {
+                    if (lane == 0) {
+                        const uint32_t e = out[run_slot(q, lr)];
+                        lpos[n] = (uint32_t)q;
+                        lcol[n] = SCALED ? (e >> 2) : e;
+                    }
+                    ++n;
+                },
+                [](int64_t) {});
+            __syncwarp();
+            for (int i = 0; i < n; ++i) {
+                const uint32_t qi = lpos[i], ci = lcol[i], bi_ = ci & 31u;
+                const int ki = cidx(qi, bi_);
+                int best = 1 << 30, bj = -1;
+                for (int j = (int)lane; j < n; j += 32) {
+                    const uint32_t qj = lpos[j], cj = lcol[j], bj_ = cj & 31u;
+                    const int kj = cidx(qj, bj_);
+                    if (j == i || bj_ == bi_ || ki < 0 || kj < 0) continue;
+                    const int si = ki - (int)bi_, sj = kj - (int)bj_;  // set bases
+                    if (si == sj) continue;
+                    const int d = 2 * ((int)cnt[si + bj_] - (int)cnt[ki]) +
+                                  2 * ((int)cnt[sj + bi_] - (int)cnt[kj]) + 4;
+                    if (d < best) {
+                        best = d;
+                        bj = j;
+                    }
+                }
+                const int m = __reduce_min_sync(RSR_FULL_MASK, best);
+                if (m >= 0) continue;
+                const int who = __ffs(__ballot_sync(RSR_FULL_MASK, best == m)) - 1;
+                const int j = __shfl_sync(RSR_FULL_MASK, bj, who);
+                if (lane == 0) {
+                    const uint32_t qj = lpos[j], cj = lcol[j], bj_ = cj & 31u;
+                    const int kj = cidx(qj, bj_);
+                    const int si = ki - (int)bi_, sj = kj - (int)bj_;
+                    --cnt[ki];
+                    ++cnt[si + bj_];
+                    --cnt[kj];
+                    ++cnt[sj + bi_];
+                    lcol[i] = cj;
+                    lcol[j] = ci;
+                    out[run_slot(qi, lr)] = enc_col(cj);
+                    out[run_slot(qj, lr)] = enc_col(ci);
+                }
+                __syncwarp();
+            }
         }
         if (lane == 0) col0_key[dc] = key0;
         __syncwarp();
@@ -710,14 +765,20 @@ rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 32);
     const int bgrid =
         (int)std::min<int64_t>((cells + BB_WARPS - 1) / BB_WARPS, (int64_t)sm_count() * 8);
-    if (format == 1)
-        stream_build_banked_kernel<true><<<bgrid, BB_WARPS * 32, 0, s>>>(
+    const size_t bsm = BB_WARPS * BB_WARP_SMEM;
+    if (format == 1) {
+        cudaFuncSetAttribute(stream_build_banked_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+        stream_build_banked_kernel<true><<<bgrid, BB_WARPS * 32, bsm, s>>>(
             words, go, perm, po, block_count, tile_count, bitwidth, e_off, gslot,
             (uint16_t *)entries, col0_key);
-    else if (format == 0)
-        stream_build_banked_kernel<false><<<bgrid, BB_WARPS * 32, 0, s>>>(
+    } else if (format == 0) {
+        cudaFuncSetAttribute(stream_build_banked_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+        stream_build_banked_kernel<false><<<bgrid, BB_WARPS * 32, bsm, s>>>(
             words, go, perm, po, block_count, tile_count, bitwidth, e_off, gslot,
             (uint16_t *)entries, col0_key);
+    }
     else
         stream_build_kernel<uint32_t, false><<<grid, 256, 0, s>>>(words, go, perm, po, block_count,
                                                            tile_count, bitwidth, chunk, e_off,

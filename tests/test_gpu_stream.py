@@ -170,9 +170,10 @@ def test_stream_structure(rsr, m, n, k, bw, tw):
 
 def test_bank_aware_order(rsr):
     """Random ternary 16384-wide cells: gathers average well under the ~3.3
-    wavefronts a key-sorted column order costs (tools/bank_sim.py)."""
+    wavefronts a key-sorted column order costs (tools/bank_sim.py); greedy
+    placement plus the swap search measures ~1.86 on C2."""
     p = orc.random_matrix(12, 16384, "ternary", 5)
     a = rsr.preprocess(rsr.PackedMatrix(12, 16384, "ternary", p.data), 6)
     assert a.format == 1
     wfs = check_stream(a, False)
-    assert wfs and float(np.mean(wfs)) < 2.2, wfs
+    assert wfs and float(np.mean(wfs)) < 2.0, wfs
