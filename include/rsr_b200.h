@@ -187,11 +187,14 @@ rsr_status rsr_matmul(const rsr_stream_view *view, const void *V, int32_t v_dtyp
 /* ---- batched multiply on the tensor cores (tcgen05) ---------------------------
  * For bf16 batches the pattern-table expansion runs on the tensor cores: the
  * key matrix holds, per row block, the pattern key of every column (u8 when
- * the pattern space has <= 256 keys, else u16; k <= 8), built once from the
- * reference arrays (tile-major cells, as rsr_group_fill writes them).
+ * the pattern space has <= 256 keys, else u16; k <= 8; laid out
+ * [ceil(cols/64)][block_count][64]), built once from the reference arrays
+ * (tile-major cells, as rsr_group_fill writes them).
  * rsr_matmul_tc: Y[b] (f32, rows of blocks [block_begin, +n_blocks)) =
  * A . V[b] for bf16 V[b*ldv + col], B <= 256; fp32 accumulation of exact +-1
- * products (the float-path tolerance).                                      */
+ * products (the float-path tolerance).  The workspace (always needed, 256-byte
+ * aligned, rsr_matmul_tc_workspace_bytes) holds the repacked V and the
+ * split-K partials.                                                         */
 size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k);
 rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,

@@ -5,65 +5,109 @@
 // dense contraction; with B vectors it is cheaper to apply T before the
 // segment sums: every column's pattern key, expanded through T, is one
 // column of the block's k rows.  So this path keeps, per row block, the
-// pattern key of every column (the RSR keys before the grouping sort, 1 byte
-// per column when the pattern space fits in a byte -- 13.4 MB at C4, less
-// than the 29 MB artifact), expands keys through a shared-memory copy of T
-// straight into the A operand of tcgen05.mma, and accumulates in TMEM:
+// pattern key of every column in the reference's 2-bit code form
+// (pattern_key, preproc.py:183-197: code(row i) at bits 2i, 2i+1; u16 for
+// k <= 8), expands it straight into the A operand of tcgen05.mma and
+// accumulates in TMEM:
 //
 //   D[row][b] += A[row][col] * B[b][col],  A = T[:, key(blk, col)] (bf16 +-1/0),
 //                                          B = V chunk (bf16, K-major)
 //
-// Tile: 16 row blocks x 8 (padded) rows = M 128, K 64 columns per step,
-// N = vectors (16..256).  A is MN-major (one 16-byte write per (block,
-// column): the block's 8 rows), B is K-major; both in the no-swizzle
-// canonical core-matrix layout (8 x 16 B core matrices).  Products with +-1
-// are exact and accumulate in fp32: the float-path tolerance holds.
-// Split-K over grid.y keeps every SM busy; partials are summed in a fixed
-// order by rsr_tc_finalize (deterministic).
+// Tile: M = 128 rows holding floor(128/k) whole row blocks back to back (no
+// per-block padding), K = 64 columns per step, N = vectors (16..256).
+// Warp-specialized, TC_STAGES-deep ring per CTA:
+//   warp 4  (producer)  bulk-copies (cp.async.bulk, mbarrier complete_tx) the
+//                       step's key chunk and its pre-packed B tile;
+//   warps 0-3 (expand)  build the MN-major A tile: per (8-row group,
+//                       column) one 16-bit slice of the concatenated codes
+//                       -> 4 PRMTs (a register byte table) -> one 16-byte
+//                       store (conflict-free: a quarter warp covers 128 B);
+//   warp 5  (MMA)       one thread issues tcgen05.mma (fp32 in TMEM) and
+//                       commits to the stage's "empty" barrier.
+// Key matrix layout [step = col / 64][block][col % 64], so the blocks of a
+// step are one contiguous chunk for any first block (row-block shards).  V is
+// repacked once per call into the K-major no-swizzle core-matrix image of
+// each step (tc_pack_v_kernel), so its B tile is one bulk copy too.  Products
+// with +-1 are exact and accumulate in fp32: the float-path tolerance holds.
+// Split-K over grid.y fills the SMs; partials are summed in a fixed order
+// by tc_finalize_kernel (deterministic).
 #include <cstdio>
+#include <cstdlib>
 
 #include "rsr_mv_impl.cuh"
 
 namespace rsr {
 
-constexpr int TC_BLOCKS = 16;       // row blocks per tile (8 padded rows each)
-constexpr int TC_M = TC_BLOCKS * 8; // 128 rows = TMEM lanes
+constexpr int TC_M = 128;           // tile rows = TMEM lanes
+constexpr int TC_MAXBPT = 128;      // row blocks per tile: floor(128 / k)
 constexpr int TC_K = 64;            // columns per pipeline step
-constexpr int TC_THREADS = 128;
+constexpr int TC_STAGES = 4;       // ring depth (at most; fewer when shared memory is short)
+constexpr int TC_EXP_WARPS = 8;
+constexpr int TC_THREADS = TC_EXP_WARPS * 32 + 64;  // expanders, producer, MMA
+constexpr int TC_UNITS = 16 * TC_K / (TC_EXP_WARPS * 32);  // (row group, column) units per thread
+constexpr int TC_KEY_SLACK = 9;    // zero key rows past the tile (8-row groups read ahead)
 
-// ---- key matrix: KM[blk][col] = pattern key of column col in block blk ----
-template <typename KeyT>
+__host__ __device__ constexpr int tc_nb(int k) { return (8 + k - 1) / k + 1; }
+
+__host__ __device__ inline int64_t tc_steps(int64_t n) { return (n + TC_K - 1) / TC_K; }
+
+// ---- key matrix: KM[step][blk][col % 64] = 2-bit row codes of column col in block blk ----
 __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                               const uint16_t *__restrict__ perm, const int64_t *__restrict__ po,
-                              int64_t bc, int64_t tc, int64_t tw, int bitwidth, int64_t n,
-                              KeyT *__restrict__ km) {
+                              int64_t bc, int64_t tc, int64_t tw, uint16_t *__restrict__ km) {
     const uint32_t lane = lane_id();
     const int64_t cells = bc * tc;
     for (int64_t cell = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < cells;
          cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t t = cell / bc, b = cell - t * bc;  // reference cells are tile-major
         const int64_t c0 = t * tw;
-        KeyT *row = km + b * n + c0;
         for (int64_t g = go[cell]; g < go[cell + 1]; ++g) {
             const uint64_t w = words[g];
             const int64_t ps = (int64_t)(w & 0xFFFFu), L = (int64_t)((w >> 16) & 0xFFFFu);
-            const uint32_t pos = (uint32_t)((w >> 32) & 0xFFFFu), neg = (uint32_t)(w >> 48);
-            uint32_t key = pos;
-            if (bitwidth != RSR_BINARY) {
-                key = 0;
-                uint32_t p3 = 1;
-                for (int i = 0; i < 16; ++i) {
-                    key += (((pos >> i) & 1u) + 2u * ((neg >> i) & 1u)) * p3;
-                    p3 *= 3u;
-                }
-            }
+            const uint32_t pos = (uint32_t)((w >> 32) & 0xFFu), neg = (uint32_t)((w >> 48) & 0xFFu);
+            uint32_t code = 0;  // +1 -> 01, -1 -> 10 (binary keys have no neg bits)
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                code |= (((pos >> i) & 1u) | (((neg >> i) & 1u) << 1)) << (2 * i);
             const uint16_t *cols = perm + po[cell] + ps;
-            for (int64_t j = lane; j < L; j += 32) row[cols[j]] = (KeyT)key;
+            for (int64_t j = lane; j < L; j += 32) {
+                const int64_t col = c0 + cols[j];
+                km[((col / TC_K) * bc + b) * TC_K + (col % TC_K)] = (uint16_t)code;
+            }
         }
     }
 }
 
-// ---- tcgen05 helpers ---------------------------------------------------------
+// ---- V repack: vp[step][N/8][kg 8][8 vectors][8 columns] bf16 (the B tile image) ----
+__global__ void tc_pack_v_kernel(const uint16_t *__restrict__ V, int64_t ldv, int64_t n, int B,
+                                 int N, int64_t steps, uint4 *__restrict__ vp) {
+    const int64_t pieces = steps * N * 8;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pieces;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        // e = ((st * N/8 + vg) * 8 + kg) * 8 + vi
+        const int vi = (int)(e & 7), kg = (int)((e >> 3) & 7);
+        const int64_t r = e >> 6;
+        const int64_t st = r / (N >> 3);
+        const int vb = (int)(r - st * (N >> 3)) * 8 + vi;
+        const int64_t c = st * TC_K + kg * 8;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (vb < B) {
+            const uint16_t *src = V + (int64_t)vb * ldv + c;
+            if (c + 8 <= n && ((ldv & 7) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0)) {
+                val = *reinterpret_cast<const uint4 *>(src);
+            } else {
+                uint32_t h[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) h[q] = c + q < n ? src[q] : 0u;
+                val = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16),
+                                 h[6] | (h[7] << 16));
+            }
+        }
+        vp[e] = val;
+    }
+}
+
+// ---- tcgen05 / mbarrier / bulk-copy helpers -------------------------------------
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     // no-swizzle canonical layout; fields in 16-byte units; version 1 (sm_100)
     uint64_t d = 0;
@@ -88,8 +132,8 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_init1(uint32_t bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
 
 __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
@@ -101,51 +145,106 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+#ifdef RSR_TC_DBG
+__device__ unsigned long long tc_dbg[64 * 4 + 4];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TC_MARK(cond, idx) \
+    if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 64 * 4 + 4) tc_dbg[idx] = gtime();
+#else
+#define TC_MARK(cond, idx)
+#endif
+
 struct TcParams {
-    const void *km;      // key matrix [bc][n] (u8 or u16)
-    const void *V;       // bf16 [B][ldv]
-    int64_t ldv;
+    const uint16_t *km;  // key matrix [steps][bc][64] (2-bit row codes)
+    const uint4 *vp;     // packed V [steps][N/8][8][8][8] bf16
     float *Y;            // [B][ldy] rows of the view
     int64_t ldy;
     float *part;         // split-K partials [ksplit][B][rows]
-    int64_t m_rows, n, nblk, blk0;
-    int k, bitwidth, nkeys, B, N, ksplit;
+    int64_t m_rows, n, nblk, blk0, bc;
+    int k, bpt, B, N, ksplit, stages;
 };
 
+// 8 row codes (2 bits each, +1 -> 01, -1 -> 10) of two units at once
+// (x = unit0 | unit1 << 16) -> the 8 bf16 signs of each as 4 words of two:
+// PRMT picks each byte from a register table {00 3F BF 00 | 00 80 80 00}
+// with selector nibbles (4 + c0, c0, 4 + c1, c1) =
+// 0x0404 + 0x11 * (c0 + (c1 << 8)), built per 16-bit half with two IMADs
+__device__ __forceinline__ void expand_codes2(uint32_t x, uint4 &lo, uint4 &hi) {
+    uint32_t w0[4], w1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t t = x >> (4 * q);
+        const uint32_t tm = t & 0x000F000Fu, th = t & 0x000C000Cu;
+        // 0x11 * (c0 + 4 c1) + 0x42F * 4 c1 = 0x11 * (c0 + (c1 << 8)), + 0x0404
+        const uint32_t sel = th * 0x42Fu + (tm * 0x11u + 0x04040404u);
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w0[q]) : "r"(0x00BF3F00u), "r"(0x00808000u), "r"(sel));
+        asm("prmt.b32 %0, %1, %2, %3;"
+            : "=r"(w1[q])
+            : "r"(0x00BF3F00u), "r"(0x00808000u), "r"(sel >> 16));
+    }
+    lo = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    hi = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+}
+
 // N = 16 * NP: MMA N (vectors padded up, <= 256)
-template <typename KeyT, int NP>
+template <int NP, int K>
 __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
-    extern __shared__ __align__(128) unsigned char tc_smem[];
+    extern __shared__ __align__(1024) unsigned char tc_smem[];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) uint64_t bars[3 * TC_STAGES + 1];
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
     constexpr int N = 16 * NP;
-    const int64_t blk_first = (int64_t)blockIdx.x * TC_BLOCKS;
-    const int nblk_here = (int)min((int64_t)TC_BLOCKS, p.nblk - blk_first);
-    // split-K: columns [kc0, kc1) of this CTA, in TC_K steps
-    const int64_t nsteps_all = (p.n + TC_K - 1) / TC_K;
+    constexpr int NB = tc_nb(K);  // blocks an 8-row group can touch
+    const int bpt = p.bpt, S = p.stages;
+    const int64_t blk_first = (int64_t)blockIdx.x * bpt;  // within the view
+    const int nblk_here = (int)min((int64_t)bpt, p.nblk - blk_first);
+    const int64_t nsteps_all = tc_steps(p.n);
     const int64_t s0 = nsteps_all * blockIdx.y / p.ksplit;
     const int64_t s1 = nsteps_all * (blockIdx.y + 1) / p.ksplit;
+    const int64_t nst = s1 - s0;
 
-    // smem: [A x2: 128 rows x 64 cols bf16 = 16 KB][B x2: N x 64 bf16][sign LUT nkeys x 16 B]
+    // smem: per stage [A 16 KB][B N x 128 B][keys (bpt + slack) x 64 x u16]
     constexpr uint32_t A_BYTES = TC_M * TC_K * 2;
     constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * 2;
-    unsigned char *sA = tc_smem;
-    unsigned char *sB = tc_smem + 2 * A_BYTES;
-    uint32_t *lut = reinterpret_cast<uint32_t *>(tc_smem + 2 * A_BYTES + 2 * B_BYTES);
-    const uint32_t aA = (uint32_t)__cvta_generic_to_shared(sA);
-    const uint32_t aB = (uint32_t)__cvta_generic_to_shared(sB);
-    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t st_bytes =
+        (A_BYTES + B_BYTES + (uint32_t)(bpt + TC_KEY_SLACK) * TC_K * 2 + 1023) / 1024 * 1024;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tc_smem);
+    const uint32_t bar_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t bar_aready = bar_full + 8 * TC_STAGES;
+    const uint32_t bar_empty = bar_aready + 8 * TC_STAGES;
+    const uint32_t bar_done = bar_empty + 8 * TC_STAGES;
 
-    // pair table: two rows' digits (d0 + 3*d1, digit 0 / +1 / -1 for 0 / 1 / 2)
-    // -> the two bf16 signs packed in one 32-bit word
-    if (tid < 9) {
-        const uint32_t d0 = tid % 3, d1 = tid / 3;
-        auto h = [](uint32_t d) -> uint32_t { return d == 0 ? 0u : (d == 1 ? 0x3F80u : 0xBF80u); };
-        lut[tid] = h(d0) | (h(d1) << 16);
+    // key rows the producer never writes (past this tile's blocks) read as 0
+    for (int s = 0; s < S; ++s) {
+        uint32_t *kz = reinterpret_cast<uint32_t *>(tc_smem + s * st_bytes + A_BYTES + B_BYTES +
+                                                    (size_t)nblk_here * TC_K * 2);
+        for (int i = tid; i < (bpt + TC_KEY_SLACK - nblk_here) * TC_K / 2; i += TC_THREADS)
+            kz[i] = 0u;
     }
-    if (warp == 0) {  // TMEM: N fp32 columns x 128 lanes
+    if (warp == TC_EXP_WARPS + 1) {  // TMEM: N fp32 columns x 128 lanes
         uint32_t cols = 32;
         while (cols < (uint32_t)N) cols <<= 1;
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -154,170 +253,159 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        mbar_init1(bar0);
-        mbar_init1(bar0 + 8);
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_aready + 8 * s, TC_EXP_WARPS * 32);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        mbar_init(bar_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_d = tmem_base_sh;
+    TC_MARK(tid == 0, 256)
 
-    // instruction descriptor: kind::f16, A = B = BF16, D = F32, A MN-major,
-    // B K-major, N >> 3 at [17,23), M >> 4 at [24,29)
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
-                           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-
-    const KeyT *km = reinterpret_cast<const KeyT *>(p.km);
-    const uint16_t *V = reinterpret_cast<const uint16_t *>(p.V);
-    // Per step each thread owns: column tid % 64 of the 8 blocks (tid / 64)*8
-    // + j (so a warp's 16-byte A stores cover all banks), and NP 16-byte
-    // pieces of the vector chunk (8 consecutive threads take 8 vectors of one
-    // 8-column group: conflict-free B stores).  Both are loaded one step
-    // ahead into registers (ping-pong), so global latency overlaps the
-    // previous step's expansion and MMAs.
-    const int c_t = tid & 63, bg_t = (tid >> 6) * 8;
-    struct Step {
-        uint32_t keys[8];
-        uint4 vp[NP];
-    };
-    auto load_step = [&](int64_t st, Step &S) {
-        const int64_t col = st * TC_K + c_t;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int bi = bg_t + j;
-            S.keys[j] = (bi < nblk_here && col < p.n)
-                            ? (uint32_t)__ldg(km + (blk_first + bi) * p.n + col) : 0u;
+    if (warp == TC_EXP_WARPS) {
+        // ---- producer ----
+        if (lane == 0) {
+            const uint32_t kbytes = (uint32_t)nblk_here * TC_K * 2;
+            for (int64_t it = 0; it < nst; ++it) {
+                const int s = (int)(it % S);
+                if (it >= S) mbar_wait_parity(bar_empty + 8 * s, (uint32_t)((it / S - 1) & 1));
+                const int64_t st = s0 + it;
+                TC_MARK(it < 64, it * 4 + 2)
+                const uint32_t sa = sbase + s * st_bytes;
+                mbar_expect_tx(bar_full + 8 * s, kbytes + B_BYTES);
+                bulk_g2s(sa + A_BYTES + B_BYTES, p.km + (st * p.bc + p.blk0 + blk_first) * TC_K,
+                         kbytes, bar_full + 8 * s);
+                bulk_g2s(sa + A_BYTES, p.vp + (size_t)st * (B_BYTES / 16), B_BYTES,
+                         bar_full + 8 * s);
+            }
         }
+    } else if (warp == TC_EXP_WARPS + 1) {
+        // ---- MMA issuer ----
+        if (lane == 0) {
+            // instruction descriptor: kind::f16, A = B = BF16, D = F32, A MN-major,
+            // B K-major, N >> 3 at [17,23), M >> 4 at [24,29)
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                                   ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+            int s = 0;
+            uint32_t par = 0;
+            for (int64_t it = 0; it < nst; ++it) {
+                mbar_wait_parity(bar_full + 8 * s, par);
+                mbar_wait_parity(bar_aready + 8 * s, par);
+                TC_MARK(it < 64, it * 4 + 3)
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a0 = sbase + s * st_bytes, b0 = a0 + A_BYTES;
 #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-            const int piece = tid + j * TC_THREADS;
-            const int vb = (piece & 7) + 8 * (piece >> 6), kg = (piece >> 3) & 7;
-            const int64_t c = st * TC_K + kg * 8;
-            uint4 val = make_uint4(0, 0, 0, 0);
-            if (vb < p.B) {
-                const uint16_t *src = V + (int64_t)vb * p.ldv + c;
-                if (c + 8 <= p.n && ((p.ldv & 7) == 0)) {
-                    val = ld_stream(reinterpret_cast<const uint4 *>(src));
-                } else {
-                    uint32_t h[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) h[q] = c + q < p.n ? src[q] : 0u;
-                    val = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16),
-                                     h[6] | (h[7] << 16));
+                for (int kk = 0; kk < TC_K / 16; ++kk) {
+                    // A MN-major: LBO = K-group stride (16 row groups x 128 B), SBO = M-group stride
+                    const uint64_t da = smem_desc(a0 + kk * 2 * (16 * 128), 16 * 128, 128);
+                    // B K-major: LBO = K-group stride (128 B), SBO = N-group stride (8 x 128 B)
+                    const uint64_t db = smem_desc(b0 + kk * 2 * 128, 128, 8 * 128);
+                    mma_bf16(tmem_d, da, db, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+                }
+                mma_commit(bar_empty + 8 * s);
+                if (++s == S) {
+                    s = 0;
+                    par ^= 1u;
                 }
             }
-            S.vp[j] = val;
+            mma_commit(bar_done);
         }
-    };
-    const bool binary = p.bitwidth == RSR_BINARY;
-    // the 8 (padded) rows of a key as 4 words of two bf16 signs
-    auto expand = [&](uint32_t key) -> uint4 {
-        uint32_t w[4];
-        if (binary) {
+    } else {
+        // ---- expanders: thread owns column c_t of row groups mg_t .. mg_t +
+        // TC_UNITS - 1 (tile rows 8 mg .. 8 mg + 7); a quarter warp's 16-byte
+        // A stores are 128 contiguous bytes ----
+        const int c_t = tid & 63, mg_t = (tid >> 6) * TC_UNITS;
+        // loop-invariant: first block of each row group and the bit offset of
+        // the group's first row inside that block's code
+        int koff[TC_UNITS], nsh[TC_UNITS];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t two = (key >> (2 * q)) & 3u;
-                w[q] = lut[(two & 1u) + 3u * (two >> 1)];
+        for (int j = 0; j < TC_UNITS; ++j) {
+            const int r0 = (mg_t + j) * 8, b0 = r0 / K;
+            koff[j] = b0 * TC_K + c_t;
+            nsh[j] = 2 * (r0 - b0 * K);
+        }
+        int s = 0;
+        uint32_t par = 0;
+        for (int64_t it = 0; it < nst; ++it) {
+            mbar_wait_parity(bar_full + 8 * s, par);
+            TC_MARK(tid == 0 && it < 64, it * 4 + 0)
+            unsigned char *stg = tc_smem + s * st_bytes;
+            const uint16_t *sk = reinterpret_cast<const uint16_t *>(stg + A_BYTES + B_BYTES);
+            uint32_t codes[TC_UNITS][NB];
+#pragma unroll
+            for (int j = 0; j < TC_UNITS; ++j)
+#pragma unroll
+                for (int q = 0; q < NB; ++q) codes[j][q] = sk[koff[j] + q * TC_K];
+            // A (MN-major core layout [kg 8][row group 16][8 columns][16 B = 8 rows])
+            unsigned char *dA = stg + (size_t)(c_t & 7) * 16 + (size_t)(c_t >> 3) * 16 * 128;
+#pragma unroll
+            for (int j = 0; j < TC_UNITS; j += 2) {
+                // bits [2 r0, 2 r0 + 16) of the concatenated row codes (shift
+                // amounts stay below 32), two units per register
+                uint32_t x0 = codes[j][0] >> nsh[j], x1 = codes[j + 1][0] >> nsh[j + 1];
+#pragma unroll
+                for (int q = 1; q < NB; ++q) {
+                    x0 |= codes[j][q] << (2 * K * q - nsh[j]);
+                    x1 |= codes[j + 1][q] << (2 * K * q - nsh[j + 1]);
+                }
+                uint32_t x;
+                asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(x) : "r"(x0), "r"(x1));
+                uint4 lo, hi;
+                expand_codes2(x, lo, hi);
+                *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j) * 128) = lo;
+                *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j + 1) * 128) = hi;
             }
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t nk = key / 9u;  // digits 2q, 2q+1 of the base-3 key
-                w[q] = lut[key - 9u * nk];
-                key = nk;
+            // generic-proxy writes -> visible to the tensor core (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(bar_aready + 8 * s);
+            TC_MARK(tid == 0 && it < 64, it * 4 + 1)
+            if (++s == S) {
+                s = 0;
+                par ^= 1u;
             }
         }
-        return make_uint4(w[0], w[1], w[2], w[3]);
-    };
-    uint32_t phase[2] = {0u, 0u};
-    auto do_step = [&](int64_t st, const Step &S) {
-        const int buf = (int)((st - s0) & 1);
-        if (st - s0 >= 2) {  // the MMAs that read this buffer two steps ago are done
-            mbar_wait_parity(bar0 + 8 * buf, phase[buf]);
-            phase[buf] ^= 1u;
-        }
-        // A (MN-major core layout [kg 8][block 16][8 columns][16 B = 8 rows])
-        unsigned char *dA = sA + buf * A_BYTES + (size_t)(c_t & 7) * 16;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4 *>(dA + ((size_t)(c_t >> 3) * TC_BLOCKS + bg_t + j) * 128) =
-                expand(S.keys[j]);
-        // B (K-major core layout [N/8][kg 8][8 vectors][16 B = 8 columns])
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-            const int piece = tid + j * TC_THREADS;
-            const int vb = (piece & 7) + 8 * (piece >> 6), kg = (piece >> 3) & 7;
-            *reinterpret_cast<uint4 *>(sB + buf * B_BYTES +
-                                       (((size_t)(vb >> 3) * 8 + kg) * 8 + (vb & 7)) * 16) = S.vp[j];
-        }
-        // generic-proxy writes -> visible to the tensor core (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t a0 = aA + buf * A_BYTES, b0 = aB + buf * B_BYTES;
-#pragma unroll
-            for (int kk = 0; kk < TC_K / 16; ++kk) {
-                // A MN-major: LBO = K-group stride (16 blocks x 128 B), SBO = M-group stride
-                const uint64_t da = smem_desc(a0 + kk * 2 * (TC_BLOCKS * 128), TC_BLOCKS * 128, 128);
-                // B K-major: LBO = K-group stride (128 B), SBO = N-group stride (8 x 128 B)
-                const uint64_t db = smem_desc(b0 + kk * 2 * 128, 128, 8 * 128);
-                mma_bf16(tmem_d, da, db, idesc, (st > s0 || kk > 0) ? 1u : 0u);
-            }
-            mma_commit(bar0 + 8 * buf);
-        }
-        __syncwarp();
-    };
-    Step SA, SB;
-    if (s0 < s1) load_step(s0, SA);
-    for (int64_t st = s0; st < s1; st += 2) {
-        if (st + 1 < s1) load_step(st + 1, SB);
-        do_step(st, SA);
-        if (st + 1 >= s1) break;
-        if (st + 2 < s1) load_step(st + 2, SA);
-        do_step(st + 1, SB);
     }
-    // wait for the last MMAs of both buffers
-    const int64_t nst = s1 - s0;
-    for (int b = 0; b < 2; ++b) {
-        // buffer b was committed ceil((nst - b) / 2) times; the waits above
-        // consumed max(0, that - 1) of them
-        const int64_t commits = (nst - b + 1) / 2;
-        if (commits > 0) mbar_wait_parity(bar0 + 8 * b, phase[b]);
-    }
+    __syncwarp();
+    mbar_wait_parity(bar_done, 0);
+    TC_MARK(tid == 0, 257)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-    // --- epilogue: warp w reads TMEM lanes 32w..32w+31 (rows), 8 columns at a time
-    const int row_t = warp * 32 + (int)lane;  // tile row = block * 8 + i
-    const int bi = row_t >> 3, i = row_t & 7;
-    const int64_t blk = blk_first + bi;
-    const bool valid = bi < nblk_here && i < p.k && (p.blk0 + blk) * p.k + i < p.m_rows;
-    const int64_t vrow = blk * p.k + i;  // row within the view
-    const int64_t rows_view = min(p.nblk * p.k, p.m_rows - p.blk0 * p.k);
-    for (int c = 0; c < N; c += 8) {
-        uint32_t r[8];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-              "=r"(r[7])
-            : "r"(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (valid) {
+    if (warp < 4) {
+        // --- epilogue: warp w reads TMEM lanes 32w..32w+31 (tile rows), 8 columns at a time
+        const int row_t = warp * 32 + (int)lane;
+        const int64_t rows_view = min(p.nblk * K, p.m_rows - p.blk0 * K);
+        const int64_t vrow = blk_first * K + row_t;  // row within the view
+        const bool valid = row_t < nblk_here * K && vrow < rows_view;
+        for (int c = 0; c < N; c += 8) {
+            uint32_t r[8];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                  "=r"(r[6]), "=r"(r[7])
+                : "r"(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (valid) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int vb = c + j;
-                if (vb < p.B) {
-                    const float x = __uint_as_float(r[j]);
-                    if (p.ksplit == 1) p.Y[(int64_t)vb * p.ldy + vrow] = x;
-                    else p.part[((int64_t)blockIdx.y * p.B + vb) * rows_view + vrow] = x;
+                for (int j = 0; j < 8; ++j) {
+                    const int vb = c + j;
+                    if (vb < p.B) {
+                        const float x = nst > 0 ? __uint_as_float(r[j]) : 0.f;
+                        if (p.ksplit == 1) p.Y[(int64_t)vb * p.ldy + vrow] = x;
+                        else p.part[((int64_t)blockIdx.y * p.B + vb) * rows_view + vrow] = x;
+                    }
                 }
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) {
+    TC_MARK(tid == 0, 258)
+    if (warp == TC_EXP_WARPS + 1) {
         uint32_t cols = 32;
         while (cols < (uint32_t)N) cols <<= 1;
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(cols));
@@ -335,16 +423,58 @@ __global__ void tc_finalize_kernel(TcParams p, int64_t rows_view) {
     }
 }
 
-static size_t tc_smem_bytes(int N, int) {
-    return 2 * (size_t)TC_M * TC_K * 2 + 2 * (size_t)N * TC_K * 2 + 64;
+static int tc_np(int B) {
+    int np = 1;
+    while (16 * np < B) np *= 2;
+    return np;
 }
 
-static int tc_ksplit(int64_t nblk, int64_t n) {
-    // about four CTAs per SM (52-100 KB of shared memory each)
-    const int64_t tiles = (nblk + TC_BLOCKS - 1) / TC_BLOCKS;
-    const int64_t steps = (n + TC_K - 1) / TC_K;
-    int64_t ks = std::max<int64_t>(1, (4 * (int64_t)sm_count() + tiles - 1) / tiles);
-    return (int)std::min<int64_t>(std::min<int64_t>(ks, std::max<int64_t>(1, steps / 4)), 32);
+static size_t tc_stage_bytes(int N, int k) {
+    const size_t bpt = TC_M / k;
+    return ((size_t)TC_M * TC_K * 2 + (size_t)N * TC_K * 2 + (bpt + TC_KEY_SLACK) * TC_K * 2 +
+            1023) / 1024 * 1024;
+}
+
+static int tc_stages(int N, int k) {
+    // deepest ring that still lets two CTAs share an SM (16 expander warps
+    // per SM); failing that the deepest ring that fits one CTA
+    const size_t sb = tc_stage_bytes(N, k);
+    for (int st = TC_STAGES; st >= 3; --st)
+        if (2 * (st * sb + 2048) <= 228 * 1024) return st;
+    int st = TC_STAGES;
+    while (st > 2 && st * sb > 220 * 1024) --st;
+    return st;
+}
+
+static size_t tc_smem_bytes(int N, int k) { return tc_stages(N, k) * tc_stage_bytes(N, k); }
+
+static int tc_ksplit(int64_t nblk, int64_t n, int B, int k) {
+    // split K so that the tiles x splits fill the resident CTA slots in as
+    // few waves as possible; a wave costs about its steps plus ~6 steps of
+    // prologue / epilogue
+    const int64_t bpt = TC_M / k;
+    const int64_t tiles = (nblk + bpt - 1) / bpt;
+    const int64_t steps = tc_steps(n);
+    const size_t smem = tc_smem_bytes(16 * tc_np(B), k) + 2048;
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (int64_t)smem));
+    const int64_t slots = per_sm * sm_count();
+    static const int forced = [] {
+        const char *e = getenv("RSR_TC_KSPLIT");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced > 0) return (int)std::max<int64_t>(1, std::min<int64_t>(forced, steps));
+    int best = 1;
+    double best_cost = 1e30;
+    for (int ks = 1; ks <= 32 && ks <= steps; ++ks) {
+        const int64_t waves = (tiles * ks + slots - 1) / slots;
+        const double cost = (double)waves * ((double)((steps + ks - 1) / ks) + 6.0) +
+                            0.02 * ks;  // partial traffic
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = ks;
+        }
+    }
+    return best;
 }
 
 }  // namespace rsr
@@ -353,10 +483,16 @@ using namespace rsr;
 
 extern "C" {
 
+#ifdef RSR_TC_DBG
+int rsr_tc_debug(unsigned long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, tc_dbg, sizeof(unsigned long long) * (64 * 4 + 4));
+}
+#endif
+
 size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k) {
-    const int64_t nkeys = bucket_count(bitwidth, k);
-    if (k > 8 || nkeys > 65536) return 0;
-    return (size_t)block_count * cols * (nkeys <= 256 ? 1 : 2);
+    (void)bitwidth;
+    if (k < 1 || k > 8 || block_count < 0 || cols < 0) return 0;
+    return (size_t)tc_steps(cols) * block_count * TC_K * 2;
 }
 
 rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
@@ -369,80 +505,92 @@ rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint
     cudaMemsetAsync(keymat, 0, bytes, s);
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 16);
-    if (bucket_count(bitwidth, k) <= 256)
-        keymat_kernel<uint8_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count,
-                                                    tile_width, bitwidth, cols, (uint8_t *)keymat);
-    else
-        keymat_kernel<uint16_t><<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count,
-                                                     tile_width, bitwidth, cols,
-                                                     (uint16_t *)keymat);
+    keymat_kernel<<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count, tile_width,
+                                       (uint16_t *)keymat);
     return launch_status();
+}
+
+// workspace: [packed V (256-byte aligned)][split-K partials]
+static size_t tc_vpack_bytes(int64_t n, int32_t B) {
+    return ((size_t)tc_steps(n) * 16 * tc_np(B) * TC_K * 2 + 255) / 256 * 256;
 }
 
 size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t block_begin,
                                      int64_t n_blocks, int32_t B) {
-    const int ks = tc_ksplit(n_blocks, n);
-    if (ks <= 1) return 0;
-    const int64_t rows = std::min(n_blocks * k, m - block_begin * k);
-    return (size_t)ks * B * rows * 4;
+    if (B < 1 || B > 256 || k < 1 || k > 8 || n_blocks < 0) return 0;
+    const int ks = tc_ksplit(n_blocks, n, B, k);
+    const int64_t rows = std::max<int64_t>(0, std::min(n_blocks * k, m - block_begin * k));
+    return tc_vpack_bytes(n, B) + (ks > 1 ? (size_t)ks * B * rows * 4 : 0);
 }
 
 rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwidth, int32_t k,
                          int64_t block_begin, int64_t n_blocks, const void *V, int32_t v_dtype,
                          int64_t ldv, int32_t B, float *Y, int64_t ldy, void *workspace,
                          size_t workspace_bytes, rsr_stream_t stream) {
+    (void)bitwidth;
     if (!keymat || !V || !Y || B < 1 || B > 256 || v_dtype != RSR_BF16 || k < 1 || k > 8)
         return RSR_ERR_INVALID;
     const int64_t rows = std::min(n_blocks * k, m - block_begin * k);
-    if (ldv < n || ldy < rows || n_blocks < 0) return RSR_ERR_INVALID;
+    if (ldv < n || ldy < rows || n_blocks < 0 || block_begin < 0) return RSR_ERR_INVALID;
     if (n_blocks == 0) return RSR_OK;
-    const int nkeys = (int)bucket_count(bitwidth, k);
-    const int ks = tc_ksplit(n_blocks, n);
+    const int ks = tc_ksplit(n_blocks, n, B, k);
     const size_t wsb = rsr_matmul_tc_workspace_bytes(m, n, k, block_begin, n_blocks, B);
-    if (wsb && (!workspace || workspace_bytes < wsb)) return RSR_ERR_WORKSPACE;
+    if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
+        return RSR_ERR_WORKSPACE;
+    const int np = tc_np(B);
     TcParams p;
-    p.km = (const char *)keymat + (size_t)block_begin * n * (nkeys <= 256 ? 1 : 2);
-    p.V = V;
-    p.ldv = ldv;
+    p.km = (const uint16_t *)keymat;
+    p.vp = (const uint4 *)workspace;
     p.Y = Y;
     p.ldy = ldy;
-    p.part = (float *)workspace;
+    p.part = (float *)((char *)workspace + tc_vpack_bytes(n, B));
     p.m_rows = m;
     p.n = n;
     p.nblk = n_blocks;
     p.blk0 = block_begin;
+    p.bc = (m + k - 1) / k;
     p.k = k;
-    p.bitwidth = bitwidth;
-    p.nkeys = nkeys;
+    p.bpt = TC_M / k;
     p.B = B;
-    int np = 1;
-    while (16 * np < B) np *= 2;
     p.N = 16 * np;
     p.ksplit = ks;
-    const size_t smem = tc_smem_bytes(p.N, nkeys);
-    if (smem > 200 * 1024) return RSR_ERR_INVALID;
+    p.stages = tc_stages(p.N, k);
+    if (block_begin + n_blocks > p.bc) return RSR_ERR_INVALID;
+    const size_t smem = tc_smem_bytes(p.N, k);
+    if (smem > 227 * 1024) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
-    dim3 grid((unsigned)((n_blocks + TC_BLOCKS - 1) / TC_BLOCKS), (unsigned)ks);
-#define RSR_TC_LAUNCH(KT, NPV)                                                                  \
-    {                                                                                          \
-        cudaFuncSetAttribute(rsr_tc_kernel<KT, NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             (int)smem);                                                       \
-        rsr_tc_kernel<KT, NPV><<<grid, TC_THREADS, smem, s>>>(p);                              \
+    {
+        const int64_t pieces = tc_steps(n) * p.N * 8;
+        const int g = (int)std::min<int64_t>((pieces + 255) / 256, (int64_t)sm_count() * 8);
+        tc_pack_v_kernel<<<g, 256, 0, s>>>((const uint16_t *)V, ldv, n, B, p.N, tc_steps(n),
+                                           (uint4 *)workspace);
     }
-#define RSR_TC_NP(KT)                          \
-    switch (np) {                              \
-        case 1: RSR_TC_LAUNCH(KT, 1) break;    \
-        case 2: RSR_TC_LAUNCH(KT, 2) break;    \
-        case 4: RSR_TC_LAUNCH(KT, 4) break;    \
-        case 8: RSR_TC_LAUNCH(KT, 8) break;    \
-        default: RSR_TC_LAUNCH(KT, 16) break;  \
+    dim3 grid((unsigned)((n_blocks + p.bpt - 1) / p.bpt), (unsigned)ks);
+#define RSR_TC_LAUNCH(NPV, KV)                                                                   \
+    {                                                                                           \
+        cudaFuncSetAttribute(rsr_tc_kernel<NPV, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)smem);                                                        \
+        rsr_tc_kernel<NPV, KV><<<grid, TC_THREADS, smem, s>>>(p);                               \
     }
-    if (nkeys <= 256) {
-        RSR_TC_NP(uint8_t)
-    } else {
-        RSR_TC_NP(uint16_t)
+#define RSR_TC_K(NPV)                              \
+    switch (k) {                                   \
+        case 1: RSR_TC_LAUNCH(NPV, 1) break;       \
+        case 2: RSR_TC_LAUNCH(NPV, 2) break;       \
+        case 3: RSR_TC_LAUNCH(NPV, 3) break;       \
+        case 4: RSR_TC_LAUNCH(NPV, 4) break;       \
+        case 5: RSR_TC_LAUNCH(NPV, 5) break;       \
+        case 6: RSR_TC_LAUNCH(NPV, 6) break;       \
+        case 7: RSR_TC_LAUNCH(NPV, 7) break;       \
+        default: RSR_TC_LAUNCH(NPV, 8) break;      \
     }
-#undef RSR_TC_NP
+    switch (np) {
+        case 1: RSR_TC_K(1) break;
+        case 2: RSR_TC_K(2) break;
+        case 4: RSR_TC_K(4) break;
+        case 8: RSR_TC_K(8) break;
+        default: RSR_TC_K(16) break;
+    }
+#undef RSR_TC_K
 #undef RSR_TC_LAUNCH
     if (ks > 1) {
         const int g2 = (int)std::min<int64_t>((rows * B + 255) / 256, 4096);

@@ -247,11 +247,6 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
     use_tc = method == "tc" or (method == "auto" and Vt.dtype == torch.bfloat16 and
                                 B >= TC_MIN_BATCH and B <= 256)
     if use_tc and Vt.dtype == torch.bfloat16 and a.keymat() is not None:
-        if Vt.stride(0) % 8 or Vt.data_ptr() % 16:  # cp.async needs 16-byte rows
-            ld = (a.n + 7) // 8 * 8
-            Vp = torch.zeros(B, ld, dtype=Vt.dtype, device=Vt.device)
-            Vp[:, :a.n] = Vt
-            Vt = Vp
         vw = a._view if view is None else view
         s = _lib.current_stream_ptr(a.device) if stream is None else stream
         L = _lib.lib()

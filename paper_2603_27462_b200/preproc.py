@@ -232,7 +232,9 @@ class RsrArtifact:
         self._view = self.view()
 
     def keymat(self):
-        """Per-block pattern key of every column (device, u8 or u16 [bc][n]),
+        """Per-block pattern key of every column (device, u8 or u16
+        [ceil(n/64)][bc][64]: the 16 blocks of a tensor-core step are one
+        contiguous chunk),
         built on first use for the tensor-core batched multiply; None when the
         pattern space is too large (k > 8)."""
         if "_keymat" not in self.__dict__:

@@ -86,6 +86,9 @@ def test_batched_errors(rsr):
     (200, 4096, 6, "ternary", 16),   # u16 keys
     (64, 2048, 8, "binary", 33),     # N padded to 48
     (2000, 1000, 4, "ternary", 2),   # several row tiles, split-K
+    (120, 1500, 8, "ternary", 8),    # 6561 keys: pair-table expansion
+    (48, 70000, 4, "ternary", 3),    # multi-tile artifact (tw 32768)
+    (64, 640, 5, "ternary", 256),    # N = 256
 ])
 def test_tensor_core_batched(rsr, m, n, k, bw, B):
     """bf16 batches on tcgen05 (key matrix -> sign expansion -> MMA): each
@@ -101,3 +104,23 @@ def test_tensor_core_batched(rsr, m, n, k, bw, B):
     dense = orc.decode(p)
     for b in range(B):
         assert float_ok(Y[b], orc.matvec_f64(ref, Vh[b]), dense, Vh[b]).all(), b
+
+
+def test_tensor_core_batched_shards(rsr):
+    """Row-block views (shards starting at any block) through the tcgen05
+    path match the rows of the whole multiply (the split-K partition may
+    differ, so fp32 rounding may too)."""
+    import torch
+    from paper_2603_27462_b200 import kernels as kn
+    m, n, k, B = 999, 2000, 5, 12
+    p = orc.random_matrix(m, n, "ternary", 17)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", p.data), k)
+    V = torch.randn(B, n, device="cuda").to(torch.bfloat16)
+    Yall = torch.empty(B, m, device="cuda")
+    kn.matmul_into(a, V, Yall, method="tc")
+    bc = a.plan.block_count
+    for b0, nb in [(0, 17), (17, 40), (57, bc - 57), (199, 1)]:
+        rows = min(nb * k, m - b0 * k)
+        Y = torch.full((B, rows), float("nan"), device="cuda")
+        kn.matmul_into(a, V, Y, view=a.view(b0, nb), method="tc")
+        torch.testing.assert_close(Y, Yall[:, b0 * k:b0 * k + rows], rtol=1e-5, atol=1e-3)

@@ -1,6 +1,7 @@
 """C4: ternary 8192^2 (k=5) batched multiply vs cuBLAS bf16 GEMM, B in 1..64.
 
-Device time per call with CUDA events over back-to-back launches; L2 is
+Device time per call with CUDA events over CUDA-graph replays of back-to-back
+calls (host launch overhead excluded); L2 is
 flushed between iterations by rotating 4 copies of the stream (and of the
 dense weight for cuBLAS).  usage: python tools/bench_batched.py [k] [Bs...]"""
 import os
@@ -27,17 +28,32 @@ print(f"C4 ternary {m}x{n} k={k}: key matrix {a.keymat().numel()/1e6:.1f} MB, RS
       f"file_bytes {a.file_bytes()/1e6:.1f} MB, dense bf16 {m*n*2/1e6:.0f} MB")
 
 
-def timeit(fn, iters=50):
-    for i in range(5):
+def timeit(fn, iters=48):
+    """Device time per call: 4 calls (one per rotated copy) captured in a CUDA
+    graph and replayed, so host launch overhead does not hide the kernels."""
+    for i in range(4):
         fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(4):
+            fn(i)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(4):
+                fn(i)
+    torch.cuda.synchronize()
+    g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(iters):
-        fn(i)
+    for _ in range(iters // 4):
+        g.replay()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) * 1e3 / iters
+    return e0.elapsed_time(e1) * 1e3 / (iters // 4 * 4)
 
 
 for B in Bs:
@@ -48,7 +64,7 @@ for B in Bs:
     def single(i):
         for b in range(B):
             kn.matvec_into(a, V[b], Y[b], view=views[i % 4])
-    us_single = timeit(single, iters=10 if B > 8 else 50)
+    us_single = timeit(single, iters=8 if B > 8 else 48)
     a.keymat()
     kms = [a.keymat()] + [a.keymat().clone() for _ in range(3)]
     def tc(i):
