@@ -42,7 +42,10 @@ constexpr int TC_M = 128;           // tile rows = TMEM lanes
 constexpr int TC_MAXBPT = 128;      // row blocks per tile: floor(128 / k)
 constexpr int TC_K = 64;            // columns per pipeline step
 constexpr int TC_STAGES = 4;       // ring depth (at most; fewer when shared memory is short)
-constexpr int TC_EXP_WARPS = 8;
+#ifndef RSR_TC_EXP_WARPS
+#define RSR_TC_EXP_WARPS 8
+#endif
+constexpr int TC_EXP_WARPS = RSR_TC_EXP_WARPS;
 constexpr int TC_THREADS = TC_EXP_WARPS * 32 + 64;  // expanders, producer, MMA
 constexpr int TC_UNITS = 16 * TC_K / (TC_EXP_WARPS * 32);  // (row group, column) units per thread
 constexpr int TC_KEY_SLACK = 9;    // zero key rows past the tile (8-row groups read ahead)
@@ -184,6 +187,7 @@ struct TcParams {
     float *part;         // split-K partials [ksplit][B][rows]
     int64_t m_rows, n, nblk, blk0, bc;
     int k, bpt, B, N, ksplit, stages;
+    uint32_t tab0, tab1;  // PRMT byte table {00 3F BF 00 | 00 80 80 00} (kept in registers)
 };
 
 // 8 row codes (2 bits each, +1 -> 01, -1 -> 10) of two units at once
@@ -191,7 +195,8 @@ struct TcParams {
 // PRMT picks each byte from a register table {00 3F BF 00 | 00 80 80 00}
 // with selector nibbles (4 + c0, c0, 4 + c1, c1) =
 // 0x0404 + 0x11 * (c0 + (c1 << 8)), built per 16-bit half with two IMADs
-__device__ __forceinline__ void expand_codes2(uint32_t x, uint4 &lo, uint4 &hi) {
+__device__ __forceinline__ void expand_codes2(uint32_t x, uint4 &lo, uint4 &hi, uint32_t tab0,
+                                              uint32_t tab1) {
     uint32_t w0[4], w1[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -199,10 +204,8 @@ __device__ __forceinline__ void expand_codes2(uint32_t x, uint4 &lo, uint4 &hi) 
         const uint32_t tm = t & 0x000F000Fu, th = t & 0x000C000Cu;
         // 0x11 * (c0 + 4 c1) + 0x42F * 4 c1 = 0x11 * (c0 + (c1 << 8)), + 0x0404
         const uint32_t sel = th * 0x42Fu + (tm * 0x11u + 0x04040404u);
-        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w0[q]) : "r"(0x00BF3F00u), "r"(0x00808000u), "r"(sel));
-        asm("prmt.b32 %0, %1, %2, %3;"
-            : "=r"(w1[q])
-            : "r"(0x00BF3F00u), "r"(0x00808000u), "r"(sel >> 16));
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w0[q]) : "r"(tab0), "r"(tab1), "r"(sel));
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w1[q]) : "r"(tab0), "r"(tab1), "r"(sel >> 16));
     }
     lo = make_uint4(w0[0], w0[1], w0[2], w0[3]);
     hi = make_uint4(w1[0], w1[1], w1[2], w1[3]);
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
             koff[j] = b0 * TC_K + c_t;
             nsh[j] = 2 * (r0 - b0 * K);
         }
+        const uint32_t tab0 = p.tab0, tab1 = p.tab1;
         int s = 0;
         uint32_t par = 0;
         for (int64_t it = 0; it < nst; ++it) {
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
                 uint32_t x;
                 asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(x) : "r"(x0), "r"(x1));
                 uint4 lo, hi;
-                expand_codes2(x, lo, hi);
+                expand_codes2(x, lo, hi, tab0, tab1);
                 *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j) * 128) = lo;
                 *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j + 1) * 128) = hi;
             }
@@ -555,6 +559,8 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     p.N = 16 * np;
     p.ksplit = ks;
     p.stages = tc_stages(p.N, k);
+    p.tab0 = 0x00BF3F00u;
+    p.tab1 = 0x00808000u;
     if (block_begin + n_blocks > p.bc) return RSR_ERR_INVALID;
     const size_t smem = tc_smem_bytes(p.N, k);
     if (smem > 227 * 1024) return RSR_ERR_INVALID;

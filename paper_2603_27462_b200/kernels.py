@@ -226,7 +226,7 @@ def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
 # fastest; bf16 batches from TC_MIN_BATCH on go to the tensor cores; the
 # CUDA-core batched stream kernel covers the rest
 SINGLE_MAX_BATCH = 2
-TC_MIN_BATCH = 8
+TC_MIN_BATCH = 3
 
 
 def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "auto"):
