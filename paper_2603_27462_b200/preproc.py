@@ -232,8 +232,8 @@ class RsrArtifact:
         self._view = self.view()
 
     def keymat(self):
-        """Per-block pattern key of every column (device, u8 or u16
-        [ceil(n/64)][bc][64]: the 16 blocks of a tensor-core step are one
+        """Per-block pattern key of every column as 2-bit row codes (device
+        u16 [ceil(n/64)][bc][64]: the blocks of a tensor-core step are one
         contiguous chunk),
         built on first use for the tensor-core batched multiply; None when the
         pattern space is too large (k > 8)."""
