@@ -195,15 +195,18 @@ def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
     bufs = a.__dict__.get(key)
     if bufs is None:
         dv = torch.empty(a.n, dtype=torch.int8 if is_int else torch.float32, device=a.device)
-        dy = torch.empty(a.m, dtype=torch.int32 if is_int else torch.float32, device=a.device)
-        bufs = a.__dict__[key] = (dv, dy)
+        ydt = torch.int32 if is_int else torch.float32
+        dy = torch.empty(a.m, dtype=ydt, device=a.device)
+        # pinned landing buffer: the D2H is a plain DMA (a pageable destination
+        # is staged by the driver); the caller gets a private copy
+        hy = torch.empty(a.m, dtype=ydt, pin_memory=True).numpy()
+        bufs = a.__dict__[key] = (dv, dy, hy)
     st = _launch_state(a, None)
-    y = np.empty(a.m, dtype=np.int32 if is_int else np.float32)
     _lib.check(_lib.lib().rsr_matvec_host(
-        st.ref, vn.ctypes.data, _lib.RSR_I8 if is_int else _lib.RSR_F32, y.ctypes.data,
+        st.ref, vn.ctypes.data, _lib.RSR_I8 if is_int else _lib.RSR_F32, bufs[2].ctypes.data,
         bufs[0].data_ptr(), bufs[1].data_ptr(), st.ws, st.wsb,
         _lib.current_stream_ptr(a.device)), "rsr_matvec")
-    return y
+    return bufs[2].copy()
 
 
 def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
