@@ -510,7 +510,7 @@ stream_build_banked_kernel(const uint64_t *__restrict__ words, const int64_t *__
             place_group_quad(
                 p, L,
                 [&](int64_t q) {
-                    if (lane == 0) out[run_slot(q, lr)] = key;
+                    if (lane == 0) out[run_slot(q, lr)] = key;  // key slots read no bank
                 },
                 [&](int64_t q, int64_t) {
                     const int ci = cand != INVALID ? cidx(q, cand & 31u) : -1;

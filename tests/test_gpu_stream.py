@@ -81,10 +81,11 @@ def decode_cell(ent, fmt):
     return out
 
 
-def wavefronts(seq):
+def wavefronts(seq, keys_read=False):
     """Mean shared-memory wavefronts per gather instruction of one u16 cell:
     at round r, slot j, the active lanes L read sequence position
-    (L*P + r)*32 + j; cost = max over banks of the distinct columns read."""
+    (L*P + r)*32 + j; cost = max over banks of the distinct columns read.
+    keys_read: the scaled format's kernel also reads v[key] at key slots."""
     N = len(seq) // 32
     P = (N + 31) // 32
     tot = n = 0
@@ -96,7 +97,7 @@ def wavefronts(seq):
                 if pair >= N or (pair // P) != L:
                     continue
                 isk, val = seq[pair * 32 + j]
-                if not isk:
+                if not isk or keys_read:
                     banks.setdefault(val % 32, set()).add(val)
             tot += max([1] + [len(v) for v in banks.values()])
             n += 1

@@ -24,7 +24,7 @@ wfs = []
 for dc in range(0, len(e_off) - 1, max(1, (len(e_off) - 1) // 40)):
     e0_, e1_ = int(e_off[dc]), int(e_off[dc + 1])
     seq = decode_cell(ent[e0_:e1_][run_slots(e1_ - e0_)], a.format)
-    wfs.append(wavefronts(seq))
+    wfs.append((wavefronts(seq), wavefronts(seq, keys_read=a.format == 1)))
 copies = [(a.entries_d.clone(), a.e_off_d.clone()) for _ in range(4)]
 views = [a.view(entries=e, e_off=o) for e, o in copies]
 v = torch.from_numpy(bench.random_vector(cfg["n"], 0)).cuda().to(torch.bfloat16)
@@ -40,5 +40,6 @@ for rep in range(5):
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1) * 1e3 / 400)
-print(f"{os.path.basename(os.environ.get('RSR_B200_LIB', 'default'))}: wavefronts {np.mean(wfs):.3f} "
+w = np.mean(np.array(wfs), axis=0)
+print(f"{os.path.basename(os.environ.get('RSR_B200_LIB', 'default'))}: wavefronts {w[0]:.3f} (with key reads {w[1]:.3f}) "
       f"preprocess {pre_ms:.1f} ms  multiply {np.median(ts):.2f} us (min {min(ts):.2f})")
