@@ -186,10 +186,11 @@ rsr_status rsr_matmul(const rsr_stream_view *view, const void *V, int32_t v_dtyp
 
 /* ---- batched multiply on the tensor cores (tcgen05) ---------------------------
  * For bf16 batches the pattern-table expansion runs on the tensor cores: the
- * key matrix holds, per row block, the pattern key of every column as 2-bit
- * row codes (the reference pattern_key code form, preproc.py:183-197; u16,
- * k <= 8), laid out [ceil(cols/64)][block_count][64], built once from the
- * reference arrays (tile-major cells, as rsr_group_fill writes them).
+ * code matrix holds every column's pattern key as 2-bit row codes (the
+ * reference pattern_key code form, preproc.py:183-197; k <= 8) concatenated
+ * down the rows and cut into 8-row groups: u16 [ceil(cols/64)][ceil(bc*k/8)]
+ * [64], built once from the reference arrays (tile-major cells, as
+ * rsr_group_fill writes them; rsr_keymat_bytes / rsr_keymat_build).
  * rsr_matmul_tc: Y[b] (f32, rows of blocks [block_begin, +n_blocks)) =
  * A . V[b] for bf16 V[b*ldv + col], B <= 256; fp32 accumulation of exact +-1
  * products (the float-path tolerance).  The workspace (always needed, 256-byte

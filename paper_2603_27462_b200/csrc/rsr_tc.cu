@@ -4,28 +4,29 @@
 // RSR's pattern-table step y_blk = T . S_blk (T in {0,+-1}^{k x P}) is a
 // dense contraction; with B vectors it is cheaper to apply T before the
 // segment sums: every column's pattern key, expanded through T, is one
-// column of the block's k rows.  So this path keeps, per row block, the
-// pattern key of every column in the reference's 2-bit code form
-// (pattern_key, preproc.py:183-197: code(row i) at bits 2i, 2i+1; u16 for
-// k <= 8), expands it straight into the A operand of tcgen05.mma and
-// accumulates in TMEM:
+// column of the block's k rows.  So this path keeps every column's pattern
+// key in the reference's 2-bit code form (pattern_key, preproc.py:183-197:
+// row i's code at bits 2i, 2i+1), concatenated down the rows and cut into
+// 8-row groups (one u16 per (row group, column); 16.8 MB at C4 -- 2 bits
+// per matrix entry), expands it straight into the A operand of tcgen05.mma
+// and accumulates in TMEM:
 //
 //   D[row][b] += A[row][col] * B[b][col],  A = T[:, key(blk, col)] (bf16 +-1/0),
 //                                          B = V chunk (bf16, K-major)
 //
-// Tile: M = 128 rows holding floor(128/k) whole row blocks back to back (no
-// per-block padding), K = 64 columns per step, N = vectors (16..256).
-// Warp-specialized, TC_STAGES-deep ring per CTA:
-//   warp 4  (producer)  bulk-copies (cp.async.bulk, mbarrier complete_tx) the
-//                       step's key chunk and its pre-packed B tile;
-//   warps 0-3 (expand)  build the MN-major A tile: per (8-row group,
-//                       column) one 16-bit slice of the concatenated codes
-//                       -> 4 PRMTs (a register byte table) -> one 16-byte
-//                       store (conflict-free: a quarter warp covers 128 B);
-//   warp 5  (MMA)       one thread issues tcgen05.mma (fp32 in TMEM) and
+// Tile: M = 128 rows (16 row groups), K = 64 columns per step, N = vectors
+// (16..256).  Warp-specialized, TC_STAGES-deep ring per CTA:
+//   warp 8  (producer)  bulk-copies (cp.async.bulk, mbarrier complete_tx) the
+//                       step's code chunk and its pre-packed B tile;
+//   warps 0-7 (expand)  build the MN-major A tile: per (row group, column)
+//                       one u16 of codes -> 4 PRMTs (a register byte table)
+//                       -> one 16-byte store (conflict-free: a quarter warp
+//                       covers 128 B);
+//   warp 9  (MMA)       one thread issues tcgen05.mma (fp32 in TMEM) and
 //                       commits to the stage's "empty" barrier.
-// Key matrix layout [step = col / 64][block][col % 64], so the blocks of a
-// step are one contiguous chunk for any first block (row-block shards).  V is
+// Code matrix layout [step = col / 64][row group][col % 64], so a tile's
+// step is one contiguous chunk; a row-block view starting mid-group takes
+// the enclosing groups and skips the outside rows in the epilogue.  V is
 // repacked once per call into the K-major no-swizzle core-matrix image of
 // each step (tc_pack_v_kernel), so its B tile is one bulk copy too.  Products
 // with +-1 are exact and accumulate in fp32: the float-path tolerance holds.
@@ -48,22 +49,25 @@ constexpr int TC_STAGES = 4;       // ring depth (at most; fewer when shared mem
 constexpr int TC_EXP_WARPS = RSR_TC_EXP_WARPS;
 constexpr int TC_THREADS = TC_EXP_WARPS * 32 + 64;  // expanders, producer, MMA
 constexpr int TC_UNITS = 16 * TC_K / (TC_EXP_WARPS * 32);  // (row group, column) units per thread
-constexpr int TC_KEY_SLACK = 9;    // zero key rows past the tile (8-row groups read ahead)
 
-__host__ __device__ constexpr int tc_nb(int k) { return (8 + k - 1) / k + 1; }
 
 __host__ __device__ inline int64_t tc_steps(int64_t n) { return (n + TC_K - 1) / TC_K; }
 
-// ---- key matrix: KM[step][blk][col % 64] = 2-bit row codes of column col in block blk ----
+// ---- key matrix: KM[step][g][col % 64] = the 2-bit row codes of rows
+// 8g .. 8g + 7 at column col (each block's pattern key, in code form, lands at
+// bit 2 (row % 8) of its row group; a block straddling two groups is split)
 __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                               const uint16_t *__restrict__ perm, const int64_t *__restrict__ po,
-                              int64_t bc, int64_t tc, int64_t tw, uint16_t *__restrict__ km) {
+                              int64_t bc, int64_t tc, int64_t tw, int k, int64_t ng,
+                              uint32_t *__restrict__ km32) {
     const uint32_t lane = lane_id();
     const int64_t cells = bc * tc;
     for (int64_t cell = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < cells;
          cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t t = cell / bc, b = cell - t * bc;  // reference cells are tile-major
         const int64_t c0 = t * tw;
+        const int64_t r0 = b * k, g0 = r0 >> 3;
+        const int sh = 2 * (int)(r0 & 7);
         for (int64_t g = go[cell]; g < go[cell + 1]; ++g) {
             const uint64_t w = words[g];
             const int64_t ps = (int64_t)(w & 0xFFFFu), L = (int64_t)((w >> 16) & 0xFFFFu);
@@ -72,10 +76,16 @@ __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t 
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 code |= (((pos >> i) & 1u) | (((neg >> i) & 1u) << 1)) << (2 * i);
+            const uint32_t lo = (code << sh) & 0xFFFFu, hi = (code << sh) >> 16;
             const uint16_t *cols = perm + po[cell] + ps;
             for (int64_t j = lane; j < L; j += 32) {
                 const int64_t col = c0 + cols[j];
-                km[((col / TC_K) * bc + b) * TC_K + (col % TC_K)] = (uint16_t)code;
+                const int64_t e = ((col / TC_K) * ng + g0) * TC_K + (col % TC_K);
+                atomicOr(km32 + (e >> 1), lo << (16 * (e & 1)));
+                if (hi) {
+                    const int64_t e2 = e + TC_K;  // next row group, same column
+                    atomicOr(km32 + (e2 >> 1), hi << (16 * (e2 & 1)));
+                }
             }
         }
     }
@@ -186,7 +196,8 @@ struct TcParams {
     int64_t ldy;
     float *part;         // split-K partials [ksplit][B][rows]
     int64_t m_rows, n, nblk, blk0, bc;
-    int k, bpt, B, N, ksplit, stages;
+    int64_t ng;           // row groups of 8 in the whole matrix
+    int k, B, N, ksplit, stages;
     uint32_t tab0, tab1;  // PRMT byte table {00 3F BF 00 | 00 80 80 00} (kept in registers)
 };
 
@@ -196,14 +207,17 @@ struct TcParams {
 // with selector nibbles (4 + c0, c0, 4 + c1, c1) =
 // 0x0404 + 0x11 * (c0 + (c1 << 8)), built per 16-bit half with two IMADs
 __device__ __forceinline__ void expand_codes2(uint32_t x, uint4 &lo, uint4 &hi, uint32_t tab0,
-                                              uint32_t tab1) {
+                                              uint32_t tab1, uint32_t c0404) {
     uint32_t w0[4], w1[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t t = x >> (4 * q);
         const uint32_t tm = t & 0x000F000Fu, th = t & 0x000C000Cu;
-        // 0x11 * (c0 + 4 c1) + 0x42F * 4 c1 = 0x11 * (c0 + (c1 << 8)), + 0x0404
-        const uint32_t sel = th * 0x42Fu + (tm * 0x11u + 0x04040404u);
+        // 0x11 * (c0 + 4 c1) + 0x42F * 4 c1 = 0x11 * (c0 + (c1 << 8)), + 0x0404;
+        // explicit mads (one immediate each: no constant rematerialization)
+        uint32_t u, sel;
+        asm("mad.lo.u32 %0, %1, 0x11, %2;" : "=r"(u) : "r"(tm), "r"(c0404));
+        asm("mad.lo.u32 %0, %1, 0x42F, %2;" : "=r"(sel) : "r"(th), "r"(u));
         asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w0[q]) : "r"(tab0), "r"(tab1), "r"(sel));
         asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w1[q]) : "r"(tab0), "r"(tab1), "r"(sel >> 16));
     }
@@ -212,7 +226,7 @@ __device__ __forceinline__ void expand_codes2(uint32_t x, uint4 &lo, uint4 &hi, 
 }
 
 // N = 16 * NP: MMA N (vectors padded up, <= 256)
-template <int NP, int K>
+template <int NP>
 __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     __shared__ uint32_t tmem_base_sh;
@@ -220,32 +234,34 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
     constexpr int N = 16 * NP;
-    constexpr int NB = tc_nb(K);  // blocks an 8-row group can touch
-    const int bpt = p.bpt, S = p.stages;
-    const int64_t blk_first = (int64_t)blockIdx.x * bpt;  // within the view
-    const int nblk_here = (int)min((int64_t)bpt, p.nblk - blk_first);
+    const int S = p.stages;
+    // this tile: row groups [g_first, g_first + 16) of the matrix, covering
+    // the view's rows [row0, row0 + rows_view) (rows outside are skipped)
+    const int64_t row0 = p.blk0 * p.k;
+    const int64_t rows_view = min(p.nblk * p.k, p.m_rows - row0);
+    const int64_t g_first = (row0 >> 3) + (int64_t)blockIdx.x * 16;
+    const int ng_here = (int)min((int64_t)16, p.ng - g_first);
     const int64_t nsteps_all = tc_steps(p.n);
     const int64_t s0 = nsteps_all * blockIdx.y / p.ksplit;
     const int64_t s1 = nsteps_all * (blockIdx.y + 1) / p.ksplit;
     const int64_t nst = s1 - s0;
 
-    // smem: per stage [A 16 KB][B N x 128 B][keys (bpt + slack) x 64 x u16]
+    // smem: per stage [A 16 KB][B N x 128 B][codes 16 x 64 x u16]
     constexpr uint32_t A_BYTES = TC_M * TC_K * 2;
     constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * 2;
-    const uint32_t st_bytes =
-        (A_BYTES + B_BYTES + (uint32_t)(bpt + TC_KEY_SLACK) * TC_K * 2 + 1023) / 1024 * 1024;
+    constexpr uint32_t C_BYTES = 16 * TC_K * 2;
+    constexpr uint32_t st_bytes = (A_BYTES + B_BYTES + C_BYTES + 1023) / 1024 * 1024;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tc_smem);
     const uint32_t bar_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     const uint32_t bar_aready = bar_full + 8 * TC_STAGES;
     const uint32_t bar_empty = bar_aready + 8 * TC_STAGES;
     const uint32_t bar_done = bar_empty + 8 * TC_STAGES;
 
-    // key rows the producer never writes (past this tile's blocks) read as 0
+    // code rows past the matrix (never written by the producer) read as 0
     for (int s = 0; s < S; ++s) {
         uint32_t *kz = reinterpret_cast<uint32_t *>(tc_smem + s * st_bytes + A_BYTES + B_BYTES +
-                                                    (size_t)nblk_here * TC_K * 2);
-        for (int i = tid; i < (bpt + TC_KEY_SLACK - nblk_here) * TC_K / 2; i += TC_THREADS)
-            kz[i] = 0u;
+                                                    (size_t)ng_here * TC_K * 2);
+        for (int i = tid; i < (16 - ng_here) * TC_K / 2; i += TC_THREADS) kz[i] = 0u;
     }
     if (warp == TC_EXP_WARPS + 1) {  // TMEM: N fp32 columns x 128 lanes
         uint32_t cols = 32;
@@ -273,7 +289,7 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
     if (warp == TC_EXP_WARPS) {
         // ---- producer ----
         if (lane == 0) {
-            const uint32_t kbytes = (uint32_t)nblk_here * TC_K * 2;
+            const uint32_t kbytes = (uint32_t)ng_here * TC_K * 2;
             for (int64_t it = 0; it < nst; ++it) {
                 const int s = (int)(it % S);
                 if (it >= S) mbar_wait_parity(bar_empty + 8 * s, (uint32_t)((it / S - 1) & 1));
@@ -281,8 +297,8 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
                 TC_MARK(it < 64, it * 4 + 2)
                 const uint32_t sa = sbase + s * st_bytes;
                 mbar_expect_tx(bar_full + 8 * s, kbytes + B_BYTES);
-                bulk_g2s(sa + A_BYTES + B_BYTES, p.km + (st * p.bc + p.blk0 + blk_first) * TC_K,
-                         kbytes, bar_full + 8 * s);
+                bulk_g2s(sa + A_BYTES + B_BYTES, p.km + (st * p.ng + g_first) * TC_K, kbytes,
+                         bar_full + 8 * s);
                 bulk_g2s(sa + A_BYTES, p.vp + (size_t)st * (B_BYTES / 16), B_BYTES,
                          bar_full + 8 * s);
             }
@@ -323,44 +339,31 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
         // TC_UNITS - 1 (tile rows 8 mg .. 8 mg + 7); a quarter warp's 16-byte
         // A stores are 128 contiguous bytes ----
         const int c_t = tid & 63, mg_t = (tid >> 6) * TC_UNITS;
-        // loop-invariant: first block of each row group and the bit offset of
-        // the group's first row inside that block's code
-        int koff[TC_UNITS], nsh[TC_UNITS];
-#pragma unroll
-        for (int j = 0; j < TC_UNITS; ++j) {
-            const int r0 = (mg_t + j) * 8, b0 = r0 / K;
-            koff[j] = b0 * TC_K + c_t;
-            nsh[j] = 2 * (r0 - b0 * K);
-        }
-        const uint32_t tab0 = p.tab0, tab1 = p.tab1;
+        // table words and the selector bias in plain registers, set once
+        // (shuffled: per-thread values ptxas keeps in vector registers
+        // instead of re-copying uniform ones at every use)
+        const uint32_t tab0 = __shfl_sync(RSR_FULL_MASK, p.tab0, 0);
+        const uint32_t tab1 = __shfl_sync(RSR_FULL_MASK, p.tab1, 0);
+        const uint32_t c0404 = __shfl_sync(RSR_FULL_MASK, 0x04040404u, 0);
         int s = 0;
         uint32_t par = 0;
         for (int64_t it = 0; it < nst; ++it) {
             mbar_wait_parity(bar_full + 8 * s, par);
             TC_MARK(tid == 0 && it < 64, it * 4 + 0)
             unsigned char *stg = tc_smem + s * st_bytes;
-            const uint16_t *sk = reinterpret_cast<const uint16_t *>(stg + A_BYTES + B_BYTES);
-            uint32_t codes[TC_UNITS][NB];
-#pragma unroll
-            for (int j = 0; j < TC_UNITS; ++j)
-#pragma unroll
-                for (int q = 0; q < NB; ++q) codes[j][q] = sk[koff[j] + q * TC_K];
+            const uint16_t *sk =
+                reinterpret_cast<const uint16_t *>(stg + A_BYTES + B_BYTES) + mg_t * TC_K + c_t;
             // A (MN-major core layout [kg 8][row group 16][8 columns][16 B = 8 rows])
             unsigned char *dA = stg + (size_t)(c_t & 7) * 16 + (size_t)(c_t >> 3) * 16 * 128;
 #pragma unroll
             for (int j = 0; j < TC_UNITS; j += 2) {
-                // bits [2 r0, 2 r0 + 16) of the concatenated row codes (shift
-                // amounts stay below 32), two units per register
-                uint32_t x0 = codes[j][0] >> nsh[j], x1 = codes[j + 1][0] >> nsh[j + 1];
-#pragma unroll
-                for (int q = 1; q < NB; ++q) {
-                    x0 |= codes[j][q] << (2 * K * q - nsh[j]);
-                    x1 |= codes[j + 1][q] << (2 * K * q - nsh[j + 1]);
-                }
+                // the row codes of two row groups, one per 16-bit half
                 uint32_t x;
-                asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(x) : "r"(x0), "r"(x1));
+                asm("prmt.b32 %0, %1, %2, 0x5410;"
+                    : "=r"(x)
+                    : "r"((uint32_t)sk[j * TC_K]), "r"((uint32_t)sk[(j + 1) * TC_K]));
                 uint4 lo, hi;
-                expand_codes2(x, lo, hi, tab0, tab1);
+                expand_codes2(x, lo, hi, tab0, tab1, c0404);
                 *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j) * 128) = lo;
                 *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j + 1) * 128) = hi;
             }
@@ -382,9 +385,8 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
     if (warp < 4) {
         // --- epilogue: warp w reads TMEM lanes 32w..32w+31 (tile rows), 8 columns at a time
         const int row_t = warp * 32 + (int)lane;
-        const int64_t rows_view = min(p.nblk * K, p.m_rows - p.blk0 * K);
-        const int64_t vrow = blk_first * K + row_t;  // row within the view
-        const bool valid = row_t < nblk_here * K && vrow < rows_view;
+        const int64_t vrow = g_first * 8 + row_t - row0;  // row within the view
+        const bool valid = vrow >= 0 && vrow < rows_view;
         for (int c = 0; c < N; c += 8) {
             uint32_t r[8];
             asm volatile(
@@ -433,16 +435,14 @@ static int tc_np(int B) {
     return np;
 }
 
-static size_t tc_stage_bytes(int N, int k) {
-    const size_t bpt = TC_M / k;
-    return ((size_t)TC_M * TC_K * 2 + (size_t)N * TC_K * 2 + (bpt + TC_KEY_SLACK) * TC_K * 2 +
-            1023) / 1024 * 1024;
+static size_t tc_stage_bytes(int N) {
+    return ((size_t)TC_M * TC_K * 2 + (size_t)N * TC_K * 2 + 16 * TC_K * 2 + 1023) / 1024 * 1024;
 }
 
-static int tc_stages(int N, int k) {
+static int tc_stages(int N) {
     // deepest ring that still lets two CTAs share an SM (16 expander warps
     // per SM); failing that the deepest ring that fits one CTA
-    const size_t sb = tc_stage_bytes(N, k);
+    const size_t sb = tc_stage_bytes(N);
     for (int st = TC_STAGES; st >= 3; --st)
         if (2 * (st * sb + 2048) <= 228 * 1024) return st;
     int st = TC_STAGES;
@@ -450,16 +450,22 @@ static int tc_stages(int N, int k) {
     return st;
 }
 
-static size_t tc_smem_bytes(int N, int k) { return tc_stages(N, k) * tc_stage_bytes(N, k); }
+static size_t tc_smem_bytes(int N) { return tc_stages(N) * tc_stage_bytes(N); }
 
-static int tc_ksplit(int64_t nblk, int64_t n, int B, int k) {
+// row tiles (16 row groups) covering the view's rows
+static int64_t tc_tiles(int64_t block_begin, int64_t n_blocks, int32_t k, int64_t m) {
+    const int64_t r0 = block_begin * k, r1 = std::min((block_begin + n_blocks) * k, m);
+    if (r1 <= r0) return 0;
+    const int64_t g0 = r0 >> 3, g1 = (r1 + 7) >> 3;
+    return (g1 - g0 + 15) / 16;
+}
+
+static int tc_ksplit(int64_t tiles, int64_t n, int B) {
     // split K so that the tiles x splits fill the resident CTA slots in as
     // few waves as possible; a wave costs about its steps plus ~6 steps of
     // prologue / epilogue
-    const int64_t bpt = TC_M / k;
-    const int64_t tiles = (nblk + bpt - 1) / bpt;
     const int64_t steps = tc_steps(n);
-    const size_t smem = tc_smem_bytes(16 * tc_np(B), k) + 2048;
+    const size_t smem = tc_smem_bytes(16 * tc_np(B)) + 2048;
     const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (int64_t)smem));
     const int64_t slots = per_sm * sm_count();
     static const int forced = [] {
@@ -496,7 +502,8 @@ int rsr_tc_debug(unsigned long long *out) {
 size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k) {
     (void)bitwidth;
     if (k < 1 || k > 8 || block_count < 0 || cols < 0) return 0;
-    return (size_t)tc_steps(cols) * block_count * TC_K * 2;
+    const int64_t ng = (block_count * k + 7) / 8;
+    return (size_t)tc_steps(cols) * ng * TC_K * 2;
 }
 
 rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
@@ -504,13 +511,14 @@ rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint
                             int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
                             void *keymat, rsr_stream_t stream) {
     const size_t bytes = rsr_keymat_bytes(block_count, cols, bitwidth, k);
-    if (!bytes || !keymat || !go || !po) return RSR_ERR_INVALID;
+    if (!bytes || !keymat || !go || !po || (reinterpret_cast<uintptr_t>(keymat) & 3))
+        return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(keymat, 0, bytes, s);
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 16);
-    keymat_kernel<<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count, tile_width,
-                                       (uint16_t *)keymat);
+    keymat_kernel<<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count, tile_width, k,
+                                       (block_count * k + 7) / 8, (uint32_t *)keymat);
     return launch_status();
 }
 
@@ -522,7 +530,7 @@ static size_t tc_vpack_bytes(int64_t n, int32_t B) {
 size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t block_begin,
                                      int64_t n_blocks, int32_t B) {
     if (B < 1 || B > 256 || k < 1 || k > 8 || n_blocks < 0) return 0;
-    const int ks = tc_ksplit(n_blocks, n, B, k);
+    const int ks = tc_ksplit(tc_tiles(block_begin, n_blocks, k, m), n, B);
     const int64_t rows = std::max<int64_t>(0, std::min(n_blocks * k, m - block_begin * k));
     return tc_vpack_bytes(n, B) + (ks > 1 ? (size_t)ks * B * rows * 4 : 0);
 }
@@ -537,7 +545,8 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     const int64_t rows = std::min(n_blocks * k, m - block_begin * k);
     if (ldv < n || ldy < rows || n_blocks < 0 || block_begin < 0) return RSR_ERR_INVALID;
     if (n_blocks == 0) return RSR_OK;
-    const int ks = tc_ksplit(n_blocks, n, B, k);
+    const int64_t tiles = tc_tiles(block_begin, n_blocks, k, m);
+    const int ks = tc_ksplit(tiles, n, B);
     const size_t wsb = rsr_matmul_tc_workspace_bytes(m, n, k, block_begin, n_blocks, B);
     if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
         return RSR_ERR_WORKSPACE;
@@ -553,16 +562,16 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     p.nblk = n_blocks;
     p.blk0 = block_begin;
     p.bc = (m + k - 1) / k;
+    p.ng = (p.bc * k + 7) / 8;
     p.k = k;
-    p.bpt = TC_M / k;
     p.B = B;
     p.N = 16 * np;
     p.ksplit = ks;
-    p.stages = tc_stages(p.N, k);
+    p.stages = tc_stages(p.N);
     p.tab0 = 0x00BF3F00u;
     p.tab1 = 0x00808000u;
     if (block_begin + n_blocks > p.bc) return RSR_ERR_INVALID;
-    const size_t smem = tc_smem_bytes(p.N, k);
+    const size_t smem = tc_smem_bytes(p.N);
     if (smem > 227 * 1024) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     {
@@ -571,32 +580,20 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
         tc_pack_v_kernel<<<g, 256, 0, s>>>((const uint16_t *)V, ldv, n, B, p.N, tc_steps(n),
                                            (uint4 *)workspace);
     }
-    dim3 grid((unsigned)((n_blocks + p.bpt - 1) / p.bpt), (unsigned)ks);
-#define RSR_TC_LAUNCH(NPV, KV)                                                                   \
-    {                                                                                           \
-        cudaFuncSetAttribute(rsr_tc_kernel<NPV, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             (int)smem);                                                        \
-        rsr_tc_kernel<NPV, KV><<<grid, TC_THREADS, smem, s>>>(p);                               \
-    }
-#define RSR_TC_K(NPV)                              \
-    switch (k) {                                   \
-        case 1: RSR_TC_LAUNCH(NPV, 1) break;       \
-        case 2: RSR_TC_LAUNCH(NPV, 2) break;       \
-        case 3: RSR_TC_LAUNCH(NPV, 3) break;       \
-        case 4: RSR_TC_LAUNCH(NPV, 4) break;       \
-        case 5: RSR_TC_LAUNCH(NPV, 5) break;       \
-        case 6: RSR_TC_LAUNCH(NPV, 6) break;       \
-        case 7: RSR_TC_LAUNCH(NPV, 7) break;       \
-        default: RSR_TC_LAUNCH(NPV, 8) break;      \
+    dim3 grid((unsigned)tiles, (unsigned)ks);
+#define RSR_TC_LAUNCH(NPV)                                                                      \
+    {                                                                                          \
+        cudaFuncSetAttribute(rsr_tc_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)smem);                                                       \
+        rsr_tc_kernel<NPV><<<grid, TC_THREADS, smem, s>>>(p);                                  \
     }
     switch (np) {
-        case 1: RSR_TC_K(1) break;
-        case 2: RSR_TC_K(2) break;
-        case 4: RSR_TC_K(4) break;
-        case 8: RSR_TC_K(8) break;
-        default: RSR_TC_K(16) break;
+        case 1: RSR_TC_LAUNCH(1) break;
+        case 2: RSR_TC_LAUNCH(2) break;
+        case 4: RSR_TC_LAUNCH(4) break;
+        case 8: RSR_TC_LAUNCH(8) break;
+        default: RSR_TC_LAUNCH(16) break;
     }
-#undef RSR_TC_K
 #undef RSR_TC_LAUNCH
     if (ks > 1) {
         const int g2 = (int)std::min<int64_t>((rows * B + 255) / 256, 4096);

@@ -232,9 +232,9 @@ class RsrArtifact:
         self._view = self.view()
 
     def keymat(self):
-        """Per-block pattern key of every column as 2-bit row codes (device
-        u16 [ceil(n/64)][bc][64]: the blocks of a tensor-core step are one
-        contiguous chunk),
+        """Every column's pattern key as 2-bit row codes cut into 8-row
+        groups (device u16 [ceil(n/64)][ceil(bc*k/8)][64]: a tensor-core
+        tile's step is one contiguous chunk),
         built on first use for the tensor-core batched multiply; None when the
         pattern space is too large (k > 8)."""
         if "_keymat" not in self.__dict__:
