@@ -235,6 +235,8 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
     const uint32_t lane = lane_id();
     constexpr int N = 16 * NP;
     const int S = p.stages;
+    // PDL: the finalize may launch now (it waits for this grid to finish)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // this tile: row groups [g_first, g_first + 16) of the matrix, covering
     // the view's rows [row0, row0 + rows_view) (rows outside are skipped)
     const int64_t row0 = p.blk0 * p.k;
@@ -290,6 +292,9 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
         // ---- producer ----
         if (lane == 0) {
             const uint32_t kbytes = (uint32_t)ng_here * TC_K * 2;
+            // PDL: the packed V comes from the previous kernel; everything
+            // before this point overlapped its tail
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             for (int64_t it = 0; it < nst; ++it) {
                 const int s = (int)(it % S);
                 if (it >= S) mbar_wait_parity(bar_empty + 8 * s, (uint32_t)((it / S - 1) & 1));
@@ -419,6 +424,7 @@ __global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
 }
 
 __global__ void tc_finalize_kernel(TcParams p, int64_t rows_view) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the partials are complete
     const int64_t total = rows_view * p.B;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -581,11 +587,23 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
                                            (uint4 *)workspace);
     }
     dim3 grid((unsigned)tiles, (unsigned)ks);
+    // the tcgen05 kernel and the finalize launch as programmatic dependents
+    // (PDL): each one's prologue overlaps the previous kernel's tail
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
 #define RSR_TC_LAUNCH(NPV)                                                                      \
     {                                                                                          \
         cudaFuncSetAttribute(rsr_tc_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                              (int)smem);                                                       \
-        rsr_tc_kernel<NPV><<<grid, TC_THREADS, smem, s>>>(p);                                  \
+        cudaLaunchKernelEx(&cfg, rsr_tc_kernel<NPV>, p);                                       \
     }
     switch (np) {
         case 1: RSR_TC_LAUNCH(1) break;
@@ -596,8 +614,11 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     }
 #undef RSR_TC_LAUNCH
     if (ks > 1) {
-        const int g2 = (int)std::min<int64_t>((rows * B + 255) / 256, 4096);
-        tc_finalize_kernel<<<g2, 256, 0, s>>>(p, rows);
+        cudaLaunchConfig_t fcfg = cfg;
+        fcfg.gridDim = dim3((unsigned)std::min<int64_t>((rows * B + 255) / 256, 4096));
+        fcfg.blockDim = dim3(256);
+        fcfg.dynamicSmemBytes = 0;
+        cudaLaunchKernelEx(&fcfg, tc_finalize_kernel, p, rows);
     }
     return launch_status();
 }
