@@ -124,3 +124,26 @@ def test_tensor_core_batched_shards(rsr):
         Y = torch.full((B, rows), float("nan"), device="cuda")
         kn.matmul_into(a, V, Y, view=a.view(b0, nb), method="tc")
         torch.testing.assert_close(Y, Yall[:, b0 * k:b0 * k + rows], rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("m,n,k,bw,tw", [
+    (101, 300, 5, "ternary", None),    # blocks straddle 8-row groups, K tail
+    (64, 200, 8, "binary", None),
+    (37, 5000, 3, "ternary", 2048),    # several tiles
+])
+def test_code_matrix_layout(rsr, m, n, k, bw, tw):
+    """The tensor-core code matrix equals the dense matrix's 2-bit codes
+    (+1 -> 01, -1 -> 10; reference pattern_key code form, preproc.py:183-197)
+    at u16 [col // 64][row // 8][col % 64], bits 2 (row % 8)."""
+    p = orc.random_matrix(m, n, bw, 7 * m + n)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k, tw)
+    km = a.keymat().cpu().numpy().view(np.uint16)
+    dense = orc.decode(p).astype(np.int64)
+    code = np.where(dense == 1, 1, np.where(dense == -1, 2, 0))
+    steps, ng = (n + 63) // 64, (a.plan.block_count * k + 7) // 8
+    assert km.size == steps * ng * 64
+    rows = np.arange(m)
+    exp = np.zeros((steps, ng, 64), np.int64)
+    for c in range(n):
+        np.add.at(exp[c // 64, :, c % 64], rows // 8, code[:, c] << (2 * (rows % 8)))
+    assert np.array_equal(km.reshape(steps, ng, 64).astype(np.int64), exp)
