@@ -56,6 +56,12 @@ def test_host_queries_need_no_gpu():
     assert L.rsr_group_count(None, 4, 4, 1, 1, 11, 4, None, None, None, None, None, 0,
                              None) == _lib.RSR_ERR_K_TOO_LARGE
     assert L.rsr_matvec(ctypes.byref(v), None, 0, None, 0, None, 0, None) == _lib.RSR_ERR_INVALID
+    # tensor-core code matrix: u16 per (8-row group, column), columns padded to 64
+    assert L.rsr_keymat_bytes(1639, 8192, 1, 5) == 128 * 1025 * 64 * 2   # C4: 16.8 MB
+    assert L.rsr_keymat_bytes(3, 65, 0, 8) == 2 * 3 * 64 * 2
+    assert L.rsr_keymat_bytes(10, 100, 1, 9) == 0                          # k > 8: no tc path
+    assert L.rsr_matmul_tc(None, 8, 8, 1, 2, 0, 4, None, 1, 8, 1, None, 8, None, 0,
+                           None) == _lib.RSR_ERR_INVALID
 
 
 def test_status_mapping():
