@@ -225,11 +225,12 @@ def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
 
 
 # auto policy (measured at C4, ternary 8192^2 k=5, tools/bench_batched.py):
-# up to SINGLE_MAX_BATCH vectors the single-vector kernel per column is
-# fastest; bf16 batches from TC_MIN_BATCH on go to the tensor cores; the
+# bf16 batches from TC_MIN_BATCH on go to the tensor cores (22.3 us at B=2
+# vs 24.1 for two single-vector calls); other batches of up to
+# SINGLE_MAX_BATCH vectors take the single-vector kernel per column; the
 # CUDA-core batched stream kernel covers the rest
 SINGLE_MAX_BATCH = 2
-TC_MIN_BATCH = 3
+TC_MIN_BATCH = 2
 
 
 def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "auto"):
