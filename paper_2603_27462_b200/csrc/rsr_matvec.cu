@@ -274,6 +274,65 @@ rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t 
 
 // Host-buffer multiply for the synchronous API: H2D copy of v, the multiply,
 // D2H copy of y, stream sync -- one call instead of one per step.
+//
+// Page-locked host buffers are mapped into the device address space (UVA),
+// so the two copies run as small kernels over the host link instead of DMA
+// memcpys: a kernel launch costs less than a copy-engine round trip at 64 KB,
+// and the copy-in kernel releases the multiply early (PDL), whose pre-wait
+// prologue (sign table, bucket zeroing, first stream round) then overlaps it.
+// Pageable buffers keep the cudaMemcpyAsync path.
+static const void *mapped_device_ptr(const void *h, int dir) {
+    // experiment knob RSR_HOST_COPY_DMA: 1 both copies DMA, 2 input only, 3 output only
+    static const int dma = getenv("RSR_HOST_COPY_DMA") ? atoi(getenv("RSR_HOST_COPY_DMA")) : 0;
+    if (dma == 1 || (dma == 2 && dir == 0) || (dma == 3 && dir == 1)) return nullptr;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+    return at.devicePointer;
+}
+
+// nbytes copied with 16-byte accesses when both sides allow it, bytes otherwise.
+__global__ void host_link_copy_kernel(const void *__restrict__ src, void *__restrict__ dst,
+                                      int64_t nbytes, int wait_prev) {
+    if (wait_prev) asm volatile("griddepcontrol.wait;" ::: "memory");
+    else asm volatile("griddepcontrol.launch_dependents;");
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const bool vec = (((uintptr_t)src | (uintptr_t)dst) & 15) == 0;
+    if (vec) {
+        const int64_t nv = nbytes >> 4;
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        for (int64_t i = tid; i < nv; i += stride) d4[i] = s4[i];
+        const unsigned char *s1 = reinterpret_cast<const unsigned char *>(src);
+        unsigned char *d1 = reinterpret_cast<unsigned char *>(dst);
+        for (int64_t i = (nv << 4) + tid; i < nbytes; i += stride) d1[i] = s1[i];
+    } else {
+        const unsigned char *s1 = reinterpret_cast<const unsigned char *>(src);
+        unsigned char *d1 = reinterpret_cast<unsigned char *>(dst);
+        for (int64_t i = tid; i < nbytes; i += stride) d1[i] = s1[i];
+    }
+}
+
+static void launch_host_link_copy(const void *src, void *dst, int64_t nbytes, bool after_prev,
+                                  cudaStream_t s) {
+    const int threads = 256;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nbytes / 16 + threads - 1) / threads, 64));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = after_prev ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, host_link_copy_kernel, src, dst, nbytes, after_prev ? 1 : 0);
+}
+
 rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
                            void *y_host, void *dev_v, void *dev_y, void *workspace,
                            size_t workspace_bytes, rsr_stream_t stream) {
@@ -282,13 +341,21 @@ rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int3
     const size_t esz = v_dtype == RSR_F32 || v_dtype == RSR_I32 ? 4 : (v_dtype == RSR_I8 ? 1 : 2);
     const int64_t rows =
         std::min(view->n_blocks * view->k, view->m - view->row_begin_block * view->k);
-    if (cudaMemcpyAsync(dev_v, v_host, (size_t)view->n * esz, cudaMemcpyHostToDevice, s) !=
-        cudaSuccess)
+    const size_t vbytes = (size_t)view->n * esz, ybytes = (size_t)rows * 4;
+    const void *v_map = mapped_device_ptr(v_host, 0);
+    void *y_map = const_cast<void *>(mapped_device_ptr(y_host, 1));
+    if (v_map) {
+        launch_host_link_copy(v_map, dev_v, (int64_t)vbytes, false, s);
+    } else if (cudaMemcpyAsync(dev_v, v_host, vbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
         return launch_status();
+    }
     rsr_status st = rsr_matvec(view, dev_v, v_dtype, dev_y, 0, workspace, workspace_bytes, stream);
     if (st != RSR_OK) return st;
-    if (cudaMemcpyAsync(y_host, dev_y, (size_t)rows * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    if (y_map) {
+        launch_host_link_copy(dev_y, y_map, (int64_t)ybytes, true, s);
+    } else if (cudaMemcpyAsync(y_host, dev_y, ybytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
         return launch_status();
+    }
     if (cudaStreamSynchronize(s) != cudaSuccess) return launch_status();
     return RSR_OK;
 }

@@ -119,6 +119,29 @@ def test_random_shapes_vs_oracle(rsr, seed, bw):
         assert np.array_equal(rsr.rsr_matvec_fused(a, vf), orc.fused_matvec(ref, vf))
 
 
+@pytest.mark.parametrize("n_,off", [(2999, 0), (3000, 1), (16, 3), (1, 0)])
+def test_pinned_host_vectors_take_the_mapped_copy(rsr, n_, off):
+    """numpy vectors in page-locked memory go through the host-link copy
+    kernels (rsr_matvec_host); odd lengths and misaligned starts take the
+    byte loop.  Results equal the pageable (DMA) path and the oracle."""
+    import torch
+    m_ = 97
+    p = orc.random_matrix(m_, n_, "ternary", 5)
+    ref = orc.preprocess(p, 4)
+    a = rsr.preprocess(rsr.PackedMatrix(m_, n_, "ternary", p.data), 4)
+    rng = np.random.default_rng(7)
+    vi = rng.integers(-128, 128, n_).astype(np.int8)
+    hi = torch.empty(n_ + off, dtype=torch.int8, pin_memory=True).numpy()[off:]
+    hi[:] = vi
+    assert np.array_equal(rsr.rsr_matvec(a, hi), orc.matvec_i8(ref, vi))
+    vf = (rng.standard_normal(n_) * 3).astype(np.float32)
+    hf = torch.empty(n_ + off, dtype=torch.float32, pin_memory=True).numpy()[off:]
+    hf[:] = vf
+    yp = rsr.rsr_matvec(a, hf)
+    assert np.array_equal(yp, rsr.rsr_matvec(a, vf))
+    assert float_ok(yp, orc.matvec_f64(ref, vf), orc.decode(p), vf).all()
+
+
 def test_torch_inputs_stay_on_device(rsr):
     import torch
     p = orc.random_matrix(64, 512, "ternary", 3)
