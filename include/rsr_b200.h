@@ -151,7 +151,9 @@ rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtyp
 /* rsr_matvec_host: the synchronous host-buffer form behind the Python API's
  * numpy path -- copies v_host (n elements of v_dtype; pinned memory for full
  * speed) to dev_v, multiplies into dev_y, copies the view's rows back to
- * y_host and synchronizes the stream.                                       */
+ * y_host and synchronizes the stream.  Page-locked (device-mapped) host
+ * buffers are copied by small kernels over the host link; pageable ones by
+ * cudaMemcpyAsync.                                                          */
 rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
                            void *y_host, void *dev_v, void *dev_y, void *workspace,
                            size_t workspace_bytes, rsr_stream_t stream);
