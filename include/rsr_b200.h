@@ -158,6 +158,13 @@ rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int3
                            void *y_host, void *dev_v, void *dev_y, void *workspace,
                            size_t workspace_bytes, rsr_stream_t stream);
 
+/* rsr_fused_matvec_host: rsr_fused_matvec (float32 output) with host
+ * buffers, as rsr_matvec_host -- the numpy path of rsr_matvec_fused and of
+ * Multiplier("RsrTernary").multiply (reference kernels.py:105-125, :215).    */
+rsr_status rsr_fused_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
+                                 double beta, void *y_host, void *dev_v, void *dev_y,
+                                 void *workspace, size_t workspace_bytes, rsr_stream_t stream);
+
 /* rsr_fused_matvec: absmax-quantize v (float64 math, half away from zero,
  * +-127), exact int32 multiply, out[i] = f32(f64(y_i) * (beta / scale)).
  * Bit-identical to _native.fused_matvec (_native.py:339-353).  The

@@ -67,6 +67,7 @@ SIGNATURES = {
     "rsr_matvec_workspace_bytes": (SZ, [ctypes.POINTER(StreamView)]),
     "rsr_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, P, I32, P, SZ, P]),
     "rsr_matvec_host": (I32, [ctypes.POINTER(StreamView), P, I32, P, P, P, P, SZ, P]),
+    "rsr_fused_matvec_host": (I32, [ctypes.POINTER(StreamView), P, I32, F64, P, P, P, P, SZ, P]),
     "rsr_fused_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, F64, P, P, I32, P, P, SZ, P]),
     "rsr_matmul_workspace_bytes": (SZ, [ctypes.POINTER(StreamView), I32]),
     "rsr_matmul": (I32, [ctypes.POINTER(StreamView), P, I32, I64, I32, P, I64, P, SZ, P]),

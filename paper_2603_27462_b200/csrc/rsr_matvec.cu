@@ -333,15 +333,16 @@ static void launch_host_link_copy(const void *src, void *dst, int64_t nbytes, bo
     cudaLaunchKernelEx(&cfg, host_link_copy_kernel, src, dst, nbytes, after_prev ? 1 : 0);
 }
 
-rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
-                           void *y_host, void *dev_v, void *dev_y, void *workspace,
-                           size_t workspace_bytes, rsr_stream_t stream) {
-    if (!view || !v_host || !y_host || !dev_v || !dev_y) return RSR_ERR_INVALID;
-    cudaStream_t s = (cudaStream_t)stream;
-    const size_t esz = v_dtype == RSR_F32 || v_dtype == RSR_I32 ? 4 : (v_dtype == RSR_I8 ? 1 : 2);
+}  // extern "C"
+
+// copy-in, the multiply (`mv`), copy-out, stream sync
+template <class Mv>
+static rsr_status host_round_trip(const rsr_stream_view *view, const void *v_host, size_t vbytes,
+                                  void *y_host, void *dev_v, void *dev_y, cudaStream_t s,
+                                  Mv &&mv) {
     const int64_t rows =
         std::min(view->n_blocks * view->k, view->m - view->row_begin_block * view->k);
-    const size_t vbytes = (size_t)view->n * esz, ybytes = (size_t)rows * 4;
+    const size_t ybytes = (size_t)rows * 4;
     const void *v_map = mapped_device_ptr(v_host, 0);
     void *y_map = const_cast<void *>(mapped_device_ptr(y_host, 1));
     if (v_map) {
@@ -349,7 +350,7 @@ rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int3
     } else if (cudaMemcpyAsync(dev_v, v_host, vbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
         return launch_status();
     }
-    rsr_status st = rsr_matvec(view, dev_v, v_dtype, dev_y, 0, workspace, workspace_bytes, stream);
+    const rsr_status st = mv();
     if (st != RSR_OK) return st;
     if (y_map) {
         launch_host_link_copy(dev_y, y_map, (int64_t)ybytes, true, s);
@@ -358,6 +359,35 @@ rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int3
     }
     if (cudaStreamSynchronize(s) != cudaSuccess) return launch_status();
     return RSR_OK;
+}
+
+static size_t dtype_bytes(int32_t d) {
+    return d == RSR_F32 || d == RSR_I32 ? 4 : (d == RSR_I8 ? 1 : 2);
+}
+
+extern "C" {
+
+rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
+                           void *y_host, void *dev_v, void *dev_y, void *workspace,
+                           size_t workspace_bytes, rsr_stream_t stream) {
+    if (!view || !v_host || !y_host || !dev_v || !dev_y) return RSR_ERR_INVALID;
+    return host_round_trip(view, v_host, (size_t)view->n * dtype_bytes(v_dtype), y_host, dev_v,
+                           dev_y, (cudaStream_t)stream, [&] {
+                               return rsr_matvec(view, dev_v, v_dtype, dev_y, 0, workspace,
+                                                 workspace_bytes, stream);
+                           });
+}
+
+rsr_status rsr_fused_matvec_host(const rsr_stream_view *view, const void *v_host, int32_t v_dtype,
+                                 double beta, void *y_host, void *dev_v, void *dev_y,
+                                 void *workspace, size_t workspace_bytes, rsr_stream_t stream) {
+    if (!view || !v_host || !y_host || !dev_v || !dev_y) return RSR_ERR_INVALID;
+    return host_round_trip(view, v_host, (size_t)view->n * dtype_bytes(v_dtype), y_host, dev_v,
+                           dev_y, (cudaStream_t)stream, [&] {
+                               return rsr_fused_matvec(view, dev_v, v_dtype, beta, nullptr, dev_y,
+                                                       RSR_F32, nullptr, workspace,
+                                                       workspace_bytes, stream);
+                           });
 }
 
 void rsr_debug_set_probe(unsigned long long *probe) { g_probe = probe; }

@@ -227,9 +227,13 @@ def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
 def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
     """Quantize v to int8, multiply exactly, rescale by weight_scale/scale
     (reference kernels.py:105-125), in one kernel launch."""
-    import torch
     if a.bitwidth != TERNARY:
         raise ValueError("fused path requires a ternary artifact")
+    if type(v) is np.ndarray and v.ndim == 1 and v.shape[0] == a.n and v.dtype == np.float32:
+        if counter is not None:
+            _count(a, counter)
+        return _fused_host(a, v if v.flags.c_contiguous else np.ascontiguousarray(v))
+    import torch
     vt, host = _prepare_vec(a, v)
     _count(a, counter)
     if vt.dtype == torch.int8:
@@ -237,6 +241,31 @@ def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
     out = torch.empty(a.m, dtype=torch.float32, device=a.device)
     fused_into(a, vt, out)
     return out.cpu().numpy() if host else out
+
+
+def _fused_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
+    """numpy float32 in, numpy float32 out through rsr_fused_matvec_host (one
+    C call, constant arguments bound once per artifact; see _matvec_host)."""
+    hc = a.__dict__.get("_host_call_fused")
+    if hc is None or hc[0] is not a._view or hc[2] != float(a.weight_scale):
+        import torch
+        dv = torch.empty(a.n, dtype=torch.float32, device=a.device)
+        dy = torch.empty(a.m, dtype=torch.float32, device=a.device)
+        hy = torch.empty(a.m, dtype=torch.float32, pin_memory=True).numpy()
+        st = _launch_state(a, None)
+        dev_idx = torch.device(a.device).index
+        if dev_idx is None:
+            dev_idx = torch.cuda.current_device()
+        hc = a.__dict__["_host_call_fused"] = (
+            a._view, _lib.lib().rsr_fused_matvec_host, float(a.weight_scale), st.ref, hy,
+            hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st.ws, st.wsb,
+            torch._C._cuda_getCurrentRawStream, dev_idx, (dv, dy))
+    _, fn, beta, ref, hy, hyp, dvp, dyp, ws, wsb, cur_stream, dev_idx, _keep = hc
+    status = fn(ref, vn.ctypes.data, _lib.RSR_F32, beta, hyp, dvp, dyp, ws, wsb,
+                cur_stream(dev_idx))
+    if status:
+        _lib.check(status, "rsr_matvec_fused")
+    return hy.copy()
 
 
 # auto policy (measured at C4, ternary 8192^2 k=5, tools/bench_batched.py):

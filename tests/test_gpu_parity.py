@@ -140,6 +140,11 @@ def test_pinned_host_vectors_take_the_mapped_copy(rsr, n_, off):
     yp = rsr.rsr_matvec(a, hf)
     assert np.array_equal(yp, rsr.rsr_matvec(a, vf))
     assert float_ok(yp, orc.matvec_f64(ref, vf), orc.decode(p), vf).all()
+    a.weight_scale = ref.weight_scale = 0.37
+    assert np.array_equal(rsr.rsr_matvec_fused(a, hf), orc.fused_matvec(ref, vf))
+    assert np.array_equal(rsr.rsr_matvec_fused(a, vf), orc.fused_matvec(ref, vf))
+    mul = rsr.Multiplier("RsrTernary", rsr.PackedMatrix(m_, n_, "ternary", p.data, 0.37), k=4)
+    assert np.array_equal(mul.multiply(hf), orc.fused_matvec(ref, vf))
 
 
 def test_torch_inputs_stay_on_device(rsr):

@@ -46,3 +46,4 @@ def dev_sync():
     kn.matvec_into(a, dv, dy); torch.cuda.synchronize()
 print(f"device-only launch + sync            {t(dev_sync):7.1f} us")
 print(f"launch only (back to back)           {t(lambda: kn.matvec_into(a, dv, dy)):7.1f} us")
+print(f"public API rsr_matvec_fused(numpy pinned) {t(lambda: rsr.rsr_matvec_fused(a, vh)):7.1f} us")
