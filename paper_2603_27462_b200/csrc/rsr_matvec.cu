@@ -350,7 +350,10 @@ static rsr_status host_round_trip(const rsr_stream_view *view, const void *v_hos
     } else if (cudaMemcpyAsync(dev_v, v_host, vbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
         return launch_status();
     }
-    const rsr_status st = mv();
+    // (the multiply's epilogue storing y straight into the mapped buffer
+    // measured slower end to end: its scattered 4-byte host writes cost the
+    // host's read of the result more than the copy kernel saves)
+    const rsr_status st = mv(dev_y);
     if (st != RSR_OK) return st;
     if (y_map) {
         launch_host_link_copy(dev_y, y_map, (int64_t)ybytes, true, s);
@@ -372,8 +375,8 @@ rsr_status rsr_matvec_host(const rsr_stream_view *view, const void *v_host, int3
                            size_t workspace_bytes, rsr_stream_t stream) {
     if (!view || !v_host || !y_host || !dev_v || !dev_y) return RSR_ERR_INVALID;
     return host_round_trip(view, v_host, (size_t)view->n * dtype_bytes(v_dtype), y_host, dev_v,
-                           dev_y, (cudaStream_t)stream, [&] {
-                               return rsr_matvec(view, dev_v, v_dtype, dev_y, 0, workspace,
+                           dev_y, (cudaStream_t)stream, [&](void *yt) {
+                               return rsr_matvec(view, dev_v, v_dtype, yt, 0, workspace,
                                                  workspace_bytes, stream);
                            });
 }
@@ -383,8 +386,8 @@ rsr_status rsr_fused_matvec_host(const rsr_stream_view *view, const void *v_host
                                  void *workspace, size_t workspace_bytes, rsr_stream_t stream) {
     if (!view || !v_host || !y_host || !dev_v || !dev_y) return RSR_ERR_INVALID;
     return host_round_trip(view, v_host, (size_t)view->n * dtype_bytes(v_dtype), y_host, dev_v,
-                           dev_y, (cudaStream_t)stream, [&] {
-                               return rsr_fused_matvec(view, dev_v, v_dtype, beta, nullptr, dev_y,
+                           dev_y, (cudaStream_t)stream, [&](void *yt) {
+                               return rsr_fused_matvec(view, dev_v, v_dtype, beta, nullptr, yt,
                                                        RSR_F32, nullptr, workspace,
                                                        workspace_bytes, stream);
                            });
