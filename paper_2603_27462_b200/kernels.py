@@ -14,6 +14,7 @@ on the device, nothing synchronizes).
 
 from __future__ import annotations
 
+import ctypes
 import os
 from dataclasses import dataclass
 
@@ -191,6 +192,21 @@ def rsr_matvec(a: RsrArtifact, v, counter: OpCounter | None = None,
     return y.cpu().numpy() if host else y
 
 
+try:  # CPython fast-call binding of the host round trips (csrc/hostcall.c)
+    from . import _hostcall
+except ImportError:  # not built: the same C entry points through ctypes
+    _hostcall = None
+
+_FN_ADDR: dict = {}
+
+
+def _fn_addr(fn) -> int:
+    a = _FN_ADDR.get(id(fn))
+    if a is None:
+        a = _FN_ADDR[id(fn)] = ctypes.cast(fn, ctypes.c_void_p).value
+    return a
+
+
 def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
     """numpy in, numpy out in one C call (H2D, multiply, D2H, sync) using
     device buffers cached on the artifact.  The call's constant arguments
@@ -218,7 +234,11 @@ def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
             hy, hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st.ws, st.wsb,
             torch._C._cuda_getCurrentRawStream, dev_idx, (dv, dy))
     _, fn, ref, code, hy, hyp, dvp, dyp, ws, wsb, cur_stream, dev_idx, _keep = hc
-    status = fn(ref, vn.ctypes.data, code, hyp, dvp, dyp, ws, wsb, cur_stream(dev_idx))
+    if _hostcall is not None:
+        status = _hostcall.matvec_host(_fn_addr(fn), ctypes.addressof(a._view), vn, code, hyp,
+                                       dvp, dyp, ws or 0, wsb, cur_stream(dev_idx))
+    else:
+        status = fn(ref, vn.ctypes.data, code, hyp, dvp, dyp, ws, wsb, cur_stream(dev_idx))
     if status:
         _lib.check(status, "rsr_matvec")
     return hy.copy()
@@ -261,8 +281,12 @@ def _fused_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
             hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st.ws, st.wsb,
             torch._C._cuda_getCurrentRawStream, dev_idx, (dv, dy))
     _, fn, beta, ref, hy, hyp, dvp, dyp, ws, wsb, cur_stream, dev_idx, _keep = hc
-    status = fn(ref, vn.ctypes.data, _lib.RSR_F32, beta, hyp, dvp, dyp, ws, wsb,
-                cur_stream(dev_idx))
+    if _hostcall is not None:
+        status = _hostcall.fused_host(_fn_addr(fn), ctypes.addressof(a._view), vn, _lib.RSR_F32,
+                                      beta, hyp, dvp, dyp, ws or 0, wsb, cur_stream(dev_idx))
+    else:
+        status = fn(ref, vn.ctypes.data, _lib.RSR_F32, beta, hyp, dvp, dyp, ws, wsb,
+                    cur_stream(dev_idx))
     if status:
         _lib.check(status, "rsr_matvec_fused")
     return hy.copy()

@@ -138,3 +138,23 @@ def test_ternarize_host_matches_oracle():
     assert np.array_equal(a.data, b.data) and a.weight_scale == b.weight_scale
     with pytest.raises(rsr.NonFinite):
         rsr.ternarize_weights(np.array([[1.0, np.nan]]))
+
+
+def test_hostcall_binding_passes_through_without_a_gpu():
+    """The CPython fast-call binding (csrc/hostcall.c) is built in-tree and
+    reaches the C entry points: a null view returns RSR_ERR_INVALID before
+    any CUDA call; bad arguments raise TypeError."""
+    import ctypes
+    import numpy as np
+    from paper_2603_27462_b200 import _hostcall, _lib
+    L = _lib.lib()
+    f1 = ctypes.cast(L.rsr_matvec_host, ctypes.c_void_p).value
+    f2 = ctypes.cast(L.rsr_fused_matvec_host, ctypes.c_void_p).value
+    v = np.zeros(8, np.float32)
+    assert _hostcall.matvec_host(f1, 0, v, _lib.RSR_F32, 1, 1, 1, 0, 0, 0) == _lib.RSR_ERR_INVALID
+    assert _hostcall.fused_host(f2, 0, v, _lib.RSR_F32, 1.0, 1, 1, 1, 0, 0, 0) == \
+        _lib.RSR_ERR_INVALID
+    with pytest.raises(TypeError):
+        _hostcall.matvec_host(f1, 0, v)
+    with pytest.raises((TypeError, ValueError, BufferError)):
+        _hostcall.matvec_host(f1, 0, np.zeros((4, 4), np.float32)[:, 0], 0, 1, 1, 1, 0, 0, 0)
