@@ -6,17 +6,25 @@ Workloads (BASELINE.json configs):
       (rsrmv bench.py:102-113), seed 0.  A step is one matvec.
   c5  (default at N>1) ternary 131072x131072, k=6, row-block sharded across
       the ranks (each rank generates and preprocesses only its strip with the
-      device generator) + NCCL all-gather of the output slices.  Strong
-      scaling: every step is one full 131072^2 matvec for the whole job.
+      device generator) + NCCL all-gather of the output slices + reassembly
+      of the full output in row order.  Strong scaling: every step is one
+      full 131072^2 matvec for the whole job.
   c1, c4 (binary 4096^2 k=8 f32 vector; ternary 8192^2 k=5) on request.
 
 `value` = matvec/s with the stream resident in HBM; L2 is defeated by
-rotating >= 3 copies of the stream (inputs larger than L2 per step).  `e2e` =
-the same metric through the public API with a host (numpy float32) vector
-and a host result (rank 0, unsharded configs).  `decode` (N=1) = greedy
-decode tok/s of BitNetForCausalLM(BitNetConfig()) with the HF linear
-replacement vs the same model with dense bf16 nn.Linear (cuBLAS), identical
-graph-captured loop.  --impl reference times the CPU restatement of the
+rotating >= 3 copies of the stream (inputs larger than L2 per step).  The K
+timed launches are queued behind a short device spin, so the region measures
+the device back to back (not the host's launch rate or a cold first launch
+after an idle gap).  `e2e` = the same metric through the public API with a
+host (numpy float32) vector and a host result (rank 0, unsharded configs).
+
+Sub-objects (N=1): `cublas_bf16` (the dense bf16 GEMV of the same matrix,
+north_star's context number), `c4` (ternary 8192^2 batched multiply, B =
+1..64, vs the cuBLAS bf16 GEMM), `decode` (greedy decode tok/s of
+BitNetForCausalLM(BitNetConfig()) with the HF linear replacement vs dense
+bf16 nn.Linear, identical graph-captured loop, plus linear-only time per
+token), and `roofline.traffic` measured by an ncu child process on one
+launch of the same kernel.  --impl reference times the CPU restatement of the
 reference float path (oracle/, all host cores) on the same config.
 """
 
@@ -48,6 +56,18 @@ CONFIGS = {
 }
 METRIC = "ternary matvec/s & %HBM roofline at 16384^2; BitNet-2B-shape decode tok/s"
 UNIT = "matvec/s"
+L2_DEFEAT = "rotating >= 3 copies of the chunk stream (each step's inputs exceed L2)"
+
+
+def make_config(cname: str, cfg: dict, world: int) -> dict:
+    """The workload description, identical for both arms."""
+    return {"workload": cfg["workload"], "name": cname, "m": cfg["m"], "n": cfg["n"],
+            "k": cfg["k"], "bitwidth": cfg["bitwidth"], "vector_dtype": cfg["vdtype"],
+            "seed": 0, "density": 0.5,
+            "generator": "rsrmv random_matrix (numpy)" if cfg["gen"] == "numpy"
+            else "counter-based splitmix64 (device; CPU restatement in oracle/)",
+            "l2_defeat": L2_DEFEAT,
+            "parallelism": f"rowblock{world}" if world > 1 else "single"}
 
 
 def random_packed(m, n, bitwidth, seed, density=0.5):
@@ -177,12 +197,127 @@ def cpu_reference_run(cfg, steps, warmup, seconds=None):
 
 
 # ---------------------------------------------------------------------------
+# device timing helpers
+
+def spin_cycles(steps: int) -> int:
+    """Device spin long enough for the host to enqueue `steps` launches
+    behind it (~15 us of host time per launch, generous), >= 2 ms."""
+    return int(max(2000.0, 40.0 * steps) * 1965)
+
+
+def graph_time_us(fn, copies: int = 4, iters: int = 48) -> float:
+    """Device time per call: `copies` calls (fn(i), one per rotated input
+    copy) captured in one CUDA graph and replayed back to back."""
+    import torch
+    for i in range(copies):
+        fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(copies):
+            fn(i)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(copies):
+                fn(i)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(1, iters // copies)
+    torch.cuda._sleep(spin_cycles(reps))
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / (reps * copies)
+
+
+# ---------------------------------------------------------------------------
+# cuBLAS bf16 dense GEMV of the same matrix (north_star: "reported for context")
+
+def cublas_bf16_bench(packed, m, n, v_bf16, hbm, rsr_value):
+    import torch
+    from paper_2603_27462_b200.matcore import dense_device
+    W = dense_device(packed).to(torch.bfloat16)  # [m, n] bf16, 2*m*n bytes (> L2)
+    y = torch.empty(m, dtype=torch.bfloat16, device=W.device)
+    for _ in range(5):
+        torch.mv(W, v_bf16, out=y)
+    torch.cuda.synchronize()
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(spin_cycles(reps))
+    e0.record()
+    for _ in range(reps):
+        torch.mv(W, v_bf16, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    nbytes = 2 * m * n + 2 * n + 2 * m
+    del W
+    torch.cuda.empty_cache()
+    return {"op": f"torch.mv(W bf16 [{m}x{n}], v bf16) -> cuBLAS GEMV, same matrix decoded",
+            "us": us, "matvec_s": 1e6 / us, "bytes": nbytes, "gbs": nbytes / us / 1e3,
+            "frac_hbm": nbytes / us / 1e3 / hbm, "rsr_speedup": rsr_value / (1e6 / us)}
+
+
+# ---------------------------------------------------------------------------
+# C4: batched multiply vs cuBLAS bf16 GEMM
+
+def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
+    import torch
+    import paper_2603_27462_b200 as rsr
+    from paper_2603_27462_b200 import kernels as kn
+    from paper_2603_27462_b200.matcore import dense_device
+    m = n = 8192
+    k = 5
+    pm = rsr.PackedMatrix(m, n, "ternary", random_packed(m, n, "ternary", 0))
+    a = rsr.preprocess(pm, k)
+    copies = [(a.entries_d, a.e_off_d)] + [(a.entries_d.clone(), a.e_off_d.clone())
+                                           for _ in range(3)]
+    views = [a.view(entries=e, e_off=o) for e, o in copies]
+    km = a.keymat()
+    kms = [km] + ([km.clone() for _ in range(3)] if km is not None else [])
+    dense = dense_device(pm).to(torch.bfloat16)
+    Wb = [dense, dense.clone()]  # 2 x 134 MB > L2
+    rows = []
+    for B in Bs:
+        V = torch.stack([torch.from_numpy(random_vector(n, b)) for b in range(B)]).to(
+            torch.bfloat16).cuda()
+        Y = torch.empty(B, m, dtype=torch.float32, device="cuda")
+
+        def ours(i):
+            if kms:
+                a.__dict__["_keymat"] = kms[i % 4]
+            kn.matmul_into(a, V, Y, view=views[i % 4])
+        us = graph_time_us(ours)
+        Yd = torch.empty(B, m, dtype=torch.bfloat16, device="cuda")
+        us_cub = graph_time_us(lambda i: torch.matmul(V, Wb[i % 2].t(), out=Yd))
+        alg = (a.file_bytes() - 24) + B * (n * 2 + m * 4)
+        rows.append({"B": B, "us": us, "vectors_s": B / us * 1e6, "cublas_us": us_cub,
+                     "vs_cublas": us_cub / us, "alg_bytes": int(alg),
+                     "alg_gbs": alg / us / 1e3})
+    if kms:
+        a.__dict__["_keymat"] = kms[0]
+    del Wb, dense
+    torch.cuda.empty_cache()
+    return {"workload": "ternary 8192x8192, k=5, bf16 vectors [B, 8192] -> f32 [B, 8192]",
+            "api": "rsr_matvec_batched / kernels.matmul_into(method='auto')",
+            "timing": "CUDA-graph replays of 4 back-to-back calls over rotated stream copies",
+            "cublas": "torch.matmul(V bf16 [B, 8192], W bf16 [8192, 8192]^T)",
+            "rows": rows}
+
+
+# ---------------------------------------------------------------------------
 # decode sub-benchmark (C3)
 
 def decode_bench(steps=64, k=5):
     import torch
     from transformers import BitNetConfig, BitNetForCausalLM
-    from paper_2603_27462_b200.decode import GraphDecoder
+    from paper_2603_27462_b200.decode import GraphDecoder, linear_time_per_token
     from paper_2603_27462_b200.hf import replace_linear_with_rsr
     torch.manual_seed(0)
     cfg = BitNetConfig()
@@ -208,13 +343,70 @@ def decode_bench(steps=64, k=5):
     res = {name: float(np.median(v)) for name, v in samples.items()}
     del decs
     torch.cuda.empty_cache()
+    lin = {"dense_bf16_cublas": linear_time_per_token(model),
+           "rsr": linear_time_per_token(rsr_model)}
     return {"model": "BitNetForCausalLM(BitNetConfig()) random init, bf16, 30 layers, "
                      "hidden 2560, FFN 6912",
             "loop": "greedy, HF StaticCache, one CUDA graph per step, batch 1",
             "k": k, "steps": steps, "reps": "median of 5 interleaved runs per arm",
             "rsr_tok_s": res["rsr"],
             "dense_tok_s": res["dense_bf16_cublas"],
-            "speedup": res["rsr"] / res["dense_bf16_cublas"]}
+            "speedup": res["rsr"] / res["dense_bf16_cublas"],
+            "linear_us_per_token": {name: v["us"] for name, v in lin.items()},
+            "linear_speedup": lin["dense_bf16_cublas"]["us"] / lin["rsr"]["us"],
+            "linear_detail": lin}
+
+
+# ---------------------------------------------------------------------------
+# roofline.traffic: DRAM bytes of one launch, measured by an ncu child
+
+def traffic_child(cname: str, k: int):
+    """Run under ncu by measure_traffic(): preprocess + 3 launches."""
+    import torch
+    import paper_2603_27462_b200 as rsr
+    from paper_2603_27462_b200 import kernels as kn
+    cfg = CONFIGS[cname]
+    m, n = cfg["m"], cfg["n"]
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, cfg["bitwidth"],
+                                        random_packed(m, n, cfg["bitwidth"], 0)), k)
+    v = torch.from_numpy(random_vector(n, 0)).cuda()
+    if cfg["vdtype"] == "bf16":
+        v = v.to(torch.bfloat16)
+    y = torch.empty(m, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        kn.matvec_into(a, v, y)
+    torch.cuda.synchronize()
+
+
+def measure_traffic(cname: str, k: int, timeout: int = 300):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the third launch of the
+    multiply kernel (ncu flushes caches before the replay: cold HBM bytes)."""
+    ncu = "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "-k", "regex:rsr_mv_kernel", "--launch-skip", "2", "-c", "1", "--csv",
+           sys.executable, os.path.abspath(__file__), "--traffic-child", "--config", cname,
+           "--k", str(k)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout).stdout
+    except Exception as e:
+        return None, f"ncu child failed: {e!r}"[:200]
+    vals = {}
+    for line in out.splitlines():
+        f = [x.strip('"') for x in line.split('","')]
+        if len(f) >= 3 and f[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum",
+                                     "gpu__time_duration.sum"):
+            unit, val = f[-2], float(f[-1].replace(",", "").strip('"'))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+                     "KB": 1e3, "MB": 1e6, "GB": 1e9, "nsecond": 1e-3, "usecond": 1.0,
+                     "msecond": 1e3}.get(unit, 1.0)
+            vals[f[-3]] = val * scale
+    if "dram__bytes_read.sum" not in vals:
+        return None, "ncu output not parsed"
+    rd, wr = vals["dram__bytes_read.sum"], vals.get("dram__bytes_write.sum", 0.0)
+    return {"bytes": int(rd + wr), "read": int(rd), "write": int(wr),
+            "ncu_us": vals.get("gpu__time_duration.sum")}, None
 
 
 # ---------------------------------------------------------------------------
@@ -230,6 +422,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip cublas_bf16 / c4 / traffic sub-measurements")
+    ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -239,12 +434,11 @@ def main():
     cfg = dict(CONFIGS[cname])
     if args.k:
         cfg["k"] = args.k
+    if args.traffic_child:
+        traffic_child(cname, cfg["k"])
+        return
     warmup = max(args.warmup, 3)
-    config = {"workload": cfg["workload"], "name": cname, "m": cfg["m"], "n": cfg["n"],
-              "k": cfg["k"], "bitwidth": cfg["bitwidth"], "vector_dtype": cfg["vdtype"],
-              "seed": 0, "density": 0.5,
-              "generator": "rsrmv random_matrix (numpy)" if cfg["gen"] == "numpy"
-              else "counter-based splitmix64 (device; CPU restatement in oracle/)"}
+    config = make_config(cname, cfg, world)
 
     if args.impl == "reference":
         if rank != 0:
@@ -276,8 +470,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     m, n, k = cfg["m"], cfg["n"], cfg["k"]
+    full_packed = None
     if cfg["gen"] == "numpy":
         full = random_packed(m, n, cfg["bitwidth"], 0)
+        full_packed = rsr.PackedMatrix(m, n, cfg["bitwidth"], full)
         strip = lambda r0, r1: rsr.PackedMatrix(r1 - r0, n, cfg["bitwidth"], full[r0:r1])
     else:
         strip = lambda r0, r1: random_ternary_device(r1 - r0, n, 0, 0.5, row0=r0, device=dev)
@@ -287,7 +483,7 @@ def main():
     torch.cuda.synchronize()
     preprocess_ms = 1e3 * (time.perf_counter() - t0)
     a = sm.local
-    nb = a.plan.block_count
+    tc = a.plan.tile_count
 
     # L2 defeat: rotate copies of the local stream
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -305,11 +501,13 @@ def main():
     rows = sm.r1 - sm.r0
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
+    y_full = torch.empty(m, dtype=torch.float32, device=dev)
 
     def step(i):
         kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies], stream=sptr)
         if world > 1:
             dist.all_gather_into_tensor(y_all, y_local)
+            torch.index_select(y_all, 0, sm.index, out=y_full)  # full y in row order
 
     for i in range(warmup):
         step(i)
@@ -325,13 +523,18 @@ def main():
     torch.cuda.synchronize()
     kernel_ms = float(np.median([e0.elapsed_time(e1) for e0, e1 in kev]))
 
-    # ---- timed region: exactly K steps
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
+    # ---- timed region: exactly K steps, queued behind a device spin
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        time.sleep(0.3)
+        t_load = time.perf_counter()  # untimed load while the sampler starts
+        while time.perf_counter() - t_load < 0.3:
+            for i in range(20):
+                step(i)
+            torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(spin_cycles(args.steps))
         start.record(stream)
         for i in range(args.steps):
             step(i)
@@ -383,14 +586,19 @@ def main():
     launch_ms = ms_per_step if world == 1 else kernel_ms
     achieved = local_alg / (launch_ms * 1e-3) / 1e9
     own = sb + n * vbytes + rows * 4
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(f"{cname}_k{k}_world{world}")
-    except Exception:
-        pass
+    traffic, traffic_note = None, "skipped (--no-extras)"
+    if world == 1 and not args.no_extras:
+        tr, err = measure_traffic(cname, k)
+        if tr is not None:
+            traffic = tr["bytes"]
+            traffic_note = (f"ncu child process (dram__bytes_read.sum {tr['read']} + "
+                            f"dram__bytes_write.sum {tr['write']}) on the 3rd launch of "
+                            f"rsr_mv_kernel, caches flushed; ncu duration {tr['ncu_us']} us")
+        else:
+            traffic_note = err
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+            "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_note,
+            "peak_kind": peak_kind,
             "algorithmic_bytes": int(local_alg), "stream_bytes": int(own),
             "achieved_own_bytes_gbs": own / (launch_ms * 1e-3) / 1e9,
             "launch_us": launch_ms * 1e3,
@@ -402,6 +610,17 @@ def main():
         val, threads, nn_, el, sample = cpu_reference_run(cfg, 0, 1, seconds=args.cpu_seconds)
         cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
 
+    extras = {}
+    if world == 1 and not args.no_extras:
+        for name, fn in (("cublas_bf16", lambda: cublas_bf16_bench(full_packed, m, n, vt, hbm,
+                                                                     value)
+                          if full_packed is not None and cfg["vdtype"] == "bf16" else None),
+                         ("c4", c4_bench)):
+            try:
+                extras[name] = fn()
+            except Exception as e:  # reported, never silently replaced
+                extras[name] = {"error": repr(e)[:300]}
+
     decode = None
     if world == 1 and not args.no_decode:
         try:
@@ -409,16 +628,20 @@ def main():
         except Exception as e:  # reported, never silently replaced
             decode = {"error": repr(e)[:300]}
 
+    launches_per_step = 1 + (1 if tc > 1 else 0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(config, l2_defeat=f"rotating {ncopies} stream copies "
-                                              f"({sb / 1e6:.1f} MB each, L2 {l2 / 1e6:.0f} MB)",
-                           parallelism=f"rowblock{world}" if world > 1 else "single"),
-            "preprocess_ms": preprocess_ms, "gpu_launches": args.steps,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "decode": decode,
-            "clocks": clk.summary()}
+            "config": config,
+            "l2_copies": f"{ncopies} stream copies ({sb / 1e6:.1f} MB each, L2 {l2 / 1e6:.0f} MB)",
+            "timing": "K launches queued behind a device spin; CUDA events on the launch "
+                      "stream; max over ranks",
+            "preprocess_ms": preprocess_ms, "gpu_launches": args.steps * launches_per_step,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
+    line.update(extras)
+    line["decode"] = decode
+    line["clocks"] = clk.summary()
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

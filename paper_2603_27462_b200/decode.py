@@ -97,3 +97,59 @@ class GraphDecoder:
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / 1e3
+
+
+@torch.no_grad()
+def linear_time_per_token(model, reps: int = 20) -> dict:
+    """Device time of one token's worth of the model's linear layers alone
+    (batch 1), lm_head excluded (dense bf16 in both arms).
+
+    Every linear of every layer runs once, in model order, on a (1, in)
+    bf16 input, all captured in one CUDA graph (so the host launch rate is
+    not measured) and replayed `reps` times; weights stream from HBM as in
+    decode (the whole set exceeds L2).  RSR linears are timed per stacked
+    sibling group (one fused launch computes q|k|v or gate|up)."""
+    from torch import nn
+
+    from .hf import RSRLinear
+    dev = next(model.parameters()).device if any(True for _ in model.parameters()) \
+        else torch.device("cuda")
+    calls, seen = [], set()
+    for name, mod in model.named_modules():
+        if name.endswith("lm_head"):
+            continue
+        if isinstance(mod, RSRLinear):
+            g = mod.group
+            if id(g) in seen:
+                continue
+            seen.add(id(g))
+            x = torch.randn(1, g.in_features, device=dev, dtype=torch.bfloat16)
+            calls.append((lambda g=g, x=x: g.compute(x), g.artifact.stream_bytes()))
+        elif isinstance(mod, nn.Linear):
+            x = torch.randn(1, mod.in_features, device=dev, dtype=mod.weight.dtype)
+            calls.append((lambda mod=mod, x=x: mod(x),
+                          mod.weight.numel() * mod.weight.element_size()))
+    if not calls:
+        return {"us": 0.0, "launches": 0, "bytes": 0}
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for fn, _ in calls:
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for fn, _ in calls:
+                fn()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    nbytes = int(sum(b for _, b in calls))
+    return {"us": us, "launches": len(calls), "bytes": nbytes, "gbs": nbytes / us / 1e3}
