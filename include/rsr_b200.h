@@ -5,8 +5,9 @@
  * (pkg/src/rsrmv/_native.py): the reference binds flat numpy arrays and
  * scalars into numba cores; this library takes flat DEVICE arrays, sizes and
  * a cudaStream_t.  No torch types cross this boundary.  Every entry point is
- * stream-ordered, never synchronizes, never allocates, and returns an
- * rsr_status (0 = success).  The Python shim (paper_2603_27462_b200/_lib.py)
+ * stream-ordered and never allocates; all but the *_host round trips (which
+ * synchronize the stream before returning host results) never synchronize.
+ * Each returns an rsr_status (0 = success).  The Python shim (paper_2603_27462_b200/_lib.py)
  * maps status codes onto the reference's exception kinds
  * (pkg/src/rsrmv/errors.py:23-74).
  *
@@ -56,7 +57,8 @@ typedef enum {
     RSR_BF16 = 1,
     RSR_F16 = 2,
     RSR_I8 = 3,
-    RSR_I32 = 4
+    RSR_I32 = 4,
+    RSR_F64 = 5   /* rsr_absmax_quantize only (reference float64 activations) */
 } rsr_dtype;
 
 /* Device view of a matrix's chunk stream (built by rsr_stream_build). */
@@ -72,6 +74,9 @@ typedef struct {
     int64_t n_blocks;          /* blocks covered (== block_count unless sharded) */
     const uint32_t *col0_key;  /* device, per cell (block-major): pattern key of the
                                   tile's column 0 (u16 formats; NULL for format 2) */
+    int32_t device;            /* CUDA device ordinal holding the arrays; launches
+                                  switch to it (and back) when it is not current;
+                                  -1 = the current device */
 } rsr_stream_view;
 
 /* ---- library info ---------------------------------------------------- */
@@ -247,7 +252,9 @@ void rsr_debug_set_probe(unsigned long long *probe);
  * gather adds, scatter adds, groups.                                         */
 rsr_status rsr_count_ops(const uint64_t *words, int64_t n_words, int64_t *out3,
                          rsr_stream_t stream);
-/* _native.absmax_quantize (_native.py:313-336): q int8[n], *scale_out f64.  */
+/* _native.absmax_quantize (_native.py:313-336) / matcore.quantize_activations
+ * (matcore.py:176-194): q int8[n], *scale_out f64.  v_dtype F32/BF16/F16 or
+ * F64 (float64 vectors keep their float64 values, as the reference does). */
 rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t *q,
                                double *scale_out, rsr_stream_t stream);
 

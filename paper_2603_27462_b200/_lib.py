@@ -30,7 +30,7 @@ RSR_ERR_WORKSPACE = 6
 RSR_BINARY = 0
 RSR_TERNARY = 1
 
-RSR_F32, RSR_BF16, RSR_F16, RSR_I8, RSR_I32 = 0, 1, 2, 3, 4
+RSR_F32, RSR_BF16, RSR_F16, RSR_I8, RSR_I32, RSR_F64 = 0, 1, 2, 3, 4, 5
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32
@@ -49,6 +49,7 @@ class StreamView(ctypes.Structure):
         ("entries", P), ("e_off", P),
         ("row_begin_block", I64), ("n_blocks", I64),
         ("col0_key", P),
+        ("device", I32),
     ]
 
 

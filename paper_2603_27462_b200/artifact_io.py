@@ -74,7 +74,10 @@ def to_bytes(a: RsrArtifact) -> bytes:
 
 def save(a: RsrArtifact, path) -> None:
     """Write an artifact; the bytes equal the reference writer's for the same
-    matrix and k (reference artifact_io.py:39-55)."""
+    matrix and k (reference artifact_io.py:39-55).  Like the reference, the
+    artifact is audited first: a malformed one raises CorruptArtifact and
+    no file is written."""
+    validate_artifact(a)
     blob = to_bytes(a)
     with open(path, "wb") as f:
         f.write(blob)

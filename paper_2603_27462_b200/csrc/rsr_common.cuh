@@ -27,12 +27,36 @@ inline rsr_status launch_status() {
     return RSR_OK;
 }
 
+// SM count of the current device (cached per device ordinal).
 inline int sm_count() {
-    int dev = 0, n = 0;
+    static int cache[64] = {0};
+    int dev = 0;
     cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && cache[dev] > 0) return cache[dev];
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 148;
+    n = n > 0 ? n : 148;
+    if (dev >= 0 && dev < 64) cache[dev] = n;
+    return n;
 }
+
+// Makes `device` current for the scope of a launch and restores the previous
+// device (a view's arrays may live on a device other than the current one).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int device) {
+        if (device < 0) return;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != device) {
+            cudaSetDevice(device);
+            prev = cur;
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 __device__ __forceinline__ uint32_t lane_id() {
     uint32_t l;

@@ -50,6 +50,35 @@ __global__ void stage_global_kernel(const void *v, int dtype, int64_t n, int mod
     }
 }
 
+// float64 vectors (matcore.quantize_activations keeps numpy float64 values).
+__global__ void absmax_quantize_f64_kernel(const double *v, int64_t n, int8_t *q,
+                                           double *scale_out) {
+    __shared__ double red[32];
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = fabs(v[i]);
+        a = x > a ? x : a;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+        a = o > a ? o : a;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    a = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a = red[w] > a ? red[w] : a;
+    const double scale = a == 0.0 ? 1.0 : 127.0 / a;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && scale_out) *scale_out = scale;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double xs = v[i] * scale;
+        double r = xs >= 0.0 ? floor(xs + 0.5) : -floor(-xs + 0.5);
+        r = r > 127.0 ? 127.0 : (r < -127.0 ? -127.0 : r);
+        q[i] = (int8_t)(int)r;
+    }
+}
+
 __global__ void absmax_quantize_kernel(const void *v, int dtype, int64_t n, int8_t *q,
                                        double *scale_out) {
     const double amax = cta_absmax(v, dtype, n);
@@ -98,6 +127,7 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     if (st != RSR_OK) return st;
     if (!v || !y) return RSR_ERR_INVALID;
     if (vw->n_blocks == 0) return RSR_OK;
+    DeviceGuard guard(vw->device);
     const bool need_ws = vw->tile_count > 1 || vw->format == FMT_U32;
     if (need_ws && (ws_bytes < ws_bytes_for(vw) || !ws)) return RSR_ERR_WORKSPACE;
     MvParams p;
@@ -148,7 +178,7 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     // One persistent CTA per SM (per tile) with as many warps as fit and are
     // needed.  Small matrices (few cells per SM) put a team of 2-8 warps on
     // each cell so the whole grid stays busy.
-    static const int sms = sm_count();
+    const int sms = sm_count();
     const int64_t tn = std::min(vw->tile_width, vw->n);
     const bool ring = bucket && vw->format != FMT_U32;
     const size_t vsz = (vw->format == FMT_U16_SCALED || MODE == MODE_FLOAT) ? 4 : 1;
@@ -181,17 +211,22 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
         std::min<int64_t>(cta_cap, (cells_per_tile + teams_per_cta - 1) / teams_per_cta);
     p.team = team;
     {
-        // raise the dynamic-smem limit once per kernel (not on every launch)
+        // raise the dynamic-smem limit once per (device, kernel), not on every launch
         static thread_local KernelFn last_fn[64];
         static thread_local size_t last_smem[64];
-        const size_t slot = ((uintptr_t)fn >> 4) & 63;
+        static thread_local int last_dev[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const size_t slot = (((uintptr_t)fn >> 4) + (size_t)dev * 7) & 63;
         // the default cap is 48 KiB minus the kernel's static shared memory
         // (the fused kernels keep 512 B of reduction scratch): raise it early
-        if (smem > 46 * 1024 && (last_fn[slot] != fn || last_smem[slot] < smem)) {
+        if (smem > 46 * 1024 &&
+            (last_fn[slot] != fn || last_dev[slot] != dev || last_smem[slot] < smem)) {
             const cudaError_t e =
                 cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return launch_status();
             last_fn[slot] = fn;
+            last_dev[slot] = dev;
             last_smem[slot] = smem;
         }
     }
@@ -340,6 +375,7 @@ template <class Mv>
 static rsr_status host_round_trip(const rsr_stream_view *view, const void *v_host, size_t vbytes,
                                   void *y_host, void *dev_v, void *dev_y, cudaStream_t s,
                                   Mv &&mv) {
+    DeviceGuard guard(view->device);
     const int64_t rows =
         std::min(view->n_blocks * view->k, view->m - view->row_begin_block * view->k);
     const size_t ybytes = (size_t)rows * 4;
@@ -398,11 +434,15 @@ void rsr_debug_set_probe(unsigned long long *probe) { g_probe = probe; }
 rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t *q,
                                double *scale_out, rsr_stream_t stream) {
     if (!v || !q || n < 0) return RSR_ERR_INVALID;
-    if (v_dtype != RSR_F32 && v_dtype != RSR_BF16 && v_dtype != RSR_F16) return RSR_ERR_INVALID;
+    if (v_dtype != RSR_F32 && v_dtype != RSR_BF16 && v_dtype != RSR_F16 && v_dtype != RSR_F64)
+        return RSR_ERR_INVALID;
     if (n == 0) return RSR_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int grid = (int)std::min<int64_t>((n + 1023) / 1024, 64);
-    absmax_quantize_kernel<<<grid, 1024, 0, s>>>(v, v_dtype, n, q, scale_out);
+    if (v_dtype == RSR_F64)
+        absmax_quantize_f64_kernel<<<grid, 1024, 0, s>>>((const double *)v, n, q, scale_out);
+    else
+        absmax_quantize_kernel<<<grid, 1024, 0, s>>>(v, v_dtype, n, q, scale_out);
     return launch_status();
 }
 

@@ -329,6 +329,7 @@ static rsr_status launch_mm(const rsr_stream_view *vw, const void *V, int vdtype
     const int64_t rows = std::min(vw->n_blocks * vw->k, vw->m - vw->row_begin_block * vw->k);
     if (ldv < vw->n || ldy < rows) return RSR_ERR_INVALID;
     if (vw->n_blocks == 0) return RSR_OK;
+    DeviceGuard guard(vw->device);
     const size_t pb = mm_part_bytes(vw, B);
     if (pb && (!ws || ws_bytes < pb)) return RSR_ERR_WORKSPACE;
     const int64_t nkeys = bucket_count(vw->bitwidth, vw->k);
@@ -360,7 +361,7 @@ static rsr_status launch_mm(const rsr_stream_view *vw, const void *V, int vdtype
     p.Y = Y;
     p.ldy = ldy;
     p.part = ws;
-    static const int sms = sm_count();
+    const int sms = sm_count();
     const int64_t chunks = (B + MM_BV - 1) / MM_BV;
     // one wave: the vector chunks and tiles share the SMs
     int64_t ctas = std::max<int64_t>(1, sms / (chunks * vw->tile_count));

@@ -54,14 +54,24 @@ class RSRSiblingGroup:
         return out
 
     def output_for(self, index: int, x2: torch.Tensor) -> torch.Tensor:
-        key = (x2.data_ptr(), tuple(x2.shape), x2._version)
-        if index in self._pending and self._key == key:
-            self._pending.discard(index)
+        """Sibling `index`'s slice of the stacked output for input x2.
+
+        The first sibling to see a new input computes the whole stack; the
+        others take their slices from it.  The stacked output is held only
+        until every sibling has taken its slice (then dropped), and a new
+        input -- or a sibling asking twice -- recomputes, so a stale result is
+        never served."""
+        key = (x2.data_ptr(), tuple(x2.shape), x2._version, x2.device)
+        if self._out is not None and self._key == key and index in self._pending:
             out = self._out
+            self._pending.discard(index)
         else:
             out = self.compute(x2)
-            self._out, self._key = out, key
+            self._key = key
             self._pending = set(range(len(self.offsets) - 1)) - {index}
+            self._out = out
+        if not self._pending:
+            self._out, self._key = None, None
         return out[:, self.offsets[index]:self.offsets[index + 1]]
 
 

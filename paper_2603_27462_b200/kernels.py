@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -60,24 +61,25 @@ def _count(a: RsrArtifact, counter: OpCounter | None):
 
 
 class _Workspace:
-    """Per-device scratch for tile partials (grown on demand, reused).
-
-    Superseded buffers are kept alive: launch states cache raw pointers."""
+    """Scratch for tile partials, one buffer per (device, stream), grown on
+    demand.  Keyed by stream so multiplies running concurrently on different
+    streams never share partials; a superseded buffer is simply released
+    (torch's caching allocator only hands its block to later work on the
+    same stream, i.e. after the kernels that used it)."""
     _bufs: dict = {}
-    _retired: list = []
+    _lock = threading.Lock()
 
     @classmethod
-    def get(cls, device, nbytes: int):
+    def get(cls, device, nbytes: int, stream: int = 0):
         import torch
         if nbytes <= 0:
             return None, 0
-        key = str(device)
-        b = cls._bufs.get(key)
-        if b is None or b.numel() < nbytes:
-            if b is not None:
-                cls._retired.append(b)
-            b = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
-            cls._bufs[key] = b
+        key = (str(device), int(stream))
+        with cls._lock:
+            b = cls._bufs.get(key)
+            if b is None or b.numel() < nbytes:
+                b = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+                cls._bufs[key] = b
         return b, nbytes
 
 
@@ -110,15 +112,21 @@ def _prepare_vec(a: RsrArtifact, v):
 
 
 class _ViewLaunch:
-    """Per-view launch state cached on first use (ctypes byref + workspace)."""
-    __slots__ = ("ref", "ws", "wsb")
+    """Per-view launch state cached on first use (ctypes byref + workspace
+    size); the workspace itself is looked up per stream."""
+    __slots__ = ("ref", "wsb", "device")
 
     def __init__(self, a: RsrArtifact, vw):
         import ctypes
         self.ref = ctypes.byref(vw)
-        wsb = int(_lib.lib().rsr_matvec_workspace_bytes(self.ref))
-        ws, self.wsb = _Workspace.get(a.device, wsb)
-        self.ws = _lib.ptr(ws)
+        self.wsb = int(_lib.lib().rsr_matvec_workspace_bytes(self.ref))
+        self.device = a.device
+
+    def workspace(self, stream: int):
+        if self.wsb <= 0:
+            return 0, 0
+        ws, wsb = _Workspace.get(self.device, self.wsb, stream)
+        return _lib.ptr(ws), wsb
 
 
 def _launch_state(a: RsrArtifact, view) -> _ViewLaunch:
@@ -139,8 +147,9 @@ def matvec_into(a: RsrArtifact, vt, y, accumulate: bool = False, view=None, stre
     from .matcore import _dtype_code
     st = _launch_state(a, view)
     s = _lib.current_stream_ptr(a.device) if stream is None else stream
+    ws, wsb = st.workspace(s) if st.wsb else (0, 0)
     _lib.check(_lib.lib().rsr_matvec(st.ref, vt.data_ptr(), _dtype_code(vt), y.data_ptr(),
-                                     int(accumulate), st.ws, st.wsb, s), "rsr_matvec")
+                                     int(accumulate), ws, wsb, s), "rsr_matvec")
     return y
 
 
@@ -156,9 +165,10 @@ def fused_into(a: RsrArtifact, vt, out, beta: float | None = None, view=None, st
     s = _lib.current_stream_ptr(a.device) if stream is None else stream
     b = float(a.weight_scale) if beta is None else float(beta)
     odt = _lib.RSR_BF16 if out.dtype == torch.bfloat16 else _lib.RSR_F32
+    ws, wsb = st.workspace(s) if st.wsb else (0, 0)
     _lib.check(_lib.lib().rsr_fused_matvec(st.ref, vt.data_ptr(), _dtype_code(vt), b,
                                            _lib.ptr(row_beta), out.data_ptr(), odt,
-                                           _lib.ptr(scale_out), st.ws, st.wsb, s),
+                                           _lib.ptr(scale_out), ws, wsb, s),
                "rsr_matvec_fused")
     return out
 
@@ -207,12 +217,31 @@ def _fn_addr(fn) -> int:
     return a
 
 
+def _host_lock(a: RsrArtifact) -> threading.Lock:
+    lk = a.__dict__.get("_host_lock")
+    if lk is None:
+        with _HOST_LOCKS_GUARD:
+            lk = a.__dict__.setdefault("_host_lock", threading.Lock())
+    return lk
+
+
+_HOST_LOCKS_GUARD = threading.Lock()
+
+
 def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
     """numpy in, numpy out in one C call (H2D, multiply, D2H, sync) using
     device buffers cached on the artifact.  The call's constant arguments
     are bound once per (artifact, dtype); per call only the vector pointer
     and the current stream are read (the host-in/host-out latency is a few
-    tens of microseconds, so Python overhead is a visible share of it)."""
+    tens of microseconds, so Python overhead is a visible share of it).
+    The C call releases the GIL, so the cached buffers are guarded by a
+    per-artifact lock held until the result has been copied out: threads
+    sharing an artifact serialize (as the reference's GIL-held cores do)."""
+    with _host_lock(a):
+        return _matvec_host_locked(a, vn)
+
+
+def _matvec_host_locked(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
     is_int = vn.dtype == np.int8
     key = "_host_call_i8" if is_int else "_host_call_f32"
     hc = a.__dict__.get(key)
@@ -231,14 +260,16 @@ def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
             dev_idx = torch.cuda.current_device()
         hc = a.__dict__[key] = (
             a._view, _lib.lib().rsr_matvec_host, st.ref, _lib.RSR_I8 if is_int else _lib.RSR_F32,
-            hy, hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st.ws, st.wsb,
+            hy, hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st,
             torch._C._cuda_getCurrentRawStream, dev_idx, (dv, dy))
-    _, fn, ref, code, hy, hyp, dvp, dyp, ws, wsb, cur_stream, dev_idx, _keep = hc
+    _, fn, ref, code, hy, hyp, dvp, dyp, st, cur_stream, dev_idx, _keep = hc
+    s = cur_stream(dev_idx)
+    ws, wsb = st.workspace(s) if st.wsb else (0, 0)
     if _hostcall is not None:
         status = _hostcall.matvec_host(_fn_addr(fn), ctypes.addressof(a._view), vn, code, hyp,
-                                       dvp, dyp, ws or 0, wsb, cur_stream(dev_idx))
+                                       dvp, dyp, ws or 0, wsb, s)
     else:
-        status = fn(ref, vn.ctypes.data, code, hyp, dvp, dyp, ws, wsb, cur_stream(dev_idx))
+        status = fn(ref, vn.ctypes.data, code, hyp, dvp, dyp, ws, wsb, s)
     if status:
         _lib.check(status, "rsr_matvec")
     return hy.copy()
@@ -266,6 +297,11 @@ def rsr_matvec_fused(a: RsrArtifact, v, counter: OpCounter | None = None):
 def _fused_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
     """numpy float32 in, numpy float32 out through rsr_fused_matvec_host (one
     C call, constant arguments bound once per artifact; see _matvec_host)."""
+    with _host_lock(a):
+        return _fused_host_locked(a, vn)
+
+
+def _fused_host_locked(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
     hc = a.__dict__.get("_host_call_fused")
     if hc is None or hc[0] is not a._view or hc[2] != float(a.weight_scale):
         import torch
@@ -278,15 +314,16 @@ def _fused_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
             dev_idx = torch.cuda.current_device()
         hc = a.__dict__["_host_call_fused"] = (
             a._view, _lib.lib().rsr_fused_matvec_host, float(a.weight_scale), st.ref, hy,
-            hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st.ws, st.wsb,
+            hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st,
             torch._C._cuda_getCurrentRawStream, dev_idx, (dv, dy))
-    _, fn, beta, ref, hy, hyp, dvp, dyp, ws, wsb, cur_stream, dev_idx, _keep = hc
+    _, fn, beta, ref, hy, hyp, dvp, dyp, st, cur_stream, dev_idx, _keep = hc
+    s = cur_stream(dev_idx)
+    ws, wsb = st.workspace(s) if st.wsb else (0, 0)
     if _hostcall is not None:
         status = _hostcall.fused_host(_fn_addr(fn), ctypes.addressof(a._view), vn, _lib.RSR_F32,
-                                      beta, hyp, dvp, dyp, ws or 0, wsb, cur_stream(dev_idx))
+                                      beta, hyp, dvp, dyp, ws or 0, wsb, s)
     else:
-        status = fn(ref, vn.ctypes.data, _lib.RSR_F32, beta, hyp, dvp, dyp, ws, wsb,
-                    cur_stream(dev_idx))
+        status = fn(ref, vn.ctypes.data, _lib.RSR_F32, beta, hyp, dvp, dyp, ws, wsb, s)
     if status:
         _lib.check(status, "rsr_matvec_fused")
     return hy.copy()
@@ -324,11 +361,12 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
         L = _lib.lib()
         wsb = int(L.rsr_matmul_tc_workspace_bytes(a.m, a.n, a.k, vw.row_begin_block,
                                                   vw.n_blocks, B))
-        ws, wsb = _Workspace.get(a.device, wsb)
-        _lib.check(L.rsr_matmul_tc(_lib.ptr(a.keymat()), a.m, a.n, vw.bitwidth, a.k,
-                                   vw.row_begin_block, vw.n_blocks, Vt.data_ptr(),
-                                   _lib.RSR_BF16, Vt.stride(0), B, Y.data_ptr(), Y.stride(0),
-                                   _lib.ptr(ws), wsb, s), "rsr_matmul_tc")
+        ws, wsb = _Workspace.get(a.device, wsb, s)
+        with torch.cuda.device(a.device):  # raw-pointer entry point: no view device
+            _lib.check(L.rsr_matmul_tc(_lib.ptr(a.keymat()), a.m, a.n, vw.bitwidth, a.k,
+                                       vw.row_begin_block, vw.n_blocks, Vt.data_ptr(),
+                                       _lib.RSR_BF16, Vt.stride(0), B, Y.data_ptr(),
+                                       Y.stride(0), _lib.ptr(ws), wsb, s), "rsr_matmul_tc")
         return Y
     if method == "tc":
         raise ValueError("the tensor-core path needs a bf16 batch and k <= 8")
@@ -341,7 +379,7 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
     L = _lib.lib()
     ref = ctypes.byref(vw)
     wsb = int(L.rsr_matmul_workspace_bytes(ref, B))
-    ws, wsb = _Workspace.get(a.device, wsb)
+    ws, wsb = _Workspace.get(a.device, wsb, s)
     st = L.rsr_matmul(ref, Vt.data_ptr(), _dtype_code(Vt), Vt.stride(0), B, Y.data_ptr(),
                       Y.stride(0), _lib.ptr(ws), wsb, s)
     if st == _lib.RSR_ERR_INVALID:

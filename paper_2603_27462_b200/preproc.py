@@ -266,6 +266,9 @@ class RsrArtifact:
         p = self.plan
         if n_blocks is None:
             n_blocks = p.block_count - block_begin
+        if block_begin < 0 or n_blocks < 0 or block_begin + n_blocks > p.block_count:
+            raise ValueError(f"block range [{block_begin}, {block_begin + n_blocks}) outside "
+                             f"[0, {p.block_count})")
         v = _lib.StreamView()
         v.m, v.n, v.k = self.m, self.n, self.k
         v.bitwidth = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
@@ -279,6 +282,8 @@ class RsrArtifact:
                       else _lib.ptr(self.col0_d) + 4 * block_begin * p.tile_count)
         v.row_begin_block = block_begin
         v.n_blocks = n_blocks
+        idx = getattr(self.device, "index", None)
+        v.device = -1 if idx is None else int(idx)
         return v
 
     # ---- constructors ----------------------------------------------------
