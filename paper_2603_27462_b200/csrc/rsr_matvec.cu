@@ -170,9 +170,14 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
                                                                           stg, p.scale_dev);
     }
     const bool bucket = vw->format != FMT_U32 && p.nkeys <= BUCKET_MAX_KEYS;
-    KernelFn fn = vw->format == FMT_U16_SCALED ? pick_fmt1(MODE, vw->k)
-                  : vw->format == FMT_U16      ? pick_fmt0(MODE, vw->k, bucket)
-                                               : pick_fmt2(MODE, vw->k);
+    // format 3 stages v by kind: bf16 halfwords for bf16 vectors, f32 words
+    // for f32/f16 vectors, int16 for the integer and fused paths
+    const int vk = MODE == MODE_FLOAT ? (vdtype == RSR_BF16 ? VK_BF16 : VK_F32X2) : VK_I16;
+    if (vw->format == FMT_H && !bucket) return RSR_ERR_INVALID;
+    KernelFn fn = vw->format == FMT_H            ? pick_fmt3(MODE, vk, vw->k)
+                  : vw->format == FMT_U16_SCALED ? pick_fmt1(MODE, vw->k)
+                  : vw->format == FMT_U16        ? pick_fmt0(MODE, vw->k, bucket)
+                                                 : pick_fmt2(MODE, vw->k);
     if (!fn) return RSR_ERR_INVALID;
 
     // One persistent CTA per SM (per tile) with as many warps as fit and are
@@ -183,7 +188,8 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     const bool ring = bucket && vw->format != FMT_U32;
     const size_t vsz = (vw->format == FMT_U16_SCALED || MODE == MODE_FLOAT) ? 4 : 1;
     size_t fixed = 0;
-    if (vw->format != FMT_U32) fixed += ((size_t)tn * vsz + 15) & ~(size_t)15;
+    if (vw->format == FMT_H) fixed += (h_image_bytes(vk, tn) + 15) & ~(size_t)15;
+    else if (vw->format != FMT_U32) fixed += ((size_t)tn * vsz + 15) & ~(size_t)15;
     if (bucket) fixed += ((size_t)p.nkeys * vw->k * 4 + 15) & ~(size_t)15;
     size_t per_warp = bucket ? (size_t)p.nkeys * 4 : 0;
     if (ring) per_warp += 16 * 4;  // team exchange

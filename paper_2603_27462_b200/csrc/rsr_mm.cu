@@ -325,7 +325,8 @@ static rsr_status launch_mm(const rsr_stream_view *vw, const void *V, int vdtype
                             int B, void *Y, int64_t ldy, void *ws, size_t ws_bytes,
                             cudaStream_t s) {
     if (!vw || !vw->entries || !vw->e_off || !V || !Y || B < 1) return RSR_ERR_INVALID;
-    if (vw->format == FMT_U32 || !vw->col0_key) return RSR_ERR_INVALID;
+    if ((vw->format != FMT_U16 && vw->format != FMT_U16_SCALED) || !vw->col0_key)
+        return RSR_ERR_INVALID;
     const int64_t rows = std::min(vw->n_blocks * vw->k, vw->m - vw->row_begin_block * vw->k);
     if (ldv < vw->n || ldy < rows) return RSR_ERR_INVALID;
     if (vw->n_blocks == 0) return RSR_OK;

@@ -15,9 +15,10 @@
 //     once (the fused path quantizes while staging, after a CTA-local absmax
 //     over the whole vector -- no separate quantization launch);
 //   * one warp (or a team of warps) owns one (block, tile) cell at a time; a
-//     round is 64 chunks moved by one TMA bulk copy into the warp's ring, lane
-//     L owns the chunk pair (2L, 2L+1), gathers v from shared memory per
-//     column slot and keeps a running partial group sum;
+//     round is up to 32 chunk pairs (lane runs: lane L owns a contiguous run
+//     of pairs and takes one pair per round, four 16-byte loads straight into
+//     registers, one round ahead), gathers v from shared memory per column
+//     slot and keeps a running partial group sum;
 //   * at a key slot the partial sum is flushed into the warp's PATTERN BUCKET
 //     for that key (3^k ternary / 2^k binary buckets in shared memory) --
 //     branch-free, predicated;
@@ -40,8 +41,19 @@ enum MvMode { MODE_FLOAT = 0, MODE_INT = 1, MODE_FUSED = 2 };
 enum StreamFormat {
     FMT_U16 = 0,         // u16: column | key<<..., flag bit 15, tiles <= 32768
     FMT_U16_SCALED = 1,  // u16: column*4, or key*4|1; tiles <= 16384, <= 16384 keys
-    FMT_U32 = 2          // u32: column, or key | 1<<31
+    FMT_U32 = 2,         // u32: column, or key | 1<<31
+    FMT_H = 3            // u16: column*2 (2-byte elements), key*4|1, or a zero word
+                         // 32768 + 4*bank; tiles <= 16384, <= 2187 keys (rsr_stream_h.cu)
 };
+
+// How format-3 kernels stage v in shared memory (template parameter VK):
+enum VKind {
+    VK_DEFAULT = 0,  // formats 0-2: f32 (float) / int32 or int8 (integer paths)
+    VK_BF16 = 1,     // bf16 halfwords; gathers add them with add.f32.bf16
+    VK_F32X2 = 2,    // f32 words at byte 2*entry (float32 / float16 vectors)
+    VK_I16 = 3       // int16 halfwords (int8 and quantized vectors)
+};
+constexpr uint32_t H_ZERO_B = 32768u;  // format 3: byte offset of the 32 zero halfword pairs
 
 constexpr int MV_MAX_WARPS = 20;  // 640 threads: up to 102 registers per thread
 constexpr int64_t BUCKET_MAX_KEYS = 2187;  // 3^7: buckets live in smem up to here
@@ -231,14 +243,53 @@ __device__ __forceinline__ void reg_flush(Acc (&acc)[K], uint32_t key, Acc s, in
     for (int i = 0; i < K; ++i) acc[i] += (Acc)key_sign(key, i, bitwidth) * s;
 }
 
-template <int MODE, int FMT>
+template <int MODE, int FMT, int VK = VK_DEFAULT>
 struct MvTypes {
     using Acc = typename std::conditional<MODE == MODE_FLOAT, float, int32_t>::type;
-    // staged element of v: 4 bytes for the scaled format (column*4 addressing),
-    // else f32 (float) / int8 (integer paths)
-    static constexpr int VSZ = (FMT == FMT_U16_SCALED || MODE == MODE_FLOAT) ? 4 : 1;
+    // staged element of v: format 3 by VK; 4 bytes for the scaled format
+    // (column*4 addressing); else f32 (float) / int8 (integer paths)
+    static constexpr int VSZ = FMT == FMT_H ? (VK == VK_F32X2 ? 4 : 2)
+                               : ((FMT == FMT_U16_SCALED || MODE == MODE_FLOAT) ? 4 : 1);
     static constexpr bool SMEM_V = FMT != FMT_U32;
 };
+
+// Bytes of the format-3 v image in shared memory: the staged tile plus the
+// 32 zero words the padding entries name (at H_ZERO_B, or 2*H_ZERO_B for f32).
+__host__ __device__ constexpr size_t h_image_bytes(int vk, int64_t tn) {
+    return vk == VK_F32X2 ? (size_t)2 * H_ZERO_B + 256
+                          : ((size_t)tn * 2 > H_ZERO_B ? (size_t)tn * 2 : (size_t)H_ZERO_B) + 128;
+}
+
+// f32 += bf16 in one instruction (FHADD.BF16 on sm_100a).
+__device__ __forceinline__ float add_bf16(float acc, uint16_t h) {
+    asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc) : "h"(h));
+    return acc;
+}
+__device__ __forceinline__ uint16_t lds_u16(uint32_t addr) {
+    uint16_t r;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(addr));
+    return r;
+}
+__device__ __forceinline__ int lds_s16(uint32_t addr) {
+    int r;
+    asm("ld.shared.s16 %0, [%1];" : "=r"(r) : "r"(addr));
+    return r;
+}
+// u16 load unless `skip` (then +0.0 as bf16 bits)
+__device__ __forceinline__ uint16_t lds_u16_unless(uint32_t skip, uint32_t addr) {
+    uint16_t r;
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\tmov.u16 %0, 0;\n\t"
+        "@p ld.shared.u16 %0, [%2];\n\t}"
+        : "=h"(r) : "r"(skip), "r"(addr));
+    return r;
+}
+__device__ __forceinline__ int lds_s16_unless(uint32_t skip, uint32_t addr) {
+    int r;
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\tmov.u32 %0, 0;\n\t"
+        "@p ld.shared.s16 %0, [%2];\n\t}"
+        : "=r"(r) : "r"(skip), "r"(addr));
+    return r;
+}
 
 // Element loader for the staging loops, templated on the input dtype.
 template <int DT>
@@ -331,6 +382,7 @@ using KernelFn = void (*)(MvParams);
 KernelFn pick_fmt1(int mode, int k);             // FMT_U16_SCALED, buckets
 KernelFn pick_fmt0(int mode, int k, bool bucket);  // FMT_U16
 KernelFn pick_fmt2(int mode, int k);             // FMT_U32, register flush
+KernelFn pick_fmt3(int mode, int vk, int k);     // FMT_H, buckets
 
 #define RSR_K_SWITCH(EXPR)                                                                   \
     switch (k) {                                                                             \

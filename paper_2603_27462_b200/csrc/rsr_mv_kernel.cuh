@@ -48,10 +48,11 @@ __device__ __forceinline__ double cta_reduce_max(double a) {
 }
 
 
-template <int K, int MODE, int FMT, bool BUCKET>
+template <int K, int MODE, int FMT, bool BUCKET, int VK = VK_DEFAULT>
 __global__ void __launch_bounds__(MV_MAX_WARPS * 32)
 rsr_mv_kernel(MvParams p) {
-    using T = MvTypes<MODE, FMT>;
+    using T = MvTypes<MODE, FMT, VK>;
+    constexpr bool FH = FMT == FMT_H;
     using Acc = typename T::Acc;
     constexpr int VSZ = T::VSZ;
     constexpr bool SMEM_V = T::SMEM_V;
@@ -80,7 +81,8 @@ rsr_mv_kernel(MvParams p) {
     // smem: [v tile][sign table K x NB][buckets W x NB][team exchange W x 16]
     size_t off = 0;
     unsigned char *vsm = mv_smem + off;
-    if constexpr (SMEM_V) off += ((size_t)tn * VSZ + 15) & ~(size_t)15;
+    if constexpr (FH) off += (h_image_bytes(VK, tn) + 15) & ~(size_t)15;
+    else if constexpr (SMEM_V) off += ((size_t)tn * VSZ + 15) & ~(size_t)15;
     Acc *__restrict__ stab = reinterpret_cast<Acc *>(mv_smem + off);
     if constexpr (BUCKET) off += ((size_t)p.nkeys * K * sizeof(Acc) + 15) & ~(size_t)15;
     Acc *__restrict__ buckets = reinterpret_cast<Acc *>(mv_smem + off);
@@ -157,8 +159,13 @@ rsr_mv_kernel(MvParams p) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) nq[j] = ld_stream(src + 32 * j);
         } else {
+            // lanes past the round's pairs: slot 0 = the sink key, the rest
+            // padding (format 3: the bank-0 zero word; else column 0)
+            constexpr uint32_t PW = FH ? (H_ZERO_B | (H_ZERO_B << 16)) : 0u;
+            constexpr uint32_t P0 = FH ? (1u | (H_ZERO_B << 16)) : 0u;
+            nq[0] = make_uint4(P0, PW, PW, PW);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) nq[j] = make_uint4(0, 0, 0, 0);
+            for (int j = 1; j < 4; ++j) nq[j] = make_uint4(PW, PW, PW, PW);
             if (lane < np) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) nq[j] = ld_stream(src + j * np);
@@ -233,7 +240,42 @@ rsr_mv_kernel(MvParams p) {
     // round requested.
     double scale = 1.0;
     bool vstaged_float = false;
-    if constexpr (MODE == MODE_FLOAT && SMEM_V && VSZ == 4) {
+    if constexpr (MODE == MODE_FLOAT && FH && VK == VK_BF16) {
+        // bf16 v copied as halfwords (16-byte loads and stores); the stream
+        // was requested once they are issued
+        const uint16_t *src = reinterpret_cast<const uint16_t *>(p.v) + c0;
+        const int64_t nt = blockDim.x;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const int64_t nvec = tn >> 3;
+            constexpr int U = 4;
+            bool started = false;
+            for (int64_t i0 = threadIdx.x; i0 < nvec; i0 += U * nt) {
+                uint4 r[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t i = i0 + u * nt;
+                    r[u] = i < nvec ? __ldg(reinterpret_cast<const uint4 *>(src) + i)
+                                    : make_uint4(0, 0, 0, 0);
+                }
+                init_tables();
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t i = i0 + u * nt;
+                    if (i < nvec) reinterpret_cast<uint4 *>(vsm)[i] = r[u];
+                }
+                if (!started) {
+                    start_stream();
+                    started = true;
+                }
+            }
+            for (int64_t i = (nvec << 3) + threadIdx.x; i < tn; i += nt)
+                reinterpret_cast<uint16_t *>(vsm)[i] = __ldg(src + i);
+        } else {
+            for (int64_t i = threadIdx.x; i < tn; i += nt)
+                reinterpret_cast<uint16_t *>(vsm)[i] = __ldg(src + i);
+        }
+        vstaged_float = true;
+    } else if constexpr (MODE == MODE_FLOAT && SMEM_V && VSZ == 4) {
         const int esz = p.vdtype == RSR_F32 ? 4 : 2;
         const int epv = 16 / esz;  // elements per 16-byte load
         const char *src = reinterpret_cast<const char *>(p.v) + c0 * esz;
@@ -293,7 +335,7 @@ rsr_mv_kernel(MvParams p) {
     // Fused path with one tile and 4-byte staging: a single pass over v stages
     // it as f32 while tracking |v|max, then quantizes in place.
     bool staged = false;
-    if constexpr (MODE == MODE_FUSED && SMEM_V && VSZ == 4) {
+    if constexpr (MODE == MODE_FUSED && SMEM_V && (VSZ == 4 || FH)) {
         // Decode-sized bf16 vectors: the whole vector in registers (<= two
         // 16-byte loads per thread), |v|max from registers, quantize straight
         // from registers -- no f32 round trip through shared memory.
@@ -328,16 +370,25 @@ rsr_mv_kernel(MvParams p) {
                         qv[2 * q] = quantize_one(__uint_as_float(w4[q] << 16), scale);
                         qv[2 * q + 1] = quantize_one(__uint_as_float(w4[q] & 0xFFFF0000u), scale);
                     }
-                    int4 *d = reinterpret_cast<int4 *>(vsm) + 2 * i;
-                    d[0] = make_int4(qv[0], qv[1], qv[2], qv[3]);
-                    d[1] = make_int4(qv[4], qv[5], qv[6], qv[7]);
+                    if constexpr (FH) {  // eight int16 halfwords
+                        auto pk = [](int32_t lo, int32_t hi) {
+                            return (uint32_t)(uint16_t)lo | ((uint32_t)(uint16_t)hi << 16);
+                        };
+                        reinterpret_cast<uint4 *>(vsm)[i] =
+                            make_uint4(pk(qv[0], qv[1]), pk(qv[2], qv[3]), pk(qv[4], qv[5]),
+                                       pk(qv[6], qv[7]));
+                    } else {
+                        int4 *d = reinterpret_cast<int4 *>(vsm) + 2 * i;
+                        d[0] = make_int4(qv[0], qv[1], qv[2], qv[3]);
+                        d[1] = make_int4(qv[4], qv[5], qv[6], qv[7]);
+                    }
                 }
             }
             if (p.scale_dev && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
                 *p.scale_dev = scale;
             staged = true;
         }
-        if (!staged && p.tc == 1) {
+        if (!staged && p.tc == 1 && !FH) {  // (format 3's int16 image has no room for f32)
             double a = 0.0;
             for_each_v_real(p.v, p.vdtype, 0, tn, [&](int64_t i, float x) {
                 reinterpret_cast<float *>(vsm)[i] = x;
@@ -367,13 +418,16 @@ rsr_mv_kernel(MvParams p) {
         }
     }
     if (!staged && !vstaged_float) if constexpr (SMEM_V) {
-        if constexpr (MODE == MODE_FLOAT) {
+        if constexpr (MODE == MODE_FLOAT && VK == VK_BF16) {
+            // (not reached: the bf16 copy above always stages)
+        } else if constexpr (MODE == MODE_FLOAT) {
             for_each_v_real(p.v, p.vdtype, c0, tn,
                        [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
         } else {
             auto put = [&](int64_t i, float x) {
                 const int8_t q = MODE == MODE_INT ? (int8_t)x : quantize_one(x, scale);
                 if constexpr (VSZ == 4) reinterpret_cast<int32_t *>(vsm)[i] = q;
+                else if constexpr (VSZ == 2) reinterpret_cast<int16_t *>(vsm)[i] = q;
                 else reinterpret_cast<int8_t *>(vsm)[i] = q;
             };
             if constexpr (MODE == MODE_INT) for_each_v_t<RSR_I8>(p.v, c0, tn, put);
@@ -388,7 +442,12 @@ rsr_mv_kernel(MvParams p) {
     // column-0 value (as staged: f32 / int8 / quantized) is added in the
     // epilogue to the bucket of col0_key[cell].  Thread 0 staged element 0.
     Acc v0 = (Acc)0;
-    if constexpr (SMEM_V) {
+    if constexpr (FH) {
+        // format 3: every column is in the stream; padding names one of 32
+        // zero words after the image (one per bank)
+        if (threadIdx.x < (VK == VK_F32X2 ? 64 : 32))
+            reinterpret_cast<uint32_t *>(vsm + (VK == VK_F32X2 ? 2 * H_ZERO_B : H_ZERO_B))[threadIdx.x] = 0u;
+    } else if constexpr (SMEM_V) {
         if constexpr (MODE == MODE_FLOAT) v0 = load_as_f32(p.v, p.vdtype, c0);
         else if constexpr (MODE == MODE_INT) v0 = (Acc)__ldg(reinterpret_cast<const int8_t *>(p.v) + c0);
         else v0 = (Acc)quantize_one(load_as_f32(p.v, p.vdtype, c0), scale);
@@ -407,7 +466,7 @@ rsr_mv_kernel(MvParams p) {
     auto finish_cell = [&](int64_t bb, Acc (&acc)[K]) {
         // the tile's column 0 (not in the u16 stream)
         uint32_t key0 = 0;
-        if constexpr (SMEM_V) key0 = p.col0_key[bb * p.tc + t];
+        if constexpr (SMEM_V && !FH) key0 = p.col0_key[bb * p.tc + t];
         // y_i = sum_key sgn_i(key) * bucket[key]  (bucket 0 is never reduced)
         if constexpr (BUCKET) {
             if (key0 && sub == 0 && lane == 0) {
@@ -479,12 +538,43 @@ rsr_mv_kernel(MvParams p) {
         // inside a pair every other key starts a new group.  The open group
         // (cur, s) is carried from round to round.  Scaled format: entries are
         // byte offsets (column*4; key*4|1) straight into v and the buckets.
-        constexpr bool SC = FMT == FMT_U16_SCALED;
+        // entry decoding: scaled (byte offsets of 4-byte elements), format 3
+        // (byte offsets of 2-byte elements, doubled for f32 staging, keys
+        // key*4|1), else column | key flag 0x8000
+        constexpr bool SC = FMT == FMT_U16_SCALED || FH;
+        constexpr bool X2 = FH && VK == VK_F32X2;
         auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
         auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
-        auto lo_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ; };
-        auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) : (x >> 16) * VSZ; };
-        auto gat = [&](uint32_t off) -> Acc { return lds_v<Acc, VSZ>(vbase + off); };
+        auto lo_off = [](uint32_t x) -> uint32_t {
+            return X2 ? (x & 0xFFFEu) << 1 : (FH ? (x & 0xFFFFu) : (SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ));
+        };
+        auto hi_off = [](uint32_t x) -> uint32_t {
+            return X2 ? (x >> 15) & 0x1FFFEu : (SC ? (x >> 16) : (x >> 16) * VSZ);
+        };
+        auto gat = [&](uint32_t off) -> Acc {
+            if constexpr (FH && VK == VK_I16) return lds_s16(vbase + off);
+            else return lds_v<Acc, VSZ == 2 ? 4 : VSZ>(vbase + off);
+        };
+        // sum of three gathers (bf16 halfwords: f32 += bf16 adds)
+        auto gat3 = [&](uint32_t oa, uint32_t ob, uint32_t oc) -> Acc {
+            if constexpr (FH && VK == VK_BF16) {
+                const uint16_t a = lds_u16(vbase + oa), b = lds_u16(vbase + ob),
+                               c = lds_u16(vbase + oc);
+                return (Acc)add_bf16(add_bf16(add_bf16(0.0f, c), b), a);
+            } else {
+                return gat(oa) + (gat(ob) + gat(oc));
+            }
+        };
+        // a predicated gather added to the open group's sum (key slots: no load)
+        auto gat_unless_add = [&](uint32_t skip, uint32_t off, Acc s0) -> Acc {
+            if constexpr (FH && VK == VK_BF16) {
+                return (Acc)add_bf16((float)s0, lds_u16_unless(skip, vbase + off));
+            } else if constexpr (FH && VK == VK_I16) {
+                return s0 + (Acc)lds_s16_unless(skip, vbase + off);
+            } else {
+                return s0 + lds_v_unless<Acc, VSZ == 2 ? 4 : VSZ>(skip, vbase + off);
+            }
+        };
         for (; b < p.nblk; b += cstride) {
             const int64_t dc = b * p.tc + t;
             const Cell c = cell_at(b, p.e_off[dc], p.e_off[dc + 1]);
@@ -520,7 +610,7 @@ rsr_mv_kernel(MvParams p) {
                         bucket_flush_pred(ns, cur, s);  // native shared red
                     }
                     cur = k0;
-                    s = (ns ? (Acc)0 : s) + (gat(hi_off(w[0])) + (gat(lo_off(w[1])) + gat(hi_off(w[1]))));
+                    s = (ns ? (Acc)0 : s) + gat3(hi_off(w[0]), lo_off(w[1]), hi_off(w[1]));
                 }
 #pragma unroll
                 for (int qd = 1; qd < 8; ++qd) {
@@ -530,8 +620,7 @@ rsr_mv_kernel(MvParams p) {
                     // slot 4q: a column unless it is a key; the predicated-off
                     // lanes of a key slot take no shared-memory bank (an
                     // unpredicated dummy read of v[key] measured 1.6% slower)
-                    const Acc g = lds_v_unless<Acc, VSZ>(isk, vbase + lo_off(x));
-                    const Acc t3 = gat(hi_off(x)) + (gat(lo_off(y)) + gat(hi_off(y)));
+                    const Acc t3 = gat3(hi_off(x), lo_off(y), hi_off(y));
                     if constexpr (MODE == MODE_FLOAT) {
                         // record completed groups; flushed below as one batch
                         fk[qd] = isk ? cur : bkbase;
@@ -540,7 +629,7 @@ rsr_mv_kernel(MvParams p) {
                         bucket_flush_pred(isk, cur, s);
                     }
                     cur = isk ? bkbase + ko : cur;
-                    s = (isk ? (Acc)0 : s + g) + t3;
+                    s = gat_unless_add(isk, lo_off(x), isk ? (Acc)0 : s) + t3;
                 }
                 if constexpr (MODE == MODE_FLOAT) {
                     // all bucket loads, then all adds/stores: one latency per

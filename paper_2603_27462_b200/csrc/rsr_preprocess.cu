@@ -17,6 +17,7 @@
 // exactly; the stream-layout builder for the multiply kernels lives here too.
 
 #include "rsr_common.cuh"
+#include "rsr_stream_layout.cuh"
 
 namespace rsr {
 
@@ -258,114 +259,14 @@ scan2_kernel(int64_t *a, int64_t *b, int64_t cells) {
 //   u32 format (2) -- "even" layout: every chunk starts with a key, keys only at
 //     even slots, padding key 0 / column 0 (bucket 0 is never reduced).
 
-// Quad layout: slots of one group of R stream columns starting at slot p
-// (p = 0 mod 4).  emit_key(slot) / emit_col(slot, j) / emit_pad(slot).
-template <typename KeyFn, typename ColFn, typename PadFn>
-__host__ __device__ __forceinline__ void place_group_quad(int64_t &p, int64_t R, KeyFn emit_key,
-                                                         ColFn emit_col, PadFn emit_pad) {
-    if (R == 0) return;
-    emit_key(p++);
-    for (int64_t j = 0; j < R; ++j) {
-        if ((p & 31) == 0) emit_key(p++);  // pair start: the group continues
-        emit_col(p++, j);
-    }
-    while (p & 3) emit_pad(p++);
-}
-
-// Even layout: slot placement of one group of L columns (the reference word's
-// perm_len) starting at slot p (always even).  Keys only ever sit at EVEN slots: every
-// segment that ends inside a chunk has odd length (an even remainder is split
-// 1 + (R-1) with one repeated key), and a segment running to the chunk end
-// has odd length automatically.  A group crossing a chunk boundary repeats its
-// key at slot 0 of the next chunk.  emit_key(slot) / emit_col(slot, j).
-template <typename KeyFn, typename ColFn>
-__host__ __device__ __forceinline__ void place_group(int64_t &p, int64_t L, int64_t CH,
-                                                    KeyFn emit_key, ColFn emit_col) {
-    emit_key(p++);
-    int64_t R = L, j = 0;
-    while (true) {
-        const int64_t room = CH - p % CH;  // odd
-        if (R >= room) {
-            for (int64_t i = 0; i < room; ++i) emit_col(p++, j++);
-            R -= room;
-            if (R == 0) break;
-            emit_key(p++);
-            continue;
-        }
-        if (R & 1) {
-            for (int64_t i = 0; i < R; ++i) emit_col(p++, j++);
-            break;
-        }
-        for (int64_t i = 0; i < R - 1; ++i) emit_col(p++, j++);
-        emit_key(p++);
-        emit_col(p++, j++);
-        break;
-    }
-}
-
-// Physical index of logical slot p inside a cell of nch chunks (nch even).
-// A warp round is 64 chunks: lane L owns the consecutive chunk pair (2L,
-// 2L+1), i.e. 64 bytes in four 16-byte quarters; the round is stored as
-// [quarter 0 of every pair][quarter 1]...[quarter 3], so each of a lane's four
-// 16-byte loads is one coalesced 512-byte access, and the round is one
-// contiguous 2 KiB bulk copy.
-__host__ __device__ __forceinline__ int64_t phys_slot(int64_t p, int64_t CH, int64_t nch) {
-    const int64_t c = p / CH, js = p - c * CH;
-    const int64_t pair = c >> 1, cin = c & 1;
-    const int64_t r = pair >> 5, lanep = pair & 31;
-    const int64_t npairs = nch >> 1;
-    const int64_t np = min((int64_t)32, npairs - (r << 5));
-    const int64_t qe = CH >> 1;  // entries per 16-byte quarter
-    const int64_t q = cin * 2 + js / qe, within = js % qe;
-    return r * 64 * CH + q * np * qe + lanep * qe + within;
-}
-
-// Quad layout physical placement ("lane runs").  A cell of N chunk pairs is
-// processed in P = ceil(N / 32) rounds; lane L owns the CONTIGUOUS run of
-// pairs [L*P, L*P + len_L) (len_L = P for L < Lf = N / P, rem = N - Lf*P for
-// lane Lf, 0 beyond), so a lane carries its open group from round to round and
-// lanes only meet at run boundaries.  Round r holds the pairs L*P + r of its
-// np_r = Lf + (r < rem) active lanes, as four 16-byte quarters [q0 of the np_r
-// pairs][q1][q2][q3] (every lane load coalesced), starting at pair R(r) =
-// r*Lf + min(r, rem) of the cell.
-struct LaneRuns {
-    int64_t P, Lf, rem;
-};
-__host__ __device__ __forceinline__ LaneRuns lane_runs(int64_t npairs) {
-    LaneRuns lr;
-    lr.P = (npairs + 31) / 32;
-    lr.Lf = lr.P ? npairs / lr.P : 0;
-    lr.rem = npairs - lr.Lf * lr.P;
-    return lr;
-}
-// Physical u16 index (inside the cell) of logical slot p.
-__host__ __device__ __forceinline__ int64_t run_slot(int64_t p, const LaneRuns &lr) {
-    const int64_t j = p >> 5, slot = p & 31;
-    const int64_t L = j / lr.P, r = j - L * lr.P;
-    const int64_t np = lr.Lf + (r < lr.rem ? 1 : 0);
-    const int64_t R = r * lr.Lf + min(r, lr.rem);
-    return R * 32 + (slot >> 3) * np * 8 + L * 8 + (slot & 7);
-}
-
-// Dense pattern key of a group from its masks: binary -> pos mask; ternary
-// -> base-3 digits (1 = +1, 2 = -1).  Key 0 never occurs (zero patterns are
-// dropped) and marks padding.
-__device__ __forceinline__ uint32_t dense_key(uint64_t w, int bitwidth) {
-    const uint32_t pos = (uint32_t)((w >> 32) & 0xFFFFu), neg = (uint32_t)(w >> 48);
-    if (bitwidth == RSR_BINARY) return pos;
-    uint32_t key = 0, p3 = 1;
-    for (int i = 0; i < 16; ++i) {
-        key += (((pos >> i) & 1u) + 2u * ((neg >> i) & 1u)) * p3;
-        p3 *= 3u;
-    }
-    return key;
-}
-
 __global__ void stream_count_kernel(const uint64_t *__restrict__ words,
                                     const int64_t *__restrict__ go,
                                     const uint16_t *__restrict__ perm,
                                     const int64_t *__restrict__ po, int64_t bc, int64_t tc,
-                                    int64_t CH, bool quad, int64_t *e_off, int32_t *gslot) {
+                                    int64_t CH, int layout, int64_t *e_off, int32_t *gslot) {
+    // layout: 0 even (u32), 1 quad with the tile's column 0 carried outside
+    // the stream (formats 0/1), 2 quad with every column in the stream (3)
+    const bool quad = layout != 0;
     const int64_t cells = bc * tc;
     for (int64_t dc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; dc < cells;
          dc += (int64_t)gridDim.x * blockDim.x) {
@@ -378,7 +279,7 @@ __global__ void stream_count_kernel(const uint64_t *__restrict__ words,
             gslot[g] = (int32_t)p;
             if (quad) {
                 // column 0 leads its group (columns ascend inside a group)
-                const bool has0 = perm[po[src] + (int64_t)(w & 0xFFFFu)] == 0;
+                const bool has0 = layout == 1 && perm[po[src] + (int64_t)(w & 0xFFFFu)] == 0;
                 place_group_quad(p, L - has0, [](int64_t) {}, [](int64_t, int64_t) {},
                                  [](int64_t) {});
             } else {
@@ -665,6 +566,14 @@ static rsr_status check_plan(int64_t rows, int64_t cols, int64_t row_bytes, int3
 
 }  // namespace rsr
 
+namespace rsr {
+// halfword format builder (rsr_stream_h.cu)
+rsr_status stream_build_h(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                          const int64_t *po, int64_t bc, int64_t tc, int32_t bitwidth,
+                          const int64_t *e_off, const int32_t *gslot, uint16_t *entries,
+                          uint32_t *col0_key, cudaStream_t s);
+}  // namespace rsr
+
 using namespace rsr;
 
 extern "C" {
@@ -731,7 +640,7 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
 
 int32_t rsr_stream_format(int32_t bitwidth, int32_t k, int64_t tile_width) {
     const int64_t keys = bucket_count(bitwidth, k);
-    if (tile_width <= 16384 && keys <= 2187) return 1;   // scaled u16 (bucket kernel)
+    if (tile_width <= 16384 && keys <= 2187) return 3;   // halfword u16 (bucket kernel)
     if (tile_width <= 32768 && keys <= 32768) return 0;  // u16
     return 2;                                            // u32
 }
@@ -741,12 +650,13 @@ rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, const uint
                             int32_t format, int32_t chunk, int64_t *e_off, int32_t *gslot,
                             rsr_stream_t stream) {
     if (!go || !po || !e_off || block_count < 1 || tile_count < 1) return RSR_ERR_INVALID;
-    if (format < 0 || format > 2 || chunk != (format == 2 ? 8 : 16)) return RSR_ERR_INVALID;
+    if (format < 0 || format > 3 || chunk != (format == 2 ? 8 : 16)) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells + 127) / 128, 8192);
     stream_count_kernel<<<grid, 128, 0, s>>>(words, go, perm, po, block_count, tile_count, chunk,
-                                             format != 2, e_off, gslot);
+                                             format == 2 ? 0 : (format == 3 ? 2 : 1), e_off,
+                                             gslot);
     scan2_kernel<<<1, 1024, 0, s>>>(e_off, nullptr, cells);
     return launch_status();
 }
@@ -758,9 +668,12 @@ rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint
                             uint32_t *col0_key, rsr_stream_t stream) {
     if (!go || !po || !e_off || !entries || block_count < 1 || tile_count < 1)
         return RSR_ERR_INVALID;
-    if (format < 0 || format > 2 || chunk != (format == 2 ? 8 : 16)) return RSR_ERR_INVALID;
+    if (format < 0 || format > 3 || chunk != (format == 2 ? 8 : 16)) return RSR_ERR_INVALID;
     if (format != 2 && !col0_key) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
+    if (format == 3)
+        return stream_build_h(words, go, perm, po, block_count, tile_count, bitwidth, e_off,
+                              gslot, (uint16_t *)entries, col0_key, s);
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 32);
     const int bgrid =
