@@ -198,7 +198,10 @@ rsr_mv_kernel(MvParams p) {
         if (tables_done) return;
         tables_done = true;
         if constexpr (BUCKET) {
-            for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
+            // the sign table serves only the shared-bucket (integer team) and
+            // k = 1 reductions; the others use the digit-split reduction
+            const bool need_stab = K < 2 || shbk;
+            for (int key = threadIdx.x; key < (need_stab ? p.nkeys : 0); key += blockDim.x) {
                 uint32_t kk = (uint32_t)key;
 #pragma unroll
                 for (int i = 0; i < K; ++i) {
@@ -480,11 +483,72 @@ rsr_mv_kernel(MvParams p) {
                 kfirst += 32 * sub;
                 kstep *= team;
             }
-            for (int key = kfirst; key < (RSR_DBG(p, 4) ? 0 : p.nkeys); key += kstep) {
-                const Acc bv = key ? bk[key] : (Acc)0;
-                bk[key] = (Acc)0;
+            if (!shbk && K >= 2 && !RSR_DBG(p, 4)) {
+                // Digit-split reduction (no sign table): key = lane + NL * l
+                // with NL = 3^KH (ternary) or 2^KH (binary) lanes.  Rows below
+                // KH take their sign from the lane's own digits, so they need
+                // only the lane's total T = sum_l bucket; rows KH.. take it
+                // from the digits of l, compile-time constants of the
+                // unrolled loop (an add, a subtract or nothing).
+                if (p.bitwidth == RSR_TERNARY) {
+                    constexpr int KH = K >= 3 ? 3 : K;
+                    constexpr int NL = KH == 3 ? 27 : (KH == 2 ? 9 : 3);
+                    constexpr int NI = (K - KH) == 0 ? 1 : ((K - KH) == 1 ? 3 : ((K - KH) == 2 ? 9
+                                       : ((K - KH) == 3 ? 27 : ((K - KH) == 4 ? 81 : 243))));
+                    if ((int)lane < NL) {
+                        Acc tsum = (Acc)0;
 #pragma unroll
-                for (int i = 0; i < K; ++i) acc[i] += stab[i * p.nkeys + key] * bv;
+                        for (int l = 0; l < NI; ++l) {
+                            const int key = (int)lane + NL * l;
+                            const Acc bv = key ? bk[key] : (Acc)0;
+                            bk[key] = (Acc)0;
+                            tsum += bv;
+                            int q = l;
+#pragma unroll
+                            for (int i = KH; i < K; ++i) {
+                                const int d = q % 3;
+                                q /= 3;
+                                if (d == 1) acc[i] += bv;
+                                else if (d == 2) acc[i] -= bv;
+                                else acc[i] += bv * (Acc)0;  // 0 * NaN: the reference's y += sgn * s
+                            }
+                        }
+                        uint32_t q = lane;
+#pragma unroll
+                        for (int i = 0; i < KH; ++i) {
+                            const uint32_t d = q % 3u;
+                            q /= 3u;
+                            acc[i] += d == 1u ? tsum : (d == 2u ? -tsum : tsum * (Acc)0);
+                        }
+                    }
+                } else {
+                    constexpr int KH = K >= 5 ? 5 : K;
+                    constexpr int NL = 1 << KH;
+                    constexpr int NI = 1 << (K - KH);
+                    if ((int)lane < NL) {
+                        Acc tsum = (Acc)0;
+#pragma unroll
+                        for (int l = 0; l < NI; ++l) {
+                            const int key = (int)lane + NL * l;
+                            const Acc bv = key ? bk[key] : (Acc)0;
+                            bk[key] = (Acc)0;
+                            tsum += bv;
+#pragma unroll
+                            for (int i = KH; i < K; ++i)
+                                acc[i] += ((l >> (i - KH)) & 1) ? bv : bv * (Acc)0;
+                        }
+#pragma unroll
+                        for (int i = 0; i < KH; ++i)
+                            acc[i] += ((lane >> i) & 1u) ? tsum : tsum * (Acc)0;
+                    }
+                }
+            } else {
+                for (int key = kfirst; key < (RSR_DBG(p, 4) ? 0 : p.nkeys); key += kstep) {
+                    const Acc bv = key ? bk[key] : (Acc)0;
+                    bk[key] = (Acc)0;
+#pragma unroll
+                    for (int i = 0; i < K; ++i) acc[i] += stab[i * p.nkeys + key] * bv;
+                }
             }
             __syncwarp();
         } else if constexpr (SMEM_V) {
