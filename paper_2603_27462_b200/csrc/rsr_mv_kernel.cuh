@@ -483,6 +483,8 @@ rsr_mv_kernel(MvParams p) {
                 kfirst += 32 * sub;
                 kstep *= team;
             }
+            // buckets are re-zeroed for the warp's next cell only
+            const bool rezero = bb + cstride < p.nblk;
             if (!shbk && K >= 2 && !RSR_DBG(p, 4)) {
                 // Digit-split reduction (no sign table): key = lane + NL * l
                 // with NL = 3^KH (ternary) or 2^KH (binary) lanes.  Rows below
@@ -501,7 +503,7 @@ rsr_mv_kernel(MvParams p) {
                         for (int l = 0; l < NI; ++l) {
                             const int key = (int)lane + NL * l;
                             const Acc bv = key ? bk[key] : (Acc)0;
-                            bk[key] = (Acc)0;
+                            if (rezero) bk[key] = (Acc)0;
                             tsum += bv;
                             int q = l;
 #pragma unroll
@@ -531,7 +533,7 @@ rsr_mv_kernel(MvParams p) {
                         for (int l = 0; l < NI; ++l) {
                             const int key = (int)lane + NL * l;
                             const Acc bv = key ? bk[key] : (Acc)0;
-                            bk[key] = (Acc)0;
+                            if (rezero) bk[key] = (Acc)0;
                             tsum += bv;
 #pragma unroll
                             for (int i = KH; i < K; ++i)
@@ -662,49 +664,65 @@ rsr_mv_kernel(MvParams p) {
                     acc[0] += (Acc)x;
                     return;
                 }
-                uint32_t fk[8];
-                float fs[8];
-                {   // slot 0: always a key; a new one closes the open group
-                    const uint32_t k0 = bkbase + key_off(w[0]);
-                    const bool ns = k0 != cur;
-                    if constexpr (MODE == MODE_FLOAT) {
-                        fk[0] = ns ? cur : bkbase;
-                        fs[0] = s;
-                    } else {
-                        bucket_flush_pred(ns, cur, s);  // native shared red
-                    }
-                    cur = k0;
-                    s = (ns ? (Acc)0 : s) + gat3(hi_off(w[0]), lo_off(w[1]), hi_off(w[1]));
-                }
-#pragma unroll
-                for (int qd = 1; qd < 8; ++qd) {
-                    const uint32_t x = w[2 * qd], y = w[2 * qd + 1];
-                    const bool isk = is_key(x) != 0u;
-                    const uint32_t ko = key_off(x);
-                    // slot 4q: a column unless it is a key; the predicated-off
-                    // lanes of a key slot take no shared-memory bank (an
-                    // unpredicated dummy read of v[key] measured 1.6% slower)
-                    const Acc t3 = gat3(hi_off(x), lo_off(y), hi_off(y));
-                    if constexpr (MODE == MODE_FLOAT) {
-                        // record completed groups; flushed below as one batch
-                        fk[qd] = isk ? cur : bkbase;
-                        fs[qd] = s;
-                    } else {
-                        bucket_flush_pred(isk, cur, s);
-                    }
-                    cur = isk ? bkbase + ko : cur;
-                    s = gat_unless_add(isk, lo_off(x), isk ? (Acc)0 : s) + t3;
-                }
                 if constexpr (MODE == MODE_FLOAT) {
-                    // all bucket loads, then all adds/stores: one latency per
-                    // round.  The keys of one round's completed groups are
-                    // distinct (a group completes once, in the lane holding its
-                    // end), bucket 0 aside.
+                    // The bucket addresses of the groups this round closes follow
+                    // from the keys alone, so their eight bucket loads are issued
+                    // before the gathers (latency hidden); the adds and stores
+                    // follow the sums.  The keys of one round's completed groups
+                    // are distinct (a group completes once, in the lane holding
+                    // its end), bucket 0 (the sink) aside.
+                    uint32_t fk[8];
+                    bool kk[8];
+                    uint32_t cc = cur;
+                    {
+                        const uint32_t k0 = bkbase + key_off(w[0]);
+                        kk[0] = k0 != cc;
+                        fk[0] = kk[0] ? cc : bkbase;
+                        cc = k0;
+                    }
+#pragma unroll
+                    for (int qd = 1; qd < 8; ++qd) {
+                        const uint32_t x = w[2 * qd];
+                        kk[qd] = is_key(x) != 0u;
+                        fk[qd] = kk[qd] ? cc : bkbase;
+                        cc = kk[qd] ? bkbase + key_off(x) : cc;
+                    }
+                    float tb[8];
+                    if (!RSR_DBG(p, 1)) lds_bucket8(fk, tb);
+                    float fs[8];
+                    fs[0] = s;
+                    s = (kk[0] ? (Acc)0 : s) + gat3(hi_off(w[0]), lo_off(w[1]), hi_off(w[1]));
+#pragma unroll
+                    for (int qd = 1; qd < 8; ++qd) {
+                        const uint32_t x = w[2 * qd], y = w[2 * qd + 1];
+                        // slot 4q: a column unless it is a key (predicated-off
+                        // lanes of a key slot take no shared-memory bank)
+                        const Acc t3 = gat3(hi_off(x), lo_off(y), hi_off(y));
+                        fs[qd] = s;
+                        s = gat_unless_add(kk[qd], lo_off(x), kk[qd] ? (Acc)0 : s) + t3;
+                    }
+                    cur = cc;
                     if (!RSR_DBG(p, 1)) {
-                        float tb[8];
-                        lds_bucket8(fk, tb);
 #pragma unroll
                         for (int i = 0; i < 8; ++i) sts_bucket(fk[i], tb[i] + fs[i]);
+                    }
+                } else {
+                    {   // slot 0: always a key; a new one closes the open group
+                        const uint32_t k0 = bkbase + key_off(w[0]);
+                        const bool ns = k0 != cur;
+                        bucket_flush_pred(ns, cur, s);  // native shared red
+                        cur = k0;
+                        s = (ns ? (Acc)0 : s) + gat3(hi_off(w[0]), lo_off(w[1]), hi_off(w[1]));
+                    }
+#pragma unroll
+                    for (int qd = 1; qd < 8; ++qd) {
+                        const uint32_t x = w[2 * qd], y = w[2 * qd + 1];
+                        const bool isk = is_key(x) != 0u;
+                        const uint32_t ko = key_off(x);
+                        const Acc t3 = gat3(hi_off(x), lo_off(y), hi_off(y));
+                        bucket_flush_pred(isk, cur, s);
+                        cur = isk ? bkbase + ko : cur;
+                        s = gat_unless_add(isk, lo_off(x), isk ? (Acc)0 : s) + t3;
                     }
                 }
             };
