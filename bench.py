@@ -477,6 +477,10 @@ def main():
         strip = lambda r0, r1: rsr.PackedMatrix(r1 - r0, n, cfg["bitwidth"], full[r0:r1])
     else:
         strip = lambda r0, r1: random_ternary_device(r1 - r0, n, 0, 0.5, row0=r0, device=dev)
+    # warm-up preprocess of a few rows (same width and k: the same kernels),
+    # so preprocess_ms times the preprocessing, not CUDA's lazy module loading
+    rsr.preprocess(strip(0, min(m, 4 * k)), k, shard.make_plan(m, n, k, cfg["bitwidth"]).tile_width,
+                   device=dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     sm = shard.ShardedMatrix(m, n, cfg["bitwidth"], k, strip, rank, world, device=dev)

@@ -234,6 +234,13 @@ rsr_status rsr_ternarize_pack(const void *w, int32_t w_dtype, int64_t rows, int6
                               uint8_t *packed, double *beta_out, void *workspace,
                               size_t workspace_bytes, rsr_stream_t stream);
 
+/* Two-plane decomposition M = P - N of a packed ternary matrix (SURVEY 8a
+ * P7): planes (device u8, 2*rows x ceil(cols/8)) receives P = [M == +1] in
+ * rows [0, rows) and N = [M == -1] in rows [rows, 2*rows), binary-packed as
+ * the reference packs binary matrices (matcore.py:114-125).                */
+rsr_status rsr_split_planes(const uint8_t *ternary, int64_t rows, int64_t cols, int64_t row_bytes,
+                            uint8_t *planes, rsr_stream_t stream);
+
 /* Synthetic ternary rows [row0, row0+rows) of a cols-wide matrix, packed, for
  * configs too large for the reference's numpy generator (C5, 131072^2):
  * entry (r, c) = +1/-1/0 with p = density/2, density/2, 1-density from

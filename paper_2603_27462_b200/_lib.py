@@ -79,6 +79,7 @@ SIGNATURES = {
     "rsr_ternarize_workspace_bytes": (SZ, []),
     "rsr_ternarize_pack": (I32, [P, I32, I64, I64, P, P, P, SZ, P]),
     "rsr_random_ternary": (I32, [I64, I64, I64, ctypes.c_uint64, F64, P, P]),
+    "rsr_split_planes": (I32, [P, I64, I64, I64, P, P]),
     "rsr_debug_set_probe": (None, [P]),
     "rsr_count_ops": (I32, [P, I64, P, P]),
     "rsr_absmax_quantize": (I32, [P, I32, I64, P, P, P]),

@@ -143,3 +143,44 @@ extern "C" rsr_status rsr_random_ternary(int64_t row0, int64_t rows, int64_t col
                                                                         seed, thr_half, packed);
     return rsr::launch_status();
 }
+
+// ---- two-plane decomposition of a ternary matrix ------------
+// M = P - N with P = [M == +1], N = [M == -1], both binary, written stacked:
+// rows [0, rows) of `planes` are P, rows [rows, 2 rows) are N (1 bit per
+// entry, LSB-first, ceil(cols/8) bytes per row: the reference's binary
+// packing, matcore.py:114-125).  One thread per output byte of P and N.
+namespace rsr {
+__global__ void split_planes_kernel(const uint8_t *__restrict__ tern, int64_t rows, int64_t cols,
+                                    int64_t tern_row_bytes, int64_t bin_row_bytes,
+                                    uint8_t *__restrict__ planes) {
+    const int64_t total = rows * bin_row_bytes;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / bin_row_bytes, cb = (i - r * bin_row_bytes) * 8;
+        uint32_t pos = 0, neg = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t c = cb + j;
+            if (c < cols) {
+                const uint32_t code = (__ldg(tern + r * tern_row_bytes + (c >> 2)) >> (2 * (c & 3))) & 3u;
+                pos |= (code == 1u ? 1u : 0u) << j;
+                neg |= (code == 2u ? 1u : 0u) << j;
+            }
+        }
+        planes[i] = (uint8_t)pos;
+        planes[total + i] = (uint8_t)neg;
+    }
+}
+}  // namespace rsr
+
+extern "C" rsr_status rsr_split_planes(const uint8_t *ternary, int64_t rows, int64_t cols,
+                                       int64_t row_bytes, uint8_t *planes, rsr_stream_t stream) {
+    if (!ternary || !planes || rows < 1 || cols < 1 || row_bytes < (cols + 3) / 4)
+        return RSR_ERR_INVALID;
+    const int64_t brb = (cols + 7) / 8;
+    const int64_t total = rows * brb;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)rsr::sm_count() * 32);
+    rsr::split_planes_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ternary, rows, cols, row_bytes,
+                                                                      brb, planes);
+    return rsr::launch_status();
+}

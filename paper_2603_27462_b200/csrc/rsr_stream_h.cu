@@ -111,6 +111,8 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
         // lane L's run: pairs [L*P, L*P + len)
         const int64_t len = (int64_t)lane < lr.Lf ? lr.P
                             : ((int64_t)lane == lr.Lf ? lr.rem : 0);
+        int64_t cached_g = -1;  // group whose bank counts S.cnt[lane] / gmask hold
+        uint32_t gmask = 0u;
         HWalk w;
         w.g1 = g1;
         w.rem = 0;
@@ -151,7 +153,10 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
                 const int64_t p = pbase + s;
                 gcur = w.g;
                 const int ty = act ? walk_step(w, p, words) : H_SINK;
-                // ---- offers: banks of the group's unplaced columns
+                // ---- offers: banks of the group's unplaced columns, counted
+                // when the lane enters the group and kept up to date by its
+                // own picks (a group two lanes share at once -- a cell of one
+                // round -- may leave a stale count; its pick then falls back)
                 uint32_t mask = 0u;
                 const uint16_t *gc = nullptr;
                 int64_t glen = 0;
@@ -159,17 +164,28 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
                     const uint64_t wd = words[gcur];
                     gc = cperm + (int64_t)(wd & 0xFFFFu);
                     glen = (int64_t)((wd >> 16) & 0xFFFFu);
-                    uint32_t *row = reinterpret_cast<uint32_t *>(S.cnt[lane]);
+                    if (gcur != cached_g) {
+                        cached_g = gcur;
+                        uint32_t *row = reinterpret_cast<uint32_t *>(S.cnt[lane]);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) row[i] = 0u;
-                    for (int64_t j = 0; j < glen; ++j) {
-                        const uint32_t c = gc[j];
-                        if (!((S.used[c >> 5] >> (c & 31)) & 1u)) {
-                            const uint32_t bk = (c >> 1) & 31u;
-                            S.cnt[lane][bk]++;
-                            mask |= 1u << bk;
+                        for (int i = 0; i < 8; ++i) row[i] = 0u;
+                        gmask = 0u;
+                        for (int64_t j0 = 0; j0 < glen; j0 += 8) {
+                            uint32_t cs[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) cs[u] = j0 + u < glen ? gc[j0 + u] : 0xFFFFu;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const uint32_t c = cs[u];
+                                if (c != 0xFFFFu && !((S.used[c >> 5] >> (c & 31)) & 1u)) {
+                                    const uint32_t bk = (c >> 1) & 31u;
+                                    S.cnt[lane][bk]++;
+                                    gmask |= 1u << bk;
+                                }
+                            }
                         }
                     }
+                    mask = gmask;
                 }
                 S.msk[lane] = mask;
                 S.owner[lane] = -1;
@@ -177,7 +193,11 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
                 __syncwarp();
                 // ---- matching: fewest options first, most abundant free bank
                 uint32_t taken = 0u;
-                for (int lvl = 1; lvl <= 32; ++lvl) {
+                // the option counts present in this slot (bit c-1 for c options)
+                uint32_t levels = __reduce_or_sync(RSR_FULL_MASK, mask ? 1u << (__popc(mask) - 1) : 0u);
+                while (levels) {
+                    const int lvl = __ffs(levels);
+                    levels &= levels - 1u;
                     uint32_t cand = __ballot_sync(RSR_FULL_MASK, mask != 0u && __popc(mask) == lvl);
                     while (cand) {
                         const int i = __ffs(cand) - 1;
@@ -238,28 +258,38 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
                 constexpr uint32_t NONE = 0xFFFFFFFFu;
                 auto pick = [&](int want_bank, int avoid_f32, uint32_t occ) -> uint32_t {
                     for (int tries = 0; tries < 64; ++tries) {
-                        int best = -1, bestsc = 1 << 30;
-                        for (int64_t j = 0; j < glen; ++j) {
-                            const uint32_t c = gc[j];
-                            if ((S.used[c >> 5] >> (c & 31)) & 1u) continue;
-                            const int bk = (int)((c >> 1) & 31u);
-                            int sc;
-                            if (want_bank >= 0) {
-                                if (bk != want_bank) continue;
-                                sc = (int)(c & 31u) == avoid_f32 ? 1 : 0;
-                            } else {
-                                sc = ((occ >> bk) & 1u) ? 1 : 0;
-                            }
-                            if (sc < bestsc) {
-                                bestsc = sc;
-                                best = (int)j;
-                                if (sc == 0) break;
+                        uint32_t best = NONE;
+                        int bestsc = 1 << 30;
+                        for (int64_t j0 = 0; j0 < glen && bestsc > 0; j0 += 8) {
+                            uint32_t cs[8];  // eight loads in flight
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) cs[u] = j0 + u < glen ? gc[j0 + u] : 0xFFFFu;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const uint32_t c = cs[u];
+                                if (c == 0xFFFFu || bestsc == 0) continue;
+                                if ((S.used[c >> 5] >> (c & 31)) & 1u) continue;
+                                const int bk = (int)((c >> 1) & 31u);
+                                int sc;
+                                if (want_bank >= 0) {
+                                    if (bk != want_bank) continue;
+                                    sc = (int)(c & 31u) == avoid_f32 ? 1 : 0;
+                                } else {
+                                    sc = ((occ >> bk) & 1u) ? 1 : 0;
+                                }
+                                if (sc < bestsc) {
+                                    bestsc = sc;
+                                    best = c;
+                                }
                             }
                         }
-                        if (best < 0) return NONE;
-                        const uint32_t c = gc[best];
-                        const uint32_t bit = 1u << (c & 31);
-                        if (!(atomicOr(&S.used[c >> 5], bit) & bit)) return c;
+                        if (best == NONE) return NONE;
+                        const uint32_t bit = 1u << (best & 31);
+                        if (!(atomicOr(&S.used[best >> 5], bit) & bit)) {
+                            const uint32_t bk = (best >> 1) & 31u;
+                            if (--S.cnt[lane][bk] == 0) gmask &= ~(1u << bk);
+                            return best;
+                        }
                     }
                     return NONE;
                 };
