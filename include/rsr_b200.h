@@ -254,6 +254,26 @@ rsr_status rsr_random_ternary(int64_t row0, int64_t rows, int64_t cols, uint64_t
  * must be pre-set to UINT64_MAX / 0).  NULL (default) disables it.          */
 void rsr_debug_set_probe(unsigned long long *probe);
 
+/* ---- artifact audit and inverse ---------------------------------------------
+ * rsr_audit: the per-cell invariants of preproc.validate_artifact
+ * (preproc.py:305-372) over the device reference arrays (tile-major cells;
+ * the caller has checked the offset arrays span words / perm and never
+ * decrease).  *result (device u64) = (cell << 8 | check) of the first
+ * failure in cell order (check numbering: csrc/rsr_audit.cu AuditCheck), or
+ * UINT64_MAX when the artifact is sound.
+ * rsr_reconstruct: the packed matrix the artifact encodes (preproc.py:
+ * 375-400) into `packed` (rsr_reconstruct_bytes() bytes, 4-byte aligned;
+ * row-major, ceil(n/8) or ceil(n/4) bytes per row).                         */
+rsr_status rsr_audit(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                     const int64_t *po, int64_t m, int64_t n, int32_t k, int32_t bitwidth,
+                     int64_t tile_width, int64_t block_count, int64_t tile_count,
+                     unsigned long long *result, rsr_stream_t stream);
+size_t rsr_reconstruct_bytes(int64_t m, int64_t n, int32_t bitwidth);
+rsr_status rsr_reconstruct(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                           const int64_t *po, int64_t m, int64_t n, int32_t k, int32_t bitwidth,
+                           int64_t tile_width, int64_t block_count, int64_t tile_count,
+                           uint8_t *packed, rsr_stream_t stream);
+
 /* ---- helpers ---------------------------------------------------------------- */
 /* _native.count_ops (_native.py:288-307): out3 (device int64[3]) =
  * gather adds, scatter adds, groups.                                         */

@@ -145,19 +145,13 @@ def parse(blob: bytes, name: str = "<bytes>") -> dict:
 
 
 def from_bytes(blob: bytes, device=None, name: str = "<bytes>") -> RsrArtifact:
-    """Audit and upload an `.rsra` byte string as a device artifact."""
+    """Parse, upload, audit (device) and return an `.rsra` byte string as a
+    device artifact; a malformed file raises CorruptArtifact before the
+    multiply stream is derived from it."""
     d = parse(blob, name)
-
-    class _Host:  # the audit runs on host arrays before anything is uploaded
-        pass
-    h = _Host()
-    h.__dict__.update(d)
-    h.cells = d["plan"].tile_count * d["plan"].block_count
-    h.cell_index = lambda t, b: t * d["plan"].block_count + b
-    validate_artifact(h)
     return RsrArtifact.from_host(d["m"], d["n"], d["k"], d["bitwidth"], d["weight_scale"],
                                  d["plan"], d["words"], d["perm"], d["group_offsets"],
-                                 d["perm_offsets"], None, device)
+                                 d["perm_offsets"], None, device, audit=True)
 
 
 def load(path, device=None) -> RsrArtifact:

@@ -120,7 +120,7 @@ class RsrArtifact:
     """
 
     def __init__(self, m, n, k, bitwidth, weight_scale, plan, words_d, perm_d, go_d, po_d,
-                 steps_d=None, n_words=None, n_perm=None):
+                 steps_d=None, n_words=None, n_perm=None, build_stream=True):
         self.m = m
         self.n = n
         self.k = k
@@ -136,7 +136,8 @@ class RsrArtifact:
         self.n_perm = int(perm_d.numel()) if n_perm is None else n_perm
         self.device = go_d.device
         self._host = {}
-        self._build_stream()
+        if build_stream:
+            self._build_stream()
 
     # ---- reference attribute surface (host numpy, lazily copied) ----------
     def _h(self, key, fn):
@@ -289,8 +290,10 @@ class RsrArtifact:
     # ---- constructors ----------------------------------------------------
     @classmethod
     def from_host(cls, m, n, k, bitwidth, weight_scale, plan, words, perm, group_offsets,
-                  perm_offsets, sort_steps=None, device=None) -> "RsrArtifact":
-        """Upload reference-format host arrays (e.g. a loaded .rsra file)."""
+                  perm_offsets, sort_steps=None, device=None, audit=False) -> "RsrArtifact":
+        """Upload reference-format host arrays (e.g. a loaded .rsra file).
+        audit=True runs validate_artifact on the uploaded arrays before the
+        chunk stream is derived from them (CorruptArtifact otherwise)."""
         import torch
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
@@ -307,7 +310,14 @@ class RsrArtifact:
                 up(np.asarray(group_offsets, np.int64), np.int64, torch.int64),
                 up(np.asarray(perm_offsets, np.int64), np.int64, torch.int64),
                 None if sort_steps is None else
-                up(np.asarray(sort_steps, np.int64), np.int64, torch.int64))
+                up(np.asarray(sort_steps, np.int64), np.int64, torch.int64),
+                build_stream=False)
+        # reference-format host data (e.g. a file) is audited before anything
+        # is derived from it; a host copy of what was uploaded is kept
+        a._host.update(words=np.asarray(words, np.uint64), perm=np.asarray(perm, np.uint16))
+        if audit:
+            validate_artifact(a)
+        a._build_stream()
         return a
 
 
@@ -364,18 +374,18 @@ def preprocess(m: PackedMatrix, k: int, tile_width: int | None = None,
 
 
 def pattern_key(m: PackedMatrix, block_rows: range, col: int) -> int:
-    """Reference pattern key of one column (preproc.py:183-197): binary
-    sum bit*2^i, ternary sum code*4^i (host helper)."""
+    """The reference's pattern key of column `col` over `block_rows`
+    (preproc.py:183-197): row i of the block contributes its packed code
+    (binary bit / ternary 2-bit code) at bit position i (binary) or 2i
+    (ternary) -- host helper, used by tests and tools."""
     if not 0 <= col < m.cols:
         raise DimensionMismatch(f"column {col} outside 0..{m.cols - 1}")
+    rows = np.asarray(list(block_rows), dtype=np.int64)
     data = m.host_data()
-    key = 0
-    for i, r in enumerate(block_rows):
-        if m.bitwidth == BINARY:
-            key |= int((data[r, col >> 3] >> (col & 7)) & 1) << i
-        else:
-            key |= int((data[r, col >> 2] >> ((col & 3) << 1)) & 3) << (2 * i)
-    return key
+    per_byte, width = (8, 1) if m.bitwidth == BINARY else (4, 2)
+    codes = (data[rows, col // per_byte].astype(np.int64) >> (width * (col % per_byte))) \
+        & ((1 << width) - 1)
+    return int(np.sum(codes << (width * np.arange(rows.size, dtype=np.int64))))
 
 
 def preprocess_block(m: PackedMatrix, block_rows: range, tile_cols: range,
@@ -402,105 +412,87 @@ def preprocess_block(m: PackedMatrix, block_rows: range, tile_cols: range,
     return BlockMeta(_u16_host(perm).copy(), groups)
 
 
-def _cell_key_array(words: np.ndarray, bitwidth: str) -> np.ndarray:
-    pos = ((words >> np.uint64(32)) & np.uint64(0xFFFF)).astype(np.int64)
-    neg = ((words >> np.uint64(48)) & np.uint64(0xFFFF)).astype(np.int64)
-    if bitwidth == BINARY:
-        return pos
-    key = np.zeros(words.size, np.int64)
-    for i in range(16):
-        key += (((pos >> i) & 1) + 2 * ((neg >> i) & 1)) << (2 * i)
-    return key
+# messages of the device audit's per-cell checks (csrc/rsr_audit.cu AuditCheck)
+_AUDIT_MESSAGES = {
+    1: "a group with no columns",
+    2: "group perm ranges are not back to back from 0",
+    3: "group perm ranges do not end at the cell's perm length",
+    4: "pos and neg masks share a row",
+    5: "a group with the all-zero pattern",
+    6: "mask bits at or above the block height",
+    7: "a neg mask in a binary artifact",
+    8: "group keys not strictly ascending",
+    9: "a column id at or beyond the tile width",
+    10: "a column listed twice",
+    11: "columns not ascending inside a group",
+    12: "perm entries but no groups",
+}
+
+
+def _offsets_host(x) -> np.ndarray:
+    return x.cpu().numpy() if _is_torch(x) else np.asarray(x, dtype=np.int64)
 
 
 def validate_artifact(a: RsrArtifact) -> None:
-    """Structural audit on host copies; raises CorruptArtifact
-    (same invariants as reference preproc.py:305-372)."""
-    def fail(msg):
-        raise CorruptArtifact(msg)
+    """Structural audit (the reference's invariants, preproc.py:305-372);
+    raises CorruptArtifact naming the first bad cell.
 
+    Scalar and offset-array checks run on the host; the per-cell group and
+    permutation checks run on the device (rsr_audit, csrc/rsr_audit.cu) over
+    the artifact's device arrays, only after the offsets are known to be in
+    bounds."""
+    import torch
+    bad = lambda msg: CorruptArtifact(f"invalid artifact: {msg}")  # noqa: E731
     if a.bitwidth not in (BINARY, TERNARY):
-        fail(f"bad bitwidth {a.bitwidth!r}")
+        raise bad(f"bitwidth {a.bitwidth!r}")
     if a.m < 1 or a.n < 1:
-        fail("empty matrix dimensions")
+        raise bad(f"shape {a.m} x {a.n}")
     if not 1 <= a.k <= K_CAP[a.bitwidth]:
-        fail(f"k={a.k} outside caps for {a.bitwidth}")
+        raise bad(f"k={a.k} outside 1..{K_CAP[a.bitwidth]} for {a.bitwidth}")
     p = a.plan
-    if p.block_count != -(-a.m // a.k) or p.tile_count != -(-a.n // p.tile_width):
-        fail("plan grid inconsistent with matrix shape")
-    go, po = a.group_offsets, a.perm_offsets
-    words, perm = a.words, a.perm
-    cells = a.cells
-    if len(go) != cells + 1 or len(po) != cells + 1:
-        fail("offset arrays do not match the cell grid")
-    if go[0] != 0 or po[0] != 0 or go[-1] != len(words) or po[-1] != len(perm):
-        fail("offset bounds do not match array lengths")
-    if (np.diff(go) < 0).any() or (np.diff(po) < 0).any():
-        fail("offsets not monotone")
-    for t in range(p.tile_count):
-        tn = min(p.tile_width, a.n - t * p.tile_width)
-        for b in range(p.block_count):
-            c = a.cell_index(t, b)
-            h = min(a.k, a.m - b * a.k)
-            w = words[go[c]:go[c + 1]]
-            seg = perm[po[c]:po[c + 1]]
-            if w.size == 0:
-                if seg.size:
-                    fail(f"cell {c}: permutation without groups")
-                continue
-            ps = (w & np.uint64(0xFFFF)).astype(np.int64)
-            pl = ((w >> np.uint64(16)) & np.uint64(0xFFFF)).astype(np.int64)
-            pos = ((w >> np.uint64(32)) & np.uint64(0xFFFF)).astype(np.int64)
-            neg = ((w >> np.uint64(48)) & np.uint64(0xFFFF)).astype(np.int64)
-            if (pl < 1).any():
-                fail(f"cell {c}: empty group")
-            if ps[0] != 0 or (ps[1:] != ps[:-1] + pl[:-1]).any():
-                fail(f"cell {c}: permutation ranges not consecutive")
-            if ps[-1] + pl[-1] != seg.size:
-                fail(f"cell {c}: group ranges do not cover the permutation")
-            if ((pos & neg) != 0).any():
-                fail(f"cell {c}: overlapping scatter masks")
-            if ((pos | neg) == 0).any():
-                fail(f"cell {c}: stored zero pattern")
-            if h < 16 and ((pos | neg) >> h != 0).any():
-                fail(f"cell {c}: mask bits beyond block height {h}")
-            if a.bitwidth == BINARY and (neg != 0).any():
-                fail(f"cell {c}: negative mask in a binary artifact")
-            if (np.diff(_cell_key_array(w, a.bitwidth)) <= 0).any():
-                fail(f"cell {c}: group keys not strictly ascending")
-            if seg.size and int(seg.max()) >= tn:
-                fail(f"cell {c}: column index beyond tile width {tn}")
-            if np.unique(seg).size != seg.size:
-                fail(f"cell {c}: duplicate column in permutation")
-            starts = np.repeat(ps, pl)
-            idx = np.arange(seg.size)
-            inner = idx != starts
-            if inner.any() and (seg[1:][inner[1:]].astype(np.int64)
-                                <= seg[:-1][inner[1:]].astype(np.int64)).any():
-                fail(f"cell {c}: columns not ascending within a group")
+    if (p.block_count, p.tile_count) != (-(-a.m // a.k), -(-a.n // p.tile_width)):
+        raise bad("plan grid does not match the shape")
+    cells = p.block_count * p.tile_count
+    go, po = _offsets_host(a.go_d), _offsets_host(a.po_d)
+    n_words, n_perm = int(a.words_d.numel()), int(a.perm_d.numel())
+    if go.shape != (cells + 1,) or po.shape != (cells + 1,):
+        raise bad(f"offset arrays of length {go.size} / {po.size} for {cells} cells")
+    if go[0] != 0 or po[0] != 0 or go[-1] != n_words or po[-1] != n_perm:
+        raise bad("offset arrays do not span the word / perm arrays")
+    down = np.flatnonzero((np.diff(go) < 0) | (np.diff(po) < 0))
+    if down.size:
+        raise bad(f"offsets decrease at cell {int(down[0])}")
+    if cells == 0 or (n_words == 0 and n_perm == 0):
+        return
+    res = torch.empty(1, dtype=torch.int64, device=a.device)
+    bw = _lib.RSR_BINARY if a.bitwidth == BINARY else _lib.RSR_TERNARY
+    _lib.check(_lib.lib().rsr_audit(_lib.ptr(a.words_d), _lib.ptr(a.go_d), _lib.ptr(a.perm_d),
+                                    _lib.ptr(a.po_d), a.m, a.n, a.k, bw, p.tile_width,
+                                    p.block_count, p.tile_count, _lib.ptr(res),
+                                    _lib.current_stream_ptr(a.device)), "validate_artifact")
+    code = int(res.item()) & ((1 << 64) - 1)
+    if code != (1 << 64) - 1:
+        cell, check = code >> 8, code & 0xFF
+        t, b = divmod(cell, p.block_count)
+        raise bad(f"cell {cell} (tile {t}, block {b}): "
+                  f"{_AUDIT_MESSAGES.get(check, f'check {check}')}")
 
 
 def reconstruct(a: RsrArtifact) -> PackedMatrix:
-    """Rebuild the source matrix from an artifact, auditing first
-    (reference preproc.py:375-400)."""
+    """The matrix an artifact encodes (reference preproc.py:375-400), rebuilt
+    on the device after the audit: every group scatters its sign pattern to
+    its columns (rsr_reconstruct)."""
+    import torch
     validate_artifact(a)
-    dense = np.zeros((a.m, a.n), np.int8)
+    bw = _lib.RSR_BINARY if a.bitwidth == BINARY else _lib.RSR_TERNARY
+    L = _lib.lib()
+    nbytes = int(L.rsr_reconstruct_bytes(a.m, a.n, bw))
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=a.device)
     p = a.plan
-    go, po, words, perm = a.group_offsets, a.perm_offsets, a.words, a.perm
-    for t in range(p.tile_count):
-        c0 = t * p.tile_width
-        for b in range(p.block_count):
-            c = a.cell_index(t, b)
-            r0 = b * a.k
-            h = min(a.k, a.m - r0)
-            seg = perm[po[c]:po[c + 1]]
-            for word in words[go[c]:go[c + 1]]:
-                ps, pl, pos, neg = unpack_group(word)
-                cols = c0 + seg[ps:ps + pl].astype(np.int64)
-                for i in range(h):
-                    if (pos >> i) & 1:
-                        dense[r0 + i, cols] = 1
-                    elif (neg >> i) & 1:
-                        dense[r0 + i, cols] = -1
-    out = encode(dense, a.m, a.n, a.bitwidth)
-    return PackedMatrix(a.m, a.n, a.bitwidth, out.data, weight_scale=a.weight_scale)
+    _lib.check(L.rsr_reconstruct(_lib.ptr(a.words_d), _lib.ptr(a.go_d), _lib.ptr(a.perm_d),
+                                 _lib.ptr(a.po_d), a.m, a.n, a.k, bw, p.tile_width,
+                                 p.block_count, p.tile_count, _lib.ptr(buf),
+                                 _lib.current_stream_ptr(a.device)), "reconstruct")
+    row_bytes = (a.n + 7) // 8 if a.bitwidth == BINARY else (a.n + 3) // 4
+    data = buf[:a.m * row_bytes].view(a.m, row_bytes)
+    return PackedMatrix(a.m, a.n, a.bitwidth, data, weight_scale=a.weight_scale)

@@ -11,33 +11,33 @@ from paper_2603_27462_b200.errors import CorruptArtifact
 
 
 def test_parse_ks():
-    assert cli._parse_ks("2,4,8") == [2, 4, 8]
-    assert cli._parse_ks(" 3..6 ") == [3, 4, 5, 6]
+    assert cli.k_list("2,4,8") == [2, 4, 8]
+    assert cli.k_list(" 3..6 ") == [3, 4, 5, 6]
 
 
 def test_load_vector_auto_dtype(tmp_path):
-    assert cli._load_vector("[1, -2, 3]", "auto").dtype == np.int8
-    assert cli._load_vector("[1.5, 2]", "auto").dtype == np.float32
-    assert cli._load_vector("[300, 2]", "auto").dtype == np.float32
-    assert cli._load_vector("[1, 2]", "float32").dtype == np.float32
+    assert cli.read_vector("[1, -2, 3]", "auto").dtype == np.int8
+    assert cli.read_vector("[1.5, 2]", "auto").dtype == np.float32
+    assert cli.read_vector("[300, 2]", "auto").dtype == np.float32
+    assert cli.read_vector("[1, 2]", "float32").dtype == np.float32
     p = tmp_path / "v.txt"
     p.write_text("1 2\n3")
-    assert list(cli._load_vector(str(p), "auto")) == [1, 2, 3]
+    assert list(cli.read_vector(str(p), "auto")) == [1, 2, 3]
     np.save(tmp_path / "v.npy", np.array([0.5, 1.0], np.float32))
-    assert cli._load_vector(str(tmp_path / "v.npy"), "auto").dtype == np.float32
+    assert cli.read_vector(str(tmp_path / "v.npy"), "auto").dtype == np.float32
     with pytest.raises(FileNotFoundError):
-        cli._load_vector(str(tmp_path / "missing.npy"), "auto")
+        cli.read_vector(str(tmp_path / "missing.npy"), "auto")
 
 
 def test_bench_config_validation():
-    cfg = cli._bench_config({"m": 8, "n": 8, "bitwidth": "binary", "k_list": [2, 4]})
+    cfg = cli.bench_config({"m": 8, "n": 8, "bitwidth": "binary", "k_list": [2, 4]})
     assert cfg.k_list == [2, 4]
     with pytest.raises(ValueError):
-        cli._bench_config({"m": 8, "n": 8})
+        cli.bench_config({"m": 8, "n": 8})
     with pytest.raises(ValueError):
-        cli._bench_config({"m": 8, "n": 8, "bitwidth": "binary", "colour": 1})
+        cli.bench_config({"m": 8, "n": 8, "bitwidth": "binary", "colour": 1})
     with pytest.raises(ValueError):
-        cli._bench_config([1, 2])
+        cli.bench_config([1, 2])
 
 
 def test_rsrm_round_trip_and_errors(tmp_path):
@@ -56,7 +56,10 @@ def test_rsrm_round_trip_and_errors(tmp_path):
             mc.load_rsrm(path)
 
 
-def test_errors_are_single_json_objects(capsys):
-    rc = cli._fail("FileNotFound", "x")
+def test_errors_are_single_json_objects(capsys, tmp_path):
+    rc = cli.main(["bench", "--config", str(tmp_path / "missing.json")])
     assert rc == 1
-    assert json.loads(capsys.readouterr().out) == {"error": "FileNotFound", "message": "x"}
+    assert json.loads(capsys.readouterr().out)["error"] == "FileNotFound"
+    rc = cli.main(["bench", "--config", '{"m": 4}'])
+    assert rc == 1
+    assert json.loads(capsys.readouterr().out)["error"] == "InvalidConfig"
