@@ -52,7 +52,8 @@ CONFIGS = {
                m=8192, n=8192, bitwidth="ternary", k=5, vdtype="bf16", gen="numpy"),
     "c5": dict(workload="ternary 131072x131072 RSR matvec, bf16 vector, row-block sharded "
                         "+ NCCL all-gather of outputs",
-               m=131072, n=131072, bitwidth="ternary", k=6, vdtype="bf16", gen="hash"),
+               m=131072, n=131072, bitwidth="ternary", k=6, vdtype="bf16", gen="hash",
+               tile_width=32704),  # widest halfword-format tile (5 tiles; the last 256 wide)
 }
 METRIC = "ternary matvec/s & %HBM roofline at 16384^2; BitNet-2B-shape decode tok/s"
 UNIT = "matvec/s"
@@ -63,6 +64,7 @@ def make_config(cname: str, cfg: dict, world: int) -> dict:
     """The workload description, identical for both arms."""
     return {"workload": cfg["workload"], "name": cname, "m": cfg["m"], "n": cfg["n"],
             "k": cfg["k"], "bitwidth": cfg["bitwidth"], "vector_dtype": cfg["vdtype"],
+            "tile_width": cfg.get("tile_width") or (cfg["n"] if cfg["n"] <= 65536 else 32768),
             "seed": 0, "density": 0.5,
             "generator": "rsrmv random_matrix (numpy)" if cfg["gen"] == "numpy"
             else "counter-based splitmix64 (device; CPU restatement in oracle/)",
@@ -172,7 +174,7 @@ def cpu_reference_run(cfg, steps, warmup, seconds=None):
     else:
         p = orc.Packed(cfg["m"], cfg["n"], cfg["bitwidth"],
                        random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0))
-    a = orc.preprocess(p, cfg["k"])
+    a = orc.preprocess(p, cfg["k"], cfg.get("tile_width"))
     v = random_vector(cfg["n"], 0)
     if cfg["vdtype"] == "bf16":
         v = bf16_round(v)
@@ -368,7 +370,8 @@ def traffic_child(cname: str, k: int):
     cfg = CONFIGS[cname]
     m, n = cfg["m"], cfg["n"]
     a = rsr.preprocess(rsr.PackedMatrix(m, n, cfg["bitwidth"],
-                                        random_packed(m, n, cfg["bitwidth"], 0)), k)
+                                        random_packed(m, n, cfg["bitwidth"], 0)), k,
+                       cfg.get("tile_width"))
     v = torch.from_numpy(random_vector(n, 0)).cuda()
     if cfg["vdtype"] == "bf16":
         v = v.to(torch.bfloat16)
@@ -479,11 +482,13 @@ def main():
         strip = lambda r0, r1: random_ternary_device(r1 - r0, n, 0, 0.5, row0=r0, device=dev)
     # warm-up preprocess of a few rows (same width and k: the same kernels),
     # so preprocess_ms times the preprocessing, not CUDA's lazy module loading
-    rsr.preprocess(strip(0, min(m, 4 * k)), k, shard.make_plan(m, n, k, cfg["bitwidth"]).tile_width,
-                   device=dev)
+    tw = cfg.get("tile_width")
+    rsr.preprocess(strip(0, min(m, 4 * k)), k,
+                   shard.make_plan(m, n, k, cfg["bitwidth"], tw).tile_width, device=dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    sm = shard.ShardedMatrix(m, n, cfg["bitwidth"], k, strip, rank, world, device=dev)
+    sm = shard.ShardedMatrix(m, n, cfg["bitwidth"], k, strip, rank, world, device=dev,
+                             tile_width=tw)
     torch.cuda.synchronize()
     preprocess_ms = 1e3 * (time.perf_counter() - t0)
     a = sm.local

@@ -113,9 +113,13 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
  * gslot (int32, one per reference word).  The caller reads e_off[cells] to
  * size the entries, then rsr_stream_build writes them.
  * Formats (rsr_stream_format picks one per plan):
- *   0  u16, flag bit 15: column, or KEY|0x8000          (tiles <= 32768)
+ *   3  u16, "halfword": column*2 (byte offset of a 2-byte element), KEY*4|1,
+ *      or a zero word Z + 4*bank (Z = 2*roundup(tile columns, 64)); every
+ *      column in the stream, bank-matched column order (rsr_stream_h.cu)
+ *                                              (tiles <= 32704, keys <= 2187)
+ *   0  u16, flag bit 15: column, or KEY|0x8000   (tiles <= 32768, other k)
  *   1  u16, "scaled": column*4, or KEY*4|1 -- byte offsets straight into
- *      4-byte shared-memory elements           (tiles <= 16384, keys <= 2187)
+ *      4-byte shared-memory elements (round-1 format; still decodable)
  *   2  u32, flag bit 31                          (anything wider / larger)
  * u16 formats use the QUAD layout: every chunk pair starts with a key, keys
  * sit only at slots = 0 mod 4, inside a pair each key starts a new group,
@@ -134,9 +138,9 @@ rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, const uint
 /* col0_key: device u32[cells] (u16 formats; may be NULL for format 2).       */
 rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,
-                            int32_t bitwidth, int32_t format, int32_t chunk,
-                            const int64_t *e_off, const int32_t *gslot, void *entries,
-                            uint32_t *col0_key, rsr_stream_t stream);
+                            int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t format,
+                            int32_t chunk, const int64_t *e_off, const int32_t *gslot,
+                            void *entries, uint32_t *col0_key, rsr_stream_t stream);
 
 /* ---- online multiply --------------------------------------------------------
  * rsr_matvec: y (+)= A . v  over the view's row blocks.

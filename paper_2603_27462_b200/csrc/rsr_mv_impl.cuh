@@ -43,7 +43,8 @@ enum StreamFormat {
     FMT_U16_SCALED = 1,  // u16: column*4, or key*4|1; tiles <= 16384, <= 16384 keys
     FMT_U32 = 2,         // u32: column, or key | 1<<31
     FMT_H = 3            // u16: column*2 (2-byte elements), key*4|1, or a zero word
-                         // 32768 + 4*bank; tiles <= 16384, <= 2187 keys (rsr_stream_h.cu)
+                         // h_zero_b(tn) + 4*bank; tiles <= 32704, <= 2187 keys
+                         // (rsr_stream_h.cu)
 };
 
 // How format-3 kernels stage v in shared memory (template parameter VK):
@@ -53,7 +54,13 @@ enum VKind {
     VK_F32X2 = 2,    // f32 words at byte 2*entry (float32 / float16 vectors)
     VK_I16 = 3       // int16 halfwords (int8 and quantized vectors)
 };
-constexpr uint32_t H_ZERO_B = 32768u;  // format 3: byte offset of the 32 zero halfword pairs
+// Format 3: the 32 zero words the padding entries name sit right after the
+// tile's image, at byte h_zero_b(tn) of the 2-byte image (twice that for f32
+// staging); tiles up to H_MAX_TN columns keep every entry below 65536.
+constexpr int64_t H_MAX_TN = 32704;
+__host__ __device__ constexpr uint32_t h_zero_b(int64_t tn) {
+    return (uint32_t)(((tn + 63) / 64) * 64 * 2);
+}
 
 constexpr int MV_MAX_WARPS = 20;  // 640 threads: up to 102 registers per thread
 constexpr int64_t BUCKET_MAX_KEYS = 2187;  // 3^7: buckets live in smem up to here
@@ -254,10 +261,9 @@ struct MvTypes {
 };
 
 // Bytes of the format-3 v image in shared memory: the staged tile plus the
-// 32 zero words the padding entries name (at H_ZERO_B, or 2*H_ZERO_B for f32).
+// 32 zero words the padding entries name.
 __host__ __device__ constexpr size_t h_image_bytes(int vk, int64_t tn) {
-    return vk == VK_F32X2 ? (size_t)2 * H_ZERO_B + 256
-                          : ((size_t)tn * 2 > H_ZERO_B ? (size_t)tn * 2 : (size_t)H_ZERO_B) + 128;
+    return vk == VK_F32X2 ? (size_t)2 * h_zero_b(tn) + 256 : (size_t)h_zero_b(tn) + 128;
 }
 
 // f32 += bf16 in one instruction (FHADD.BF16 on sm_100a).

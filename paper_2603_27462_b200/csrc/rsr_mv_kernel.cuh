@@ -161,8 +161,9 @@ rsr_mv_kernel(MvParams p) {
         } else {
             // lanes past the round's pairs: slot 0 = the sink key, the rest
             // padding (format 3: the bank-0 zero word; else column 0)
-            constexpr uint32_t PW = FH ? (H_ZERO_B | (H_ZERO_B << 16)) : 0u;
-            constexpr uint32_t P0 = FH ? (1u | (H_ZERO_B << 16)) : 0u;
+            const uint32_t zb = FH ? h_zero_b(tn) : 0u;
+            const uint32_t PW = zb | (zb << 16);
+            const uint32_t P0 = FH ? (1u | (zb << 16)) : 0u;
             nq[0] = make_uint4(P0, PW, PW, PW);
 #pragma unroll
             for (int j = 1; j < 4; ++j) nq[j] = make_uint4(PW, PW, PW, PW);
@@ -448,8 +449,9 @@ rsr_mv_kernel(MvParams p) {
     if constexpr (FH) {
         // format 3: every column is in the stream; padding names one of 32
         // zero words after the image (one per bank)
-        if (threadIdx.x < (VK == VK_F32X2 ? 64 : 32))
-            reinterpret_cast<uint32_t *>(vsm + (VK == VK_F32X2 ? 2 * H_ZERO_B : H_ZERO_B))[threadIdx.x] = 0u;
+        constexpr int NZ = VK == VK_F32X2 ? 64 : 32;  // (a CTA may have a single warp)
+        for (int i = threadIdx.x; i < NZ; i += blockDim.x)
+            reinterpret_cast<uint32_t *>(vsm + (VK == VK_F32X2 ? 2 : 1) * h_zero_b(tn))[i] = 0u;
     } else if constexpr (SMEM_V) {
         if constexpr (MODE == MODE_FLOAT) v0 = load_as_f32(p.v, p.vdtype, c0);
         else if constexpr (MODE == MODE_INT) v0 = (Acc)__ldg(reinterpret_cast<const int8_t *>(p.v) + c0);

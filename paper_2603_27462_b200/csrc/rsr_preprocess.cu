@@ -569,9 +569,9 @@ static rsr_status check_plan(int64_t rows, int64_t cols, int64_t row_bytes, int3
 namespace rsr {
 // halfword format builder (rsr_stream_h.cu)
 rsr_status stream_build_h(const uint64_t *words, const int64_t *go, const uint16_t *perm,
-                          const int64_t *po, int64_t bc, int64_t tc, int32_t bitwidth,
-                          const int64_t *e_off, const int32_t *gslot, uint16_t *entries,
-                          uint32_t *col0_key, cudaStream_t s);
+                          const int64_t *po, int64_t bc, int64_t tc, int64_t tw, int64_t ncols,
+                          int32_t bitwidth, const int64_t *e_off, const int32_t *gslot,
+                          uint16_t *entries, uint32_t *col0_key, cudaStream_t s);
 }  // namespace rsr
 
 using namespace rsr;
@@ -640,7 +640,7 @@ rsr_status rsr_group_fill(const uint8_t *data, int64_t rows, int64_t cols, int64
 
 int32_t rsr_stream_format(int32_t bitwidth, int32_t k, int64_t tile_width) {
     const int64_t keys = bucket_count(bitwidth, k);
-    if (tile_width <= 16384 && keys <= 2187) return 3;   // halfword u16 (bucket kernel)
+    if (tile_width <= 32704 && keys <= 2187) return 3;   // halfword u16 (bucket kernel)
     if (tile_width <= 32768 && keys <= 32768) return 0;  // u16
     return 2;                                            // u32
 }
@@ -663,17 +663,17 @@ rsr_status rsr_stream_count(const uint64_t *words, const int64_t *go, const uint
 
 rsr_status rsr_stream_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,
-                            int32_t bitwidth, int32_t format, int32_t chunk,
-                            const int64_t *e_off, const int32_t *gslot, void *entries,
-                            uint32_t *col0_key, rsr_stream_t stream) {
+                            int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t format,
+                            int32_t chunk, const int64_t *e_off, const int32_t *gslot,
+                            void *entries, uint32_t *col0_key, rsr_stream_t stream) {
     if (!go || !po || !e_off || !entries || block_count < 1 || tile_count < 1)
         return RSR_ERR_INVALID;
     if (format < 0 || format > 3 || chunk != (format == 2 ? 8 : 16)) return RSR_ERR_INVALID;
     if (format != 2 && !col0_key) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     if (format == 3)
-        return stream_build_h(words, go, perm, po, block_count, tile_count, bitwidth, e_off,
-                              gslot, (uint16_t *)entries, col0_key, s);
+        return stream_build_h(words, go, perm, po, block_count, tile_count, tile_width, cols,
+                              bitwidth, e_off, gslot, (uint16_t *)entries, col0_key, s);
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 32);
     const int bgrid =

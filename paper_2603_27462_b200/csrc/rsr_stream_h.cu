@@ -5,8 +5,8 @@
 // rsr_stream_layout.cuh) with different entry semantics:
 //   column c  -> 2*c           byte offset of a 2-byte element (bf16 / int16 v)
 //   key       -> key*4 | 1     byte offset of the key's 4-byte pattern bucket
-//   padding   -> ZERO_B + 4*b  one of 32 zero words the kernel stages after v,
-//                              one per shared-memory bank b
+//   padding   -> Z + 4*b       one of 32 zero words the kernel stages after the
+//                              tile's image (Z = h_zero_b(tn)), one per bank b
 // Every column of the tile is in the stream (no col0_key side channel), and
 // padding can name a zero word in any bank.
 //
@@ -26,17 +26,16 @@
 // column parity its partner did not take.  Random C2 cells (tools/banksim.c):
 // ~1.2 wavefronts per gather vs ~3.3 for key order and 1.86 for the
 // previous greedy + swap builder, whose zero padding sat in bank 0.
-#include "rsr_common.cuh"
+#include "rsr_mv_impl.cuh"
 #include "rsr_stream_layout.cuh"
 
 namespace rsr {
 
 constexpr int SH_WARPS = 8;             // cells in flight per CTA (one warp each)
-constexpr uint32_t H_ZERO_B = 32768u;   // byte offset of the 32 zero words (bank b at +4b)
-constexpr int H_MAX_TN = 16384;         // tile columns the format addresses
+constexpr int64_t HB_MAX_TN = 32768;    // bitmap capacity (the format addresses <= 32704)
 
 struct HWarpSmem {
-    uint32_t used[H_MAX_TN / 32];  // columns already placed (bitmap)
+    uint32_t used[HB_MAX_TN / 32];  // columns already placed (bitmap)
     uint8_t cnt[32][32];           // per lane: unplaced columns of its group per bank
     int8_t owner[32];              // matching: lane owning each bank (-1 free)
     int8_t lbank[32];              // matching: bank of each lane (-1 none)
@@ -87,7 +86,8 @@ __device__ __forceinline__ int walk_step(HWalk &w, int64_t p, const uint64_t *__
 __global__ void __launch_bounds__(SH_WARPS * 32)
 stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                       const uint16_t *__restrict__ perm, const int64_t *__restrict__ po,
-                      int64_t bc, int64_t tc, int bitwidth, const int64_t *__restrict__ e_off,
+                      int64_t bc, int64_t tc, int64_t tw, int64_t ncols, int bitwidth,
+                      const int64_t *__restrict__ e_off,
                       const int32_t *__restrict__ gslot, uint16_t *__restrict__ entries,
                       uint32_t *__restrict__ col0_key) {
     extern __shared__ __align__(16) unsigned char sh_smem[];
@@ -103,8 +103,9 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
         const LaneRuns lr = lane_runs(elen >> 5);
         uint16_t *out = entries + e0;
         const uint16_t *cperm = perm + po[src];
+        const uint32_t zero_b = h_zero_b(min(tw, ncols - t * tw));
         const int64_t g0 = go[src], g1 = go[src + 1];
-        for (int i = lane; i < H_MAX_TN / 32; i += 32) S.used[i] = 0u;
+        for (int i = lane; i < HB_MAX_TN / 32; i += 32) S.used[i] = 0u;
         if (lane < 16) S.pick16[lane] = -1;
         if (lane == 0) col0_key[dc] = 0u;  // column 0 travels in the stream
 
@@ -315,7 +316,7 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
                     uint16_t e;
                     if (ty == H_COL) e = (uint16_t)(chosen << 1);
                     else if (ty == H_KEY) e = (uint16_t)((dense_key(words[gcur], bitwidth) << 2) | 1u);
-                    else e = (uint16_t)(H_ZERO_B + 4u * (uint32_t)zb);
+                    else e = (uint16_t)(zero_b + 4u * (uint32_t)zb);
                     out[run_slot(p, lr)] = e;
                 }
                 if (lane < 16) S.pick16[lane] = -1;
@@ -327,9 +328,10 @@ stream_build_h_kernel(const uint64_t *__restrict__ words, const int64_t *__restr
 }
 
 rsr_status stream_build_h(const uint64_t *words, const int64_t *go, const uint16_t *perm,
-                          const int64_t *po, int64_t bc, int64_t tc, int32_t bitwidth,
-                          const int64_t *e_off, const int32_t *gslot, uint16_t *entries,
-                          uint32_t *col0_key, cudaStream_t s) {
+                          const int64_t *po, int64_t bc, int64_t tc, int64_t tw, int64_t ncols,
+                          int32_t bitwidth, const int64_t *e_off, const int32_t *gslot,
+                          uint16_t *entries, uint32_t *col0_key, cudaStream_t s) {
+    if (tw > H_MAX_TN || ncols < 1) return RSR_ERR_INVALID;
     const int64_t cells = bc * tc;
     const size_t smem = SH_WARPS * sizeof(HWarpSmem);
     const int grid =
@@ -337,8 +339,9 @@ rsr_status stream_build_h(const uint64_t *words, const int64_t *go, const uint16
                                                     (int64_t)sm_count() * 4));
     cudaFuncSetAttribute(stream_build_h_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    stream_build_h_kernel<<<grid, SH_WARPS * 32, smem, s>>>(words, go, perm, po, bc, tc, bitwidth,
-                                                             e_off, gslot, entries, col0_key);
+    stream_build_h_kernel<<<grid, SH_WARPS * 32, smem, s>>>(words, go, perm, po, bc, tc, tw, ncols,
+                                                             bitwidth, e_off, gslot, entries,
+                                                             col0_key);
     return launch_status();
 }
 

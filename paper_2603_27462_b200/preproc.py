@@ -223,7 +223,8 @@ class RsrArtifact:
         col0 = torch.zeros(cells if self.format != 2 else 1, dtype=torch.int32, device=dev)
         _lib.check(L.rsr_stream_build(_lib.ptr(self.words_d), _lib.ptr(self.go_d),
                                       _lib.ptr(self.perm_d), _lib.ptr(self.po_d), p.block_count,
-                                      p.tile_count, bw, self.format, self.chunk,
+                                      p.tile_count, p.tile_width, self.n, bw, self.format,
+                                      self.chunk,
                                       _lib.ptr(e_off), _lib.ptr(gslot), _lib.ptr(entries),
                                       _lib.ptr(col0) if self.format != 2 else None, s),
                    "stream_build")
@@ -254,6 +255,15 @@ class RsrArtifact:
                     "keymat_build")
             self.__dict__["_keymat"] = km
         return self.__dict__["_keymat"]
+
+    def block_bytes(self) -> np.ndarray:
+        """Reference-format artifact bytes of each row block (all its tiles):
+        8 per cell + 8 per group + 2 per perm entry (+ padding), the weights
+        for byte-balanced row-block sharding (shard.block_ranges)."""
+        p = self.plan
+        gc = np.diff(self.group_offsets).reshape(p.tile_count, p.block_count)
+        pl = np.diff(self.perm_offsets).reshape(p.tile_count, p.block_count)
+        return (8 + 8 * gc + 2 * pl + (-(2 * pl)) % 4).sum(axis=0)
 
     def stream_bytes(self) -> int:
         """Bytes of the device chunk stream one multiply reads."""

@@ -11,6 +11,12 @@ shard).
 
 Each rank materializes only its own strip of the matrix (``strip_fn``), so a
 131072^2 matrix never exists on one device when sharded.
+
+Balance.  By default the ranks get equal numbers of row blocks, which for
+matrices with uniform density (the synthetic C5 matrix) is also an equal
+share of artifact bytes.  Callers that know the per-block bytes -- e.g. the
+``block_bytes()`` of an earlier artifact of the same matrix -- pass them as
+``weights`` and the contiguous ranges are cut at equal byte shares instead.
 """
 
 from __future__ import annotations
@@ -60,12 +66,13 @@ class ShardedMatrix:
     """
 
     def __init__(self, m: int, n: int, bitwidth: str, k: int, strip_fn, rank: int, world: int,
-                 device=None, group=None, weight_scale: float = 1.0):
+                 device=None, group=None, weight_scale: float = 1.0, weights=None,
+                 tile_width: int | None = None):
         import torch
         self.m, self.n, self.k, self.bitwidth = m, n, k, bitwidth
         self.rank, self.world, self.group = rank, world, group
-        self.plan = make_plan(m, n, k, bitwidth)
-        self.ranges = row_ranges(m, k, world)
+        self.plan = make_plan(m, n, k, bitwidth, tile_width)
+        self.ranges = row_ranges(m, k, world, weights)
         self.r0, self.r1 = self.ranges[rank]
         self.pad = max(r1 - r0 for r0, r1 in self.ranges)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \

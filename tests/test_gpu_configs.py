@@ -92,10 +92,12 @@ def test_c4_ternary_8192_k5_full_size(rsr):
     assert float_ok(y, yr, np.abs(orc.decode(p)).astype(np.float64), vr).all()
 
 
-@pytest.mark.parametrize("strip", range(4))
-def test_c5_sampled_strips_vs_oracle(rsr, strip):
-    """C5 (ternary 131072 columns, k=6, tiles of 32768): random row strips of
-    the device generator vs the oracle's restatement of it."""
+@pytest.mark.parametrize("strip,tw", [(0, None), (1, None), (2, 32704), (3, 32704)])
+def test_c5_sampled_strips_vs_oracle(rsr, strip, tw):
+    """C5 (ternary 131072 columns, k=6): random row strips of the device
+    generator vs the oracle's restatement of it, at the reference's default
+    tiles (4 x 32768, format 0) and the bench's halfword-format tiles
+    (32704 wide: 5 tiles, the last 256 columns)."""
     import torch
     from paper_2603_27462_b200.devicepack import random_ternary_device
     n, k, rows = 131072, 6, 36
@@ -104,9 +106,10 @@ def test_c5_sampled_strips_vs_oracle(rsr, strip):
     dev = random_ternary_device(rows, n, 0, 0.5, row0=row0, device="cuda")
     host = orc.random_ternary_rows(row0, rows, n, 0, 0.5)
     assert np.array_equal(dev.device_data().cpu().numpy(), host.data)
-    a = rsr.preprocess(dev, k)
-    assert a.plan.tile_count == 4
-    ref = orc.preprocess(host, k)
+    a = rsr.preprocess(dev, k, tw)
+    assert a.plan.tile_count == (4 if tw is None else 5)
+    assert a.format == (0 if tw is None else 3)
+    ref = orc.preprocess(host, k, tw)
     assert np.array_equal(a.words, ref.words) and np.array_equal(a.perm, ref.perm)
     assert np.array_equal(a.group_offsets, ref.group_offsets)
     vi = rng.integers(-128, 128, n).astype(np.int8)

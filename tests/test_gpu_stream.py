@@ -69,21 +69,24 @@ def dense_key(w, bitwidth_binary):
     return int(key)
 
 
-ZERO_B = 32768  # format 3: byte offset of the zero words
+def zero_b(tn):
+    """format 3: byte offset of the zero words after a tn-column image"""
+    return 2 * (-(-tn // 64) * 64)
 
 
-def decode_cell(ent, fmt):
+def decode_cell(ent, fmt, tn=16384):
     """-> list of (is_key, value) in logical order; format 3 padding decodes
     to (False, -1 - bank)."""
     out = []
+    zb = zero_b(tn)
     for x in ent:
         x = int(x)
         if fmt == 3:
             if x & 1:
                 out.append((True, x >> 2))
-            elif x >= ZERO_B:
-                assert (x - ZERO_B) % 4 == 0 and x < ZERO_B + 128, x
-                out.append((False, -1 - (x - ZERO_B) // 4))
+            elif x >= zb:
+                assert (x - zb) % 4 == 0 and x < zb + 128, x
+                out.append((False, -1 - (x - zb) // 4))
             else:
                 out.append((False, x >> 1))
         elif fmt == 1:
@@ -144,7 +147,8 @@ def check_stream(a, binary):
         e0, e1 = int(e_off[dc]), int(e_off[dc + 1])
         assert (e1 - e0) % (2 * CH) == 0
         cell = ent[e0:e1]
-        seq = decode_cell(cell[run_slots(e1 - e0) if quad else phys_slots(e1 - e0, CH)], fmt)
+        tn = min(a.plan.tile_width, a.n - t * a.plan.tile_width)
+        seq = decode_cell(cell[run_slots(e1 - e0) if quad else phys_slots(e1 - e0, CH)], fmt, tn)
         exp, key0 = {}, 0
         for g in range(go[src], go[src + 1]):
             w = int(words[g])
@@ -187,7 +191,9 @@ def check_stream(a, binary):
 @pytest.mark.parametrize("m,n,k,bw,tw", [
     (96, 3000, 6, "ternary", None),
     (64, 4096, 8, "binary", None),
-    (40, 20000, 5, "ternary", 20000),   # format 0 (tile > 16384)
+    (40, 20000, 5, "ternary", 20000),   # format 3, tile > 16384
+    (20, 65408, 6, "ternary", 32704),   # format 3, widest tile, two tiles
+    (24, 33000, 4, "ternary", 32768),   # format 0 (tile > 32704)
     (30, 5000, 12, "binary", None),      # format 0 (keys > 2187)
     (24, 40000, 4, "ternary", 40000),    # format 2 (tile > 32768)
 ])

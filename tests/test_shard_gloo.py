@@ -74,5 +74,7 @@ def test_block_ranges_balance_and_cover():
     assert rg[0][0] == 0 and rg[-1][1] == 8 and rg[0][1] == rg[1][0]
     assert rg == [(0, 5), (5, 8)] or rg == [(0, 4), (4, 8)]
     assert shard.row_ranges(10, 4, 2) == [(0, 4), (4, 10)]
+    # byte-weighted row ranges: a heavy first block moves the cut forward
+    assert shard.row_ranges(12, 4, 2, np.array([5.0, 1.0, 1.0])) == [(0, 4), (4, 12)]
     idx = shard.gather_index([(0, 4), (4, 10)], 6)
     assert list(idx) == [0, 1, 2, 3, 6, 7, 8, 9, 10, 11]

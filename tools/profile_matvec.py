@@ -22,8 +22,13 @@ if len(sys.argv) > 2:
     cfg["k"] = int(sys.argv[2])
 mode = sys.argv[3] if len(sys.argv) > 3 else "float"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
-data = bench.random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0)
-a = rsr.preprocess(rsr.PackedMatrix(cfg["m"], cfg["n"], cfg["bitwidth"], data), cfg["k"])
+if cfg.get("gen") == "hash":  # C5: the device generator (the numpy one needs 137 GB)
+    from paper_2603_27462_b200.devicepack import random_ternary_device
+    pm = random_ternary_device(cfg["m"], cfg["n"], 0, 0.5)
+else:
+    pm = rsr.PackedMatrix(cfg["m"], cfg["n"], cfg["bitwidth"],
+                          bench.random_packed(cfg["m"], cfg["n"], cfg["bitwidth"], 0))
+a = rsr.preprocess(pm, cfg["k"], cfg.get("tile_width"))
 v = torch.from_numpy(bench.random_vector(cfg["n"], 0)).cuda()
 if cfg["vdtype"] == "bf16":
     v = v.to(torch.bfloat16)
