@@ -202,6 +202,20 @@ rsr_status rsr_matmul(const rsr_stream_view *view, const void *V, int32_t v_dtyp
                       int32_t B, void *Y, int64_t ldy, void *workspace, size_t workspace_bytes,
                       rsr_stream_t stream);
 
+/* ---- batched fused path (prefill: T activation rows, one stacked linear) -----
+ * rsr_absmax_quantize_rows: Q[t] (int8, row stride ldq) and scales[t] (f64)
+ * = the reference absmax quantization of each row V[t] (_native.py:313-336).
+ * rsr_matmul then gives the exact int32 products; rsr_dequant_rows writes
+ * out[t][i] = f32(f64(Y[t][i]) * (beta_i / scales[t])) (beta_i = row_beta[i]
+ * when row_beta is non-NULL, else beta; bf16 = RNE of that f32) -- row by row
+ * the single-vector rsr_fused_matvec result, bit for bit.                  */
+rsr_status rsr_absmax_quantize_rows(const void *V, int32_t v_dtype, int64_t ldv, int64_t rows,
+                                    int64_t n, int8_t *Q, int64_t ldq, double *scales,
+                                    rsr_stream_t stream);
+rsr_status rsr_dequant_rows(const int32_t *Y, int64_t ldy, int64_t rows, int64_t m,
+                            const double *scales, const double *row_beta, double beta, void *out,
+                            int32_t out_dtype, int64_t ldo, rsr_stream_t stream);
+
 /* ---- batched multiply on the tensor cores (tcgen05) ---------------------------
  * For bf16 batches the pattern-table expansion runs on the tensor cores: the
  * code matrix holds every column's pattern key as 2-bit row codes (the

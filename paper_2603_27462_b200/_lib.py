@@ -81,6 +81,8 @@ SIGNATURES = {
     "rsr_random_ternary": (I32, [I64, I64, I64, ctypes.c_uint64, F64, P, P]),
     "rsr_split_planes": (I32, [P, I64, I64, I64, P, P]),
     "rsr_audit": (I32, [P, P, P, P, I64, I64, I32, I32, I64, I64, I64, P, P]),
+    "rsr_absmax_quantize_rows": (I32, [P, I32, I64, I64, I64, P, I64, P, P]),
+    "rsr_dequant_rows": (I32, [P, I64, I64, I64, P, P, F64, P, I32, I64, P]),
     "rsr_reconstruct_bytes": (SZ, [I64, I64, I32]),
     "rsr_reconstruct": (I32, [P, P, P, P, I64, I64, I32, I32, I64, I64, I64, P, P]),
     "rsr_debug_set_probe": (None, [P]),

@@ -453,3 +453,80 @@ rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Batched fused path (prefill: T activation rows through one stacked linear).
+// rsr_absmax_quantize_rows quantizes each row with the reference rule
+// (_native.py:313-336, float64 math, per-row scale); the int8 batch then goes
+// through rsr_matmul (exact int32); rsr_dequant_rows applies
+// f32(f64(y) * (beta_i / scale_t)) per (row i, vector t) -- the fused
+// kernel's epilogue, so every row equals the single-vector fused result.
+namespace rsr {
+__global__ void absmax_quantize_rows_kernel(const void *V, int dtype, int64_t ldv, int64_t n,
+                                            int8_t *Q, int64_t ldq, double *scales) {
+    __shared__ double red[32];
+    const int64_t row = blockIdx.x;
+    const char *vr = reinterpret_cast<const char *>(V) +
+                     row * ldv * (dtype == RSR_F32 ? 4 : 2);
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = fabs((double)load_as_f32(vr, dtype, i));
+        a = x > a ? x : a;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
+        a = o > a ? o : a;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    a = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a = red[w] > a ? red[w] : a;
+    const double scale = a == 0.0 ? 1.0 : 127.0 / a;
+    if (threadIdx.x == 0) scales[row] = scale;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        Q[row * ldq + i] = quantize_one(load_as_f32(vr, dtype, i), scale);
+}
+
+__global__ void dequant_rows_kernel(const int32_t *Y, int64_t ldy, int64_t rows, int64_t m,
+                                    const double *scales, const double *row_beta, double beta,
+                                    void *out, int out_bf16, int64_t ldo) {
+    const int64_t total = rows * m;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = e / m, i = e - t * m;
+        const double b = row_beta ? row_beta[i] : beta;
+        const float o = (float)((double)Y[t * ldy + i] * (b / scales[t]));
+        if (out_bf16) reinterpret_cast<__nv_bfloat16 *>(out)[t * ldo + i] = __float2bfloat16_rn(o);
+        else reinterpret_cast<float *>(out)[t * ldo + i] = o;
+    }
+}
+}  // namespace rsr
+
+extern "C" {
+
+rsr_status rsr_absmax_quantize_rows(const void *V, int32_t v_dtype, int64_t ldv, int64_t rows,
+                                    int64_t n, int8_t *Q, int64_t ldq, double *scales,
+                                    rsr_stream_t stream) {
+    if (!V || !Q || !scales || rows < 0 || n < 1 || ldv < n || ldq < n) return RSR_ERR_INVALID;
+    if (v_dtype != RSR_F32 && v_dtype != RSR_BF16 && v_dtype != RSR_F16) return RSR_ERR_INVALID;
+    if (rows == 0) return RSR_OK;
+    absmax_quantize_rows_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
+        V, v_dtype, ldv, n, Q, ldq, scales);
+    return launch_status();
+}
+
+rsr_status rsr_dequant_rows(const int32_t *Y, int64_t ldy, int64_t rows, int64_t m,
+                            const double *scales, const double *row_beta, double beta, void *out,
+                            int32_t out_dtype, int64_t ldo, rsr_stream_t stream) {
+    if (!Y || !scales || !out || rows < 0 || m < 1 || ldy < m || ldo < m) return RSR_ERR_INVALID;
+    if (out_dtype != RSR_F32 && out_dtype != RSR_BF16) return RSR_ERR_INVALID;
+    if (rows == 0) return RSR_OK;
+    const int grid = (int)std::min<int64_t>((rows * m + 255) / 256, (int64_t)sm_count() * 8);
+    dequant_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(Y, ldy, rows, m, scales, row_beta,
+                                                                 beta, out, out_dtype == RSR_BF16,
+                                                                 ldo);
+    return launch_status();
+}
+
+}  // extern "C"

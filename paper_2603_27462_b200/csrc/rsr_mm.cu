@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
     using Acc = typename std::conditional<MODE == MODE_FLOAT, float, int32_t>::type;
     using Vec = typename std::conditional<MODE == MODE_FLOAT, float4, int4>::type;
     constexpr int BV = MM_BV;
+    constexpr bool FH = FMT == FMT_H;  // halfword format: every column in the stream
     constexpr bool SC = FMT == FMT_U16_SCALED;
     extern __shared__ __align__(16) unsigned char mm_sbuf[];
     const int nwarps = blockDim.x >> 5;
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
 
     // smem: [v tile tn x BV][sign table K x NB][buckets W x NB x BV]
     Acc *vt = reinterpret_cast<Acc *>(mm_sbuf);
-    size_t off = (size_t)tn * BV * sizeof(Acc);
+    size_t off = (size_t)(FH ? h_zero_b(tn) / 2 + 64 : tn) * BV * sizeof(Acc);
     Acc *stab = reinterpret_cast<Acc *>(mm_sbuf + off);
     off += ((size_t)p.nkeys * K * sizeof(Acc) + 15) & ~(size_t)15;
     Acc *bk = reinterpret_cast<Acc *>(mm_sbuf + off) + (size_t)warp * p.nkeys * BV;
@@ -73,8 +74,12 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
             for (int64_t i = threadIdx.x; i < tn; i += blockDim.x) vt[i * BV + j] = (Acc)0;
         }
     }
-    if (threadIdx.x == 0) {  // column 0 is the zero padding entry (see col0_key);
-#pragma unroll               // thread 0 staged element 0 of every column
+    if constexpr (FH) {
+        // padding names the zero columns [Z, Z + 64) after the tile
+        const int64_t z = h_zero_b(tn) / 2;
+        for (int64_t i = threadIdx.x; i < 64 * BV; i += blockDim.x) vt[z * BV + i] = (Acc)0;
+    } else if (threadIdx.x == 0) {  // column 0 is the zero padding entry (see col0_key);
+#pragma unroll                      // thread 0 staged element 0 of every column
         for (int j = 0; j < BV; ++j) vt[j] = (Acc)0;
     }
     for (int key = threadIdx.x; key < p.nkeys; key += blockDim.x) {
@@ -110,11 +115,17 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
     __syncthreads();
 
     // byte offsets of a column / key entry into the v tile / bucket rows
+    // (format 3: a column entry is 2*column, a key entry key*4|1)
     auto col_off = [](uint32_t e) -> uint32_t {
-        return SC ? (e & 0xFFFCu) * BV : (e & 0x7FFFu) * (4u * BV);
+        return FH ? (e & 0xFFFEu) * (2u * BV) : (SC ? (e & 0xFFFCu) * BV : (e & 0x7FFFu) * (4u * BV));
     };
-    auto hi_off = [](uint32_t x) -> uint32_t { return SC ? (x >> 16) * BV : (x >> 16) * (4u * BV); };
-    auto is_key = [](uint32_t x) -> bool { return SC ? (x & 1u) != 0u : (x & 0x8000u) != 0u; };
+    auto key_off = [](uint32_t e) -> uint32_t {
+        return FH ? (e & 0xFFFCu) * BV : (SC ? (e & 0xFFFCu) * BV : (e & 0x7FFFu) * (4u * BV));
+    };
+    auto hi_off = [](uint32_t x) -> uint32_t {
+        return FH ? (x >> 16) * (2u * BV) : (SC ? (x >> 16) * BV : (x >> 16) * (4u * BV));
+    };
+    auto is_key = [](uint32_t x) -> bool { return (SC || FH) ? (x & 1u) != 0u : (x & 0x8000u) != 0u; };
     auto gat = [&](uint32_t o) -> Vec {
         Vec r;
         if constexpr (MODE == MODE_FLOAT) {
@@ -163,8 +174,12 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
         uint32_t cur = 0;
         Vec s = Vec{0, 0, 0, 0};
         auto load = [&](uint32_t r, uint4 (&q)[4]) {
+            // lanes past the round: the sink key, then padding
+            const uint32_t zb = FH ? h_zero_b(tn) : 0u;
+            const uint32_t PW = zb | (zb << 16);
+            q[0] = make_uint4(FH ? (1u | (zb << 16)) : 0u, PW, PW, PW);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) q[j] = make_uint4(0, 0, 0, 0);
+            for (int j = 1; j < 4; ++j) q[j] = make_uint4(PW, PW, PW, PW);
             if (r >= P) return;
             const uint32_t np = Lf + (r < rem ? 1u : 0u);
             const uint32_t R = r * Lf + min(r, rem);
@@ -182,7 +197,7 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
             const uint32_t w[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
                                     a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
             {   // slot 0: a key; a new one closes the open group
-                const uint32_t k0 = col_off(w[0]);
+                const uint32_t k0 = key_off(w[0]);
                 const bool ns = k0 != cur;
                 flush(ns, cur, s);
                 cur = k0;
@@ -198,7 +213,7 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
                 const bool isk = is_key(x);
                 const uint32_t xo = col_off(x);
                 flush(isk, cur, s);
-                cur = isk ? xo : cur;
+                cur = isk ? key_off(x) : cur;
                 Vec g = gat(hi_off(x));
                 add4(g, gat(col_off(y)));
                 add4(g, gat(hi_off(y)));
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(MM_MAX_WARPS * 32) rsr_mm_kernel(MmParams p) {
         }
         __syncwarp();
         // epilogue: column 0, then y[i][j] = sum_key sgn_i(key) * bucket[key][j]
-        const uint32_t key0 = p.col0_key[dc];
+        const uint32_t key0 = FH ? 0u : p.col0_key[dc];
         if (lane == 0 && key0) {
             Acc *row = bk + (size_t)key0 * BV;
 #pragma unroll
@@ -301,10 +316,15 @@ using MmFn = void (*)(MmParams);
 #define RSR_MMK_0_1(KK) (rsr_mm_kernel<KK, MODE_FLOAT, FMT_U16_SCALED>)
 #define RSR_MMK_1_0(KK) (rsr_mm_kernel<KK, MODE_INT, FMT_U16>)
 #define RSR_MMK_1_1(KK) (rsr_mm_kernel<KK, MODE_INT, FMT_U16_SCALED>)
+#define RSR_MMK_0_3(KK) (rsr_mm_kernel<KK, MODE_FLOAT, FMT_H>)
+#define RSR_MMK_1_3(KK) (rsr_mm_kernel<KK, MODE_INT, FMT_H>)
 static MmFn pick_mm(int mode, int fmt, int k) {
     if (k > 11) return nullptr;
-    if (mode == MODE_FLOAT) return fmt == FMT_U16 ? RSR_MM_K(0, 0)(k) : RSR_MM_K(0, 1)(k);
-    return fmt == FMT_U16 ? RSR_MM_K(1, 0)(k) : RSR_MM_K(1, 1)(k);
+    if (mode == MODE_FLOAT)
+        return fmt == FMT_U16 ? RSR_MM_K(0, 0)(k)
+               : (fmt == FMT_H ? RSR_MM_K(0, 3)(k) : RSR_MM_K(0, 1)(k));
+    return fmt == FMT_U16 ? RSR_MM_K(1, 0)(k)
+           : (fmt == FMT_H ? RSR_MM_K(1, 3)(k) : RSR_MM_K(1, 1)(k));
 }
 
 static size_t mm_part_bytes(const rsr_stream_view *vw, int B) {
@@ -316,7 +336,9 @@ static size_t mm_part_bytes(const rsr_stream_view *vw, int B) {
 static size_t mm_smem(const rsr_stream_view *vw, int warps) {
     const int64_t tn = std::min(vw->tile_width, vw->n);
     const size_t nkeys = (size_t)bucket_count(vw->bitwidth, vw->k);
-    return (size_t)tn * MM_BV * 4 + ((nkeys * vw->k * 4 + 15) & ~(size_t)15) +
+    // format 3: the tile plus the 64 zero columns the padding names
+    const size_t cols = vw->format == FMT_H ? (size_t)h_zero_b(tn) / 2 + 64 : (size_t)tn;
+    return cols * MM_BV * 4 + ((nkeys * vw->k * 4 + 15) & ~(size_t)15) +
            (size_t)warps * nkeys * MM_BV * 4;
 }
 
@@ -325,8 +347,7 @@ static rsr_status launch_mm(const rsr_stream_view *vw, const void *V, int vdtype
                             int B, void *Y, int64_t ldy, void *ws, size_t ws_bytes,
                             cudaStream_t s) {
     if (!vw || !vw->entries || !vw->e_off || !V || !Y || B < 1) return RSR_ERR_INVALID;
-    if ((vw->format != FMT_U16 && vw->format != FMT_U16_SCALED) || !vw->col0_key)
-        return RSR_ERR_INVALID;
+    if (vw->format == FMT_U32 || !vw->col0_key) return RSR_ERR_INVALID;
     const int64_t rows = std::min(vw->n_blocks * vw->k, vw->m - vw->row_begin_block * vw->k);
     if (ldv < vw->n || ldy < rows) return RSR_ERR_INVALID;
     if (vw->n_blocks == 0) return RSR_OK;

@@ -21,7 +21,7 @@ import torch
 from torch import nn
 
 from .devicepack import ternarize_pack_device
-from .kernels import batched_preprocess, fused_into
+from .kernels import batched_preprocess, fused_into, fused_rows_into
 
 DEFAULT_K = 5  # fewest artifact bytes for BitNet-2B shapes
 
@@ -46,11 +46,16 @@ class RSRSiblingGroup:
         self._pending: set = set()
 
     def compute(self, x2: torch.Tensor) -> torch.Tensor:
-        """x2: (T, in) -> (T, sum(out)) in out_dtype; one fused launch per row."""
+        """x2: (T, in) -> (T, sum(out)) in out_dtype.  One token (decode): one
+        fused quantize/multiply/dequantize launch.  Several (prefill): the
+        rows are quantized together, multiplied as one int8 batch and
+        dequantized together -- each row bit-identical to the one-token path."""
         T = x2.shape[0]
         out = torch.empty(T, self.out_features, dtype=self.out_dtype, device=x2.device)
-        for t in range(T):
-            fused_into(self.artifact, x2[t], out[t], beta=1.0, row_beta=self.row_beta)
+        if T == 1:
+            fused_into(self.artifact, x2[0], out[0], beta=1.0, row_beta=self.row_beta)
+        elif T > 1:
+            fused_rows_into(self.artifact, x2, out, beta=1.0, row_beta=self.row_beta)
         return out
 
     def output_for(self, index: int, x2: torch.Tensor) -> torch.Tensor:

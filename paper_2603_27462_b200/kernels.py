@@ -173,6 +173,37 @@ def fused_into(a: RsrArtifact, vt, out, beta: float | None = None, view=None, st
     return out
 
 
+def fused_rows_into(a: RsrArtifact, V, out, beta: float | None = None, row_beta=None,
+                    stream=None):
+    """The fused quantize/multiply/dequantize path for T activation rows at
+    once (prefill): out[t] = rsr_matvec_fused(a, V[t]) bit for bit, computed
+    as one per-row quantization launch, one batched exact int8 multiply
+    (matmul_into) and one dequantization launch.  V: [T, n] f32/bf16/f16;
+    out: [T, m] float32 or bfloat16; row_beta as fused_into."""
+    import torch
+    from .matcore import _dtype_code
+    T = int(V.shape[0])
+    if T == 0:
+        return out
+    V = V.contiguous()
+    dev = a.device
+    s = _lib.current_stream_ptr(dev) if stream is None else stream
+    L = _lib.lib()
+    Q = torch.empty(T, a.n, dtype=torch.int8, device=dev)
+    scales = torch.empty(T, dtype=torch.float64, device=dev)
+    _lib.check(L.rsr_absmax_quantize_rows(V.data_ptr(), _dtype_code(V), V.stride(0), T, a.n,
+                                          Q.data_ptr(), Q.stride(0), scales.data_ptr(), s),
+               "quantize rows")
+    Y = torch.empty(T, a.m, dtype=torch.int32, device=dev)
+    matmul_into(a, Q, Y, stream=s, method="stream")
+    b = float(a.weight_scale) if beta is None else float(beta)
+    odt = _lib.RSR_BF16 if out.dtype == torch.bfloat16 else _lib.RSR_F32
+    _lib.check(L.rsr_dequant_rows(Y.data_ptr(), Y.stride(0), T, a.m, scales.data_ptr(),
+                                  _lib.ptr(row_beta), b, out.data_ptr(), odt, out.stride(0), s),
+               "dequant rows")
+    return out
+
+
 def rsr_matvec(a: RsrArtifact, v, counter: OpCounter | None = None,
                threads: int | None = None):
     """Multiply a preprocessed matrix by v on the GPU (reference kernels.py:59-102).

@@ -76,3 +76,23 @@ def test_replace_linear_small_bitnet_decode(torch_cuda):
     dec.capture()
     toks_graph, _ = dec.generate(prompt, 12)
     assert toks_graph == toks_eager  # graph replay == eager, integer-exact linears
+
+
+@pytest.mark.parametrize("m,n,k,T", [(2560, 2560, 5, 7), (300, 6912, 5, 3), (97, 1000, 4, 16)])
+def test_prefill_rows_equal_single_token_path(torch_cuda, m, n, k, T):
+    """The batched prefill path (per-row quantization, one int8 batch,
+    per-row dequantization) equals the one-token fused kernel row by row."""
+    torch = torch_cuda
+    import paper_2603_27462_b200 as rsr
+    from paper_2603_27462_b200 import kernels as kn
+    p = orc.random_matrix(m, n, "ternary", m + T)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", p.data, 0.031), k)
+    X = (torch.randn(T, n, device="cuda") * 3).to(torch.bfloat16)
+    row_beta = torch.rand(m, device="cuda", dtype=torch.float64) + 0.5
+    for odt in (torch.float32, torch.bfloat16):
+        out = torch.empty(T, m, dtype=odt, device="cuda")
+        kn.fused_rows_into(a, X, out, beta=1.0, row_beta=row_beta)
+        for t in range(T):
+            one = torch.empty(m, dtype=odt, device="cuda")
+            kn.fused_into(a, X[t], one, beta=1.0, row_beta=row_beta)
+            assert torch.equal(out[t], one), (odt, t)
