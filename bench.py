@@ -320,7 +320,7 @@ def decode_bench(steps=64, k=5):
     import torch
     from transformers import BitNetConfig, BitNetForCausalLM
     from paper_2603_27462_b200.decode import GraphDecoder, linear_time_per_token
-    from paper_2603_27462_b200.hf import replace_linear_with_rsr
+    from paper_2603_27462_b200.hf import fuse_rms_norms, replace_linear_with_rsr
     torch.manual_seed(0)
     cfg = BitNetConfig()
     cfg._attn_implementation = "sdpa"
@@ -330,8 +330,13 @@ def decode_bench(steps=64, k=5):
     import copy
     rsr_model = copy.deepcopy(model)
     replace_linear_with_rsr(rsr_model, k=k)
+    bl_model = copy.deepcopy(model)
+    replace_linear_with_rsr(bl_model, k=k, fuse_norms=True)
+    dn_model = copy.deepcopy(model)
+    fuse_rms_norms(dn_model)
     decs = {}
-    for name, mdl in (("dense_bf16_cublas", model), ("rsr", rsr_model)):
+    for name, mdl in (("dense_bf16_cublas", model), ("rsr", rsr_model), ("rsr_bitlinear", bl_model),
+                      ("dense_fused_norm", dn_model)):
         dec = GraphDecoder(mdl, max_len=16 + steps + 8)
         dec.prefill(prompt)
         dec.capture()
@@ -347,6 +352,7 @@ def decode_bench(steps=64, k=5):
     torch.cuda.empty_cache()
     lin = {"dense_bf16_cublas": linear_time_per_token(model),
            "rsr": linear_time_per_token(rsr_model)}
+    del bl_model, dn_model
     return {"model": "BitNetForCausalLM(BitNetConfig()) random init, bf16, 30 layers, "
                      "hidden 2560, FFN 6912",
             "loop": "greedy, HF StaticCache, one CUDA graph per step, batch 1",
@@ -354,6 +360,16 @@ def decode_bench(steps=64, k=5):
             "rsr_tok_s": res["rsr"],
             "dense_tok_s": res["dense_bf16_cublas"],
             "speedup": res["rsr"] / res["dense_bf16_cublas"],
+            "rsr_bitlinear_tok_s": res["rsr_bitlinear"],
+            "bitlinear_speedup": res["rsr_bitlinear"] / res["dense_bf16_cublas"],
+            "bitlinear": "replace_linear_with_rsr(fuse_norms=True): the four RMSNorms of each "
+                         "layer run inside the following RSR launches (BitLinear); the dense "
+                         "arm keeps HF's unfused norms",
+            "dense_fused_norm_tok_s": res["dense_fused_norm"],
+            "bitlinear_vs_dense_fused_norm": res["rsr_bitlinear"] / res["dense_fused_norm"],
+            "dense_fused_norm": "dense bf16 linears with each RMSNorm as one launch "
+                                "(hf.fuse_rms_norms, same arithmetic as the BitLinear prologue): "
+                                "the like-for-like comparison for rsr_bitlinear",
             "linear_us_per_token": {name: v["us"] for name, v in lin.items()},
             "linear_speedup": lin["dense_bf16_cublas"]["us"] / lin["rsr"]["us"],
             "linear_detail": lin}

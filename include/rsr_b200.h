@@ -188,6 +188,24 @@ rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t 
                             double *scale_out, void *workspace, size_t workspace_bytes,
                             rsr_stream_t stream);
 
+/* rsr_fused_matvec_norm: rsr_fused_matvec of the RMS-normalized vector
+ * (BitNet's BitLinear = RMSNorm + absmax quantization + ternary product, with
+ * the norm of HF BitNetRMSNorm: x * rsqrt(mean(x^2) + eps) rounded to bf16,
+ * times the bf16 weight norm_w, rounded to bf16) in ONE launch.  bf16 v of
+ * one tile (n % 8 == 0, 16-byte aligned v and norm_w); the mean of squares
+ * is an fp32 sum in a fixed order (it may differ from torch's reduction in
+ * the last bit).  Out: as rsr_fused_matvec; no scale output.              */
+rsr_status rsr_fused_matvec_norm(const rsr_stream_view *view, const void *v, int32_t v_dtype,
+                                 const void *norm_w, float norm_eps, double beta,
+                                 const double *row_beta, void *out, int32_t out_dtype,
+                                 void *workspace, size_t workspace_bytes, rsr_stream_t stream);
+
+/* rsr_rmsnorm_rows: out[r] = the norm of rsr_fused_matvec_norm applied to
+ * each bf16 row x[r] (rows x n, contiguous) with bf16 weight w -- a single
+ * launch per norm (the dense arm of the decode comparison uses it).        */
+rsr_status rsr_rmsnorm_rows(const void *x, const void *w, int64_t rows, int64_t n, float eps,
+                            void *out, rsr_stream_t stream);
+
 /* ---- batched multi-vector multiply (not in the reference) ----
  * rsr_matmul: Y[b] = A . V[b] for b < B, over the view's row blocks.
  *   V: B vectors, element (b, col) at V[b*ldv + col] (ldv >= n);
@@ -208,10 +226,12 @@ rsr_status rsr_matmul(const rsr_stream_view *view, const void *V, int32_t v_dtyp
  * rsr_matmul then gives the exact int32 products; rsr_dequant_rows writes
  * out[t][i] = f32(f64(Y[t][i]) * (beta_i / scales[t])) (beta_i = row_beta[i]
  * when row_beta is non-NULL, else beta; bf16 = RNE of that f32) -- row by row
- * the single-vector rsr_fused_matvec result, bit for bit.                  */
+ * the single-vector rsr_fused_matvec result, bit for bit.  norm_w (bf16
+ * rows only, may be NULL): each row first goes through the fused RMSNorm of
+ * rsr_fused_matvec_norm.                                                    */
 rsr_status rsr_absmax_quantize_rows(const void *V, int32_t v_dtype, int64_t ldv, int64_t rows,
-                                    int64_t n, int8_t *Q, int64_t ldq, double *scales,
-                                    rsr_stream_t stream);
+                                    int64_t n, const void *norm_w, float norm_eps, int8_t *Q,
+                                    int64_t ldq, double *scales, rsr_stream_t stream);
 rsr_status rsr_dequant_rows(const int32_t *Y, int64_t ldy, int64_t rows, int64_t m,
                             const double *scales, const double *row_beta, double beta, void *out,
                             int32_t out_dtype, int64_t ldo, rsr_stream_t stream);

@@ -80,8 +80,11 @@ SIGNATURES = {
     "rsr_ternarize_pack": (I32, [P, I32, I64, I64, P, P, P, SZ, P]),
     "rsr_random_ternary": (I32, [I64, I64, I64, ctypes.c_uint64, F64, P, P]),
     "rsr_split_planes": (I32, [P, I64, I64, I64, P, P]),
+    "rsr_rmsnorm_rows": (I32, [P, P, I64, I64, ctypes.c_float, P, P]),
     "rsr_audit": (I32, [P, P, P, P, I64, I64, I32, I32, I64, I64, I64, P, P]),
-    "rsr_absmax_quantize_rows": (I32, [P, I32, I64, I64, I64, P, I64, P, P]),
+    "rsr_absmax_quantize_rows": (I32, [P, I32, I64, I64, I64, P, ctypes.c_float, P, I64, P, P]),
+    "rsr_fused_matvec_norm": (I32, [ctypes.POINTER(StreamView), P, I32, P, ctypes.c_float, F64, P,
+                                    P, I32, P, SZ, P]),
     "rsr_dequant_rows": (I32, [P, I64, I64, I64, P, P, F64, P, I32, I64, P]),
     "rsr_reconstruct_bytes": (SZ, [I64, I64, I32]),
     "rsr_reconstruct": (I32, [P, P, P, P, I64, I64, I32, I32, I64, I64, I64, P, P]),

@@ -122,7 +122,8 @@ template <int MODE>
 static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype, void *y,
                             int accumulate, double beta, double *scale_out, void *ws,
                             size_t ws_bytes, cudaStream_t s, const double *row_beta = nullptr,
-                            int out_bf16 = 0) {
+                            int out_bf16 = 0, const uint16_t *norm_w = nullptr,
+                            float norm_eps = 0.f) {
     rsr_status st = check_view(vw);
     if (st != RSR_OK) return st;
     if (!v || !y) return RSR_ERR_INVALID;
@@ -151,6 +152,8 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     p.beta = beta;
     p.row_beta = row_beta;
     p.out_bf16 = out_bf16;
+    p.norm_w = norm_w;
+    p.norm_eps = norm_eps;
     p.scale_dev = scale_out;
     p.probe = g_probe;
     {
@@ -209,6 +212,15 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     int64_t warps = (cells_per_tile * team + cta_cap - 1) / cta_cap;
     warps = (warps + team - 1) / team * team;
     warps = std::max<int64_t>(team, std::min<int64_t>(warps, MV_MAX_WARPS / team * team));
+    if (norm_w) {
+        // the fused RMSNorm runs in the register-staged prologue: one tile,
+        // bf16, 8-aligned, at most 16 elements per thread
+        if (vw->tile_count != 1 || vdtype != RSR_BF16 || (tn & 7) != 0 ||
+            ((uintptr_t)v & 15) != 0 || ((uintptr_t)norm_w & 15) != 0 || tn > 16 * 32 * MV_MAX_WARPS)
+            return RSR_ERR_INVALID;
+        const int64_t need = (tn + 511) / 512;
+        if (warps < need) warps = std::min<int64_t>((need + team - 1) / team * team, MV_MAX_WARPS);
+    }
     while (warps > team && fixed + warps * per_warp > smem_cap) warps -= team;
     if (fixed + warps * per_warp > smem_cap) return RSR_ERR_INVALID;
     const size_t smem = fixed + warps * per_warp;
@@ -299,6 +311,17 @@ rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtyp
         return launch_mv<MODE_FLOAT>(view, v, v_dtype, y, accumulate, 1.0, nullptr, workspace,
                                      workspace_bytes, s);
     return RSR_ERR_INVALID;
+}
+
+rsr_status rsr_fused_matvec_norm(const rsr_stream_view *view, const void *v, int32_t v_dtype,
+                                 const void *norm_w, float norm_eps, double beta,
+                                 const double *row_beta, void *out, int32_t out_dtype,
+                                 void *workspace, size_t workspace_bytes, rsr_stream_t stream) {
+    if (!norm_w || out_dtype != RSR_F32 && out_dtype != RSR_BF16) return RSR_ERR_INVALID;
+    if (view && view->bitwidth != RSR_TERNARY) return RSR_ERR_INVALID;
+    return launch_mv<MODE_FUSED>(view, v, v_dtype, out, 0, beta, nullptr, workspace,
+                                 workspace_bytes, (cudaStream_t)stream, row_beta,
+                                 out_dtype == RSR_BF16, (const uint16_t *)norm_w, norm_eps);
 }
 
 rsr_status rsr_fused_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtype,
@@ -462,15 +485,34 @@ rsr_status rsr_absmax_quantize(const void *v, int32_t v_dtype, int64_t n, int8_t
 // f32(f64(y) * (beta_i / scale_t)) per (row i, vector t) -- the fused
 // kernel's epilogue, so every row equals the single-vector fused result.
 namespace rsr {
+// element i of row vr, through the fused RMSNorm when norm_w is set (bf16 rows)
+__device__ __forceinline__ float row_elem(const char *vr, int dtype, int64_t i,
+                                          const uint16_t *norm_w, float rs) {
+    const float x = load_as_f32(vr, dtype, i);
+    if (!norm_w) return x;
+    const float nx = __bfloat162float(__float2bfloat16_rn(x * rs));
+    return __bfloat162float(__float2bfloat16_rn(bf16_bits_to_f32(__ldg(norm_w + i)) * nx));
+}
+
 __global__ void absmax_quantize_rows_kernel(const void *V, int dtype, int64_t ldv, int64_t n,
-                                            int8_t *Q, int64_t ldq, double *scales) {
+                                            int8_t *Q, int64_t ldq, double *scales,
+                                            const uint16_t *norm_w, float norm_eps) {
     __shared__ double red[32];
     const int64_t row = blockIdx.x;
     const char *vr = reinterpret_cast<const char *>(V) +
                      row * ldv * (dtype == RSR_F32 ? 4 : 2);
+    float rs = 0.f;
+    if (norm_w) {
+        float ss = 0.f;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const float x = load_as_f32(vr, dtype, i);
+            ss += x * x;
+        }
+        rs = rsqrtf(cta_reduce_sum_f32(ss) * (1.0f / (float)n) + norm_eps);
+    }
     double a = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double x = fabs((double)load_as_f32(vr, dtype, i));
+        const double x = fabs((double)row_elem(vr, dtype, i, norm_w, rs));
         a = x > a ? x : a;
     }
 #pragma unroll
@@ -485,7 +527,7 @@ __global__ void absmax_quantize_rows_kernel(const void *V, int dtype, int64_t ld
     const double scale = a == 0.0 ? 1.0 : 127.0 / a;
     if (threadIdx.x == 0) scales[row] = scale;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        Q[row * ldq + i] = quantize_one(load_as_f32(vr, dtype, i), scale);
+        Q[row * ldq + i] = quantize_one(row_elem(vr, dtype, i, norm_w, rs), scale);
 }
 
 __global__ void dequant_rows_kernel(const int32_t *Y, int64_t ldy, int64_t rows, int64_t m,
@@ -506,13 +548,14 @@ __global__ void dequant_rows_kernel(const int32_t *Y, int64_t ldy, int64_t rows,
 extern "C" {
 
 rsr_status rsr_absmax_quantize_rows(const void *V, int32_t v_dtype, int64_t ldv, int64_t rows,
-                                    int64_t n, int8_t *Q, int64_t ldq, double *scales,
-                                    rsr_stream_t stream) {
+                                    int64_t n, const void *norm_w, float norm_eps, int8_t *Q,
+                                    int64_t ldq, double *scales, rsr_stream_t stream) {
     if (!V || !Q || !scales || rows < 0 || n < 1 || ldv < n || ldq < n) return RSR_ERR_INVALID;
     if (v_dtype != RSR_F32 && v_dtype != RSR_BF16 && v_dtype != RSR_F16) return RSR_ERR_INVALID;
+    if (norm_w && v_dtype != RSR_BF16) return RSR_ERR_INVALID;
     if (rows == 0) return RSR_OK;
     absmax_quantize_rows_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
-        V, v_dtype, ldv, n, Q, ldq, scales);
+        V, v_dtype, ldv, n, Q, ldq, scales, (const uint16_t *)norm_w, norm_eps);
     return launch_status();
 }
 
@@ -530,3 +573,35 @@ rsr_status rsr_dequant_rows(const int32_t *Y, int64_t ldy, int64_t rows, int64_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Standalone fused RMSNorm (one launch per norm), the same arithmetic as the
+// prologue of rsr_fused_matvec_norm: used for the dense comparison arm of the
+// decode benchmark so both arms run their norms as single kernels.
+namespace rsr {
+__global__ void rmsnorm_rows_kernel(const uint16_t *x, const uint16_t *w, int64_t n, float eps,
+                                    uint16_t *out) {
+    const int64_t row = blockIdx.x;
+    const uint16_t *xr = x + row * n;
+    float ss = 0.f;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const float v = bf16_bits_to_f32(xr[i]);
+        ss += v * v;
+    }
+    const float rs = rsqrtf(cta_reduce_sum_f32(ss) * (1.0f / (float)n) + eps);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const float nx = __bfloat162float(__float2bfloat16_rn(bf16_bits_to_f32(xr[i]) * rs));
+        out[row * n + i] =
+            __bfloat16_as_ushort(__float2bfloat16_rn(bf16_bits_to_f32(w[i]) * nx));
+    }
+}
+}  // namespace rsr
+
+extern "C" rsr_status rsr_rmsnorm_rows(const void *x, const void *w, int64_t rows, int64_t n,
+                                       float eps, void *out, rsr_stream_t stream) {
+    if (!x || !w || !out || rows < 0 || n < 1) return RSR_ERR_INVALID;
+    if (rows == 0) return RSR_OK;
+    rsr::rmsnorm_rows_kernel<<<(unsigned)rows, 512, 0, (cudaStream_t)stream>>>(
+        (const uint16_t *)x, (const uint16_t *)w, n, eps, (uint16_t *)out);
+    return rsr::launch_status();
+}

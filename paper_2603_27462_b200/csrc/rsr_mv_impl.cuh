@@ -92,7 +92,41 @@ struct MvParams {
     const double *row_beta;  // fused: per-row beta (sibling stacks), or null
     int out_bf16;        // fused: write bf16 instead of f32
     unsigned long long *probe;  // debug timeline (rsr_debug_set_probe), null in production
+    const uint16_t *norm_w;  // fused: RMSNorm weight (bf16, n) applied before quantizing, or null
+    float norm_eps;
 };
+
+// CTA-wide sum of one float per thread, fixed order (identical in every CTA
+// of the same shape); the result is broadcast to every thread.
+__device__ __forceinline__ float cta_reduce_sum_f32(float a) {
+    __shared__ float red_s[32];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) a += __shfl_xor_sync(RSR_FULL_MASK, a, d);
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red_s[warp] = a;
+    __syncthreads();
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red_s[w];
+    __syncthreads();
+    return t;
+}
+
+// HF BitNetRMSNorm on eight bf16 values packed in a uint4 (in place):
+// bf16(w * bf16(x * rs)), each product in fp32 as torch computes it.
+__device__ __forceinline__ void rmsnorm8(uint4 &r, const uint4 &w8, float rs) {
+    uint32_t *x = reinterpret_cast<uint32_t *>(&r);
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(&w8);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float lo = __uint_as_float(x[q] << 16), hi = __uint_as_float(x[q] & 0xFFFF0000u);
+        const float wl = __uint_as_float(w[q] << 16), wh = __uint_as_float(w[q] & 0xFFFF0000u);
+        const float nl = __bfloat162float(__float2bfloat16_rn(lo * rs));
+        const float nh = __bfloat162float(__float2bfloat16_rn(hi * rs));
+        const uint32_t ol = __bfloat16_as_ushort(__float2bfloat16_rn(wl * nl));
+        const uint32_t oh = __bfloat16_as_ushort(__float2bfloat16_rn(wh * nh));
+        x[q] = ol | (oh << 16);
+    }
+}
 
 __device__ __forceinline__ float load_as_f32(const void *v, int dtype, int64_t i) {
     switch (dtype) {

@@ -354,6 +354,32 @@ rsr_mv_kernel(MvParams p) {
                 const int64_t i = threadIdx.x + u * nt;
                 r[u] = i < nvec ? __ldg(reinterpret_cast<const uint4 *>(p.v) + i)
                                 : make_uint4(0, 0, 0, 0);
+            }
+            if (p.norm_w) {
+                // fused RMSNorm (BitLinear): mean of squares in fp32 over the
+                // whole vector, then bf16(w * bf16(x * rsqrt(mean + eps)))
+                float ss = 0.f;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t w4[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float lo = __uint_as_float(w4[q] << 16);
+                        const float hi = __uint_as_float(w4[q] & 0xFFFF0000u);
+                        ss += lo * lo;
+                        ss += hi * hi;
+                    }
+                }
+                const float tot = cta_reduce_sum_f32(ss);
+                const float rs = rsqrtf(tot * (1.0f / (float)tn) + p.norm_eps);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int64_t i = threadIdx.x + u * nt;
+                    if (i < nvec) rmsnorm8(r[u], __ldg(reinterpret_cast<const uint4 *>(p.norm_w) + i), rs);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
                 const uint32_t w4[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {

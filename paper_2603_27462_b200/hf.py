@@ -21,15 +21,29 @@ import torch
 from torch import nn
 
 from .devicepack import ternarize_pack_device
-from .kernels import batched_preprocess, fused_into, fused_rows_into
+from .kernels import batched_preprocess, fused_into, fused_norm_into, fused_rows_into
 
 DEFAULT_K = 5  # fewest artifact bytes for BitNet-2B shapes
 
 
-class RSRSiblingGroup:
-    """One stacked artifact for linears that share an input."""
+def rms_norm_reference(x: torch.Tensor, weight: torch.Tensor, eps: float) -> torch.Tensor:
+    """HF BitNetRMSNorm / LlamaRMSNorm arithmetic (fp32 mean of squares,
+    x * rsqrt(mean + eps) rounded to the input dtype, times the weight)."""
+    h = x.to(torch.float32)
+    h = h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + eps)
+    return weight * h.to(x.dtype)
 
-    def __init__(self, weights: list, k: int = DEFAULT_K, out_dtype=torch.bfloat16):
+
+class RSRSiblingGroup:
+    """One stacked artifact for linears that share an input.
+
+    With `norm` (an RMSNorm module whose output feeds only these linears)
+    the group is a BitLinear: the norm runs inside the fused kernel's
+    prologue (rsr_fused_matvec_norm) and the caller replaces the norm module
+    by an identity.  Shapes the fused prologue cannot take fall back to the
+    norm in torch followed by the plain fused kernel."""
+
+    def __init__(self, weights: list, k: int = DEFAULT_K, out_dtype=torch.bfloat16, norm=None):
         dev = weights[0].device
         mats = [ternarize_pack_device(w) for w in weights]
         self.artifact, self.offsets = batched_preprocess(mats, k)
@@ -41,6 +55,13 @@ class RSRSiblingGroup:
         self.out_features = self.offsets[-1]
         self.out_dtype = out_dtype
         self.k = k
+        self.norm_w = None if norm is None else \
+            norm.weight.data.to(device=dev, dtype=torch.bfloat16).contiguous()
+        self.norm_eps = 0.0 if norm is None else float(norm.variance_epsilon)
+        # the fused kernel's register-staged prologue: one tile, n % 8 == 0,
+        # at most 16 elements per thread of a 20-warp CTA
+        self.norm_in_kernel = (self.in_features % 8 == 0 and self.in_features <= 10240
+                               and self.artifact.plan.tile_count == 1)
         self._out = None
         self._key = None
         self._pending: set = set()
@@ -52,10 +73,22 @@ class RSRSiblingGroup:
         dequantized together -- each row bit-identical to the one-token path."""
         T = x2.shape[0]
         out = torch.empty(T, self.out_features, dtype=self.out_dtype, device=x2.device)
+        if self.norm_w is not None and x2.dtype != torch.bfloat16:
+            x2 = rms_norm_reference(x2, self.norm_w.to(x2.dtype), self.norm_eps)
+            norm = None
+        else:
+            norm = self.norm_w
         if T == 1:
+            if norm is not None and self.norm_in_kernel:
+                fused_norm_into(self.artifact, x2[0], out[0], norm, self.norm_eps, beta=1.0,
+                                row_beta=self.row_beta)
+                return out
+            if norm is not None:
+                x2 = rms_norm_reference(x2, norm, self.norm_eps)
             fused_into(self.artifact, x2[0], out[0], beta=1.0, row_beta=self.row_beta)
         elif T > 1:
-            fused_rows_into(self.artifact, x2, out, beta=1.0, row_beta=self.row_beta)
+            fused_rows_into(self.artifact, x2, out, beta=1.0, row_beta=self.row_beta,
+                            norm_w=norm, norm_eps=self.norm_eps)
         return out
 
     def output_for(self, index: int, x2: torch.Tensor) -> torch.Tensor:
@@ -110,26 +143,116 @@ class RSRLinear(nn.Module):
 # sibling sets of the Llama/BitNet family (names under one parent module)
 DEFAULT_SIBLINGS = (("q_proj", "k_proj", "v_proj"), ("gate_proj", "up_proj"))
 
+# BitNet decoder layer: RMSNorms whose output feeds only the listed linears
+# (modeling_bitnet.py: BitNetDecoderLayer, BitNetAttention, BitNetMLP):
+# (norm owner path, norm name, linears' parent path, linear names)
+BITNET_NORMS = (("", "input_layernorm", "self_attn", ("q_proj", "k_proj", "v_proj")),
+                ("", "post_attention_layernorm", "mlp", ("gate_proj", "up_proj")),
+                ("self_attn", "attn_sub_norm", "self_attn", ("o_proj",)),
+                ("mlp", "ffn_sub_norm", "mlp", ("down_proj",)))
+
+
+def _sub(mod, path):
+    for part in [p for p in path.split(".") if p]:
+        mod = getattr(mod, part, None)
+        if mod is None:
+            return None
+    return mod
+
+
+def _norm_plan(model: nn.Module) -> dict:
+    """{id(linear parent): {linear names tuple: (norm owner, norm name, norm)}}
+    for every decoder layer that has the BitNet structure."""
+    plan = {}
+    for layer in model.modules():
+        if not (hasattr(layer, "input_layernorm") and hasattr(layer, "self_attn")
+                and hasattr(layer, "mlp")):
+            continue
+        for owner_path, norm_name, parent_path, names in BITNET_NORMS:
+            owner, parent = _sub(layer, owner_path), _sub(layer, parent_path)
+            norm = getattr(owner, norm_name, None) if owner is not None else None
+            if norm is None or parent is None or not hasattr(norm, "variance_epsilon"):
+                continue
+            if all(isinstance(getattr(parent, nm, None), nn.Linear) for nm in names):
+                plan.setdefault(id(parent), {})[names] = (owner, norm_name, norm)
+    return plan
+
+
+class FusedRMSNorm(nn.Module):
+    """An RMSNorm in one launch (rsr_rmsnorm_rows; the BitLinear prologue's
+    arithmetic) for bf16 activations -- the norm side of a like-for-like dense
+    comparison with fused-norm RSR layers.  Other dtypes use the torch form."""
+
+    def __init__(self, norm: nn.Module):
+        super().__init__()
+        self.weight = nn.Parameter(norm.weight.data.clone(), requires_grad=False)
+        self.variance_epsilon = float(norm.variance_epsilon)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        from . import _lib
+        if x.dtype != torch.bfloat16 or self.weight.dtype != torch.bfloat16:
+            return rms_norm_reference(x, self.weight, self.variance_epsilon)
+        x2 = x.reshape(-1, x.shape[-1]).contiguous()
+        out = torch.empty_like(x2)
+        _lib.check(_lib.lib().rsr_rmsnorm_rows(x2.data_ptr(), self.weight.data_ptr(), x2.shape[0],
+                                               x2.shape[1], self.variance_epsilon,
+                                               out.data_ptr(), _lib.current_stream_ptr(x.device)),
+                   "rmsnorm")
+        return out.view(x.shape)
+
+
+def fuse_rms_norms(model: nn.Module) -> int:
+    """Swap the BitNet decoder layers' RMSNorms (BITNET_NORMS) for
+    FusedRMSNorm; returns how many were swapped."""
+    count = 0
+    for layer in list(model.modules()):
+        if not (hasattr(layer, "input_layernorm") and hasattr(layer, "self_attn")):
+            continue
+        for owner_path, norm_name, _, _ in BITNET_NORMS:
+            owner = _sub(layer, owner_path)
+            norm = getattr(owner, norm_name, None) if owner is not None else None
+            if norm is not None and hasattr(norm, "variance_epsilon"):
+                setattr(owner, norm_name, FusedRMSNorm(norm))
+                count += 1
+    return count
+
 
 def replace_linear_with_rsr(model: nn.Module, k: int = DEFAULT_K, sibling_groups=DEFAULT_SIBLINGS,
-                            skip=("lm_head",), out_dtype=None) -> nn.Module:
+                            skip=("lm_head",), out_dtype=None, fuse_norms: bool = False) -> nn.Module:
     """Replace every bias-free nn.Linear (except `skip`) by an RSRLinear.
 
     Modeled on transformers' replace_with_bitnet_linear
     (transformers/integrations/bitnet.py:315-370).  Linears named in one
     tuple of `sibling_groups` under the same parent share a stacked artifact.
     The dense weights are released after conversion.
+
+    fuse_norms=True additionally turns each (RMSNorm -> linears) pair of a
+    BitNet decoder layer (BITNET_NORMS) into a BitLinear: the norm moves into
+    the linears' fused kernel and its module becomes nn.Identity.  Outputs
+    equal the unfused layer's up to the fp32 summation order of the norm's
+    mean of squares.
     """
     if out_dtype is None:
         out_dtype = next(model.parameters()).dtype
+    norms = _norm_plan(model) if fuse_norms else {}
+    to_identity = []
     converted = 0
     for parent in list(model.modules()):
         children = dict(parent.named_children())
+        pnorms = norms.get(id(parent), {})
         done = set()
+
+        def make_group(names):
+            hit = pnorms.get(tuple(names))
+            if hit is not None:
+                to_identity.append(hit[:2])
+            return RSRSiblingGroup([children[nm].weight.data for nm in names], k, out_dtype,
+                                   norm=None if hit is None else hit[2])
+
         for names in sibling_groups:
             if all(isinstance(children.get(nm), nn.Linear) and children[nm].bias is None
                    and nm not in skip for nm in names):
-                group = RSRSiblingGroup([children[nm].weight.data for nm in names], k, out_dtype)
+                group = make_group(names)
                 for i, nm in enumerate(names):
                     setattr(parent, nm, RSRLinear(group, i))
                     done.add(nm)
@@ -137,9 +260,12 @@ def replace_linear_with_rsr(model: nn.Module, k: int = DEFAULT_K, sibling_groups
         for nm, ch in children.items():
             if nm in done or nm in skip or not isinstance(ch, nn.Linear) or ch.bias is not None:
                 continue
-            group = RSRSiblingGroup([ch.weight.data], k, out_dtype)
+            group = make_group((nm,))
             setattr(parent, nm, RSRLinear(group, 0))
             converted += 1
+    for owner, norm_name in to_identity:
+        setattr(owner, norm_name, nn.Identity())
     model._rsr_converted = converted
+    model._rsr_fused_norms = len(to_identity)
     torch.cuda.empty_cache()
     return model

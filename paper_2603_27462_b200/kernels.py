@@ -173,13 +173,34 @@ def fused_into(a: RsrArtifact, vt, out, beta: float | None = None, view=None, st
     return out
 
 
+def fused_norm_into(a: RsrArtifact, vt, out, norm_w, norm_eps: float, beta: float | None = None,
+                    row_beta=None, stream=None):
+    """BitLinear in one launch: the fused kernel of the RMS-normalized bf16
+    vector (HF BitNetRMSNorm with weight norm_w and eps; rsr_fused_matvec_norm).
+    Raises CorruptArtifact (invalid argument) when the shape has no register-
+    staged prologue (several tiles, n % 8 != 0, n > 10240)."""
+    import torch
+    from .matcore import _dtype_code
+    st = _launch_state(a, None)
+    s = _lib.current_stream_ptr(a.device) if stream is None else stream
+    b = float(a.weight_scale) if beta is None else float(beta)
+    odt = _lib.RSR_BF16 if out.dtype == torch.bfloat16 else _lib.RSR_F32
+    ws, wsb = st.workspace(s) if st.wsb else (0, 0)
+    _lib.check(_lib.lib().rsr_fused_matvec_norm(st.ref, vt.data_ptr(), _dtype_code(vt),
+                                                norm_w.data_ptr(), float(norm_eps), b,
+                                                _lib.ptr(row_beta), out.data_ptr(), odt, ws, wsb,
+                                                s), "rsr_fused_matvec_norm")
+    return out
+
+
 def fused_rows_into(a: RsrArtifact, V, out, beta: float | None = None, row_beta=None,
-                    stream=None):
+                    stream=None, norm_w=None, norm_eps: float = 0.0):
     """The fused quantize/multiply/dequantize path for T activation rows at
     once (prefill): out[t] = rsr_matvec_fused(a, V[t]) bit for bit, computed
     as one per-row quantization launch, one batched exact int8 multiply
     (matmul_into) and one dequantization launch.  V: [T, n] f32/bf16/f16;
-    out: [T, m] float32 or bfloat16; row_beta as fused_into."""
+    out: [T, m] float32 or bfloat16; row_beta as fused_into; norm_w / norm_eps
+    as fused_norm_into (bf16 rows)."""
     import torch
     from .matcore import _dtype_code
     T = int(V.shape[0])
@@ -192,7 +213,8 @@ def fused_rows_into(a: RsrArtifact, V, out, beta: float | None = None, row_beta=
     Q = torch.empty(T, a.n, dtype=torch.int8, device=dev)
     scales = torch.empty(T, dtype=torch.float64, device=dev)
     _lib.check(L.rsr_absmax_quantize_rows(V.data_ptr(), _dtype_code(V), V.stride(0), T, a.n,
-                                          Q.data_ptr(), Q.stride(0), scales.data_ptr(), s),
+                                          _lib.ptr(norm_w), float(norm_eps), Q.data_ptr(),
+                                          Q.stride(0), scales.data_ptr(), s),
                "quantize rows")
     Y = torch.empty(T, a.m, dtype=torch.int32, device=dev)
     matmul_into(a, Q, Y, stream=s, method="stream")

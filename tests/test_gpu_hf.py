@@ -96,3 +96,71 @@ def test_prefill_rows_equal_single_token_path(torch_cuda, m, n, k, T):
             one = torch.empty(m, dtype=odt, device="cuda")
             kn.fused_into(a, X[t], one, beta=1.0, row_beta=row_beta)
             assert torch.equal(out[t], one), (odt, t)
+
+
+@pytest.mark.parametrize("n,T", [(2560, 1), (6912, 1), (2560, 5), (1000, 1)])
+def test_bitlinear_fused_norm_matches_norm_then_linear(torch_cuda, n, T):
+    """A sibling group with the RMSNorm fused into its kernel (BitLinear)
+    equals HF's norm followed by the plain group, except where the fp32 mean
+    of squares rounds differently (a fixed-order sum vs torch's reduction),
+    which can move a bf16 value by one ulp."""
+    torch = torch_cuda
+    from paper_2603_27462_b200.hf import RSRSiblingGroup, rms_norm_reference
+    norm = torch.nn.Module()
+    norm.weight = torch.nn.Parameter((torch.rand(n, device="cuda") + 0.5).to(torch.bfloat16))
+    norm.variance_epsilon = 1e-6
+    ws = [torch.randn(r, n, device="cuda", dtype=torch.bfloat16) * 0.02 for r in (320, 64)]
+    fused = RSRSiblingGroup(ws, k=5, out_dtype=torch.float32, norm=norm)
+    plain = RSRSiblingGroup(ws, k=5, out_dtype=torch.float32)
+    same = total = 0
+    for trial in range(8):
+        x = (torch.randn(T, n, device="cuda") * (trial + 1)).to(torch.bfloat16)
+        a = fused.compute(x)
+        b = plain.compute(rms_norm_reference(x, norm.weight.data, 1e-6))
+        same += int((a == b).sum())
+        total += a.numel()
+        rel = ((a - b).abs() / b.abs().clamp_min(1e-3)).max().item()
+        assert rel < 0.05, rel
+    assert same >= 0.98 * total, (same, total)
+    assert fused.norm_in_kernel == (n % 8 == 0)
+
+
+def test_bitlinear_small_bitnet_decode_tokens(torch_cuda):
+    torch = torch_cuda
+    from transformers import BitNetConfig, BitNetForCausalLM
+    from paper_2603_27462_b200.decode import GraphDecoder
+    from paper_2603_27462_b200.hf import replace_linear_with_rsr
+    torch.manual_seed(1)
+    cfg = BitNetConfig(hidden_size=256, intermediate_size=512, num_hidden_layers=2,
+                       num_attention_heads=4, num_key_value_heads=2, vocab_size=500)
+    cfg._attn_implementation = "sdpa"
+    with torch.device("cuda"):
+        base = BitNetForCausalLM(cfg).to(torch.bfloat16).eval()
+    import copy
+    a = replace_linear_with_rsr(copy.deepcopy(base), k=5)
+    b = replace_linear_with_rsr(copy.deepcopy(base), k=5, fuse_norms=True)
+    assert b._rsr_fused_norms == 8 and isinstance(b.model.layers[0].input_layernorm,
+                                                   torch.nn.Identity)
+    prompt = torch.randint(0, cfg.vocab_size, (1, 8), device="cuda")
+    toks = []
+    for mdl in (a, b):
+        dec = GraphDecoder(mdl, max_len=40)
+        dec.prefill(prompt)
+        dec.capture()
+        toks.append(dec.generate(prompt, 12)[0])
+    agree = sum(x == y for x, y in zip(*toks))
+    assert agree >= 10, toks
+
+
+def test_fused_rmsnorm_module_matches_hf_norm(torch_cuda):
+    torch = torch_cuda
+    from paper_2603_27462_b200.hf import FusedRMSNorm, rms_norm_reference
+    norm = torch.nn.Module()
+    norm.weight = torch.nn.Parameter((torch.rand(2560, device="cuda") + 0.5).to(torch.bfloat16))
+    norm.variance_epsilon = 1e-6
+    f = FusedRMSNorm(norm)
+    x = (torch.randn(3, 2560, device="cuda") * 4).to(torch.bfloat16)
+    a, b = f(x), rms_norm_reference(x, norm.weight.data, 1e-6)
+    assert a.shape == b.shape and a.dtype == torch.bfloat16
+    assert (a == b).float().mean().item() > 0.99
+    assert torch.allclose(a.float(), b.float(), rtol=1e-2, atol=1e-2)
