@@ -263,10 +263,18 @@ int main(int argc, char **argv) {
                         int qi[64], qh = 0, qt = 0; qi[qt++] = i0;
                         int parent_lane[32]; for (int b = 0; b < 32; ++b) parent_lane[b] = -1;
                         int endb = -1;
-                        if (PREFER) {  // a free bank first, the pool's most abundant one
+                        if (PREFER == 1) {  // a free bank first, the pool's most abundant one
                             int bb = -1, bc = 0;
                             for (int b = 0; b < 32; ++b)
                                 if (cntb[i0][b] > bc && bank_lane[b] < 0) { bc = cntb[i0][b]; bb = b; }
+                            if (bb >= 0) { vis[bb] = 1; parent_lane[bb] = i0; endb = bb; found = 1; }
+                        } else if (PREFER >= 2) {  // O(1): a free bank holding >= 2 columns, else any free
+                            int bb = -1;
+                            for (int pass = 0; pass < 2 && bb < 0; ++pass)
+                                for (int t = 0; t < 32; ++t) {
+                                    int b = (t + (PREFER == 3 ? 7 * i0 : 0)) & 31;
+                                    if (bank_lane[b] < 0 && cntb[i0][b] >= (pass == 0 ? 2 : 1)) { bb = b; break; }
+                                }
                             if (bb >= 0) { vis[bb] = 1; parent_lane[bb] = i0; endb = bb; found = 1; }
                         }
                         while (qh < qt && !found) {
