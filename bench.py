@@ -267,6 +267,50 @@ def cublas_bf16_bench(packed, m, n, v_bf16, hbm, rsr_value):
 
 
 # ---------------------------------------------------------------------------
+# single-vector side configs: C1 (binary 4096^2, f32 vector, k=8) and C5 on
+# one GPU (ternary 131072^2, 32704-wide tiles, device generator)
+
+def side_config_bench(cname: str, hbm: float):
+    import torch
+    import paper_2603_27462_b200 as rsr
+    from paper_2603_27462_b200 import kernels as kn
+    from paper_2603_27462_b200.devicepack import random_ternary_device
+    cfg = CONFIGS[cname]
+    m, n, k = cfg["m"], cfg["n"], cfg["k"]
+    if cfg["gen"] == "hash":
+        pm = random_ternary_device(m, n, 0, 0.5)
+    else:
+        pm = rsr.PackedMatrix(m, n, cfg["bitwidth"], random_packed(m, n, cfg["bitwidth"], 0))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a = rsr.preprocess(pm, k, cfg.get("tile_width"))
+    torch.cuda.synchronize()
+    pre_ms = 1e3 * (time.perf_counter() - t0)
+    del pm
+    v = torch.from_numpy(random_vector(n, 0)).cuda()
+    if cfg["vdtype"] == "bf16":
+        v = v.to(torch.bfloat16)
+    y = torch.empty(m, dtype=torch.float32, device="cuda")
+    sb = a.stream_bytes()
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    nc = int(max(1, min(4, -(-3 * l2 // max(sb, 1)))))
+    copies = [(a.entries_d, a.e_off_d)] + [(a.entries_d.clone(), a.e_off_d.clone())
+                                           for _ in range(nc - 1)]
+    views = [a.view(entries=e, e_off=o) for e, o in copies]
+    us = graph_time_us(lambda i: kn.matvec_into(a, v, y, view=views[i % nc]), copies=nc,
+                       iters=max(nc, 40 if sb < 1e9 else 8))
+    alg = (a.file_bytes() - 24) + n * (2 if cfg["vdtype"] == "bf16" else 4) + m * 4
+    out = {"workload": cfg["workload"], "k": k, "tile_width": a.plan.tile_width,
+           "format": a.format, "us": us, "matvec_s": 1e6 / us, "alg_bytes": int(alg),
+           "alg_gbs": alg / us / 1e3, "frac_hbm": alg / us / 1e3 / hbm,
+           "preprocess_ms": pre_ms,
+           "l2": f"{nc} rotated stream copies" if nc > 1 else "stream larger than L2"}
+    del copies, views, a
+    torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------
 # C4: batched multiply vs cuBLAS bf16 GEMM
 
 def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
@@ -640,7 +684,9 @@ def main():
         for name, fn in (("cublas_bf16", lambda: cublas_bf16_bench(full_packed, m, n, vt, hbm,
                                                                      value)
                           if full_packed is not None and cfg["vdtype"] == "bf16" else None),
-                         ("c4", c4_bench)):
+                         ("c4", c4_bench),
+                         ("c1", lambda: side_config_bench("c1", hbm)),
+                         ("c5_1gpu", lambda: side_config_bench("c5", hbm))):
             try:
                 extras[name] = fn()
             except Exception as e:  # reported, never silently replaced
