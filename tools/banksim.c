@@ -92,7 +92,9 @@ static double hung(int n, const double *a, int *assign) {
 
 static double W_MAX = 64.0;  // weight of raising an instruction's max load
 static int ALG = 0;
-static int PREFER = 0;           // 0: Hungarian coordinate descent, 1: pairwise swaps
+static int PREFER = 0;
+static int NOBFS = 0;
+static int NOORDER = 0;           // 0: Hungarian coordinate descent, 1: pairwise swaps
 
 static double inst_obj(int r, int s) {
     int *l = load + ((size_t)r * 32 + s) * NB;
@@ -129,6 +131,8 @@ int main(int argc, char **argv) {
     if (argc > 7) PADFREE = atoi(argv[7]);
     if (argc > 8) ALG = atoi(argv[8]);
     if (argc > 9) PREFER = atoi(argv[9]);
+    if (argc > 10) NOBFS = atoi(argv[10]);
+    if (argc > 11) NOORDER = atoi(argv[11]);
     int nk = 1;
     for (int i = 0; i < K; ++i) nk *= 3;
     for (int cell = 0; cell < cells; ++cell) {
@@ -247,7 +251,7 @@ int main(int argc, char **argv) {
                     // Kuhn: try augmenting from each lane (fewest options first)
                     int order[32];
                     for (int i = 0; i < nl; ++i) order[i] = i;
-                    for (int a = 0; a < nl; ++a) for (int b2 = a + 1; b2 < nl; ++b2) {
+                    for (int a = 0; a < (NOORDER ? 0 : nl); ++a) for (int b2 = a + 1; b2 < nl; ++b2) {
                         int da = 0, db = 0;
                         for (int b = 0; b < 32; ++b) { da += cntb[order[a]][b] > 0; db += cntb[order[b2]][b] > 0; }
                         if (db < da) { int t = order[a]; order[a] = order[b2]; order[b2] = t; }
@@ -277,7 +281,7 @@ int main(int argc, char **argv) {
                                 }
                             if (bb >= 0) { vis[bb] = 1; parent_lane[bb] = i0; endb = bb; found = 1; }
                         }
-                        while (qh < qt && !found) {
+                        while (!NOBFS && qh < qt && !found) {
                             int i = qi[qh++];
                             for (int pass = 0; pass < 2 && !found; ++pass)
                             for (int b = 0; b < 32; ++b) {
