@@ -198,13 +198,31 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     if (ring) per_warp += 16 * 4;  // team exchange
     const size_t smem_cap = 227 * 1024;
     const int64_t cells_per_tile = vw->n_blocks;
-    const int64_t cta_cap = std::max<int64_t>(1, sms / vw->tile_count);
+    static const int ctas_per_sm = getenv("RSR_MV_CTAS_PER_SM") ? atoi(getenv("RSR_MV_CTAS_PER_SM")) : 1;
+    const int64_t cta_cap = std::max<int64_t>(1, (int64_t)sms * ctas_per_sm / vw->tile_count);
     int team = 1;
     if (ring) {
         const int64_t est_rounds = std::max<int64_t>(1, (tn * 9 / 8 + 1023) / 1024);
         while (team < 8 && cells_per_tile * team * 2 <= cta_cap * MV_MAX_WARPS &&
                est_rounds >= 2 * team)
             team *= 2;
+        // More cells than one wave of warps: a team size that shortens the
+        // longest warp's share (makespan in cells, teams of t warps take 1/t
+        // of a cell each) -- e.g. 3277 cells on 2960 warps: 2 cells per warp
+        // alone, 1.25 with teams of 4.
+        if (cells_per_tile > cta_cap * MV_MAX_WARPS) {
+            double best = 1e30;
+            for (int t = 1; t <= 8 && est_rounds >= 2 * t; t *= 2) {
+                if (fixed + t * per_warp > smem_cap) break;
+                const int64_t slots = cta_cap * (MV_MAX_WARPS / t * t);
+                const double span = (double)((cells_per_tile * t + slots - 1) / slots) / t +
+                                    0.15 * (t - 1);  // measured cost of each extra member
+                if (span < best) {
+                    best = span;
+                    team = t;
+                }
+            }
+        }
         static const int force_team = getenv("RSR_MV_TEAM") ? atoi(getenv("RSR_MV_TEAM")) : 0;
         if (force_team > 0) team = force_team;  // experiment knob
         while (team > 1 && fixed + team * per_warp > smem_cap) team /= 2;
