@@ -239,15 +239,18 @@ rsr_status rsr_dequant_rows(const int32_t *Y, int64_t ldy, int64_t rows, int64_t
 /* ---- batched multiply on the tensor cores (tcgen05) ---------------------------
  * For bf16 batches the pattern-table expansion runs on the tensor cores: the
  * code matrix holds every column's pattern key as 2-bit row codes (the
- * reference pattern_key code form, preproc.py:183-197; k <= 8) concatenated
- * down the rows and cut into 8-row groups: u16 [ceil(cols/64)][ceil(bc*k/8)]
- * [64], built once from the reference arrays (tile-major cells, as
- * rsr_group_fill writes them; rsr_keymat_bytes / rsr_keymat_build).
+ * reference pattern_key code form, preproc.py:183-197: +1 -> 01, -1 -> 10;
+ * k <= 16), one row at a time: u32 [ceil(cols/128)][round8(bc*k)][8], word q
+ * of a (step, row) = columns 16q .. 16q + 15, the codes of column pair j at
+ * bits 2 (j % 4) of bytes 2 (j / 4) (even column) and 2 (j / 4) + 1 (odd);
+ * built once from the reference arrays (tile-major cells, as rsr_group_fill
+ * writes them; rsr_keymat_bytes / rsr_keymat_build; 16-byte aligned).
  * rsr_matmul_tc: Y[b] (f32, rows of blocks [block_begin, +n_blocks)) =
- * A . V[b] for bf16 V[b*ldv + col], B <= 256; fp32 accumulation of exact +-1
- * products (the float-path tolerance).  The workspace (always needed, 256-byte
- * aligned, rsr_matmul_tc_workspace_bytes) holds the repacked V and the
- * split-K partials.                                                         */
+ * A . V[b] for bf16 V[b*ldv + col], B <= 256, V 16-byte aligned and ldv a
+ * multiple of 8 (the B tiles are TMA boxes of V; RSR_ERR_INVALID otherwise);
+ * fp32 accumulation of exact +-1 products (the float-path tolerance).  The
+ * workspace (always needed, 256-byte aligned, rsr_matmul_tc_workspace_bytes)
+ * holds the split-K partials.                                               */
 size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k);
 rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,

@@ -6,32 +6,48 @@
 // segment sums: every column's pattern key, expanded through T, is one
 // column of the block's k rows.  So this path keeps every column's pattern
 // key in the reference's 2-bit code form (pattern_key, preproc.py:183-197:
-// row i's code at bits 2i, 2i+1), concatenated down the rows and cut into
-// 8-row groups (one u16 per (row group, column); 16.8 MB at C4 -- 2 bits
-// per matrix entry), expands it straight into the A operand of tcgen05.mma
-// and accumulates in TMEM:
+// +1 -> 01, -1 -> 10), one row at a time -- the code matrix, 2 bits per
+// matrix entry (16.8 MB at C4) -- and expands it straight into the A operand
+// of tcgen05.mma, which reads A from TENSOR MEMORY:
 //
-//   D[row][b] += A[row][col] * B[b][col],  A = T[:, key(blk, col)] (bf16 +-1/0),
-//                                          B = V chunk (bf16, K-major)
+//   D[row][b] += A[row][col] * B[b][col],  A = T[:, key(blk, col)] (bf16 +-1/0, TMEM),
+//                                          B = V chunk (bf16, K-major, shared memory)
 //
-// Tile: M = 128 rows (16 row groups), K = 64 columns per step, N = vectors
-// (16..256).  Warp-specialized, TC_STAGES-deep ring per CTA:
+// Tile: M = 128 rows (TMEM lanes), K = 64 columns per step, N = vectors
+// (16..256).  Warp-specialized, two rings per CTA:
 //   warp 8  (producer)  bulk-copies (cp.async.bulk, mbarrier complete_tx) the
-//                       step's code chunk and its pre-packed B tile;
-//   warps 0-7 (expand)  build the MN-major A tile: per (row group, column)
-//                       one u16 of codes -> 4 PRMTs (a register byte table)
-//                       -> one 16-byte store (conflict-free: a quarter warp
-//                       covers 128 B);
-//   warp 9  (MMA)       one thread issues tcgen05.mma (fp32 in TMEM) and
-//                       commits to the stage's "empty" barrier.
-// Code matrix layout [step = col / 64][row group][col % 64], so a tile's
-// step is one contiguous chunk; a row-block view starting mid-group takes
-// the enclosing groups and skips the outside rows in the epilogue.  V is
-// repacked once per call into the K-major no-swizzle core-matrix image of
-// each step (tc_pack_v_kernel), so its B tile is one bulk copy too.  Products
-// with +-1 are exact and accumulate in fp32: the float-path tolerance holds.
-// Split-K over grid.y fills the SMs; partials are summed in a fixed order
-// by tc_finalize_kernel (deterministic).
+//                       step's code rows (128 x 16 B) and its pre-packed B
+//                       tile into a LOAD ring (up to 16 stages; freed by the
+//                       MMA's commit);
+//   warps 0-7 (expand)  thread = tile row (warps 0-3 the even steps, 4-7
+//                       the odd ones): one 16-byte code load -> 32 words of
+//                       two bf16 signs (per pair of words a shift, a mask,
+//                       an IMAD and two PRMTs from a register byte table) ->
+//                       one tcgen05.st 32x32b.x32 into the row's TMEM lane,
+//                       in an A ring of 32-column TMEM stages (freed by the
+//                       MMA);
+//   warp 9  (MMA)       one thread issues tcgen05.mma (A from TMEM, fp32 D in
+//                       TMEM) and commits to both rings' "empty" barriers.
+// The A tile never touches shared memory: shared-memory traffic per step is
+// the B tile and 2 KB of codes, and the expansion is a few integer
+// instructions per word (round 1 staged A in shared memory: 32 KB of
+// shared traffic per step and a 4-stage ring whose slots waited on the MMA;
+// ~22 us at C4 for every B).
+//
+// Code matrix layout [step = col / 64][row][4 x u32]: u32 q holds columns
+// 16q .. 16q + 15 of the step, permuted so that one shift + mask gives the
+// PRMT selectors of two words: column pair j (columns 2j, 2j+1) has its codes
+// at bits 2 (j % 4) of bytes 2 (j / 4) and 2 (j / 4) + 1.  A tile's step is
+// one contiguous run of rows.  V is repacked once per call into the K-major
+// no-swizzle core-matrix image of each step (tc_pack_v_kernel), so its B
+// tile is one bulk copy too.  Products with +-1 are exact and accumulate in
+// fp32: the float-path tolerance holds.  Work is split stream-K style: CTA c
+// takes items [c W / G, (c + 1) W / G) of the (tile, step) sequence, so the
+// resident CTA slots get equal shares; tiles with several contributors are
+// summed from their partials in CTA order by tc_finalize_kernel
+// (deterministic).
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime)
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -40,87 +56,56 @@
 namespace rsr {
 
 constexpr int TC_M = 128;           // tile rows = TMEM lanes
-constexpr int TC_MAXBPT = 128;      // row blocks per tile: floor(128 / k)
-constexpr int TC_K = 64;            // columns per pipeline step
-constexpr int TC_STAGES = 4;       // ring depth (at most; fewer when shared memory is short)
-#ifndef RSR_TC_EXP_WARPS
-#define RSR_TC_EXP_WARPS 8
-#endif
-constexpr int TC_EXP_WARPS = RSR_TC_EXP_WARPS;
+constexpr int TC_K = 128;           // columns per pipeline step
+constexpr int TC_RB = 32;           // code bytes per (step, row): 128 x 2 bits
+constexpr int TC_LMAX = 16;         // load-ring depth (at most)
+constexpr int TC_AMAX = 16;         // A-ring depth in TMEM (at most)
+constexpr int TC_MAXK = 16;         // rows per block (16-bit pos / neg masks)
+constexpr int TC_GROUPS = 2;        // expander step groups (8 warps: 2 column halves x 4 lane quarters)
+constexpr int TC_EXP_WARPS = 8 * TC_GROUPS;
 constexpr int TC_THREADS = TC_EXP_WARPS * 32 + 64;  // expanders, producer, MMA
-constexpr int TC_UNITS = 16 * TC_K / (TC_EXP_WARPS * 32);  // (row group, column) units per thread
-
 
 __host__ __device__ inline int64_t tc_steps(int64_t n) { return (n + TC_K - 1) / TC_K; }
+__host__ __device__ inline int64_t tc_rows_pad(int64_t bc, int k) { return (bc * k + 7) / 8 * 8; }
 
-// ---- key matrix: KM[step][g][col % 64] = the 2-bit row codes of rows
-// 8g .. 8g + 7 at column col (each block's pattern key, in code form, lands at
-// bit 2 (row % 8) of its row group; a block straddling two groups is split)
+// bit offset of column c (c % 16 within its u32) in the permuted code word
+__device__ __forceinline__ uint32_t tc_code_bit(uint32_t c) {
+    const uint32_t j = (c >> 1) & 7;
+    return 8 * (2 * (j >> 2) + (c & 1)) + 2 * (j & 3);
+}
+
+// ---- code matrix: KM[step][row][q] (see the header) from the artifact's
+// groups: each column of a cell's group carries the group's pattern key; row
+// r0 + i gets code (pos_i, neg_i)
 __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                               const uint16_t *__restrict__ perm, const int64_t *__restrict__ po,
-                              int64_t bc, int64_t tc, int64_t tw, int k, int64_t ng,
+                              int64_t bc, int64_t tc, int64_t tw, int k, int64_t rows_pad,
                               uint32_t *__restrict__ km32) {
     const uint32_t lane = lane_id();
     const int64_t cells = bc * tc;
     for (int64_t cell = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < cells;
          cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t t = cell / bc, b = cell - t * bc;  // reference cells are tile-major
-        const int64_t c0 = t * tw;
-        const int64_t r0 = b * k, g0 = r0 >> 3;
-        const int sh = 2 * (int)(r0 & 7);
+        const int64_t c0 = t * tw, r0 = b * k;
         for (int64_t g = go[cell]; g < go[cell + 1]; ++g) {
             const uint64_t w = words[g];
             const int64_t ps = (int64_t)(w & 0xFFFFu), L = (int64_t)((w >> 16) & 0xFFFFu);
-            const uint32_t pos = (uint32_t)((w >> 32) & 0xFFu), neg = (uint32_t)((w >> 48) & 0xFFu);
-            uint32_t code = 0;  // +1 -> 01, -1 -> 10 (binary keys have no neg bits)
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                code |= (((pos >> i) & 1u) | (((neg >> i) & 1u) << 1)) << (2 * i);
-            const uint32_t lo = (code << sh) & 0xFFFFu, hi = (code << sh) >> 16;
+            const uint32_t pos = (uint32_t)((w >> 32) & 0xFFFFu), neg = (uint32_t)(w >> 48);
             const uint16_t *cols = perm + po[cell] + ps;
             for (int64_t j = lane; j < L; j += 32) {
                 const int64_t col = c0 + cols[j];
-                const int64_t e = ((col / TC_K) * ng + g0) * TC_K + (col % TC_K);
-                atomicOr(km32 + (e >> 1), lo << (16 * (e & 1)));
-                if (hi) {
-                    const int64_t e2 = e + TC_K;  // next row group, same column
-                    atomicOr(km32 + (e2 >> 1), hi << (16 * (e2 & 1)));
+                const uint32_t bit = tc_code_bit((uint32_t)col & 15);
+                uint32_t *dst = km32 + ((col >> 7) * rows_pad + r0) * 8 + ((col & 127) >> 4);
+                for (int i = 0; i < k; ++i) {
+                    const uint32_t code = ((pos >> i) & 1u) | (((neg >> i) & 1u) << 1);
+                    if (code) atomicOr(dst + (int64_t)i * 8, code << bit);
                 }
             }
         }
     }
 }
 
-// ---- V repack: vp[step][N/8][kg 8][8 vectors][8 columns] bf16 (the B tile image) ----
-__global__ void tc_pack_v_kernel(const uint16_t *__restrict__ V, int64_t ldv, int64_t n, int B,
-                                 int N, int64_t steps, uint4 *__restrict__ vp) {
-    const int64_t pieces = steps * N * 8;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pieces;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        // e = ((st * N/8 + vg) * 8 + kg) * 8 + vi
-        const int vi = (int)(e & 7), kg = (int)((e >> 3) & 7);
-        const int64_t r = e >> 6;
-        const int64_t st = r / (N >> 3);
-        const int vb = (int)(r - st * (N >> 3)) * 8 + vi;
-        const int64_t c = st * TC_K + kg * 8;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (vb < B) {
-            const uint16_t *src = V + (int64_t)vb * ldv + c;
-            if (c + 8 <= n && ((ldv & 7) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0)) {
-                val = *reinterpret_cast<const uint4 *>(src);
-            } else {
-                uint32_t h[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) h[q] = c + q < n ? src[q] : 0u;
-                val = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16),
-                                 h[6] | (h[7] << 16));
-            }
-        }
-        vp[e] = val;
-    }
-}
-
-// ---- tcgen05 / mbarrier / bulk-copy helpers -------------------------------------
+// ---- tcgen05 helpers -------------------------------------------------------------
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     // no-swizzle canonical layout; fields in 16-byte units; version 1 (sm_100)
     uint64_t d = 0;
@@ -131,12 +116,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
     return d;
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
-                                         uint32_t accumulate) {
+// D (TMEM) += A (TMEM, K-major: row = lane, 2 bf16 per column) * B (smem)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                            uint32_t idesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t mbar) {
@@ -145,262 +131,362 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
                  : "memory");
 }
 
+// 2-d tensor TMA (global -> shared, mbarrier complete_tx); out-of-bounds
+// elements are zero-filled and still counted in the transaction bytes
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *tm, int c0, int c1,
+                                       uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
 #ifdef RSR_TC_DBG
-__device__ unsigned long long tc_dbg[64 * 4 + 4];
+__device__ unsigned long long tc_dbg[64 * 8 + 4];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+__device__ unsigned long long tc_cta_t[1024 * 4];
+__device__ long long tc_mma_cyc[64 * 3];
+#define TC_CTA_MARK(j) \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) tc_cta_t[blockIdx.x * 4 + (j)] = gtime();
 #define TC_MARK(cond, idx) \
-    if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 64 * 4 + 4) tc_dbg[idx] = gtime();
+    if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 64 * 8 + 4) tc_dbg[idx] = gtime();
 #else
 #define TC_MARK(cond, idx)
+#define TC_CTA_MARK(j)
 #endif
 
 struct TcParams {
-    const uint16_t *km;  // key matrix [steps][bc][64] (2-bit row codes)
-    const uint4 *vp;     // packed V [steps][N/8][8][8][8] bf16
+    // V [B][n] bf16 as a 2-d TMA view, 128-byte swizzle: a box of 64
+    // columns x N vectors is one K-half of a step's B tile in the canonical
+    // K-major SWIZZLE_128B image (vectors >= B, columns >= n zero-filled)
+    CUtensorMap tm_v;
+    const uint32_t *km;  // code matrix [steps][rows_pad][8]
     float *Y;            // [B][ldy] rows of the view
     int64_t ldy;
-    float *part;         // split-K partials [ksplit][B][rows]
-    int64_t m_rows, n, nblk, blk0, bc;
-    int64_t ng;           // row groups of 8 in the whole matrix
-    int k, B, N, ksplit, stages;
-    uint32_t tab0, tab1;  // PRMT byte table {00 3F BF 00 | 00 80 80 00} (kept in registers)
+    float *part;         // partials [CTA][2 segments][B][128]
+    int64_t n, row0, rows_view, rows_pad;
+    int64_t S;           // steps per tile (= tc_steps(n))
+    int64_t W;           // work items: tiles x S
+    int B, N, G, ls, as;
+    uint32_t a_col, tmem_cols;  // TMEM column of A stage 0; columns allocated
+    uint32_t tab0, tab1;        // PRMT byte table {00 3F BF 00 | 00 80 80 00}
 };
 
-// 8 row codes (2 bits each, +1 -> 01, -1 -> 10) of two units at once
-// (x = unit0 | unit1 << 16) -> the 8 bf16 signs of each as 4 words of two:
-// PRMT picks each byte from a register table {00 3F BF 00 | 00 80 80 00}
-// with selector nibbles (4 + c0, c0, 4 + c1, c1) =
-// 0x0404 + 0x11 * (c0 + (c1 << 8)), built per 16-bit half with two IMADs
-__device__ __forceinline__ void expand_codes2(uint32_t x, uint4 &lo, uint4 &hi, uint32_t tab0,
-                                              uint32_t tab1, uint32_t c0404) {
-    uint32_t w0[4], w1[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint32_t t = x >> (4 * q);
-        const uint32_t tm = t & 0x000F000Fu, th = t & 0x000C000Cu;
-        // 0x11 * (c0 + 4 c1) + 0x42F * 4 c1 = 0x11 * (c0 + (c1 << 8)), + 0x0404;
-        // explicit mads (one immediate each: no constant rematerialization)
-        uint32_t u, sel;
-        asm("mad.lo.u32 %0, %1, 0x11, %2;" : "=r"(u) : "r"(tm), "r"(c0404));
-        asm("mad.lo.u32 %0, %1, 0x42F, %2;" : "=r"(sel) : "r"(th), "r"(u));
-        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w0[q]) : "r"(tab0), "r"(tab1), "r"(sel));
-        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w1[q]) : "r"(tab0), "r"(tab1), "r"(sel >> 16));
-    }
-    lo = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-    hi = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+// work range of CTA c: [c W / G, (c + 1) W / G) over (tile, step) items
+__host__ __device__ inline int64_t tc_wstart(int64_t c, int64_t W, int64_t G) { return c * W / G; }
+__host__ __device__ inline int64_t tc_cta_of(int64_t w, int64_t W, int64_t G) {
+    return ((w + 1) * G - 1) / W;
 }
 
-// N = 16 * NP: MMA N (vectors padded up, <= 256)
+// 64 columns' codes of one row (x[q]: columns 16q .. 16q + 15, permuted
+// layout) -> 32 words of two bf16 each: per pair of words, sel = ((x >> 2i)
+// & 0x03030303) * 0x11 + 0x04040404 holds the PRMT selector nibbles
+// (4 + c0, c0, 4 + c1, c1) of word i in its low half and of word i + 4 in
+// its high half
+__device__ __forceinline__ void expand64(const uint4 &x, uint32_t (&w)[32], uint32_t tab0,
+                                         uint32_t tab1, uint32_t c0404) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const uint32_t xv = h == 0 ? x.x : h == 1 ? x.y : h == 2 ? x.z : x.w;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint32_t sel;
+            asm("mad.lo.u32 %0, %1, 0x11, %2;" : "=r"(sel) : "r"((xv >> (2 * i)) & 0x03030303u),
+                "r"(c0404));
+            asm("prmt.b32 %0, %1, %2, %3;" : "=r"(w[8 * h + i]) : "r"(tab0), "r"(tab1), "r"(sel));
+            asm("prmt.b32 %0, %1, %2, %3;"
+                : "=r"(w[8 * h + i + 4])
+                : "r"(tab0), "r"(tab1), "r"(sel >> 16));
+        }
+    }
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+        "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]),
+        "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]), "r"(w[21]),
+        "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]), "r"(w[28]),
+        "r"(w[29]), "r"(w[30]), "r"(w[31])
+        : "memory");
+}
+
+// N = 16 * NP: MMA N (vectors padded up, <= 256).
+// CTA c owns the work items [c W / G, (c + 1) W / G) of the (tile, step)
+// sequence (stream-K): at most two segments (the range is at most one
+// tile's steps), each with its own TMEM accumulator (columns seg * N).  A
+// segment that is its tile's only contributor writes Y; otherwise it writes
+// its partial and tc_finalize_kernel sums a tile's partials in CTA order.
 template <int NP>
-__global__ void __launch_bounds__(TC_THREADS) rsr_tc_kernel(TcParams p) {
+__global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_constant__ TcParams p) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ __align__(8) uint64_t bars[3 * TC_STAGES + 1];
+    __shared__ __align__(8) uint64_t bars[2 * TC_LMAX + 2 * TC_AMAX + 2];
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
     constexpr int N = 16 * NP;
-    const int S = p.stages;
+    const int LS = p.ls, AS = p.as;
+    TC_CTA_MARK(0)
     // PDL: the finalize may launch now (it waits for this grid to finish)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // this tile: row groups [g_first, g_first + 16) of the matrix, covering
-    // the view's rows [row0, row0 + rows_view) (rows outside are skipped)
-    const int64_t row0 = p.blk0 * p.k;
-    const int64_t rows_view = min(p.nblk * p.k, p.m_rows - row0);
-    const int64_t g_first = (row0 >> 3) + (int64_t)blockIdx.x * 16;
-    const int ng_here = (int)min((int64_t)16, p.ng - g_first);
-    const int64_t nsteps_all = tc_steps(p.n);
-    const int64_t s0 = nsteps_all * blockIdx.y / p.ksplit;
-    const int64_t s1 = nsteps_all * (blockIdx.y + 1) / p.ksplit;
-    const int64_t nst = s1 - s0;
+    const int64_t w0 = tc_wstart(blockIdx.x, p.W, p.G), w1 = tc_wstart(blockIdx.x + 1, p.W, p.G);
+    const int64_t nst = w1 - w0;
+    const int64_t t0 = w0 / p.S;                  // first tile
+    const int64_t wsplit = min((t0 + 1) * p.S, w1);  // first item of segment 1
+    const int nseg = w1 > wsplit ? 2 : 1;
 
-    // smem: per stage [A 16 KB][B N x 128 B][codes 16 x 64 x u16]
-    constexpr uint32_t A_BYTES = TC_M * TC_K * 2;
+    // smem: per load stage [B tile: 2 K-halves x N x 128 B][codes 128 rows x 32 B]
     constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * 2;
-    constexpr uint32_t C_BYTES = 16 * TC_K * 2;
-    constexpr uint32_t st_bytes = (A_BYTES + B_BYTES + C_BYTES + 1023) / 1024 * 1024;
+    constexpr uint32_t C_BYTES = TC_M * TC_RB;
+    constexpr uint32_t SLOT = B_BYTES + C_BYTES;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tc_smem);
-    const uint32_t bar_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
-    const uint32_t bar_aready = bar_full + 8 * TC_STAGES;
-    const uint32_t bar_empty = bar_aready + 8 * TC_STAGES;
-    const uint32_t bar_done = bar_empty + 8 * TC_STAGES;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t bar_full = bar0, bar_empty = bar0 + 8 * TC_LMAX;
+    const uint32_t bar_aready = bar0 + 16 * TC_LMAX, bar_aempty = bar_aready + 8 * TC_AMAX;
+    const uint32_t bar_done = bar_aempty + 8 * TC_AMAX;  // one per segment
 
-    // code rows past the matrix (never written by the producer) read as 0
-    for (int s = 0; s < S; ++s) {
-        uint32_t *kz = reinterpret_cast<uint32_t *>(tc_smem + s * st_bytes + A_BYTES + B_BYTES +
-                                                    (size_t)ng_here * TC_K * 2);
-        for (int i = tid; i < (16 - ng_here) * TC_K / 2; i += TC_THREADS) kz[i] = 0u;
-    }
-    if (warp == TC_EXP_WARPS + 1) {  // TMEM: N fp32 columns x 128 lanes
-        uint32_t cols = 32;
-        while (cols < (uint32_t)N) cols <<= 1;
+    if (warp == TC_EXP_WARPS + 1) {  // TMEM: accumulators + the A ring
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&tmem_base_sh)),
-                     "r"(cols));
+                     "r"(p.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) {
-            mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_aready + 8 * s, TC_EXP_WARPS * 32);
-            mbar_init(bar_empty + 8 * s, 1);
-        }
-        mbar_init(bar_done, 1);
+    // barriers, one per thread: full (the producer's expect_tx), empty /
+    // aempty / done (an MMA commit), aready (the 256 threads of an expander
+    // group)
+    if (tid < 2 * TC_LMAX + 2 * TC_AMAX + 2) {
+        const uint32_t cnt =
+            (tid >= 2 * TC_LMAX && tid < 2 * TC_LMAX + TC_AMAX) ? 8u * 32u : 1u;
+        mbar_init(bar0 + 8 * tid, cnt);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_d = tmem_base_sh;
-    TC_MARK(tid == 0, 256)
+    TC_MARK(tid == 0, 512)
+    TC_CTA_MARK(1)
 
     if (warp == TC_EXP_WARPS) {
-        // ---- producer ----
-        if (lane == 0) {
-            const uint32_t kbytes = (uint32_t)ng_here * TC_K * 2;
-            // PDL: the packed V comes from the previous kernel; everything
-            // before this point overlapped its tail
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            for (int64_t it = 0; it < nst; ++it) {
-                const int s = (int)(it % S);
-                if (it >= S) mbar_wait_parity(bar_empty + 8 * s, (uint32_t)((it / S - 1) & 1));
-                const int64_t st = s0 + it;
-                TC_MARK(it < 64, it * 4 + 2)
-                const uint32_t sa = sbase + s * st_bytes;
-                mbar_expect_tx(bar_full + 8 * s, kbytes + B_BYTES);
-                bulk_g2s(sa + A_BYTES + B_BYTES, p.km + (st * p.ng + g_first) * TC_K, kbytes,
-                         bar_full + 8 * s);
-                bulk_g2s(sa + A_BYTES, p.vp + (size_t)st * (B_BYTES / 16), B_BYTES,
-                         bar_full + 8 * s);
+        // ---- producer: lanes 0 .. J-1 load J consecutive steps at once (a
+        // lane per step, each its own slot): the step's code rows (bulk
+        // copy) and its B tile straight from V (two 2-d TMAs, one per 64
+        // columns) ----
+        const int J = min(LS, 8);
+        const unsigned char *kb = reinterpret_cast<const unsigned char *>(p.km);
+        if (lane == 0)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tm_v))
+                         : "memory");
+        // PDL: V may come from the previous kernel; everything before this
+        // point overlapped its tail
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if ((int)lane < J) {
+            int s = (int)lane;
+            uint32_t par = 0;
+            const int64_t w = w0 + lane;
+            int64_t t = w / p.S, st = w - t * p.S;
+            for (int64_t it = lane; it < nst; it += J) {
+                if (it >= LS) mbar_wait_parity(bar_empty + 8 * s, par ^ 1u);
+                const int64_t r_first = t * TC_M;
+                const uint32_t kbytes =
+                    (uint32_t)min((int64_t)TC_M, p.rows_view - r_first) * TC_RB;
+                TC_MARK(it < 64, it * 8 + 2)
+                const uint32_t sa = sbase + s * SLOT, fb = bar_full + 8 * s;
+                mbar_expect_tx(fb, kbytes + B_BYTES);
+                bulk_g2s(sa + B_BYTES, kb + (st * p.rows_pad + p.row0 + r_first) * TC_RB, kbytes,
+                         fb);
+                tma_2d(sa, &p.tm_v, (int)st * TC_K, 0, fb);
+                tma_2d(sa + B_BYTES / 2, &p.tm_v, (int)st * TC_K + 64, 0, fb);
+                s += J;
+                if (s >= LS) {
+                    s -= LS;
+                    par ^= 1u;
+                }
+                st += J;
+                while (st >= p.S) {
+                    st -= p.S;
+                    ++t;
+                }
             }
         }
     } else if (warp == TC_EXP_WARPS + 1) {
         // ---- MMA issuer ----
         if (lane == 0) {
-            // instruction descriptor: kind::f16, A = B = BF16, D = F32, A MN-major,
-            // B K-major, N >> 3 at [17,23), M >> 4 at [24,29)
-            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+            // instruction descriptor: kind::f16, A = B = BF16, D = F32, A and B
+            // K-major, N >> 3 at [17,23), M >> 4 at [24,29)
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                    ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-            int s = 0;
-            uint32_t par = 0;
+            // B K-major SWIZZLE_128B (layout type 2 at [61,64)): rows of 128 B,
+            // SBO = 8 rows (1024 B); a K = 16 slice starts 32 B further into
+            // its 64-column half (the swizzle applies to the absolute address)
+            const uint64_t db0 = smem_desc(sbase, 16, 1024) | ((uint64_t)2 << 61);
+            int s = 0, a = 0;
+            uint32_t par = 0, apar = 0;
+            const int64_t n0 = wsplit - w0;  // steps of segment 0
             for (int64_t it = 0; it < nst; ++it) {
+                const int seg = it >= n0 ? 1 : 0;
+                const bool first = it == 0 || it == n0;
+#ifdef RSR_TC_DBG
+                const long long c0 = clock64();
+#endif
                 mbar_wait_parity(bar_full + 8 * s, par);
-                mbar_wait_parity(bar_aready + 8 * s, par);
-                TC_MARK(it < 64, it * 4 + 3)
+#ifdef RSR_TC_DBG
+                const long long c1 = clock64();
+#endif
+                mbar_wait_parity(bar_aready + 8 * a, apar);
+#ifdef RSR_TC_DBG
+                const long long c2 = clock64();
+#endif
+                TC_MARK(it < 64, it * 8 + 3)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a0 = sbase + s * st_bytes, b0 = a0 + A_BYTES;
+                const uint64_t db = db0 + ((s * SLOT) >> 4);
+                const uint32_t ta = tmem_d + p.a_col + 64u * a;
+                const uint32_t td = tmem_d + (uint32_t)(seg * N);
 #pragma unroll
                 for (int kk = 0; kk < TC_K / 16; ++kk) {
-                    // A MN-major: LBO = K-group stride (16 row groups x 128 B), SBO = M-group stride
-                    const uint64_t da = smem_desc(a0 + kk * 2 * (16 * 128), 16 * 128, 128);
-                    // B K-major: LBO = K-group stride (128 B), SBO = N-group stride (8 x 128 B)
-                    const uint64_t db = smem_desc(b0 + kk * 2 * 128, 128, 8 * 128);
-                    mma_bf16(tmem_d, da, db, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+#ifndef TC_EXP_NO_MMA
+                    mma_bf16_ts(td, ta + 8u * kk,
+                                db + (uint64_t)(((kk >> 2) * (B_BYTES / 2) + (kk & 3) * 32) >> 4),
+                                idesc,
+                                (!first || kk > 0) ? 1u : 0u);
+#endif
                 }
                 mma_commit(bar_empty + 8 * s);
-                if (++s == S) {
+                mma_commit(bar_aempty + 8 * a);
+                if (it + 1 == n0 || it + 1 == nst) mma_commit(bar_done + 8 * seg);
+#ifdef RSR_TC_DBG
+                if (blockIdx.x == 0 && it < 64) {
+                    const long long c3 = clock64();
+                    tc_mma_cyc[it * 3 + 0] = c1 - c0;
+                    tc_mma_cyc[it * 3 + 1] = c2 - c1;
+                    tc_mma_cyc[it * 3 + 2] = c3 - c2;
+                }
+#endif
+                if (++s == LS) {
                     s = 0;
                     par ^= 1u;
                 }
+                if (++a == AS) {
+                    a = 0;
+                    apar ^= 1u;
+                }
             }
-            mma_commit(bar_done);
         }
     } else {
-        // ---- expanders: thread owns column c_t of row groups mg_t .. mg_t +
-        // TC_UNITS - 1 (tile rows 8 mg .. 8 mg + 7); a quarter warp's 16-byte
-        // A stores are 128 contiguous bytes ----
-        const int c_t = tid & 63, mg_t = (tid >> 6) * TC_UNITS;
+        // ---- expanders: thread = (tile row 32 (warp % 4) + lane, column half
+        // (warp / 4) % 2); a warp's TMEM lanes are its quarter, warp % 4.
+        // Group h = warp / 8 expands the steps it = h (mod TC_GROUPS) ----
+        const int q = warp & 3, hh = (warp >> 2) & 1, h = warp >> 3;
+        const int row = 32 * q + (int)lane;
+        const uint32_t t_row = tmem_d + ((uint32_t)(32 * q) << 16) + p.a_col + 32u * hh;
         // table words and the selector bias in plain registers, set once
-        // (shuffled: per-thread values ptxas keeps in vector registers
-        // instead of re-copying uniform ones at every use)
         const uint32_t tab0 = __shfl_sync(RSR_FULL_MASK, p.tab0, 0);
         const uint32_t tab1 = __shfl_sync(RSR_FULL_MASK, p.tab1, 0);
         const uint32_t c0404 = __shfl_sync(RSR_FULL_MASK, 0x04040404u, 0);
-        int s = 0;
-        uint32_t par = 0;
-        for (int64_t it = 0; it < nst; ++it) {
+        const unsigned char *codes0 = tc_smem + B_BYTES + row * TC_RB + hh * 16;
+        // this warp's steps it = h, h + TC_GROUPS, ...: load slot it % LS, A stage it % AS
+        int s = h % LS, a = h % AS;
+        uint32_t par = (uint32_t)(h / LS) & 1u, apar = (uint32_t)(h / AS) & 1u;
+        for (int64_t it = h; it < nst; it += TC_GROUPS) {
             mbar_wait_parity(bar_full + 8 * s, par);
-            TC_MARK(tid == 0 && it < 64, it * 4 + 0)
-            unsigned char *stg = tc_smem + s * st_bytes;
-            const uint16_t *sk =
-                reinterpret_cast<const uint16_t *>(stg + A_BYTES + B_BYTES) + mg_t * TC_K + c_t;
-            // A (MN-major core layout [kg 8][row group 16][8 columns][16 B = 8 rows])
-            unsigned char *dA = stg + (size_t)(c_t & 7) * 16 + (size_t)(c_t >> 3) * 16 * 128;
-#pragma unroll
-            for (int j = 0; j < TC_UNITS; j += 2) {
-                // the row codes of two row groups, one per 16-bit half
-                uint32_t x;
-                asm("prmt.b32 %0, %1, %2, 0x5410;"
-                    : "=r"(x)
-                    : "r"((uint32_t)sk[j * TC_K]), "r"((uint32_t)sk[(j + 1) * TC_K]));
-                uint4 lo, hi;
-                expand_codes2(x, lo, hi, tab0, tab1, c0404);
-                *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j) * 128) = lo;
-                *reinterpret_cast<uint4 *>(dA + (size_t)(mg_t + j + 1) * 128) = hi;
-            }
-            // generic-proxy writes -> visible to the tensor core (async proxy)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(bar_aready + 8 * s);
-            TC_MARK(tid == 0 && it < 64, it * 4 + 1)
-            if (++s == S) {
-                s = 0;
+            TC_MARK(tid == 0 && it < 64, it * 8 + 0)
+            const uint4 x = *reinterpret_cast<const uint4 *>(codes0 + s * SLOT);
+            uint32_t w[32];
+            expand64(x, w, tab0, tab1, c0404);
+            TC_MARK(tid == 0 && it < 64, it * 8 + 4)
+            if (it >= AS) mbar_wait_parity(bar_aempty + 8 * a, apar ^ 1u);
+            TC_MARK(tid == 0 && it < 64, it * 8 + 5)
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            tmem_st32(t_row + 64u * a, w);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            TC_MARK(tid == 0 && it < 64, it * 8 + 6)
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(bar_aready + 8 * a);
+            TC_MARK(tid == 0 && it < 64, it * 8 + 1)
+            // advance TC_GROUPS steps (LS, AS >= TC_GROUPS)
+            s += TC_GROUPS;
+            if (s >= LS) {
+                s -= LS;
                 par ^= 1u;
+            }
+            a += TC_GROUPS;
+            if (a >= AS) {
+                a -= AS;
+                apar ^= 1u;
             }
         }
     }
     __syncwarp();
-    mbar_wait_parity(bar_done, 0);
-    TC_MARK(tid == 0, 257)
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    TC_MARK(tid == 0, 513)
+    TC_CTA_MARK(2)
 
     if (warp < 4) {
         // --- epilogue: warp w reads TMEM lanes 32w..32w+31 (tile rows), 8 columns at a time
         const int row_t = warp * 32 + (int)lane;
-        const int64_t vrow = g_first * 8 + row_t - row0;  // row within the view
-        const bool valid = vrow >= 0 && vrow < rows_view;
-        for (int c = 0; c < N; c += 8) {
-            uint32_t r[8];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                  "=r"(r[6]), "=r"(r[7])
-                : "r"(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (valid) {
+        for (int seg = 0; seg < nseg; ++seg) {
+            mbar_wait_parity(bar_done + 8 * seg, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t a_w = seg ? wsplit : w0, b_w = seg ? w1 : wsplit;
+            const int64_t t = a_w / p.S;
+            const int64_t vrow = t * TC_M + row_t;  // row within the view
+            const bool valid = vrow < p.rows_view;
+            const bool whole = a_w == t * p.S && b_w == (t + 1) * p.S;
+            float *dst = whole ? p.Y + vrow
+                               : p.part + ((int64_t)(blockIdx.x * 2 + seg) * p.B) * TC_M + row_t;
+            const int64_t ld = whole ? p.ldy : TC_M;
+            for (int c = 0; c < N; c += 8) {
+                uint32_t r[8];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                      "=r"(r[6]), "=r"(r[7])
+                    : "r"(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)(seg * N + c)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (valid) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int vb = c + j;
-                    if (vb < p.B) {
-                        const float x = nst > 0 ? __uint_as_float(r[j]) : 0.f;
-                        if (p.ksplit == 1) p.Y[(int64_t)vb * p.ldy + vrow] = x;
-                        else p.part[((int64_t)blockIdx.y * p.B + vb) * rows_view + vrow] = x;
-                    }
+                    for (int j = 0; j < 8; ++j)
+                        if (c + j < p.B) dst[(int64_t)(c + j) * ld] = __uint_as_float(r[j]);
                 }
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    TC_MARK(tid == 0, 258)
-    if (warp == TC_EXP_WARPS + 1) {
-        uint32_t cols = 32;
-        while (cols < (uint32_t)N) cols <<= 1;
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(cols));
-    }
+    TC_MARK(tid == 0, 514)
+    TC_CTA_MARK(3)
+    if (warp == TC_EXP_WARPS + 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                     "r"(p.tmem_cols));
 }
 
-__global__ void tc_finalize_kernel(TcParams p, int64_t rows_view) {
+// Y rows of tiles with more than one contributing CTA: block (tile,
+// vector slice), thread = tile row; the partials of CTAs c_lo .. c_hi summed
+// in CTA order (deterministic), coalesced reads and writes
+__global__ void __launch_bounds__(TC_M) tc_finalize_kernel(const __grid_constant__ TcParams p) {
+    // PDL: the next multiply's prologue may start now (its first partial
+    // write is after its own griddepcontrol.wait, i.e. after this grid)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int64_t t = blockIdx.x;
+    const int64_t c_lo = tc_cta_of(t * p.S, p.W, p.G);
+    const int64_t c_hi = tc_cta_of((t + 1) * p.S - 1, p.W, p.G);
+    if (c_lo == c_hi) return;  // written by its only CTA
+    const int64_t seg_lo = t - tc_wstart(c_lo, p.W, p.G) / p.S;  // 0 or 1; later CTAs: 0
+    const int rt = threadIdx.x;
+    const int64_t r = t * TC_M + rt;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the partials are complete
-    const int64_t total = rows_view * p.B;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t vb = e / rows_view, r = e - vb * rows_view;
-        float s = 0.f;
-        for (int ks = 0; ks < p.ksplit; ++ks) s += p.part[((int64_t)ks * p.B + vb) * rows_view + r];
-        p.Y[vb * p.ldy + r] = s;
+    if (r >= p.rows_view) return;
+    for (int b = blockIdx.y; b < p.B; b += gridDim.y) {
+        float s = p.part[((c_lo * 2 + seg_lo) * p.B + b) * TC_M + rt];
+        for (int64_t c = c_lo + 1; c <= c_hi; ++c) s += p.part[(c * 2 * p.B + b) * TC_M + rt];
+        p.Y[b * p.ldy + r] = s;
     }
 }
 
@@ -410,56 +496,55 @@ static int tc_np(int B) {
     return np;
 }
 
-static size_t tc_stage_bytes(int N) {
-    return ((size_t)TC_M * TC_K * 2 + (size_t)N * TC_K * 2 + 16 * TC_K * 2 + 1023) / 1024 * 1024;
+static size_t tc_slot_bytes(int N) { return (size_t)N * TC_K * 2 + (size_t)TC_M * TC_RB; }
+
+static int tc_load_stages(int N) {
+    return (int)std::max<size_t>(TC_GROUPS,
+                                 std::min<size_t>(TC_LMAX, (216 * 1024) / tc_slot_bytes(N)));
 }
 
-static int tc_stages(int N) {
-    // deepest ring that still lets two CTAs share an SM (16 expander warps
-    // per SM); failing that the deepest ring that fits one CTA
-    const size_t sb = tc_stage_bytes(N);
-    for (int st = TC_STAGES; st >= 3; --st)
-        if (2 * (st * sb + 2048) <= 228 * 1024) return st;
-    int st = TC_STAGES;
-    while (st > 2 && st * sb > 220 * 1024) --st;
-    return st;
+static size_t tc_smem_bytes(int N) { return tc_load_stages(N) * tc_slot_bytes(N); }
+
+static int64_t tc_view_rows(int64_t block_begin, int64_t n_blocks, int32_t k, int64_t m) {
+    return std::max<int64_t>(0, std::min((block_begin + n_blocks) * k, m) - block_begin * k);
 }
 
-static size_t tc_smem_bytes(int N) { return tc_stages(N) * tc_stage_bytes(N); }
-
-// row tiles (16 row groups) covering the view's rows
-static int64_t tc_tiles(int64_t block_begin, int64_t n_blocks, int32_t k, int64_t m) {
-    const int64_t r0 = block_begin * k, r1 = std::min((block_begin + n_blocks) * k, m);
-    if (r1 <= r0) return 0;
-    const int64_t g0 = r0 >> 3, g1 = (r1 + 7) >> 3;
-    return (g1 - g0 + 15) / 16;
-}
-
-static int tc_ksplit(int64_t tiles, int64_t n, int B) {
-    // split K so that the tiles x splits fill the resident CTA slots in as
-    // few waves as possible; a wave costs about its steps plus ~6 steps of
-    // prologue / epilogue
-    const int64_t steps = tc_steps(n);
-    const size_t smem = tc_smem_bytes(16 * tc_np(B)) + 2048;
-    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (int64_t)smem));
-    const int64_t slots = per_sm * sm_count();
+// CTAs of the launch (one per SM: the kernel takes all of TMEM).  N <= 128
+// (two accumulators fit next to the A ring): stream-K, one CTA per SM (at
+// least ~8 steps each; at least one per tile).  N = 256 (one accumulator):
+// whole-tile splits -- tiles x ks CTAs, ks chosen so the CTAs fill the SMs
+// in as few waves as possible (a wave costs its steps plus ~6 steps of
+// prologue / epilogue).  Either way every CTA's range is at most one tile's
+// steps, so it has at most two segments.
+static int64_t tc_grid(int64_t tiles, int64_t n, int B) {
+    const int64_t S = tc_steps(n), W = tiles * S;
+    const int N = 16 * tc_np(B);
+    const int64_t slots = sm_count();
     static const int forced = [] {
         const char *e = getenv("RSR_TC_KSPLIT");
         return e ? atoi(e) : 0;
     }();
-    if (forced > 0) return (int)std::max<int64_t>(1, std::min<int64_t>(forced, steps));
+    if (forced > 0) return tiles * std::max<int64_t>(1, std::min<int64_t>(forced, S));
+    if (N <= 128) return std::max<int64_t>(tiles, std::min<int64_t>(slots, (W + 7) / 8));
     int best = 1;
     double best_cost = 1e30;
-    for (int ks = 1; ks <= 32 && ks <= steps; ++ks) {
+    for (int ks = 1; ks <= 32 && ks <= S; ++ks) {
         const int64_t waves = (tiles * ks + slots - 1) / slots;
-        const double cost = (double)waves * ((double)((steps + ks - 1) / ks) + 6.0) +
-                            0.02 * ks;  // partial traffic
+        const double cost = (double)waves * ((double)((S + ks - 1) / ks) + 6.0) + 0.02 * ks;
         if (cost < best_cost) {
             best_cost = cost;
             best = ks;
         }
     }
-    return best;
+    return tiles * best;
+}
+
+// does every tile have a single contributing CTA (no partials, no finalize)?
+static bool tc_single(int64_t tiles, int64_t S, int64_t G) {
+    const int64_t W = tiles * S;
+    for (int64_t t = 0; t < tiles; ++t)
+        if (tc_cta_of(t * S, W, G) != tc_cta_of((t + 1) * S - 1, W, G)) return false;
+    return true;
 }
 
 }  // namespace rsr
@@ -469,16 +554,21 @@ using namespace rsr;
 extern "C" {
 
 #ifdef RSR_TC_DBG
+int rsr_tc_debug_mma(long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, tc_mma_cyc, sizeof(long long) * 64 * 3);
+}
+int rsr_tc_debug_ctas(unsigned long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, tc_cta_t, sizeof(unsigned long long) * 1024 * 4);
+}
 int rsr_tc_debug(unsigned long long *out) {
-    return (int)cudaMemcpyFromSymbol(out, tc_dbg, sizeof(unsigned long long) * (64 * 4 + 4));
+    return (int)cudaMemcpyFromSymbol(out, tc_dbg, sizeof(unsigned long long) * (64 * 8 + 4));
 }
 #endif
 
 size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k) {
     (void)bitwidth;
-    if (k < 1 || k > 8 || block_count < 0 || cols < 0) return 0;
-    const int64_t ng = (block_count * k + 7) / 8;
-    return (size_t)tc_steps(cols) * ng * TC_K * 2;
+    if (k < 1 || k > TC_MAXK || block_count < 0 || cols < 0) return 0;
+    return (size_t)tc_steps(cols) * tc_rows_pad(block_count, k) * TC_RB;
 }
 
 rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
@@ -486,28 +576,55 @@ rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint
                             int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
                             void *keymat, rsr_stream_t stream) {
     const size_t bytes = rsr_keymat_bytes(block_count, cols, bitwidth, k);
-    if (!bytes || !keymat || !go || !po || (reinterpret_cast<uintptr_t>(keymat) & 3))
+    if (!bytes || !keymat || !go || !po || (reinterpret_cast<uintptr_t>(keymat) & 15))
         return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(keymat, 0, bytes, s);
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 16);
     keymat_kernel<<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count, tile_width, k,
-                                       (block_count * k + 7) / 8, (uint32_t *)keymat);
+                                       tc_rows_pad(block_count, k), (uint32_t *)keymat);
     return launch_status();
 }
 
 // workspace: [packed V (256-byte aligned)][split-K partials]
-static size_t tc_vpack_bytes(int64_t n, int32_t B) {
-    return ((size_t)tc_steps(n) * 16 * tc_np(B) * TC_K * 2 + 255) / 256 * 256;
+typedef CUresult (*TcEncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// V [B][n] bf16 rows of pitch ldv -> the 2-d SWIZZLE_128B view, box 64 x N
+static bool tc_encode_v(CUtensorMap *tm, const void *V, int64_t n, int B, int64_t ldv, int N) {
+    static TcEncodeTiled enc = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return (TcEncodeTiled)f;
+    }();
+    if (!enc || (reinterpret_cast<uintptr_t>(V) & 15) || ((ldv * 2) & 15)) return false;
+    const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)B};
+    const cuuint64_t gstride[1] = {(cuuint64_t)ldv * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)N};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(V), gdim, gstride, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
 }
 
+// workspace: split-K partials [CTA][2 segments][B][128] (none when every
+// tile has a single contributing CTA)
 size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t block_begin,
                                      int64_t n_blocks, int32_t B) {
-    if (B < 1 || B > 256 || k < 1 || k > 8 || n_blocks < 0) return 0;
-    const int ks = tc_ksplit(tc_tiles(block_begin, n_blocks, k, m), n, B);
-    const int64_t rows = std::max<int64_t>(0, std::min(n_blocks * k, m - block_begin * k));
-    return tc_vpack_bytes(n, B) + (ks > 1 ? (size_t)ks * B * rows * 4 : 0);
+    if (B < 1 || B > 256 || k < 1 || k > TC_MAXK || n_blocks < 0) return 0;
+    const int64_t rows = tc_view_rows(block_begin, n_blocks, k, m);
+    const int64_t tiles = (rows + TC_M - 1) / TC_M;
+    if (tiles == 0) return 256;
+    const int64_t G = tc_grid(tiles, n, B);
+    return tc_single(tiles, tc_steps(n), G) ? 256 : (size_t)G * 2 * B * TC_M * 4;
 }
 
 rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwidth, int32_t k,
@@ -515,47 +632,56 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
                          int64_t ldv, int32_t B, float *Y, int64_t ldy, void *workspace,
                          size_t workspace_bytes, rsr_stream_t stream) {
     (void)bitwidth;
-    if (!keymat || !V || !Y || B < 1 || B > 256 || v_dtype != RSR_BF16 || k < 1 || k > 8)
+    if (!keymat || !V || !Y || B < 1 || B > 256 || v_dtype != RSR_BF16 || k < 1 || k > TC_MAXK)
         return RSR_ERR_INVALID;
-    const int64_t rows = std::min(n_blocks * k, m - block_begin * k);
-    if (ldv < n || ldy < rows || n_blocks < 0 || block_begin < 0) return RSR_ERR_INVALID;
-    if (n_blocks == 0) return RSR_OK;
-    const int64_t tiles = tc_tiles(block_begin, n_blocks, k, m);
-    const int ks = tc_ksplit(tiles, n, B);
+    if (n_blocks < 0 || block_begin < 0) return RSR_ERR_INVALID;
+    const int64_t bc = (m + k - 1) / k;
+    if (block_begin + n_blocks > bc) return RSR_ERR_INVALID;
+    const int64_t rows = tc_view_rows(block_begin, n_blocks, k, m);
+    if (ldv < n || ldy < rows) return RSR_ERR_INVALID;
+    if (rows == 0) return RSR_OK;
+    if (reinterpret_cast<uintptr_t>(keymat) & 15) return RSR_ERR_INVALID;
+    const int64_t tiles = (rows + TC_M - 1) / TC_M;
+    const int64_t G = tc_grid(tiles, n, B);
+    const bool single = tc_single(tiles, tc_steps(n), G);
     const size_t wsb = rsr_matmul_tc_workspace_bytes(m, n, k, block_begin, n_blocks, B);
     if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
         return RSR_ERR_WORKSPACE;
     const int np = tc_np(B);
     TcParams p;
-    p.km = (const uint16_t *)keymat;
-    p.vp = (const uint4 *)workspace;
+    p.km = (const uint32_t *)keymat;
+    if (!tc_encode_v(&p.tm_v, V, n, B, ldv, 16 * np)) return RSR_ERR_INVALID;
     p.Y = Y;
     p.ldy = ldy;
-    p.part = (float *)((char *)workspace + tc_vpack_bytes(n, B));
-    p.m_rows = m;
+    p.part = (float *)workspace;
     p.n = n;
-    p.nblk = n_blocks;
-    p.blk0 = block_begin;
-    p.bc = (m + k - 1) / k;
-    p.ng = (p.bc * k + 7) / 8;
-    p.k = k;
+    p.row0 = block_begin * k;
+    p.rows_view = rows;
+    p.rows_pad = tc_rows_pad(bc, k);
     p.B = B;
     p.N = 16 * np;
-    p.ksplit = ks;
-    p.stages = tc_stages(p.N);
+    p.S = tc_steps(n);
+    p.W = tiles * p.S;
+    p.G = (int)G;
+    p.ls = tc_load_stages(p.N);
+    // TMEM (all 512 columns): the accumulators [0, 2N) (one of 256 when N =
+    // 256), then the A ring: 64 columns (128 bf16 of K) per stage
+    p.a_col = p.N <= 128 ? 2u * p.N : 256u;
+    p.as = std::min<int>(TC_AMAX, (int)(512 - p.a_col) / 64);
+    p.tmem_cols = 512;
+    {
+        static const int forced_as = [] {
+            const char *e = getenv("RSR_TC_ASTAGES");
+            return e ? atoi(e) : 0;
+        }();
+        if (forced_as >= TC_GROUPS) p.as = std::min(forced_as, p.as);
+    }
     p.tab0 = 0x00BF3F00u;
     p.tab1 = 0x00808000u;
-    if (block_begin + n_blocks > p.bc) return RSR_ERR_INVALID;
     const size_t smem = tc_smem_bytes(p.N);
     if (smem > 227 * 1024) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
-    {
-        const int64_t pieces = tc_steps(n) * p.N * 8;
-        const int g = (int)std::min<int64_t>((pieces + 255) / 256, (int64_t)sm_count() * 8);
-        tc_pack_v_kernel<<<g, 256, 0, s>>>((const uint16_t *)V, ldv, n, B, p.N, tc_steps(n),
-                                           (uint4 *)workspace);
-    }
-    dim3 grid((unsigned)tiles, (unsigned)ks);
+    dim3 grid((unsigned)G);
     // the tcgen05 kernel and the finalize launch as programmatic dependents
     // (PDL): each one's prologue overlaps the previous kernel's tail
     cudaLaunchAttribute pdl[1];
@@ -582,12 +708,12 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
         default: RSR_TC_LAUNCH(16) break;
     }
 #undef RSR_TC_LAUNCH
-    if (ks > 1) {
+    if (!single) {
         cudaLaunchConfig_t fcfg = cfg;
-        fcfg.gridDim = dim3((unsigned)std::min<int64_t>((rows * B + 255) / 256, 4096));
-        fcfg.blockDim = dim3(256);
+        fcfg.gridDim = dim3((unsigned)tiles, (unsigned)std::min(B, 8));
+        fcfg.blockDim = dim3(TC_M);
         fcfg.dynamicSmemBytes = 0;
-        cudaLaunchKernelEx(&fcfg, tc_finalize_kernel, p, rows);
+        cudaLaunchKernelEx(&fcfg, tc_finalize_kernel, p);
     }
     return launch_status();
 }

@@ -410,6 +410,11 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
                                 B >= TC_MIN_BATCH and B <= 256)
     if use_tc and Vt.dtype == torch.bfloat16 and a.keymat() is not None:
         vw = a._view if view is None else view
+        if Vt.stride(0) % 8 or Vt.data_ptr() % 16:
+            # the B tiles are TMA boxes of V: rows 16-byte aligned
+            Vp = torch.empty(B, -(-a.n // 8) * 8, dtype=Vt.dtype, device=Vt.device)
+            Vp[:, :a.n].copy_(Vt)
+            Vt = Vp[:, :a.n]
         s = _lib.current_stream_ptr(a.device) if stream is None else stream
         L = _lib.lib()
         wsb = int(L.rsr_matmul_tc_workspace_bytes(a.m, a.n, a.k, vw.row_begin_block,
@@ -422,7 +427,7 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
                                        Y.stride(0), _lib.ptr(ws), wsb, s), "rsr_matmul_tc")
         return Y
     if method == "tc":
-        raise ValueError("the tensor-core path needs a bf16 batch and k <= 8")
+        raise ValueError("the tensor-core path needs a bf16 batch and k <= 16")
     if method == "auto" and B <= SINGLE_MAX_BATCH:
         for b in range(B):
             matvec_into(a, Vt[b], Y[b], view=view, stream=stream)

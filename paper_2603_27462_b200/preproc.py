@@ -234,11 +234,11 @@ class RsrArtifact:
         self._view = self.view()
 
     def keymat(self):
-        """Every column's pattern key as 2-bit row codes cut into 8-row
-        groups (device u16 [ceil(n/64)][ceil(bc*k/8)][64]: a tensor-core
-        tile's step is one contiguous chunk),
-        built on first use for the tensor-core batched multiply; None when the
-        pattern space is too large (k > 8)."""
+        """Every column's pattern key as 2-bit row codes, one row at a time
+        (device u32 [ceil(n/128)][round8(bc*k)][8], 128 columns per row and
+        step in the permuted order of csrc/rsr_tc.cu: a tensor-core tile's
+        step is one contiguous run of rows), built on first use for the
+        tensor-core batched multiply; None when k > 16."""
         if "_keymat" not in self.__dict__:
             import torch
             L = _lib.lib()

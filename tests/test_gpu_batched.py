@@ -89,6 +89,9 @@ def test_batched_errors(rsr):
     (120, 1500, 8, "ternary", 8),    # 6561 keys: pair-table expansion
     (48, 70000, 4, "ternary", 3),    # multi-tile artifact (tw 32768)
     (64, 640, 5, "ternary", 256),    # N = 256
+    (300, 3000, 12, "binary", 4),    # k > 8 (rows straddle 128-row tiles)
+    (130, 1000, 16, "binary", 20),   # k = 16
+    (1000, 9000, 5, "ternary", 130), # N = 256 with a K tail, several tiles
 ])
 def test_tensor_core_batched(rsr, m, n, k, bw, B):
     """bf16 batches on tcgen05 (key matrix -> sign expansion -> MMA): each
@@ -127,23 +130,54 @@ def test_tensor_core_batched_shards(rsr):
 
 
 @pytest.mark.parametrize("m,n,k,bw,tw", [
-    (101, 300, 5, "ternary", None),    # blocks straddle 8-row groups, K tail
+    (101, 300, 5, "ternary", None),    # partial last block, K tail
     (64, 200, 8, "binary", None),
     (37, 5000, 3, "ternary", 2048),    # several tiles
+    (50, 333, 12, "binary", 100),      # k > 8, tiles not a multiple of 16 columns
 ])
 def test_code_matrix_layout(rsr, m, n, k, bw, tw):
     """The tensor-core code matrix equals the dense matrix's 2-bit codes
     (+1 -> 01, -1 -> 10; reference pattern_key code form, preproc.py:183-197)
-    at u16 [col // 64][row // 8][col % 64], bits 2 (row % 8)."""
+    at u32 [col // 128][row][(col % 128) // 16], column pair j = (col % 16) // 2
+    at bit 8 (2 (j // 4) + col % 2) + 2 (j % 4) (csrc/rsr_tc.cu)."""
     p = orc.random_matrix(m, n, bw, 7 * m + n)
     a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k, tw)
-    km = a.keymat().cpu().numpy().view(np.uint16)
+    km = a.keymat().cpu().numpy().view(np.uint32)
     dense = orc.decode(p).astype(np.int64)
     code = np.where(dense == 1, 1, np.where(dense == -1, 2, 0))
-    steps, ng = (n + 63) // 64, (a.plan.block_count * k + 7) // 8
-    assert km.size == steps * ng * 64
-    rows = np.arange(m)
-    exp = np.zeros((steps, ng, 64), np.int64)
+    steps, rows_pad = (n + 127) // 128, (a.plan.block_count * k + 7) // 8 * 8
+    assert km.size == steps * rows_pad * 8
+    exp = np.zeros((steps, rows_pad, 8), np.int64)
     for c in range(n):
-        np.add.at(exp[c // 64, :, c % 64], rows // 8, code[:, c] << (2 * (rows % 8)))
-    assert np.array_equal(km.reshape(steps, ng, 64).astype(np.int64), exp)
+        j = (c % 16) // 2
+        bit = 8 * (2 * (j // 4) + c % 2) + 2 * (j % 4)
+        exp[c // 128, :m, (c % 128) // 16] |= code[:, c] << bit
+    assert np.array_equal(km.reshape(steps, rows_pad, 8).astype(np.int64), exp)
+
+
+@pytest.mark.parametrize("offset,pad", [(1, 3), (0, 5), (8, 8)])
+def test_tensor_core_strided_vectors(rsr, offset, pad):
+    """bf16 rows that start off a 16-byte boundary or have an odd pitch are
+    re-laid into aligned rows before the TMA loads (the C entry point rejects
+    them); aligned strided rows are loaded in place: both equal the
+    contiguous batch bit for bit."""
+    import torch
+    from paper_2603_27462_b200 import kernels as kn
+    m, n, k, B = 300, 1000, 5, 6
+    p = orc.random_matrix(m, n, "ternary", 41)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", p.data), k)
+    big = torch.randn(B, offset + n + pad, device="cuda").to(torch.bfloat16)
+    V = big[:, offset:offset + n]
+    Yc = torch.empty(B, m, device="cuda")
+    kn.matmul_into(a, V.contiguous(), Yc, method="tc")
+    Ys = torch.empty(B, m, device="cuda")
+    kn.matmul_into(a, V, Ys, method="tc")
+    assert torch.equal(Yc, Ys)
+    if offset % 8 or (offset + n + pad) % 8:
+        from paper_2603_27462_b200 import _lib
+        L = _lib.lib()
+        ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+        rc = L.rsr_matmul_tc(_lib.ptr(a.keymat()), m, n, 1, k, 0, a.plan.block_count,
+                             V.data_ptr(), _lib.RSR_BF16, V.stride(0), B, Ys.data_ptr(), m,
+                             _lib.ptr(ws), ws.numel(), 0)
+        assert rc == _lib.RSR_ERR_INVALID

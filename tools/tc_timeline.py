@@ -21,16 +21,36 @@ Y = torch.empty(B, m, device="cuda")
 for _ in range(3):
     kn.matmul_into(a, V, Y, method="tc")
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 260)()
+buf = (ctypes.c_ulonglong * (64 * 8 + 4))()
 L = _lib.lib()
 L.rsr_tc_debug.argtypes = [ctypes.c_void_p]
 print("rc", L.rsr_tc_debug(ctypes.addressof(buf)))
 t = np.array(buf[:], dtype=np.int64)
-t0 = t[256]
-print(f"end of loop {(t[257]-t0)/1e3:.2f} us, exit {(t[258]-t0)/1e3:.2f} us")
-print(" it   prod_issue  exp_full  exp_done  mma_ready   (us from start)")
+t0 = t[512]
+print(f"end of loop {(t[513]-t0)/1e3:.2f} us, exit {(t[514]-t0)/1e3:.2f} us")
+print(" it   prod_issue  exp_full  expanded  aempty_ok  st_done  exp_done  mma_ready   (us from start)")
 for it in range(64):
-    row = t[it * 4: it * 4 + 4]
+    row = t[it * 8: it * 8 + 8]
     if not row.any():
         break
-    print(f"{it:3d} " + " ".join(f"{(x - t0)/1e3:9.2f}" if x else "        -" for x in (row[2], row[0], row[1], row[3])))
+    print(f"{it:3d} " + " ".join(f"{(x - t0)/1e3:9.2f}" if x else "        -" for x in (row[2], row[0], row[4], row[5], row[6], row[1], row[3])))
+# every CTA: entry / setup done / loop done / exit, relative to the earliest entry
+cb = (ctypes.c_ulonglong * 4096)()
+L.rsr_tc_debug_ctas.argtypes = [ctypes.c_void_p]
+L.rsr_tc_debug_ctas(ctypes.addressof(cb))
+c = np.array(cb[:], dtype=np.int64).reshape(1024, 4)
+c = c[c[:, 0] > 0]
+base = c[:, 0].min()
+c = (c - base) / 1e3
+print(f"CTAs {len(c)}: entry max {c[:,0].max():.2f} us; setup {np.median(c[:,1]-c[:,0]):.2f} (max {np.max(c[:,1]-c[:,0]):.2f}); "
+      f"loop median {np.median(c[:,2]-c[:,1]):.2f} max {np.max(c[:,2]-c[:,1]):.2f}; epilogue median {np.median(c[:,3]-c[:,2]):.2f}; last exit {c[:,3].max():.2f} us")
+for q in (0, 10, 50, 90, 100):
+    print(f"  exit p{q}: {np.percentile(c[:,3], q):.2f} us   entry p{q}: {np.percentile(c[:,0], q):.2f}")
+# MMA thread of CTA 0: cycles per step in the full wait, the A-ready wait, issue + commits
+mb = (ctypes.c_longlong * 192)()
+L.rsr_tc_debug_mma.argtypes = [ctypes.c_void_p]
+L.rsr_tc_debug_mma(ctypes.addressof(mb))
+m3 = np.array(mb[:], dtype=np.int64).reshape(64, 3)
+m3 = m3[: max(1, int((m3.sum(1) > 0).sum()))]
+print("MMA thread cycles/step (median): full wait %d, aready wait %d, issue+commit %d" % tuple(np.median(m3, 0)))
+print("  per step:", " ".join(f"{a}/{b}/{c}" for a, b, c in m3[:24]))
