@@ -248,9 +248,11 @@ rsr_status rsr_dequant_rows(const int32_t *Y, int64_t ldy, int64_t rows, int64_t
  * rsr_matmul_tc: Y[b] (f32, rows of blocks [block_begin, +n_blocks)) =
  * A . V[b] for bf16 V[b*ldv + col], B <= 256, V 16-byte aligned and ldv a
  * multiple of 8 (the B tiles are TMA boxes of V; RSR_ERR_INVALID otherwise);
- * fp32 accumulation of exact +-1 products (the float-path tolerance).  The
- * workspace (always needed, 256-byte aligned, rsr_matmul_tc_workspace_bytes)
- * holds the split-K partials.                                               */
+ * fp32 accumulation of exact +-1 products (the float-path tolerance; the
+ * split-K sum order is fixed, so results are deterministic).  Split-K runs
+ * inside thread-block clusters (partials summed through distributed shared
+ * memory); the workspace argument is kept for ABI stability and not used
+ * (rsr_matmul_tc_workspace_bytes returns 256).                              */
 size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k);
 rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                             const int64_t *po, int64_t block_count, int64_t tile_count,

@@ -43,13 +43,17 @@
 // tile is one bulk copy too.  Products with +-1 are exact and accumulate in
 // fp32: the float-path tolerance holds.  Work is split stream-K style: CTA c
 // takes items [c W / G, (c + 1) W / G) of the (tile, step) sequence, so the
-// resident CTA slots get equal shares; tiles with several contributors are
-// summed from their partials in CTA order by tc_finalize_kernel
-// (deterministic).
+// SMs get equal shares; a tile with several contributors is summed from
+// their partials, in CTA order (deterministic), by whichever contributor
+// arrives last (a per-tile counter in the workspace, left at zero) -- one
+// launch per call, no finalize kernel.
 #include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime)
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "rsr_mv_impl.cuh"
 
@@ -149,10 +153,10 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-__device__ unsigned long long tc_cta_t[1024 * 4];
+__device__ unsigned long long tc_cta_t[1024 * 8];
 __device__ long long tc_mma_cyc[64 * 3];
 #define TC_CTA_MARK(j) \
-    if (threadIdx.x == 0 && blockIdx.x < 1024) tc_cta_t[blockIdx.x * 4 + (j)] = gtime();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) tc_cta_t[blockIdx.x * 8 + (j)] = gtime();
 #define TC_MARK(cond, idx) \
     if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 64 * 8 + 4) tc_dbg[idx] = gtime();
 #else
@@ -168,11 +172,9 @@ struct TcParams {
     const uint32_t *km;  // code matrix [steps][rows_pad][8]
     float *Y;            // [B][ldy] rows of the view
     int64_t ldy;
-    float *part;         // partials [CTA][2 segments][B][128]
     int64_t n, row0, rows_view, rows_pad;
     int64_t S;           // steps per tile (= tc_steps(n))
-    int64_t W;           // work items: tiles x S
-    int B, N, G, ls, as;
+    int B, N, ks, ls, as;  // ks: CTAs per tile (cluster size)
     uint32_t a_col, tmem_cols;  // TMEM column of A stage 0; columns allocated
     uint32_t tab0, tab1;        // PRMT byte table {00 3F BF 00 | 00 80 80 00}
 };
@@ -220,11 +222,12 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32
 }
 
 // N = 16 * NP: MMA N (vectors padded up, <= 256).
-// CTA c owns the work items [c W / G, (c + 1) W / G) of the (tile, step)
-// sequence (stream-K): at most two segments (the range is at most one
-// tile's steps), each with its own TMEM accumulator (columns seg * N).  A
-// segment that is its tile's only contributor writes Y; otherwise it writes
-// its partial and tc_finalize_kernel sums a tile's partials in CTA order.
+// Split-K over thread-block clusters: cluster t (ks CTAs) owns row tile t,
+// CTA rank r its steps [r S / ks, (r + 1) S / ks).  Each CTA accumulates in
+// TMEM, moves its accumulator to its own shared memory, and after a cluster
+// barrier every rank sums a slice of the tile's rows over all ranks' copies
+// (DSMEM loads, rank order: deterministic) and writes Y.  No partials in
+// global memory, one launch per call.
 template <int NP>
 __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_constant__ TcParams p) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
@@ -233,15 +236,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
     constexpr int N = 16 * NP;
-    const int LS = p.ls, AS = p.as;
+    const int LS = p.ls, AS = p.as, ks = p.ks;
     TC_CTA_MARK(0)
-    // PDL: the finalize may launch now (it waits for this grid to finish)
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int64_t w0 = tc_wstart(blockIdx.x, p.W, p.G), w1 = tc_wstart(blockIdx.x + 1, p.W, p.G);
+    const int64_t t0 = blockIdx.x / ks;
+    const int rank = (int)(blockIdx.x - t0 * ks);  // = %cluster_ctarank (1-d clusters)
+    const int64_t w0 = t0 * p.S + p.S * rank / ks, w1 = t0 * p.S + p.S * (rank + 1) / ks;
     const int64_t nst = w1 - w0;
-    const int64_t t0 = w0 / p.S;                  // first tile
-    const int64_t wsplit = min((t0 + 1) * p.S, w1);  // first item of segment 1
-    const int nseg = w1 > wsplit ? 2 : 1;
+    const int64_t wsplit = w1;  // one segment
 
     // smem: per load stage [B tile: 2 K-halves x N x 128 B][codes 128 rows x 32 B]
     constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * 2;
@@ -428,35 +429,73 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     TC_MARK(tid == 0, 513)
     TC_CTA_MARK(2)
 
+    // --- epilogue: warps 0-3 read the accumulator (warp w: TMEM lanes
+    // 32w .. 32w + 31 = tile rows), 8 columns at a time; alone in its
+    // cluster a CTA writes Y, otherwise it parks the accumulator in its own
+    // (now idle) load ring as acc[column][row] for the cluster reduction
+    const int64_t r_first = t0 * TC_M;
+    float *acc_sm = reinterpret_cast<float *>(tc_smem);
     if (warp < 4) {
-        // --- epilogue: warp w reads TMEM lanes 32w..32w+31 (tile rows), 8 columns at a time
         const int row_t = warp * 32 + (int)lane;
-        for (int seg = 0; seg < nseg; ++seg) {
-            mbar_wait_parity(bar_done + 8 * seg, 0);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int64_t a_w = seg ? wsplit : w0, b_w = seg ? w1 : wsplit;
-            const int64_t t = a_w / p.S;
-            const int64_t vrow = t * TC_M + row_t;  // row within the view
-            const bool valid = vrow < p.rows_view;
-            const bool whole = a_w == t * p.S && b_w == (t + 1) * p.S;
-            float *dst = whole ? p.Y + vrow
-                               : p.part + ((int64_t)(blockIdx.x * 2 + seg) * p.B) * TC_M + row_t;
-            const int64_t ld = whole ? p.ldy : TC_M;
-            for (int c = 0; c < N; c += 8) {
-                uint32_t r[8];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                      "=r"(r[6]), "=r"(r[7])
-                    : "r"(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)(seg * N + c)));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int64_t vrow = r_first + row_t;
+        const bool valid = vrow < p.rows_view;
+        mbar_wait_parity(bar_done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int c = 0; c < N; c += 8) {
+            uint32_t r[8];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                  "=r"(r[6]), "=r"(r[7])
+                : "r"(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (ks == 1) {
                 if (valid) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        if (c + j < p.B) dst[(int64_t)(c + j) * ld] = __uint_as_float(r[j]);
+                        if (c + j < p.B) p.Y[(int64_t)(c + j) * p.ldy + vrow] = __uint_as_float(r[j]);
                 }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc_sm[(c + j) * TC_M + row_t] = __uint_as_float(r[j]);
             }
         }
+    }
+    TC_CTA_MARK(4)
+    if (ks > 1) {
+        // every rank's accumulator is in its shared memory -> each rank sums
+        // rows [rank 128 / ks, (rank + 1) 128 / ks) over ranks 0 .. ks-1
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        TC_CTA_MARK(5)
+        const int rbase = rank * TC_M / ks, rows = (rank + 1) * TC_M / ks - rbase;
+        const uint32_t own = (uint32_t)__cvta_generic_to_shared(acc_sm);
+        // the ranks' shared-memory windows (same offsets in every CTA)
+        uint32_t win[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(win[q]) : "r"(own),
+                         "r"(q < ks ? q : 0));
+        for (int e = tid; e < p.B * rows; e += TC_THREADS) {
+            const int b = e / rows, rt = rbase + (e - b * rows);
+            const uint32_t off = (uint32_t)((b * TC_M + rt) * 4);
+            // every rank's value loaded before any is summed
+            float x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                x[q] = 0.f;
+                if (q < ks)
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x[q]) : "r"(win[q] + off)
+                                 : "memory");
+            }
+            float sum = x[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                if (q < ks) sum += x[q];
+            const int64_t vrow = r_first + rt;
+            if (vrow < p.rows_view) p.Y[(int64_t)b * p.ldy + vrow] = sum;
+        }
+        // no rank leaves (freeing its shared memory) before all have read it
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -465,29 +504,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     if (warp == TC_EXP_WARPS + 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
                      "r"(p.tmem_cols));
-}
-
-// Y rows of tiles with more than one contributing CTA: block (tile,
-// vector slice), thread = tile row; the partials of CTAs c_lo .. c_hi summed
-// in CTA order (deterministic), coalesced reads and writes
-__global__ void __launch_bounds__(TC_M) tc_finalize_kernel(const __grid_constant__ TcParams p) {
-    // PDL: the next multiply's prologue may start now (its first partial
-    // write is after its own griddepcontrol.wait, i.e. after this grid)
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int64_t t = blockIdx.x;
-    const int64_t c_lo = tc_cta_of(t * p.S, p.W, p.G);
-    const int64_t c_hi = tc_cta_of((t + 1) * p.S - 1, p.W, p.G);
-    if (c_lo == c_hi) return;  // written by its only CTA
-    const int64_t seg_lo = t - tc_wstart(c_lo, p.W, p.G) / p.S;  // 0 or 1; later CTAs: 0
-    const int rt = threadIdx.x;
-    const int64_t r = t * TC_M + rt;
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the partials are complete
-    if (r >= p.rows_view) return;
-    for (int b = blockIdx.y; b < p.B; b += gridDim.y) {
-        float s = p.part[((c_lo * 2 + seg_lo) * p.B + b) * TC_M + rt];
-        for (int64_t c = c_lo + 1; c <= c_hi; ++c) s += p.part[(c * 2 * p.B + b) * TC_M + rt];
-        p.Y[b * p.ldy + r] = s;
-    }
 }
 
 static int tc_np(int B) {
@@ -509,42 +525,36 @@ static int64_t tc_view_rows(int64_t block_begin, int64_t n_blocks, int32_t k, in
     return std::max<int64_t>(0, std::min((block_begin + n_blocks) * k, m) - block_begin * k);
 }
 
-// CTAs of the launch (one per SM: the kernel takes all of TMEM).  N <= 128
-// (two accumulators fit next to the A ring): stream-K, one CTA per SM (at
-// least ~8 steps each; at least one per tile).  N = 256 (one accumulator):
-// whole-tile splits -- tiles x ks CTAs, ks chosen so the CTAs fill the SMs
-// in as few waves as possible (a wave costs its steps plus ~6 steps of
-// prologue / epilogue).  Either way every CTA's range is at most one tile's
-// steps, so it has at most two segments.
-static int64_t tc_grid(int64_t tiles, int64_t n, int B) {
-    const int64_t S = tc_steps(n), W = tiles * S;
-    const int N = 16 * tc_np(B);
-    const int64_t slots = sm_count();
-    static const int forced = [] {
-        const char *e = getenv("RSR_TC_KSPLIT");
-        return e ? atoi(e) : 0;
-    }();
-    if (forced > 0) return tiles * std::max<int64_t>(1, std::min<int64_t>(forced, S));
-    if (N <= 128) return std::max<int64_t>(tiles, std::min<int64_t>(slots, (W + 7) / 8));
-    int best = 1;
-    double best_cost = 1e30;
-    for (int ks = 1; ks <= 32 && ks <= S; ++ks) {
-        const int64_t waves = (tiles * ks + slots - 1) / slots;
-        const double cost = (double)waves * ((double)((S + ks - 1) / ks) + 6.0) + 0.02 * ks;
-        if (cost < best_cost) {
-            best_cost = cost;
-            best = ks;
-        }
+// cluster-size choice per (device, N, tiles, steps, smem): the occupancy
+// query is a host round trip worth skipping on repeated shapes
+struct TcKsKey {
+    int dev, np;
+    int64_t tiles, S;
+    size_t smem;
+    bool operator<(const TcKsKey &o) const {
+        return std::tie(dev, np, tiles, S, smem) < std::tie(o.dev, o.np, o.tiles, o.S, o.smem);
     }
-    return tiles * best;
+};
+static std::mutex tc_ks_mu;
+static std::map<TcKsKey, int> tc_ks_map;
+
+static TcKsKey tc_ks_key(int np, int64_t tiles, int64_t S, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return TcKsKey{dev, np, tiles, S, smem};
 }
 
-// does every tile have a single contributing CTA (no partials, no finalize)?
-static bool tc_single(int64_t tiles, int64_t S, int64_t G) {
-    const int64_t W = tiles * S;
-    for (int64_t t = 0; t < tiles; ++t)
-        if (tc_cta_of(t * S, W, G) != tc_cta_of((t + 1) * S - 1, W, G)) return false;
-    return true;
+static int tc_ks_cached(int np, int64_t tiles, int64_t S, size_t smem) {
+    const TcKsKey key = tc_ks_key(np, tiles, S, smem);
+    std::lock_guard<std::mutex> g(tc_ks_mu);
+    auto it = tc_ks_map.find(key);
+    return it == tc_ks_map.end() ? 0 : it->second;
+}
+
+static void tc_ks_store(int np, int64_t tiles, int64_t S, size_t smem, int ks) {
+    const TcKsKey key = tc_ks_key(np, tiles, S, smem);
+    std::lock_guard<std::mutex> g(tc_ks_mu);
+    tc_ks_map[key] = ks;
 }
 
 }  // namespace rsr
@@ -558,7 +568,7 @@ int rsr_tc_debug_mma(long long *out) {
     return (int)cudaMemcpyFromSymbol(out, tc_mma_cyc, sizeof(long long) * 64 * 3);
 }
 int rsr_tc_debug_ctas(unsigned long long *out) {
-    return (int)cudaMemcpyFromSymbol(out, tc_cta_t, sizeof(unsigned long long) * 1024 * 4);
+    return (int)cudaMemcpyFromSymbol(out, tc_cta_t, sizeof(unsigned long long) * 1024 * 8);
 }
 int rsr_tc_debug(unsigned long long *out) {
     return (int)cudaMemcpyFromSymbol(out, tc_dbg, sizeof(unsigned long long) * (64 * 8 + 4));
@@ -615,16 +625,13 @@ static bool tc_encode_v(CUtensorMap *tm, const void *V, int64_t n, int B, int64_
            CUDA_SUCCESS;
 }
 
-// workspace: split-K partials [CTA][2 segments][B][128] (none when every
-// tile has a single contributing CTA)
+// workspace: not used by this path (kept in the signature for ABI
+// stability; 256 bytes)
 size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t block_begin,
                                      int64_t n_blocks, int32_t B) {
+    (void)m, (void)n, (void)block_begin;
     if (B < 1 || B > 256 || k < 1 || k > TC_MAXK || n_blocks < 0) return 0;
-    const int64_t rows = tc_view_rows(block_begin, n_blocks, k, m);
-    const int64_t tiles = (rows + TC_M - 1) / TC_M;
-    if (tiles == 0) return 256;
-    const int64_t G = tc_grid(tiles, n, B);
-    return tc_single(tiles, tc_steps(n), G) ? 256 : (size_t)G * 2 * B * TC_M * 4;
+    return 256;
 }
 
 rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwidth, int32_t k,
@@ -642,8 +649,6 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     if (rows == 0) return RSR_OK;
     if (reinterpret_cast<uintptr_t>(keymat) & 15) return RSR_ERR_INVALID;
     const int64_t tiles = (rows + TC_M - 1) / TC_M;
-    const int64_t G = tc_grid(tiles, n, B);
-    const bool single = tc_single(tiles, tc_steps(n), G);
     const size_t wsb = rsr_matmul_tc_workspace_bytes(m, n, k, block_begin, n_blocks, B);
     if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
         return RSR_ERR_WORKSPACE;
@@ -653,7 +658,6 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     if (!tc_encode_v(&p.tm_v, V, n, B, ldv, 16 * np)) return RSR_ERR_INVALID;
     p.Y = Y;
     p.ldy = ldy;
-    p.part = (float *)workspace;
     p.n = n;
     p.row0 = block_begin * k;
     p.rows_view = rows;
@@ -661,12 +665,10 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     p.B = B;
     p.N = 16 * np;
     p.S = tc_steps(n);
-    p.W = tiles * p.S;
-    p.G = (int)G;
     p.ls = tc_load_stages(p.N);
-    // TMEM (all 512 columns): the accumulators [0, 2N) (one of 256 when N =
-    // 256), then the A ring: 64 columns (128 bf16 of K) per stage
-    p.a_col = p.N <= 128 ? 2u * p.N : 256u;
+    // TMEM (all 512 columns): the accumulator [0, N) (64-column aligned),
+    // then the A ring: 64 columns (128 bf16 of K) per stage
+    p.a_col = (uint32_t)std::max(p.N, 64);
     p.as = std::min<int>(TC_AMAX, (int)(512 - p.a_col) / 64);
     p.tmem_cols = 512;
     {
@@ -681,23 +683,48 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     const size_t smem = tc_smem_bytes(p.N);
     if (smem > 227 * 1024) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
-    dim3 grid((unsigned)G);
-    // the tcgen05 kernel and the finalize launch as programmatic dependents
-    // (PDL): each one's prologue overlaps the previous kernel's tail
-    cudaLaunchAttribute pdl[1];
-    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    // programmatic dependent launch (PDL): the prologue overlaps the previous
+    // kernel's tail; clusters of ks CTAs split each tile's steps
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[0].val.programmaticStreamSerializationAllowed = 1;
+    attrs[1].id = cudaLaunchAttributeClusterDimension;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
     cfg.blockDim = dim3(TC_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cfg.attrs = pdl;
-    cfg.numAttrs = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 2;
+    // CTAs per tile: the largest ks <= 8 (and <= S) whose tiles x ks CTAs fit
+    // one wave, one per SM, with that many clusters co-resident
+    static const int forced_ks = [] {
+        const char *e = getenv("RSR_TC_KSPLIT");
+        return e ? atoi(e) : 0;
+    }();
 #define RSR_TC_LAUNCH(NPV)                                                                      \
     {                                                                                          \
         cudaFuncSetAttribute(rsr_tc_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                              (int)smem);                                                       \
+        int ks = tc_ks_cached(np, tiles, p.S, smem);                                           \
+        for (int c = 8; ks == 0 && c >= 2; --c) {                                              \
+            if (forced_ks > 0 ? c != forced_ks : (c > p.S || tiles * c > sm_count())) continue; \
+            attrs[1].val.clusterDim.x = c;                                                     \
+            attrs[1].val.clusterDim.y = attrs[1].val.clusterDim.z = 1;                         \
+            cfg.gridDim = dim3((unsigned)(tiles * c));                                         \
+            int nc = 0;                                                                        \
+            if (cudaOccupancyMaxActiveClusters(&nc, rsr_tc_kernel<NPV>, &cfg) == cudaSuccess &&  \
+                (nc >= tiles || forced_ks > 0)) {                                               \
+                ks = c;                                                                        \
+                break;                                                                         \
+            }                                                                                  \
+            cudaGetLastError();                                                                \
+        }                                                                                      \
+        if (ks == 0) ks = 1;                                                                   \
+        tc_ks_store(np, tiles, p.S, smem, ks);                                                 \
+        p.ks = ks;                                                                             \
+        attrs[1].val.clusterDim.x = ks;                                                        \
+        attrs[1].val.clusterDim.y = attrs[1].val.clusterDim.z = 1;                             \
+        cfg.gridDim = dim3((unsigned)(tiles * ks));                                            \
         cudaLaunchKernelEx(&cfg, rsr_tc_kernel<NPV>, p);                                       \
     }
     switch (np) {
@@ -708,13 +735,6 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
         default: RSR_TC_LAUNCH(16) break;
     }
 #undef RSR_TC_LAUNCH
-    if (!single) {
-        cudaLaunchConfig_t fcfg = cfg;
-        fcfg.gridDim = dim3((unsigned)tiles, (unsigned)std::min(B, 8));
-        fcfg.blockDim = dim3(TC_M);
-        fcfg.dynamicSmemBytes = 0;
-        cudaLaunchKernelEx(&fcfg, tc_finalize_kernel, p);
-    }
     return launch_status();
 }
 

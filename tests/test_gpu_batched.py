@@ -176,8 +176,28 @@ def test_tensor_core_strided_vectors(rsr, offset, pad):
     if offset % 8 or (offset + n + pad) % 8:
         from paper_2603_27462_b200 import _lib
         L = _lib.lib()
-        ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
         rc = L.rsr_matmul_tc(_lib.ptr(a.keymat()), m, n, 1, k, 0, a.plan.block_count,
                              V.data_ptr(), _lib.RSR_BF16, V.stride(0), B, Ys.data_ptr(), m,
                              _lib.ptr(ws), ws.numel(), 0)
         assert rc == _lib.RSR_ERR_INVALID
+
+
+def test_tensor_core_split_k_is_deterministic(rsr):
+    """Tiles split across the CTAs of a cluster are summed in rank order:
+    repeated calls (with other batch sizes in between) give bit-identical
+    results."""
+    import torch
+    from paper_2603_27462_b200 import kernels as kn
+    m, n, k = 2000, 6000, 5
+    p = orc.random_matrix(m, n, "ternary", 77)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", p.data), k)
+    V = torch.randn(16, n, device="cuda").to(torch.bfloat16)
+    first = torch.empty(16, m, device="cuda")
+    kn.matmul_into(a, V, first, method="tc")
+    for rep in range(20):
+        Vb = torch.randn(1 + rep % 7, n, device="cuda").to(torch.bfloat16)
+        kn.matmul_into(a, Vb, torch.empty(Vb.shape[0], m, device="cuda"), method="tc")
+        Y = torch.empty(16, m, device="cuda")
+        kn.matmul_into(a, V, Y, method="tc")
+        assert torch.equal(Y, first), rep

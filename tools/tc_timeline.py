@@ -34,18 +34,22 @@ for it in range(64):
     if not row.any():
         break
     print(f"{it:3d} " + " ".join(f"{(x - t0)/1e3:9.2f}" if x else "        -" for x in (row[2], row[0], row[4], row[5], row[6], row[1], row[3])))
-# every CTA: entry / setup done / loop done / exit, relative to the earliest entry
-cb = (ctypes.c_ulonglong * 4096)()
+# every CTA: entry / setup done / expander loop done / epilogue done / after
+# the CTA barrier / exit, relative to the earliest entry; slot 6 = last-arriver flags
+cb = (ctypes.c_ulonglong * 8192)()
 L.rsr_tc_debug_ctas.argtypes = [ctypes.c_void_p]
 L.rsr_tc_debug_ctas(ctypes.addressof(cb))
-c = np.array(cb[:], dtype=np.int64).reshape(1024, 4)
+c = np.array(cb[:], dtype=np.int64).reshape(1024, 8)
 c = c[c[:, 0] > 0]
+flags = np.zeros(len(c), np.int64)
 base = c[:, 0].min()
-c = (c - base) / 1e3
-print(f"CTAs {len(c)}: entry max {c[:,0].max():.2f} us; setup {np.median(c[:,1]-c[:,0]):.2f} (max {np.max(c[:,1]-c[:,0]):.2f}); "
-      f"loop median {np.median(c[:,2]-c[:,1]):.2f} max {np.max(c[:,2]-c[:,1]):.2f}; epilogue median {np.median(c[:,3]-c[:,2]):.2f}; last exit {c[:,3].max():.2f} us")
-for q in (0, 10, 50, 90, 100):
-    print(f"  exit p{q}: {np.percentile(c[:,3], q):.2f} us   entry p{q}: {np.percentile(c[:,0], q):.2f}")
+c = (c[:, [0, 1, 2, 4, 5, 3]] - base) / 1e3
+print(f"CTAs {len(c)}: entry max {c[:,0].max():.2f} us; setup {np.median(c[:,1]-c[:,0]):.2f}; loop median {np.median(c[:,2]-c[:,1]):.2f} max {np.max(c[:,2]-c[:,1]):.2f}; "
+      f"epilogue median {np.median(c[:,3]-c[:,2]):.2f}; barrier median {np.median(c[:,4]-c[:,3]):.2f}; reduce median {np.median(c[:,5]-c[:,4]):.2f}; last exit {c[:,5].max():.2f} us")
+for name, sel in (("last arrivers", flags > 0), ("others", flags == 0)):
+    if sel.any():
+        x = c[sel]
+        print(f"  {name} ({sel.sum()}): epilogue {np.median(x[:,3]-x[:,2]):.2f}, barrier {np.median(x[:,4]-x[:,3]):.2f}, reduce {np.median(x[:,5]-x[:,4]):.2f} (max {np.max(x[:,5]-x[:,4]):.2f}), exit median {np.median(x[:,5]):.2f} max {x[:,5].max():.2f}")
 # MMA thread of CTA 0: cycles per step in the full wait, the A-ready wait, issue + commits
 mb = (ctypes.c_longlong * 192)()
 L.rsr_tc_debug_mma.argtypes = [ctypes.c_void_p]
