@@ -260,6 +260,31 @@ rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint
                             void *keymat, rsr_stream_t stream);
 size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t block_begin,
                                      int64_t n_blocks, int32_t B);
+/* int8 batches on tcgen05 kind::i8 (s8 x s8 -> s32, exact): the same code
+ * matrix in the int8 path's permuted order (rsr_keymat_build_i8, same size:
+ * column 4w + i of a 16-column word in nibble i + 4 (w / 2) at bit offset
+ * 2 (w % 2)); rsr_matmul_tc_i8: Y[b] (int32) = A . V[b] for int8
+ * V[b*ldv + col] (V 16-byte aligned, ldv a multiple of 16), bit-exact with
+ * the integer path of rsr_matvec per column.                                */
+rsr_status rsr_keymat_build_i8(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                               const int64_t *po, int64_t block_count, int64_t tile_count,
+                               int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
+                               void *keymat_i8, rsr_stream_t stream);
+rsr_status rsr_matmul_tc_i8(const void *keymat_i8, int64_t m, int64_t n, int32_t bitwidth,
+                            int32_t k, int64_t block_begin, int64_t n_blocks, const int8_t *V,
+                            int64_t ldv, int32_t B, int32_t *Y, int64_t ldy, void *workspace,
+                            size_t workspace_bytes, rsr_stream_t stream);
+/* The same multiply with rsr_dequant_rows fused into its epilogue (batched
+ * fused prefill: rsr_absmax_quantize_rows -> this): out[t][i] =
+ * f32(f64(y[t][i]) * (beta_i / scales[t])) (beta_i = row_beta[i] or beta;
+ * out f32 or bf16 = RNE of that f32), row for row the single-vector
+ * rsr_fused_matvec result.                                                  */
+rsr_status rsr_matmul_tc_i8_dequant(const void *keymat_i8, int64_t m, int64_t n,
+                                    int32_t bitwidth, int32_t k, int64_t block_begin,
+                                    int64_t n_blocks, const int8_t *Q, int64_t ldq, int32_t B,
+                                    const double *scales, const double *row_beta, double beta,
+                                    void *out, int32_t out_dtype, int64_t ldo, void *workspace,
+                                    size_t workspace_bytes, rsr_stream_t stream);
 rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwidth, int32_t k,
                          int64_t block_begin, int64_t n_blocks, const void *V, int32_t v_dtype,
                          int64_t ldv, int32_t B, float *Y, int64_t ldy, void *workspace,

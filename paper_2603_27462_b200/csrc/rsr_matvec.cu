@@ -512,39 +512,44 @@ __device__ __forceinline__ float row_elem(const char *vr, int dtype, int64_t i,
     return __bfloat162float(__float2bfloat16_rn(bf16_bits_to_f32(__ldg(norm_w + i)) * nx));
 }
 
-__global__ void absmax_quantize_rows_kernel(const void *V, int dtype, int64_t ldv, int64_t n,
-                                            int8_t *Q, int64_t ldq, double *scales,
-                                            const uint16_t *norm_w, float norm_eps) {
-    __shared__ double red[32];
+// one CTA (1024 threads) per row; the element loops are unrolled so a
+// thread's loads are in flight together (a row is only n / 1024 elements per
+// thread).  max |x| is taken in f32 (exact: the conversion to f64 is exact),
+// the scale in f64 (the reference rule)
+constexpr int QROWS_THREADS = 1024;
+__global__ void __launch_bounds__(QROWS_THREADS) absmax_quantize_rows_kernel(
+    const void *V, int dtype, int64_t ldv, int64_t n, int8_t *Q, int64_t ldq, double *scales,
+    const uint16_t *norm_w, float norm_eps) {
+    __shared__ float red[32];
     const int64_t row = blockIdx.x;
     const char *vr = reinterpret_cast<const char *>(V) +
                      row * ldv * (dtype == RSR_F32 ? 4 : 2);
     float rs = 0.f;
     if (norm_w) {
         float ss = 0.f;
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+#pragma unroll 8
+        for (int64_t i = threadIdx.x; i < n; i += QROWS_THREADS) {
             const float x = load_as_f32(vr, dtype, i);
             ss += x * x;
         }
         rs = rsqrtf(cta_reduce_sum_f32(ss) * (1.0f / (float)n) + norm_eps);
     }
-    double a = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double x = fabs((double)row_elem(vr, dtype, i, norm_w, rs));
-        a = x > a ? x : a;
-    }
+    float a = 0.f;
+#pragma unroll 8
+    for (int64_t i = threadIdx.x; i < n; i += QROWS_THREADS)
+        a = fmaxf(a, fabsf(row_elem(vr, dtype, i, norm_w, rs)));
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        const double o = __shfl_xor_sync(RSR_FULL_MASK, a, d);
-        a = o > a ? o : a;
-    }
+    for (int d = 16; d > 0; d >>= 1) a = fmaxf(a, __shfl_xor_sync(RSR_FULL_MASK, a, d));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
     __syncthreads();
-    a = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a = red[w] > a ? red[w] : a;
-    const double scale = a == 0.0 ? 1.0 : 127.0 / a;
+    a = 0.f;
+#pragma unroll
+    for (int w = 0; w < QROWS_THREADS / 32; ++w) a = fmaxf(a, red[w]);
+    const double amax = (double)a;
+    const double scale = amax == 0.0 ? 1.0 : 127.0 / amax;
     if (threadIdx.x == 0) scales[row] = scale;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll 8
+    for (int64_t i = threadIdx.x; i < n; i += QROWS_THREADS)
         Q[row * ldq + i] = quantize_one(row_elem(vr, dtype, i, norm_w, rs), scale);
 }
 
@@ -572,7 +577,7 @@ rsr_status rsr_absmax_quantize_rows(const void *V, int32_t v_dtype, int64_t ldv,
     if (v_dtype != RSR_F32 && v_dtype != RSR_BF16 && v_dtype != RSR_F16) return RSR_ERR_INVALID;
     if (norm_w && v_dtype != RSR_BF16) return RSR_ERR_INVALID;
     if (rows == 0) return RSR_OK;
-    absmax_quantize_rows_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
+    absmax_quantize_rows_kernel<<<(unsigned)rows, QROWS_THREADS, 0, (cudaStream_t)stream>>>(
         V, v_dtype, ldv, n, Q, ldq, scales, (const uint16_t *)norm_w, norm_eps);
     return launch_status();
 }

@@ -73,14 +73,25 @@ __host__ __device__ inline int64_t tc_steps(int64_t n) { return (n + TC_K - 1) /
 __host__ __device__ inline int64_t tc_rows_pad(int64_t bc, int k) { return (bc * k + 7) / 8 * 8; }
 
 // bit offset of column c (c % 16 within its u32) in the permuted code word
+// of the bf16 path: column pair j at bits 2 (j % 4) of bytes 2 (j / 4) and
+// 2 (j / 4) + 1
 __device__ __forceinline__ uint32_t tc_code_bit(uint32_t c) {
     const uint32_t j = (c >> 1) & 7;
     return 8 * (2 * (j >> 2) + (c & 1)) + 2 * (j & 3);
 }
 
+// ... and of the int8 path: column 4w + i (word w of 4 int8) in nibble
+// i + 4 (w / 2) at bit offset 2 (w % 2), so (x >> 2j) & 0x33333333 holds the
+// PRMT selectors of words j (low half) and j + 2 (high half)
+__device__ __forceinline__ uint32_t tc_code_bit_i8(uint32_t c) {
+    const uint32_t w = (c >> 2) & 3, i = c & 3;
+    return 4 * (i + 4 * (w >> 1)) + 2 * (w & 1);
+}
+
 // ---- code matrix: KM[step][row][q] (see the header) from the artifact's
 // groups: each column of a cell's group carries the group's pattern key; row
 // r0 + i gets code (pos_i, neg_i)
+template <bool I8>
 __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                               const uint16_t *__restrict__ perm, const int64_t *__restrict__ po,
                               int64_t bc, int64_t tc, int64_t tw, int k, int64_t rows_pad,
@@ -98,7 +109,8 @@ __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t 
             const uint16_t *cols = perm + po[cell] + ps;
             for (int64_t j = lane; j < L; j += 32) {
                 const int64_t col = c0 + cols[j];
-                const uint32_t bit = tc_code_bit((uint32_t)col & 15);
+                const uint32_t bit =
+                    I8 ? tc_code_bit_i8((uint32_t)col & 15) : tc_code_bit((uint32_t)col & 15);
                 uint32_t *dst = km32 + ((col >> 7) * rows_pad + r0) * 8 + ((col & 127) >> 4);
                 for (int i = 0; i < k; ++i) {
                     const uint32_t code = ((pos >> i) & 1u) | (((neg >> i) & 1u) << 1);
@@ -165,13 +177,20 @@ __device__ long long tc_mma_cyc[64 * 3];
 #endif
 
 struct TcParams {
-    // V [B][n] bf16 as a 2-d TMA view, 128-byte swizzle: a box of 64
-    // columns x N vectors is one K-half of a step's B tile in the canonical
-    // K-major SWIZZLE_128B image (vectors >= B, columns >= n zero-filled)
+    // V [B][n] (bf16 / int8) as a 2-d TMA view, 128-byte swizzle: a box of
+    // 128 bytes of columns x N vectors is one K-half (bf16) / the whole K of
+    // a step's B tile in the canonical K-major SWIZZLE_128B image (vectors
+    // >= B, columns >= n zero-filled)
     CUtensorMap tm_v;
     const uint32_t *km;  // code matrix [steps][rows_pad][8]
-    float *Y;            // [B][ldy] rows of the view
+    float *Y;            // [B][ldy] rows of the view (f32; int32 on the int8 path)
     int64_t ldy;
+    // int8 path with the fused dequantization (prefill): out[b][i] =
+    // f32(f64(y) * (beta_i / scales[b])), beta_i = row_beta[i] or beta; f32
+    // or bf16 (RNE of that f32) -- rsr_dequant_rows' arithmetic
+    const double *dq_scales, *dq_row_beta;
+    double dq_beta;
+    int dq_bf16;
     int64_t n, row0, rows_view, rows_pad;
     int64_t S;           // steps per tile (= tc_steps(n))
     int B, N, ks, ls, as;  // ks: CTAs per tile (cluster size)
@@ -179,10 +198,19 @@ struct TcParams {
     uint32_t tab0, tab1;        // PRMT byte table {00 3F BF 00 | 00 80 80 00}
 };
 
-// work range of CTA c: [c W / G, (c + 1) W / G) over (tile, step) items
-__host__ __device__ inline int64_t tc_wstart(int64_t c, int64_t W, int64_t G) { return c * W / G; }
-__host__ __device__ inline int64_t tc_cta_of(int64_t w, int64_t W, int64_t G) {
-    return ((w + 1) * G - 1) / W;
+// one output element from its raw accumulator bits (fp32 bits; int32 bits
+// on the int8 path, optionally dequantized)
+template <bool I8>
+__device__ __forceinline__ void tc_store(const TcParams &p, int b, int64_t vrow, uint32_t bits) {
+    const int64_t o = (int64_t)b * p.ldy + vrow;
+    if (I8 && p.dq_scales) {
+        const double beta = p.dq_row_beta ? p.dq_row_beta[vrow] : p.dq_beta;
+        const float v = (float)((double)(int32_t)bits * (beta / p.dq_scales[b]));
+        if (p.dq_bf16) reinterpret_cast<__nv_bfloat16 *>(p.Y)[o] = __float2bfloat16_rn(v);
+        else p.Y[o] = v;
+    } else {
+        reinterpret_cast<uint32_t *>(p.Y)[o] = bits;
+    }
 }
 
 // 64 columns' codes of one row (x[q]: columns 16q .. 16q + 15, permuted
@@ -208,6 +236,39 @@ __device__ __forceinline__ void expand64(const uint4 &x, uint32_t (&w)[32], uint
     }
 }
 
+// 64 columns' codes of one row (int8 layout) -> 16 words of four int8 (+1,
+// -1, 0): one mask + one PRMT per word from the byte table {00 01 FF 00}
+__device__ __forceinline__ void expand64_i8(const uint4 &x, uint32_t (&w)[16], uint32_t tab) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const uint32_t xv = h == 0 ? x.x : h == 1 ? x.y : h == 2 ? x.z : x.w;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const uint32_t sel = (xv >> (2 * j)) & 0x33333333u;
+            asm("prmt.b32 %0, %1, 0, %2;" : "=r"(w[4 * h + j]) : "r"(tab), "r"(sel));
+            asm("prmt.b32 %0, %1, 0, %2;" : "=r"(w[4 * h + j + 2]) : "r"(tab), "r"(sel >> 16));
+        }
+    }
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&w)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+        "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+        "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]),
+        "r"(w[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -228,7 +289,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32
 // barrier every rank sums a slice of the tile's rows over all ranks' copies
 // (DSMEM loads, rank order: deterministic) and writes Y.  No partials in
 // global memory, one launch per call.
-template <int NP>
+template <int NP, bool I8>
 __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_constant__ TcParams p) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     __shared__ uint32_t tmem_base_sh;
@@ -245,7 +306,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     const int64_t wsplit = w1;  // one segment
 
     // smem: per load stage [B tile: 2 K-halves x N x 128 B][codes 128 rows x 32 B]
-    constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * 2;
+    constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * (I8 ? 1 : 2);
+    constexpr uint32_t ASC = I8 ? 32u : 64u;  // TMEM columns per A stage
     constexpr uint32_t C_BYTES = TC_M * TC_RB;
     constexpr uint32_t SLOT = B_BYTES + C_BYTES;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tc_smem);
@@ -305,7 +367,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 bulk_g2s(sa + B_BYTES, kb + (st * p.rows_pad + p.row0 + r_first) * TC_RB, kbytes,
                          fb);
                 tma_2d(sa, &p.tm_v, (int)st * TC_K, 0, fb);
-                tma_2d(sa + B_BYTES / 2, &p.tm_v, (int)st * TC_K + 64, 0, fb);
+                if (!I8) tma_2d(sa + B_BYTES / 2, &p.tm_v, (int)st * TC_K + 64, 0, fb);
                 s += J;
                 if (s >= LS) {
                     s -= LS;
@@ -323,7 +385,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         if (lane == 0) {
             // instruction descriptor: kind::f16, A = B = BF16, D = F32, A and B
             // K-major, N >> 3 at [17,23), M >> 4 at [24,29)
-            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+            // (kind::i8: D = S32 (2), A = B = S8 (1))
+            const uint32_t idesc = ((I8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) |
                                    ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
             // B K-major SWIZZLE_128B (layout type 2 at [61,64)): rows of 128 B,
             // SBO = 8 rows (1024 B); a K = 16 slice starts 32 B further into
@@ -349,16 +412,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 TC_MARK(it < 64, it * 8 + 3)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint64_t db = db0 + ((s * SLOT) >> 4);
-                const uint32_t ta = tmem_d + p.a_col + 64u * a;
+                const uint32_t ta = tmem_d + p.a_col + ASC * a;
                 const uint32_t td = tmem_d + (uint32_t)(seg * N);
+                if (I8) {
+                    // K = 32 int8 per MMA: 32 B into the 128-byte swizzled rows
 #pragma unroll
-                for (int kk = 0; kk < TC_K / 16; ++kk) {
-#ifndef TC_EXP_NO_MMA
-                    mma_bf16_ts(td, ta + 8u * kk,
-                                db + (uint64_t)(((kk >> 2) * (B_BYTES / 2) + (kk & 3) * 32) >> 4),
-                                idesc,
-                                (!first || kk > 0) ? 1u : 0u);
-#endif
+                    for (int kk = 0; kk < TC_K / 32; ++kk)
+                        mma_i8_ts(td, ta + 8u * kk, db + (uint64_t)((kk * 32) >> 4), idesc,
+                                  (!first || kk > 0) ? 1u : 0u);
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < TC_K / 16; ++kk)
+                        mma_bf16_ts(
+                            td, ta + 8u * kk,
+                            db + (uint64_t)(((kk >> 2) * (B_BYTES / 2) + (kk & 3) * 32) >> 4), idesc,
+                            (!first || kk > 0) ? 1u : 0u);
                 }
                 mma_commit(bar_empty + 8 * s);
                 mma_commit(bar_aempty + 8 * a);
@@ -387,7 +455,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         // Group h = warp / 8 expands the steps it = h (mod TC_GROUPS) ----
         const int q = warp & 3, hh = (warp >> 2) & 1, h = warp >> 3;
         const int row = 32 * q + (int)lane;
-        const uint32_t t_row = tmem_d + ((uint32_t)(32 * q) << 16) + p.a_col + 32u * hh;
+        const uint32_t t_row = tmem_d + ((uint32_t)(32 * q) << 16) + p.a_col + (ASC / 2) * hh;
         // table words and the selector bias in plain registers, set once
         const uint32_t tab0 = __shfl_sync(RSR_FULL_MASK, p.tab0, 0);
         const uint32_t tab1 = __shfl_sync(RSR_FULL_MASK, p.tab1, 0);
@@ -400,13 +468,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             mbar_wait_parity(bar_full + 8 * s, par);
             TC_MARK(tid == 0 && it < 64, it * 8 + 0)
             const uint4 x = *reinterpret_cast<const uint4 *>(codes0 + s * SLOT);
-            uint32_t w[32];
-            expand64(x, w, tab0, tab1, c0404);
-            TC_MARK(tid == 0 && it < 64, it * 8 + 4)
-            if (it >= AS) mbar_wait_parity(bar_aempty + 8 * a, apar ^ 1u);
-            TC_MARK(tid == 0 && it < 64, it * 8 + 5)
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            tmem_st32(t_row + 64u * a, w);
+            if (I8) {
+                uint32_t w[16];
+                expand64_i8(x, w, tab0);
+                if (it >= AS) mbar_wait_parity(bar_aempty + 8 * a, apar ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                tmem_st16(t_row + ASC * a, w);
+            } else {
+                uint32_t w[32];
+                expand64(x, w, tab0, tab1, c0404);
+                TC_MARK(tid == 0 && it < 64, it * 8 + 4)
+                if (it >= AS) mbar_wait_parity(bar_aempty + 8 * a, apar ^ 1u);
+                TC_MARK(tid == 0 && it < 64, it * 8 + 5)
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                tmem_st32(t_row + ASC * a, w);
+            }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             TC_MARK(tid == 0 && it < 64, it * 8 + 6)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -453,11 +529,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 if (valid) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        if (c + j < p.B) p.Y[(int64_t)(c + j) * p.ldy + vrow] = __uint_as_float(r[j]);
+                        if (c + j < p.B)
+                            tc_store<I8>(p, c + j, vrow, r[j]);
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc_sm[(c + j) * TC_M + row_t] = __uint_as_float(r[j]);
+                for (int j = 0; j < 8; ++j)
+                    reinterpret_cast<uint32_t *>(acc_sm)[(c + j) * TC_M + row_t] = r[j];
             }
         }
     }
@@ -478,21 +556,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         for (int e = tid; e < p.B * rows; e += TC_THREADS) {
             const int b = e / rows, rt = rbase + (e - b * rows);
             const uint32_t off = (uint32_t)((b * TC_M + rt) * 4);
-            // every rank's value loaded before any is summed
-            float x[8];
+            // every rank's value loaded before any is summed (fp32 in rank
+            // order; int32 for the int8 path, exact)
+            uint32_t x[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                x[q] = 0.f;
+                x[q] = 0u;
                 if (q < ks)
-                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x[q]) : "r"(win[q] + off)
+                    asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(x[q]) : "r"(win[q] + off)
                                  : "memory");
             }
-            float sum = x[0];
+            uint32_t sum;
+            if (I8) {
+                sum = x[0];
 #pragma unroll
-            for (int q = 1; q < 8; ++q)
-                if (q < ks) sum += x[q];
+                for (int q = 1; q < 8; ++q)
+                    if (q < ks) sum += x[q];
+            } else {
+                float f = __uint_as_float(x[0]);
+#pragma unroll
+                for (int q = 1; q < 8; ++q)
+                    if (q < ks) f += __uint_as_float(x[q]);
+                sum = __float_as_uint(f);
+            }
             const int64_t vrow = r_first + rt;
-            if (vrow < p.rows_view) p.Y[(int64_t)b * p.ldy + vrow] = sum;
+            if (vrow < p.rows_view) tc_store<I8>(p, b, vrow, sum);
         }
         // no rank leaves (freeing its shared memory) before all have read it
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -512,14 +600,19 @@ static int tc_np(int B) {
     return np;
 }
 
-static size_t tc_slot_bytes(int N) { return (size_t)N * TC_K * 2 + (size_t)TC_M * TC_RB; }
-
-static int tc_load_stages(int N) {
-    return (int)std::max<size_t>(TC_GROUPS,
-                                 std::min<size_t>(TC_LMAX, (216 * 1024) / tc_slot_bytes(N)));
+// load-ring slot: the B tile (N x 128 elements of esize bytes) + 128 code rows
+static size_t tc_slot_bytes(int N, int esize) {
+    return (size_t)N * TC_K * esize + (size_t)TC_M * TC_RB;
 }
 
-static size_t tc_smem_bytes(int N) { return tc_load_stages(N) * tc_slot_bytes(N); }
+static int tc_load_stages(int N, int esize) {
+    return (int)std::max<size_t>(
+        TC_GROUPS, std::min<size_t>(TC_LMAX, (216 * 1024) / tc_slot_bytes(N, esize)));
+}
+
+static size_t tc_smem_bytes(int N, int esize) {
+    return tc_load_stages(N, esize) * tc_slot_bytes(N, esize);
+}
 
 static int64_t tc_view_rows(int64_t block_begin, int64_t n_blocks, int32_t k, int64_t m) {
     return std::max<int64_t>(0, std::min((block_begin + n_blocks) * k, m) - block_begin * k);
@@ -581,10 +674,13 @@ size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int
     return (size_t)tc_steps(cols) * tc_rows_pad(block_count, k) * TC_RB;
 }
 
-rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
-                            const int64_t *po, int64_t block_count, int64_t tile_count,
-                            int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
-                            void *keymat, rsr_stream_t stream) {
+}  // extern "C"
+
+template <bool I8>
+static rsr_status keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                               const int64_t *po, int64_t block_count, int64_t tile_count,
+                               int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
+                               void *keymat, rsr_stream_t stream) {
     const size_t bytes = rsr_keymat_bytes(block_count, cols, bitwidth, k);
     if (!bytes || !keymat || !go || !po || (reinterpret_cast<uintptr_t>(keymat) & 15))
         return RSR_ERR_INVALID;
@@ -592,19 +688,41 @@ rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint
     cudaMemsetAsync(keymat, 0, bytes, s);
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 16);
-    keymat_kernel<<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count, tile_width, k,
-                                       tc_rows_pad(block_count, k), (uint32_t *)keymat);
+    keymat_kernel<I8><<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count,
+                                           tile_width, k, tc_rows_pad(block_count, k),
+                                           (uint32_t *)keymat);
     return launch_status();
 }
 
-// workspace: [packed V (256-byte aligned)][split-K partials]
+extern "C" {
+
+rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                            const int64_t *po, int64_t block_count, int64_t tile_count,
+                            int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
+                            void *keymat, rsr_stream_t stream) {
+    return keymat_build<false>(words, go, perm, po, block_count, tile_count, tile_width, cols,
+                               bitwidth, k, keymat, stream);
+}
+
+rsr_status rsr_keymat_build_i8(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                               const int64_t *po, int64_t block_count, int64_t tile_count,
+                               int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
+                               void *keymat, rsr_stream_t stream) {
+    return keymat_build<true>(words, go, perm, po, block_count, tile_count, tile_width, cols,
+                              bitwidth, k, keymat, stream);
+}
+
+}  // extern "C"
+
 typedef CUresult (*TcEncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// V [B][n] bf16 rows of pitch ldv -> the 2-d SWIZZLE_128B view, box 64 x N
-static bool tc_encode_v(CUtensorMap *tm, const void *V, int64_t n, int B, int64_t ldv, int N) {
+// V [B][n] (bf16 or int8) rows of pitch ldv elements -> the 2-d
+// SWIZZLE_128B view, box (128 bytes of columns) x N vectors
+static bool tc_encode_v(CUtensorMap *tm, const void *V, int64_t n, int B, int64_t ldv, int N,
+                        bool i8) {
     static TcEncodeTiled enc = [] {
         void *f = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -614,16 +732,20 @@ static bool tc_encode_v(CUtensorMap *tm, const void *V, int64_t n, int B, int64_
             f = nullptr;
         return (TcEncodeTiled)f;
     }();
-    if (!enc || (reinterpret_cast<uintptr_t>(V) & 15) || ((ldv * 2) & 15)) return false;
+    const int esize = i8 ? 1 : 2;
+    if (!enc || (reinterpret_cast<uintptr_t>(V) & 15) || ((ldv * esize) & 15)) return false;
     const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)B};
-    const cuuint64_t gstride[1] = {(cuuint64_t)ldv * 2};
-    const cuuint32_t box[2] = {64, (cuuint32_t)N};
+    const cuuint64_t gstride[1] = {(cuuint64_t)ldv * esize};
+    const cuuint32_t box[2] = {(cuuint32_t)(128 / esize), (cuuint32_t)N};
     const cuuint32_t estr[2] = {1, 1};
-    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(V), gdim, gstride, box,
+    return enc(tm, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+               const_cast<void *>(V), gdim, gstride, box,
                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
            CUDA_SUCCESS;
 }
+
+extern "C" {
 
 // workspace: not used by this path (kept in the signature for ABI
 // stability; 256 bytes)
@@ -634,13 +756,16 @@ size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t bl
     return 256;
 }
 
-rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwidth, int32_t k,
-                         int64_t block_begin, int64_t n_blocks, const void *V, int32_t v_dtype,
-                         int64_t ldv, int32_t B, float *Y, int64_t ldy, void *workspace,
-                         size_t workspace_bytes, rsr_stream_t stream) {
-    (void)bitwidth;
-    if (!keymat || !V || !Y || B < 1 || B > 256 || v_dtype != RSR_BF16 || k < 1 || k > TC_MAXK)
-        return RSR_ERR_INVALID;
+}  // extern "C"
+
+template <bool I8>
+static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
+                            int64_t block_begin, int64_t n_blocks, const void *V, int64_t ldv,
+                            int32_t B, void *Y, int64_t ldy, void *workspace,
+                            size_t workspace_bytes, rsr_stream_t stream,
+                            const double *dq_scales = nullptr, const double *dq_row_beta = nullptr,
+                            double dq_beta = 1.0, int dq_bf16 = 0) {
+    if (!keymat || !V || !Y || B < 1 || B > 256 || k < 1 || k > TC_MAXK) return RSR_ERR_INVALID;
     if (n_blocks < 0 || block_begin < 0) return RSR_ERR_INVALID;
     const int64_t bc = (m + k - 1) / k;
     if (block_begin + n_blocks > bc) return RSR_ERR_INVALID;
@@ -652,12 +777,16 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     const size_t wsb = rsr_matmul_tc_workspace_bytes(m, n, k, block_begin, n_blocks, B);
     if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
         return RSR_ERR_WORKSPACE;
-    const int np = tc_np(B);
+    const int np = tc_np(B), esize = I8 ? 1 : 2;
     TcParams p;
     p.km = (const uint32_t *)keymat;
-    if (!tc_encode_v(&p.tm_v, V, n, B, ldv, 16 * np)) return RSR_ERR_INVALID;
-    p.Y = Y;
+    if (!tc_encode_v(&p.tm_v, V, n, B, ldv, 16 * np, I8)) return RSR_ERR_INVALID;
+    p.Y = (float *)Y;
     p.ldy = ldy;
+    p.dq_scales = dq_scales;
+    p.dq_row_beta = dq_row_beta;
+    p.dq_beta = dq_beta;
+    p.dq_bf16 = dq_bf16;
     p.n = n;
     p.row0 = block_begin * k;
     p.rows_view = rows;
@@ -665,11 +794,13 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     p.B = B;
     p.N = 16 * np;
     p.S = tc_steps(n);
-    p.ls = tc_load_stages(p.N);
+    p.ls = tc_load_stages(p.N, esize);
     // TMEM (all 512 columns): the accumulator [0, N) (64-column aligned),
-    // then the A ring: 64 columns (128 bf16 of K) per stage
+    // then the A ring: one step's 128 K elements per stage (64 columns of
+    // bf16 pairs, 32 of int8 quads)
+    const int asc = I8 ? 32 : 64;
     p.a_col = (uint32_t)std::max(p.N, 64);
-    p.as = std::min<int>(TC_AMAX, (int)(512 - p.a_col) / 64);
+    p.as = std::min<int>(TC_AMAX, (int)(512 - p.a_col) / asc);
     p.tmem_cols = 512;
     {
         static const int forced_as = [] {
@@ -678,9 +809,10 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
         }();
         if (forced_as >= TC_GROUPS) p.as = std::min(forced_as, p.as);
     }
-    p.tab0 = 0x00BF3F00u;
+    // PRMT byte tables: bf16 {00 3F BF 00 | 00 80 80 00}; int8 {00 01 FF 00}
+    p.tab0 = I8 ? 0x00FF0100u : 0x00BF3F00u;
     p.tab1 = 0x00808000u;
-    const size_t smem = tc_smem_bytes(p.N);
+    const size_t smem = tc_smem_bytes(p.N, esize);
     if (smem > 227 * 1024) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     // programmatic dependent launch (PDL): the prologue overlaps the previous
@@ -701,18 +833,19 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
         const char *e = getenv("RSR_TC_KSPLIT");
         return e ? atoi(e) : 0;
     }();
+    const int key_np = np + (I8 ? 1000 : 0);
 #define RSR_TC_LAUNCH(NPV)                                                                      \
     {                                                                                          \
-        cudaFuncSetAttribute(rsr_tc_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                             (int)smem);                                                       \
-        int ks = tc_ks_cached(np, tiles, p.S, smem);                                           \
+        auto kern = rsr_tc_kernel<NPV, I8>;                                                    \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+        int ks = tc_ks_cached(key_np, tiles, p.S, smem);                                       \
         for (int c = 8; ks == 0 && c >= 2; --c) {                                              \
             if (forced_ks > 0 ? c != forced_ks : (c > p.S || tiles * c > sm_count())) continue; \
             attrs[1].val.clusterDim.x = c;                                                     \
             attrs[1].val.clusterDim.y = attrs[1].val.clusterDim.z = 1;                         \
             cfg.gridDim = dim3((unsigned)(tiles * c));                                         \
             int nc = 0;                                                                        \
-            if (cudaOccupancyMaxActiveClusters(&nc, rsr_tc_kernel<NPV>, &cfg) == cudaSuccess &&  \
+            if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess &&              \
                 (nc >= tiles || forced_ks > 0)) {                                               \
                 ks = c;                                                                        \
                 break;                                                                         \
@@ -720,12 +853,12 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
             cudaGetLastError();                                                                \
         }                                                                                      \
         if (ks == 0) ks = 1;                                                                   \
-        tc_ks_store(np, tiles, p.S, smem, ks);                                                 \
+        tc_ks_store(key_np, tiles, p.S, smem, ks);                                             \
         p.ks = ks;                                                                             \
         attrs[1].val.clusterDim.x = ks;                                                        \
         attrs[1].val.clusterDim.y = attrs[1].val.clusterDim.z = 1;                             \
         cfg.gridDim = dim3((unsigned)(tiles * ks));                                            \
-        cudaLaunchKernelEx(&cfg, rsr_tc_kernel<NPV>, p);                                       \
+        cudaLaunchKernelEx(&cfg, kern, p);                                                     \
     }
     switch (np) {
         case 1: RSR_TC_LAUNCH(1) break;
@@ -736,6 +869,40 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     }
 #undef RSR_TC_LAUNCH
     return launch_status();
+}
+
+extern "C" {
+
+rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwidth, int32_t k,
+                         int64_t block_begin, int64_t n_blocks, const void *V, int32_t v_dtype,
+                         int64_t ldv, int32_t B, float *Y, int64_t ldy, void *workspace,
+                         size_t workspace_bytes, rsr_stream_t stream) {
+    (void)bitwidth;
+    if (v_dtype != RSR_BF16) return RSR_ERR_INVALID;
+    return tc_launch<false>(keymat, m, n, k, block_begin, n_blocks, V, ldv, B, Y, ldy, workspace,
+                            workspace_bytes, stream);
+}
+
+rsr_status rsr_matmul_tc_i8(const void *keymat_i8, int64_t m, int64_t n, int32_t bitwidth,
+                            int32_t k, int64_t block_begin, int64_t n_blocks, const int8_t *V,
+                            int64_t ldv, int32_t B, int32_t *Y, int64_t ldy, void *workspace,
+                            size_t workspace_bytes, rsr_stream_t stream) {
+    (void)bitwidth;
+    return tc_launch<true>(keymat_i8, m, n, k, block_begin, n_blocks, V, ldv, B, Y, ldy,
+                           workspace, workspace_bytes, stream);
+}
+
+rsr_status rsr_matmul_tc_i8_dequant(const void *keymat_i8, int64_t m, int64_t n,
+                                    int32_t bitwidth, int32_t k, int64_t block_begin,
+                                    int64_t n_blocks, const int8_t *Q, int64_t ldq, int32_t B,
+                                    const double *scales, const double *row_beta, double beta,
+                                    void *out, int32_t out_dtype, int64_t ldo, void *workspace,
+                                    size_t workspace_bytes, rsr_stream_t stream) {
+    (void)bitwidth;
+    if (!scales || (out_dtype != RSR_F32 && out_dtype != RSR_BF16)) return RSR_ERR_INVALID;
+    return tc_launch<true>(keymat_i8, m, n, k, block_begin, n_blocks, Q, ldq, B, out, ldo,
+                           workspace, workspace_bytes, stream, scales, row_beta, beta,
+                           out_dtype == RSR_BF16);
 }
 
 }  // extern "C"

@@ -200,7 +200,8 @@ def fused_rows_into(a: RsrArtifact, V, out, beta: float | None = None, row_beta=
     as one per-row quantization launch, one batched exact int8 multiply
     (matmul_into) and one dequantization launch.  V: [T, n] f32/bf16/f16;
     out: [T, m] float32 or bfloat16; row_beta as fused_into; norm_w / norm_eps
-    as fused_norm_into (bf16 rows)."""
+    as fused_norm_into (bf16 rows).  From TC_MIN_BATCH rows the multiply and
+    the dequantization are one int8 tensor-core launch."""
     import torch
     from .matcore import _dtype_code
     T = int(V.shape[0])
@@ -210,16 +211,30 @@ def fused_rows_into(a: RsrArtifact, V, out, beta: float | None = None, row_beta=
     dev = a.device
     s = _lib.current_stream_ptr(dev) if stream is None else stream
     L = _lib.lib()
-    Q = torch.empty(T, a.n, dtype=torch.int8, device=dev)
+    # pitch a multiple of 16 bytes: the int8 tensor-core path loads rows by TMA
+    Q = torch.empty(T, -(-a.n // 16) * 16, dtype=torch.int8, device=dev)[:, :a.n]
     scales = torch.empty(T, dtype=torch.float64, device=dev)
     _lib.check(L.rsr_absmax_quantize_rows(V.data_ptr(), _dtype_code(V), V.stride(0), T, a.n,
                                           _lib.ptr(norm_w), float(norm_eps), Q.data_ptr(),
                                           Q.stride(0), scales.data_ptr(), s),
                "quantize rows")
-    Y = torch.empty(T, a.m, dtype=torch.int32, device=dev)
-    matmul_into(a, Q, Y, stream=s, method="stream")
     b = float(a.weight_scale) if beta is None else float(beta)
     odt = _lib.RSR_BF16 if out.dtype == torch.bfloat16 else _lib.RSR_F32
+    if TC_MIN_BATCH <= T <= 256 and a.keymat("i8") is not None:
+        # int8 tensor cores with the dequantization in the epilogue: one launch
+        vw = a._view
+        wsb = int(L.rsr_matmul_tc_workspace_bytes(a.m, a.n, a.k, vw.row_begin_block,
+                                                  vw.n_blocks, T))
+        ws, wsb = _Workspace.get(dev, wsb, s)
+        with torch.cuda.device(dev):
+            _lib.check(L.rsr_matmul_tc_i8_dequant(
+                _lib.ptr(a.keymat("i8")), a.m, a.n, vw.bitwidth, a.k, vw.row_begin_block,
+                vw.n_blocks, Q.data_ptr(), Q.stride(0), T, scales.data_ptr(),
+                _lib.ptr(row_beta), b, out.data_ptr(), odt, out.stride(0), _lib.ptr(ws), wsb, s),
+                "rsr_matmul_tc_i8_dequant")
+        return out
+    Y = torch.empty(T, a.m, dtype=torch.int32, device=dev)
+    matmul_into(a, Q, Y, stream=s)
     _lib.check(L.rsr_dequant_rows(Y.data_ptr(), Y.stride(0), T, a.m, scales.data_ptr(),
                                   _lib.ptr(row_beta), b, out.data_ptr(), odt, out.stride(0), s),
                "dequant rows")
@@ -383,8 +398,8 @@ def _fused_host_locked(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
 
 
 # auto policy (measured at C4, ternary 8192^2 k=5, tools/bench_batched.py):
-# bf16 batches from TC_MIN_BATCH on go to the tensor cores (22.3 us at B=2
-# vs 24.1 for two single-vector calls); other batches of up to
+# bf16 and int8 batches from TC_MIN_BATCH on go to the tensor cores (bf16:
+# 15.0 us at B=2 vs 21.7 for two single-vector calls); other batches of up to
 # SINGLE_MAX_BATCH vectors take the single-vector kernel per column; the
 # CUDA-core batched stream kernel covers the rest
 SINGLE_MAX_BATCH = 2
@@ -395,10 +410,11 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
     """Batched multiply on device tensors: Y[b] = A . Vt[b].
 
     Vt: [B, n] (int8 -> Y int32; float32/bfloat16/float16 -> Y float32), rows
-    contiguous; Y: [B, rows].  method: "tc" (bf16 batches on tcgen05 via the
-    key matrix), "stream" (CUDA-core kernel on the chunk stream) or "auto"
-    (single-vector kernel per column up to SINGLE_MAX_BATCH, tc for bf16
-    batches of >= TC_MIN_BATCH vectors, else stream).  Streams without a
+    contiguous; Y: [B, rows].  method: "tc" (bf16 batches on tcgen05
+    kind::f16, int8 batches on kind::i8 -- exact int32 -- via the code
+    matrix), "stream" (CUDA-core kernel on the chunk stream) or "auto" (tc
+    for bf16 / int8 batches of TC_MIN_BATCH .. 256 vectors, else the
+    single-vector kernel per column up to SINGLE_MAX_BATCH, else stream).  Streams without a
     batched kernel (u32 format, > 2187 pattern keys, tiles above ~13k
     columns) run the single-vector kernel column by column.
     """
@@ -406,13 +422,14 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
     import torch
     from .matcore import _dtype_code
     B = int(Vt.shape[0])
-    use_tc = method == "tc" or (method == "auto" and Vt.dtype == torch.bfloat16 and
-                                B >= TC_MIN_BATCH and B <= 256)
-    if use_tc and Vt.dtype == torch.bfloat16 and a.keymat() is not None:
+    tc_dtype = Vt.dtype in (torch.bfloat16, torch.int8)
+    use_tc = method == "tc" or (method == "auto" and tc_dtype and TC_MIN_BATCH <= B <= 256)
+    i8 = Vt.dtype == torch.int8
+    if use_tc and tc_dtype and B <= 256 and a.keymat("i8" if i8 else "bf16") is not None:
         vw = a._view if view is None else view
-        if Vt.stride(0) % 8 or Vt.data_ptr() % 16:
-            # the B tiles are TMA boxes of V: rows 16-byte aligned
-            Vp = torch.empty(B, -(-a.n // 8) * 8, dtype=Vt.dtype, device=Vt.device)
+        align = 16 if i8 else 8  # TMA: rows 16-byte aligned
+        if Vt.stride(0) % align or Vt.data_ptr() % 16:
+            Vp = torch.empty(B, -(-a.n // align) * align, dtype=Vt.dtype, device=Vt.device)
             Vp[:, :a.n].copy_(Vt)
             Vt = Vp[:, :a.n]
         s = _lib.current_stream_ptr(a.device) if stream is None else stream
@@ -421,13 +438,21 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
                                                   vw.n_blocks, B))
         ws, wsb = _Workspace.get(a.device, wsb, s)
         with torch.cuda.device(a.device):  # raw-pointer entry point: no view device
-            _lib.check(L.rsr_matmul_tc(_lib.ptr(a.keymat()), a.m, a.n, vw.bitwidth, a.k,
-                                       vw.row_begin_block, vw.n_blocks, Vt.data_ptr(),
-                                       _lib.RSR_BF16, Vt.stride(0), B, Y.data_ptr(),
-                                       Y.stride(0), _lib.ptr(ws), wsb, s), "rsr_matmul_tc")
+            if i8:
+                _lib.check(L.rsr_matmul_tc_i8(_lib.ptr(a.keymat("i8")), a.m, a.n, vw.bitwidth,
+                                              a.k, vw.row_begin_block, vw.n_blocks,
+                                              Vt.data_ptr(), Vt.stride(0), B, Y.data_ptr(),
+                                              Y.stride(0), _lib.ptr(ws), wsb, s),
+                           "rsr_matmul_tc_i8")
+            else:
+                _lib.check(L.rsr_matmul_tc(_lib.ptr(a.keymat()), a.m, a.n, vw.bitwidth, a.k,
+                                           vw.row_begin_block, vw.n_blocks, Vt.data_ptr(),
+                                           _lib.RSR_BF16, Vt.stride(0), B, Y.data_ptr(),
+                                           Y.stride(0), _lib.ptr(ws), wsb, s), "rsr_matmul_tc")
         return Y
     if method == "tc":
-        raise ValueError("the tensor-core path needs a bf16 batch and k <= 16")
+        raise ValueError("the tensor-core path needs a bf16 or int8 batch of at most 256 "
+                         "vectors and k <= 16")
     if method == "auto" and B <= SINGLE_MAX_BATCH:
         for b in range(B):
             matvec_into(a, Vt[b], Y[b], view=view, stream=stream)

@@ -233,13 +233,16 @@ class RsrArtifact:
         self.col0_d = col0 if self.format != 2 else None
         self._view = self.view()
 
-    def keymat(self):
+    def keymat(self, kind: str = "bf16"):
         """Every column's pattern key as 2-bit row codes, one row at a time
         (device u32 [ceil(n/128)][round8(bc*k)][8], 128 columns per row and
-        step in the permuted order of csrc/rsr_tc.cu: a tensor-core tile's
-        step is one contiguous run of rows), built on first use for the
-        tensor-core batched multiply; None when k > 16."""
-        if "_keymat" not in self.__dict__:
+        step, in the permuted order of csrc/rsr_tc.cu for the bf16 ("bf16")
+        or the int8 ("i8") tensor-core multiply: a tile's step is one
+        contiguous run of rows), built on first use; None when k > 16."""
+        attr = "_keymat" if kind == "bf16" else "_keymat_i8"
+        if kind not in ("bf16", "i8"):
+            raise ValueError(f"unknown code-matrix kind {kind!r}")
+        if attr not in self.__dict__:
             import torch
             L = _lib.lib()
             bw = _lib.RSR_BINARY if self.bitwidth == BINARY else _lib.RSR_TERNARY
@@ -248,13 +251,14 @@ class RsrArtifact:
             km = None
             if nb:
                 km = torch.empty(nb, dtype=torch.uint8, device=self.device)
-                _lib.check(L.rsr_keymat_build(
+                build = L.rsr_keymat_build if kind == "bf16" else L.rsr_keymat_build_i8
+                _lib.check(build(
                     _lib.ptr(self.words_d), _lib.ptr(self.go_d), _lib.ptr(self.perm_d),
                     _lib.ptr(self.po_d), p.block_count, p.tile_count, p.tile_width, self.n,
                     bw, self.k, _lib.ptr(km), _lib.current_stream_ptr(self.device)),
                     "keymat_build")
-            self.__dict__["_keymat"] = km
-        return self.__dict__["_keymat"]
+            self.__dict__[attr] = km
+        return self.__dict__[attr]
 
     def block_bytes(self) -> np.ndarray:
         """Reference-format artifact bytes of each row block (all its tiles):

@@ -201,3 +201,54 @@ def test_tensor_core_split_k_is_deterministic(rsr):
         Y = torch.empty(16, m, device="cuda")
         kn.matmul_into(a, V, Y, method="tc")
         assert torch.equal(Y, first), rep
+
+
+@pytest.mark.parametrize("m,n,k,bw,B", [
+    (96, 3000, 5, "ternary", 5),
+    (200, 4096, 6, "ternary", 16),
+    (64, 2048, 8, "binary", 33),
+    (2000, 1000, 4, "ternary", 2),
+    (300, 3000, 12, "binary", 4),
+    (130, 1000, 16, "binary", 20),
+    (1000, 9000, 5, "ternary", 130),
+    (64, 640, 5, "ternary", 256),
+])
+def test_tensor_core_int8_batched_is_exact(rsr, m, n, k, bw, B):
+    """int8 batches on tcgen05 kind::i8: every column equals the reference
+    integer core bit for bit (int32, saturating-free exact sums)."""
+    import torch
+    from paper_2603_27462_b200 import kernels as kn
+    p = orc.random_matrix(m, n, bw, m + 5 * n)
+    ref = orc.preprocess(p, k)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k)
+    rng = np.random.default_rng(B + 1)
+    Vi = rng.integers(-128, 128, (B, n)).astype(np.int8)
+    Vi[0, :7] = -128  # extremes
+    Y = torch.empty(B, m, dtype=torch.int32, device="cuda")
+    kn.matmul_into(a, torch.from_numpy(Vi).cuda(), Y, method="tc")
+    Yh = Y.cpu().numpy()
+    for b in range(B):
+        assert np.array_equal(Yh[b], orc.matvec_i8(ref, Vi[b])), b
+    # numpy through the public batched API (auto policy -> tensor cores)
+    assert np.array_equal(rsr.rsr_matvec_batched(a, Vi), Yh)
+
+
+@pytest.mark.parametrize("m,n,k,bw,tw", [
+    (101, 300, 5, "ternary", None),
+    (50, 333, 12, "binary", 100),
+])
+def test_code_matrix_layout_i8(rsr, m, n, k, bw, tw):
+    """The int8 path's code matrix: column 4w + i of a 16-column word in
+    nibble i + 4 (w // 2) at bit offset 2 (w % 2) (csrc/rsr_tc.cu)."""
+    p = orc.random_matrix(m, n, bw, 3 * m + n)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k, tw)
+    km = a.keymat("i8").cpu().numpy().view(np.uint32)
+    dense = orc.decode(p).astype(np.int64)
+    code = np.where(dense == 1, 1, np.where(dense == -1, 2, 0))
+    steps, rows_pad = (n + 127) // 128, (a.plan.block_count * k + 7) // 8 * 8
+    exp = np.zeros((steps, rows_pad, 8), np.int64)
+    for c in range(n):
+        w, i = (c % 16) // 4, c % 4
+        bit = 4 * (i + 4 * (w // 2)) + 2 * (w % 2)
+        exp[c // 128, :m, (c % 128) // 16] |= code[:, c] << bit
+    assert np.array_equal(km.reshape(steps, rows_pad, 8).astype(np.int64), exp)

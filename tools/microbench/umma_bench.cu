@@ -22,6 +22,7 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 // mode bit 0: commit after every 4 MMAs; bit 1: warps 1-3 store into TMEM
 // (columns 288+) with tcgen05.st while the MMAs run; bit 2: A (TS) at
 // columns 32+ (next to D) instead of 256+
+// mode bit 3: kind::i8 (s8 x s8 -> s32, K = 32 per instruction)
 template <bool TS>
 __global__ void __launch_bounds__(128) umma_kernel(int N, int R, int mode,
                                                    unsigned long long *cycles) {
@@ -51,14 +52,26 @@ __global__ void __launch_bounds__(128) umma_kernel(int N, int R, int mode,
     const uint32_t td = tbase;
     if (tid == 0) {
         const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sm);
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (TS ? 0u : (1u << 15)) |
+        const bool i8 = (mode & 8) != 0;
+        const uint32_t idesc = ((i8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) |
+                               (TS || i8 ? 0u : (1u << 15)) |
                                ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         const uint64_t da = smem_desc(s0, 16 * 128, 128);
         const uint64_t db = smem_desc(s0 + 32768, 128, 8 * 128);
         const long long t0 = clock64();
         for (int i = 0; i < R; ++i) {
             const uint32_t acc = i > 0;
-            if (TS) {
+            if (TS && i8) {
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(td),
+                    "r"(td + 256u + 8u * (i & 7)), "l"(db), "r"(idesc), "r"(acc));
+            } else if (i8) {
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(td),
+                    "l"(smem_desc(s0, 128, 1024)), "l"(db), "r"(idesc), "r"(acc));
+            } else if (TS) {
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(td),
@@ -117,7 +130,7 @@ int main() {
     CK(cudaFuncSetAttribute(umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int R = 4096;
-    for (int mode : {0, 4, 5})
+    for (int mode : {0, 8})
     for (int ts = 0; ts < 2; ++ts) {
         for (int N : {16, 64, 256}) {
             for (int rep = 0; rep < 2; ++rep) {
@@ -136,9 +149,9 @@ int main() {
                 double avg = 0;
                 for (int i = 0; i < sms; ++i) avg += (double)h[i];
                 avg /= sms;
-                const double flops = 2.0 * 128 * N * 16 * R * sms;
+                const double flops = 2.0 * 128 * N * ((mode & 8) ? 32 : 16) * R * sms;
                 if (rep)
-                    printf("mode %d %s N=%3d: %.1f cycles per MMA (M128 K16), %.1f TFLOP/s over %d SMs (%.3f ms)\n",
+                    printf("mode %d %s N=%3d: %.1f cycles per MMA (M128, K16 bf16 / K32 i8), %.1f TFLOP/s over %d SMs (%.3f ms)\n",
                            mode, ts ? "TS (A in TMEM)" : "SS (A in smem)", N, avg / R,
                            flops / (ms * 1e-3) / 1e12, sms, ms);
             }
