@@ -329,6 +329,7 @@ def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
     kms = [km] + ([km.clone() for _ in range(3)] if km is not None else [])
     dense = dense_device(pm).to(torch.bfloat16)
     Wb = [dense, dense.clone()]  # 2 x 134 MB > L2
+    Wi = [dense.to(torch.int8), dense.to(torch.int8)]  # 2 x 67 MB
     rows = []
     for B in Bs:
         V = torch.stack([torch.from_numpy(random_vector(n, b)) for b in range(B)]).to(
@@ -343,17 +344,38 @@ def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
         Yd = torch.empty(B, m, dtype=torch.bfloat16, device="cuda")
         us_cub = graph_time_us(lambda i: torch.matmul(V, Wb[i % 2].t(), out=Yd))
         alg = (a.file_bytes() - 24) + B * (n * 2 + m * 4)
-        rows.append({"B": B, "us": us, "vectors_s": B / us * 1e6, "cublas_us": us_cub,
-                     "vs_cublas": us_cub / us, "alg_bytes": int(alg),
-                     "alg_gbs": alg / us / 1e3})
+        row = {"B": B, "us": us, "vectors_s": B / us * 1e6, "cublas_us": us_cub,
+               "vs_cublas": us_cub / us, "alg_bytes": int(alg), "alg_gbs": alg / us / 1e3}
+        if B >= 2:
+            # the exact integer path on the int8 tensor cores (int8 batch ->
+            # int32), beside cuBLASLt's dense int8 GEMM of the same matrix
+            Vi = torch.randint(-128, 128, (B, n), dtype=torch.int8, device="cuda")
+            Yi = torch.empty(B, m, dtype=torch.int32, device="cuda")
+            kmi = [a.keymat("i8")] + [a.keymat("i8").clone() for _ in range(3)]
+
+            def ours_i8(i):
+                a.__dict__["_keymat_i8"] = kmi[i % 4]
+                kn.matmul_into(a, Vi, Yi)
+            row["int8_us"] = graph_time_us(ours_i8)
+            a.__dict__["_keymat_i8"] = kmi[0]
+            if B > 16 and Wi is not None:
+                try:
+                    row["cublas_int8_us"] = graph_time_us(
+                        lambda i: torch._int_mm(Vi, Wi[i % 2].t()))
+                    row["int8_vs_cublas_int8"] = row["cublas_int8_us"] / row["int8_us"]
+                except RuntimeError:
+                    pass
+        rows.append(row)
     if kms:
         a.__dict__["_keymat"] = kms[0]
-    del Wb, dense
+    del Wb, Wi, dense
     torch.cuda.empty_cache()
     return {"workload": "ternary 8192x8192, k=5, bf16 vectors [B, 8192] -> f32 [B, 8192]",
             "api": "rsr_matvec_batched / kernels.matmul_into(method='auto')",
             "timing": "CUDA-graph replays of 4 back-to-back calls over rotated stream copies",
             "cublas": "torch.matmul(V bf16 [B, 8192], W bf16 [8192, 8192]^T)",
+            "int8": "int8_us: int8 batch -> exact int32 on tcgen05 kind::i8 (matmul_into auto); "
+                    "cublas_int8_us: torch._int_mm(V int8, W int8^T) (cuBLASLt, B > 16)",
             "rows": rows}
 
 
