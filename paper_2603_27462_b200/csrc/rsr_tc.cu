@@ -303,7 +303,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     const int rank = (int)(blockIdx.x - t0 * ks);  // = %cluster_ctarank (1-d clusters)
     const int64_t w0 = t0 * p.S + p.S * rank / ks, w1 = t0 * p.S + p.S * (rank + 1) / ks;
     const int64_t nst = w1 - w0;
-    const int64_t wsplit = w1;  // one segment
 
     // smem: per load stage [B tile: 2 K-halves x N x 128 B][codes 128 rows x 32 B]
     constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * (I8 ? 1 : 2);
@@ -337,6 +336,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     const uint32_t tmem_d = tmem_base_sh;
     TC_MARK(tid == 0, 512)
     TC_CTA_MARK(1)
+#ifdef RSR_TC_DBG
+    if (threadIdx.x == 0 && blockIdx.x < 1024) tc_cta_t[blockIdx.x * 8 + 6] = clock64();
+#endif
 
     if (warp == TC_EXP_WARPS) {
         // ---- producer: lanes 0 .. J-1 load J consecutive steps at once (a
@@ -393,18 +395,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             // its 64-column half (the swizzle applies to the absolute address)
             const uint64_t db0 = smem_desc(sbase, 16, 1024) | ((uint64_t)2 << 61);
             int s = 0, a = 0;
-            uint32_t par = 0, apar = 0;
-            const int64_t n0 = wsplit - w0;  // steps of segment 0
+            uint32_t apar = 0;
+#ifdef RSR_TC_DBG
+            long long c_prev = 0;
+#endif
             for (int64_t it = 0; it < nst; ++it) {
-                const int seg = it >= n0 ? 1 : 0;
-                const bool first = it == 0 || it == n0;
+                const bool first = it == 0;
 #ifdef RSR_TC_DBG
                 const long long c0 = clock64();
+                const long long c1 = c0;
+                const long long dstep = it ? c0 - c_prev : 0;
+                c_prev = c0;
 #endif
-                mbar_wait_parity(bar_full + 8 * s, par);
-#ifdef RSR_TC_DBG
-                const long long c1 = clock64();
-#endif
+                // A stage ready: its expanders waited on the load slot's full
+                // barrier (the TMA'd B tile) before arriving, so this one wait
+                // orders both operands before the MMAs
                 mbar_wait_parity(bar_aready + 8 * a, apar);
 #ifdef RSR_TC_DBG
                 const long long c2 = clock64();
@@ -413,7 +418,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint64_t db = db0 + ((s * SLOT) >> 4);
                 const uint32_t ta = tmem_d + p.a_col + ASC * a;
-                const uint32_t td = tmem_d + (uint32_t)(seg * N);
+                const uint32_t td = tmem_d;
                 if (I8) {
                     // K = 32 int8 per MMA: 32 B into the 128-byte swizzled rows
 #pragma unroll
@@ -430,19 +435,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 }
                 mma_commit(bar_empty + 8 * s);
                 mma_commit(bar_aempty + 8 * a);
-                if (it + 1 == n0 || it + 1 == nst) mma_commit(bar_done + 8 * seg);
+                if (it + 1 == nst) mma_commit(bar_done);
 #ifdef RSR_TC_DBG
                 if (blockIdx.x == 0 && it < 64) {
                     const long long c3 = clock64();
-                    tc_mma_cyc[it * 3 + 0] = c1 - c0;
+                    tc_mma_cyc[it * 3 + 0] = dstep + (c1 - c0);
                     tc_mma_cyc[it * 3 + 1] = c2 - c1;
                     tc_mma_cyc[it * 3 + 2] = c3 - c2;
                 }
 #endif
-                if (++s == LS) {
-                    s = 0;
-                    par ^= 1u;
-                }
+                if (++s == LS) s = 0;
                 if (++a == AS) {
                     a = 0;
                     apar ^= 1u;
@@ -504,6 +506,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     __syncwarp();
     TC_MARK(tid == 0, 513)
     TC_CTA_MARK(2)
+#ifdef RSR_TC_DBG
+    if (threadIdx.x == 0 && blockIdx.x < 1024) tc_cta_t[blockIdx.x * 8 + 7] = clock64();
+#endif
 
     // --- epilogue: warps 0-3 read the accumulator (warp w: TMEM lanes
     // 32w .. 32w + 31 = tile rows), 8 columns at a time; alone in its

@@ -42,6 +42,8 @@ L.rsr_tc_debug_ctas(ctypes.addressof(cb))
 c = np.array(cb[:], dtype=np.int64).reshape(1024, 8)
 c = c[c[:, 0] > 0]
 flags = np.zeros(len(c), np.int64)
+mhz = (c[:, 7] - c[:, 6]) / ((c[:, 2] - c[:, 1]) / 1e3)
+print(f"SM clock over the main loop (clock64 / globaltimer): median {np.median(mhz):.0f} MHz, min {mhz.min():.0f}")
 base = c[:, 0].min()
 c = (c[:, [0, 1, 2, 4, 5, 3]] - base) / 1e3
 print(f"CTAs {len(c)}: entry max {c[:,0].max():.2f} us; setup {np.median(c[:,1]-c[:,0]):.2f}; loop median {np.median(c[:,2]-c[:,1]):.2f} max {np.max(c[:,2]-c[:,1]):.2f}; "
@@ -56,5 +58,5 @@ L.rsr_tc_debug_mma.argtypes = [ctypes.c_void_p]
 L.rsr_tc_debug_mma(ctypes.addressof(mb))
 m3 = np.array(mb[:], dtype=np.int64).reshape(64, 3)
 m3 = m3[: max(1, int((m3.sum(1) > 0).sum()))]
-print("MMA thread cycles/step (median): full wait %d, aready wait %d, issue+commit %d" % tuple(np.median(m3, 0)))
+print("MMA thread cycles/step (median): step period %d, aready wait %d, issue+commit %d" % tuple(np.median(m3, 0)))
 print("  per step:", " ".join(f"{a}/{b}/{c}" for a, b, c in m3[:24]))
