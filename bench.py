@@ -15,7 +15,7 @@ Workloads (BASELINE.json configs):
 rotating >= 3 copies of the stream (inputs larger than L2 per step).  The K
 timed launches are queued behind a short device spin, so the region measures
 the device back to back (not the host's launch rate or a cold first launch
-after an idle gap).  `e2e` = the same metric through the public API with a
+after an idle gap); --graph (one GPU) replays them as one CUDA graph instead.  `e2e` = the same metric through the public API with a
 host (numpy float32) vector and a host result (rank 0, unsharded configs).
 
 Sub-objects (N=1): `cublas_bf16` (the dense bf16 GEMV of the same matrix,
@@ -507,6 +507,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="one GPU: time the K steps as one CUDA-graph replay (pays the graph "
+                         "launch once: slower than queued launches at K = 20, faster at 200)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip cublas_bf16 / c4 / traffic sub-measurements")
     ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
@@ -594,8 +597,9 @@ def main():
     sptr = stream.cuda_stream
     y_full = torch.empty(m, dtype=torch.float32, device=dev)
 
-    def step(i):
-        kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies], stream=sptr)
+    def step(i, sp=None):
+        kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies],
+                       stream=sptr if sp is None else sp)
         if world > 1:
             dist.all_gather_into_tensor(y_all, y_local)
             torch.index_select(y_all, 0, sm.index, out=y_full)  # full y in row order
@@ -614,7 +618,25 @@ def main():
     torch.cuda.synchronize()
     kernel_ms = float(np.median([e0.elapsed_time(e1) for e0, e1 in kev]))
 
-    # ---- timed region: exactly K steps, queued behind a device spin
+    # ---- timed region: exactly K steps, queued behind a device spin (or, with
+    # --graph on one GPU, captured as one CUDA graph and replayed once)
+    use_graph = world == 1 and args.graph
+    graph = None
+    if use_graph:
+        gstream = torch.cuda.Stream(dev)
+        gstream.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gstream):
+            for i in range(args.steps):  # warm the capture stream's path
+                step(i, gstream.cuda_stream)
+            gstream.synchronize()
+            with torch.cuda.graph(graph, stream=gstream):
+                for i in range(args.steps):
+                    step(i, gstream.cuda_stream)
+        stream.wait_stream(gstream)
+        for _ in range(max(1, warmup // max(1, args.steps))):
+            graph.replay()
+        torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t_load = time.perf_counter()  # untimed load while the sampler starts
@@ -625,11 +647,16 @@ def main():
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        torch.cuda._sleep(spin_cycles(args.steps))
-        start.record(stream)
-        for i in range(args.steps):
-            step(i)
-        end.record(stream)
+        if use_graph:
+            start.record(stream)
+            graph.replay()
+            end.record(stream)
+        else:
+            torch.cuda._sleep(spin_cycles(args.steps))
+            start.record(stream)
+            for i in range(args.steps):
+                step(i)
+            end.record(stream)
         torch.cuda.synchronize()
         t_hold = time.perf_counter()  # keep the GPU loaded for the sampler (untimed)
         while time.perf_counter() - t_hold < 0.5:
@@ -728,8 +755,9 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config,
             "l2_copies": f"{ncopies} stream copies ({sb / 1e6:.1f} MB each, L2 {l2 / 1e6:.0f} MB)",
-            "timing": "K launches queued behind a device spin; CUDA events on the launch "
-                      "stream; max over ranks",
+            "timing": ("the K steps as one CUDA-graph replay (captured launches, PDL edges kept)"
+                       if use_graph else "K launches queued behind a device spin")
+                      + "; CUDA events on the launch stream; max over ranks",
             "preprocess_ms": preprocess_ms, "gpu_launches": args.steps * launches_per_step,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
     line.update(extras)
