@@ -194,6 +194,7 @@ struct TcParams {
     int64_t n, row0, rows_view, rows_pad;
     int64_t S;           // steps per tile (= tc_steps(n))
     int B, N, ks, ls, as;  // ks: CTAs per tile (cluster size)
+    uint32_t recv_off;     // N <= 64: byte offset of the cluster-reduction receive buffer
     uint32_t a_col, tmem_cols;  // TMEM column of A stage 0; columns allocated
     uint32_t tab0, tab1;        // PRMT byte table {00 3F BF 00 | 00 80 80 00}
 };
@@ -336,9 +337,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     const uint32_t tmem_d = tmem_base_sh;
     TC_MARK(tid == 0, 512)
     TC_CTA_MARK(1)
-#ifdef RSR_TC_DBG
-    if (threadIdx.x == 0 && blockIdx.x < 1024) tc_cta_t[blockIdx.x * 8 + 6] = clock64();
-#endif
 
     if (warp == TC_EXP_WARPS) {
         // ---- producer: lanes 0 .. J-1 load J consecutive steps at once (a
@@ -506,9 +504,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     __syncwarp();
     TC_MARK(tid == 0, 513)
     TC_CTA_MARK(2)
-#ifdef RSR_TC_DBG
-    if (threadIdx.x == 0 && blockIdx.x < 1024) tc_cta_t[blockIdx.x * 8 + 7] = clock64();
-#endif
 
     // --- epilogue: warps 0-3 read the accumulator (warp w: TMEM lanes
     // 32w .. 32w + 31 = tile rows), 8 columns at a time; alone in its
@@ -516,10 +511,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     // (now idle) load ring as acc[column][row] for the cluster reduction
     const int64_t r_first = t0 * TC_M;
     float *acc_sm = reinterpret_cast<float *>(tc_smem);
+    // N <= 64: push mode -- each rank stores its accumulator straight into
+    // the owning rank's receive buffer recv[rank][b][row - owner's first row]
+    // (DSMEM stores, no round trip), one cluster barrier, local sums
+    constexpr bool PUSH = N <= 64;
+    const int RM = (TC_M + ks - 1) / ks;  // rows per rank slot
     if (warp < 4) {
         const int row_t = warp * 32 + (int)lane;
         const int64_t vrow = r_first + row_t;
         const bool valid = vrow < p.rows_view;
+        const int owner = ((row_t + 1) * ks - 1) / TC_M;
+        const int orow = row_t - owner * TC_M / ks;
+        uint32_t owin = 0;
+        if (PUSH && ks > 1)
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(owin)
+                         : "r"((uint32_t)__cvta_generic_to_shared(tc_smem) + p.recv_off),
+                           "r"(owner));
         mbar_wait_parity(bar_done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         for (int c = 0; c < N; c += 8) {
@@ -537,6 +545,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                         if (c + j < p.B)
                             tc_store<I8>(p, c + j, vrow, r[j]);
                 }
+            } else if (PUSH) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (c + j < p.B)
+                        asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(
+                                         owin + (uint32_t)(((rank * p.B + c + j) * RM + orow) * 4)),
+                                     "r"(r[j])
+                                     : "memory");
             } else {
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -545,7 +561,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         }
     }
     TC_CTA_MARK(4)
-    if (ks > 1) {
+    if (PUSH && ks > 1) {
+        // every rank's pushes are in (release / acquire): sum this rank's rows
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        TC_CTA_MARK(5)
+        const int rbase = rank * TC_M / ks, rows = (rank + 1) * TC_M / ks - rbase;
+        const uint32_t *recv = reinterpret_cast<const uint32_t *>(tc_smem + p.recv_off);
+        for (int e = tid; e < p.B * rows; e += TC_THREADS) {
+            const int b = e / rows, rr = e - b * rows;
+            uint32_t sum;
+            if (I8) {
+                sum = 0u;
+                for (int q = 0; q < ks; ++q) sum += recv[(q * p.B + b) * RM + rr];
+            } else {
+                float f = __uint_as_float(recv[b * RM + rr]);
+                for (int q = 1; q < ks; ++q) f += __uint_as_float(recv[(q * p.B + b) * RM + rr]);
+                sum = __float_as_uint(f);
+            }
+            const int64_t vrow = r_first + rbase + rr;
+            if (vrow < p.rows_view) tc_store<I8>(p, b, vrow, sum);
+        }
+    } else if (ks > 1) {
         // every rank's accumulator is in its shared memory -> each rank sums
         // rows [rank 128 / ks, (rank + 1) 128 / ks) over ranks 0 .. ks-1
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -587,8 +623,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             const int64_t vrow = r_first + rt;
             if (vrow < p.rows_view) tc_store<I8>(p, b, vrow, sum);
         }
+        TC_CTA_MARK(6)
         // no rank leaves (freeing its shared memory) before all have read it
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        TC_CTA_MARK(7)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -610,13 +648,18 @@ static size_t tc_slot_bytes(int N, int esize) {
     return (size_t)N * TC_K * esize + (size_t)TC_M * TC_RB;
 }
 
+// N <= 64: the cluster reduction's receive buffer after the ring, sized for
+// any ks <= 8 (ks x B x ceil(128 / ks) words <= N x 135)
+static size_t tc_recv_bytes(int N) { return N <= 64 ? (size_t)N * (TC_M + 7) * 4 : 0; }
+
 static int tc_load_stages(int N, int esize) {
     return (int)std::max<size_t>(
-        TC_GROUPS, std::min<size_t>(TC_LMAX, (216 * 1024) / tc_slot_bytes(N, esize)));
+        TC_GROUPS, std::min<size_t>(TC_LMAX, (216 * 1024 - tc_recv_bytes(N)) /
+                                                 tc_slot_bytes(N, esize)));
 }
 
 static size_t tc_smem_bytes(int N, int esize) {
-    return tc_load_stages(N, esize) * tc_slot_bytes(N, esize);
+    return tc_load_stages(N, esize) * tc_slot_bytes(N, esize) + tc_recv_bytes(N);
 }
 
 static int64_t tc_view_rows(int64_t block_begin, int64_t n_blocks, int32_t k, int64_t m) {
@@ -800,6 +843,7 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     p.N = 16 * np;
     p.S = tc_steps(n);
     p.ls = tc_load_stages(p.N, esize);
+    p.recv_off = (uint32_t)(p.ls * tc_slot_bytes(p.N, esize));
     // TMEM (all 512 columns): the accumulator [0, N) (64-column aligned),
     // then the A ring: one step's 128 K elements per stage (64 columns of
     // bf16 pairs, 32 of int8 quads)

@@ -42,8 +42,9 @@ L.rsr_tc_debug_ctas(ctypes.addressof(cb))
 c = np.array(cb[:], dtype=np.int64).reshape(1024, 8)
 c = c[c[:, 0] > 0]
 flags = np.zeros(len(c), np.int64)
-mhz = (c[:, 7] - c[:, 6]) / ((c[:, 2] - c[:, 1]) / 1e3)
-print(f"SM clock over the main loop (clock64 / globaltimer): median {np.median(mhz):.0f} MHz, min {mhz.min():.0f}")
+if (c[:, 6] > 0).all():
+    print(f"cluster reduction: loads+stores median {np.median(c[:,6]-c[:,5])/1e3:.2f} us, "
+          f"2nd barrier {np.median(c[:,7]-c[:,6])/1e3:.2f} us, then to exit {np.median(c[:,3]-c[:,7])/1e3:.2f} us")
 base = c[:, 0].min()
 c = (c[:, [0, 1, 2, 4, 5, 3]] - base) / 1e3
 print(f"CTAs {len(c)}: entry max {c[:,0].max():.2f} us; setup {np.median(c[:,1]-c[:,0]):.2f}; loop median {np.median(c[:,2]-c[:,1]):.2f} max {np.max(c[:,2]-c[:,1]):.2f}; "
