@@ -8,7 +8,10 @@ Workloads (BASELINE.json configs):
       the ranks (each rank generates and preprocesses only its strip with the
       device generator) + NCCL all-gather of the output slices + reassembly
       of the full output in row order.  Strong scaling: every step is one
-      full 131072^2 matvec for the whole job.
+      full 131072^2 matvec for the whole job.  The N > 1 line also carries
+      the same matrix on rank 0's GPU alone, timed in the same run
+      (`c5_1gpu`, `scaling_vs_1gpu_same_run`): the N = 1 bench line is the
+      C2 headline, not this matrix.
   c1, c4 (binary 4096^2 k=8 f32 vector; ternary 8192^2 k=5) on request.
 
 `value` = matvec/s with the stream resident in HBM; L2 is defeated by
@@ -740,6 +743,20 @@ def main():
                 extras[name] = fn()
             except Exception as e:  # reported, never silently replaced
                 extras[name] = {"error": repr(e)[:300]}
+    if world > 1 and not args.no_extras:
+        # the same matrix on rank 0's GPU alone, in this run: the N = 1 point
+        # of this strong-scaling line (the N = 1 bench line is C2, the headline)
+        try:
+            c5 = side_config_bench(cname, hbm)
+            extras["c5_1gpu"] = c5
+            extras["scaling_vs_1gpu_same_run"] = {
+                "one_gpu_matvec_s": c5["matvec_s"], "n_gpus": world,
+                "speedup": value / c5["matvec_s"],
+                "efficiency": value / c5["matvec_s"] / world,
+                "note": "whole-job matvec/s of this sharded run over rank 0's GPU alone on the "
+                        "unsharded matrix (same process, same box)"}
+        except Exception as e:  # reported, never silently replaced
+            extras["c5_1gpu"] = {"error": repr(e)[:300]}
 
     decode = None
     if world == 1 and not args.no_decode:
