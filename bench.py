@@ -303,7 +303,9 @@ def side_config_bench(cname: str, hbm: float):
     us = graph_time_us(lambda i: kn.matvec_into(a, v, y, view=views[i % nc]), copies=nc,
                        iters=max(nc, 40 if sb < 1e9 else 8))
     alg = (a.file_bytes() - 24) + n * (2 if cfg["vdtype"] == "bf16" else 4) + m * 4
-    out = {"workload": cfg["workload"], "k": k, "tile_width": a.plan.tile_width,
+    wl = cfg["workload"].split(", row-block sharded")[0]
+    out = {"workload": wl + (", one GPU, unsharded" if wl != cfg["workload"] else ""),
+           "k": k, "tile_width": a.plan.tile_width,
            "format": a.format, "us": us, "matvec_s": 1e6 / us, "alg_bytes": int(alg),
            "alg_gbs": alg / us / 1e3, "frac_hbm": alg / us / 1e3 / hbm,
            "preprocess_ms": pre_ms,
@@ -553,12 +555,21 @@ def main():
     from paper_2603_27462_b200 import shard
     from paper_2603_27462_b200.devicepack import random_ternary_device
 
+    # functional check of the N > 1 code path on a one-GPU box (never a
+    # measurement): RSR_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 and
+    # RSR_BENCH_DIST_BACKEND=gloo carries the collective
+    if os.environ.get("RSR_BENCH_ONE_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("RSR_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     m, n, k = cfg["m"], cfg["n"], cfg["k"]
     full_packed = None
