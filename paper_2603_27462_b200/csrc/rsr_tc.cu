@@ -1,5 +1,8 @@
 // rsr_tc.cu -- batched multi-vector multiply on the 5th-generation tensor
-// cores: Y[b] = M . V[b] for bf16 V.
+// cores: Y[b] = M . V[b] for a batch of
+// bf16 vectors (kind::f16, fp32 accumulation) or int8 vectors (kind::i8,
+// exact int32 -- optionally dequantized in the epilogue for the batched
+// fused path).
 //
 // RSR's pattern-table step y_blk = T . S_blk (T in {0,+-1}^{k x P}) is a
 // dense contraction; with B vectors it is cheaper to apply T before the
@@ -10,43 +13,38 @@
 // matrix entry (16.8 MB at C4) -- and expands it straight into the A operand
 // of tcgen05.mma, which reads A from TENSOR MEMORY:
 //
-//   D[row][b] += A[row][col] * B[b][col],  A = T[:, key(blk, col)] (bf16 +-1/0, TMEM),
-//                                          B = V chunk (bf16, K-major, shared memory)
+//   D[row][b] += A[row][col] * B[b][col],  A = T[:, key(blk, col)] (TMEM),
+//                                          B = V (TMA box, shared memory)
 //
-// Tile: M = 128 rows (TMEM lanes), K = 64 columns per step, N = vectors
-// (16..256).  Warp-specialized, two rings per CTA:
-//   warp 8  (producer)  bulk-copies (cp.async.bulk, mbarrier complete_tx) the
-//                       step's code rows (128 x 16 B) and its pre-packed B
-//                       tile into a LOAD ring (up to 16 stages; freed by the
-//                       MMA's commit);
-//   warps 0-7 (expand)  thread = tile row (warps 0-3 the even steps, 4-7
-//                       the odd ones): one 16-byte code load -> 32 words of
-//                       two bf16 signs (per pair of words a shift, a mask,
-//                       an IMAD and two PRMTs from a register byte table) ->
-//                       one tcgen05.st 32x32b.x32 into the row's TMEM lane,
-//                       in an A ring of 32-column TMEM stages (freed by the
-//                       MMA);
-//   warp 9  (MMA)       one thread issues tcgen05.mma (A from TMEM, fp32 D in
-//                       TMEM) and commits to both rings' "empty" barriers.
-// The A tile never touches shared memory: shared-memory traffic per step is
-// the B tile and 2 KB of codes, and the expansion is a few integer
-// instructions per word (round 1 staged A in shared memory: 32 KB of
-// shared traffic per step and a 4-stage ring whose slots waited on the MMA;
-// ~22 us at C4 for every B).
+// Tile: M = 128 rows (TMEM lanes), K = 128 columns per step, N = vectors
+// padded to 16 .. 256.  One 576-thread CTA per SM (all 512 TMEM columns),
+// warp-specialized:
+//   warp 16 (producer)  lanes 0-7 each own a step of a ring of up to 16 load
+//                       slots: one cp.async.bulk of the step's 128 code rows
+//                       (4 KB) and the step's B tile as 2-d TMA boxes of V
+//                       itself (SWIZZLE_128B K-major; vectors >= B and
+//                       columns >= n zero-filled), all on the slot's "full"
+//                       mbarrier (complete_tx);
+//   warps 0-15 (expand) 2 step groups x 2 column halves x 4 TMEM lane
+//                       quarters; thread = (row, 64 columns): one 16-byte
+//                       code load -> 32 bf16-pair words (shift, mask, IMAD,
+//                       2 PRMT per pair) or 16 int8-quad words (mask + PRMT)
+//                       -> one tcgen05.st into the row's TMEM lane, in an A
+//                       ring of TMEM stages (64 / 32 columns per step);
+//   warp 17 (MMA)       one thread waits on the A stage (its expanders waited
+//                       on the load slot), issues 8 x K16 (bf16) / 4 x K32
+//                       (int8) MMAs, commits to the slot's and the stage's
+//                       "empty" barriers.
+// The A tile never touches shared memory (round 1 staged it there: 32 KB of
+// shared traffic per step and ~22 us at C4 for every B).  Split-K runs
+// inside thread-block clusters (below); the tensor pipe's A rate -- ~45
+// cycles per M128 x K16 / K32 instruction at N <= 64 -- is the bound
+// (profiles/r02_umma_microbench.txt).
 //
-// Code matrix layout [step = col / 64][row][4 x u32]: u32 q holds columns
-// 16q .. 16q + 15 of the step, permuted so that one shift + mask gives the
-// PRMT selectors of two words: column pair j (columns 2j, 2j+1) has its codes
-// at bits 2 (j % 4) of bytes 2 (j / 4) and 2 (j / 4) + 1.  A tile's step is
-// one contiguous run of rows.  V is repacked once per call into the K-major
-// no-swizzle core-matrix image of each step (tc_pack_v_kernel), so its B
-// tile is one bulk copy too.  Products with +-1 are exact and accumulate in
-// fp32: the float-path tolerance holds.  Work is split stream-K style: CTA c
-// takes items [c W / G, (c + 1) W / G) of the (tile, step) sequence, so the
-// SMs get equal shares; a tile with several contributors is summed from
-// their partials, in CTA order (deterministic), by whichever contributor
-// arrives last (a per-tile counter in the workspace, left at zero) -- one
-// launch per call, no finalize kernel.
+// Code matrix layout [step = col / 128][row][8 x u32]: u32 q holds columns
+// 16q .. 16q + 15 of the step, permuted so the expansion needs one shift +
+// mask per pair of words (bf16: tc_code_bit; int8: tc_code_bit_i8).  A
+// tile's step is one contiguous run of rows.
 #include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime)
 
 #include <cstdio>
@@ -286,10 +284,12 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32
 // N = 16 * NP: MMA N (vectors padded up, <= 256).
 // Split-K over thread-block clusters: cluster t (ks CTAs) owns row tile t,
 // CTA rank r its steps [r S / ks, (r + 1) S / ks).  Each CTA accumulates in
-// TMEM, moves its accumulator to its own shared memory, and after a cluster
-// barrier every rank sums a slice of the tile's rows over all ranks' copies
-// (DSMEM loads, rank order: deterministic) and writes Y.  No partials in
-// global memory, one launch per call.
+// TMEM; rank r then owns rows [r 128 / ks, (r + 1) 128 / ks) of the tile and
+// sums them over all ranks' accumulators in rank order (deterministic):
+// N <= 64 pushes every accumulator row into its owner's receive buffer
+// (DSMEM stores, one cluster barrier); larger N parks the accumulator in the
+// CTA's idle load ring and the owners read it through DSMEM.  No partials
+// in global memory, one launch per call.
 template <int NP, bool I8>
 __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_constant__ TcParams p) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     const uint32_t bar_full = bar0, bar_empty = bar0 + 8 * TC_LMAX;
     const uint32_t bar_aready = bar0 + 16 * TC_LMAX, bar_aempty = bar_aready + 8 * TC_AMAX;
-    const uint32_t bar_done = bar_aempty + 8 * TC_AMAX;  // one per segment
+    const uint32_t bar_done = bar_aempty + 8 * TC_AMAX;  // accumulator complete
 
     if (warp == TC_EXP_WARPS + 1) {  // TMEM: accumulators + the A ring
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
