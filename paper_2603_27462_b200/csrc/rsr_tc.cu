@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             const int64_t vrow = r_first + rbase + rr;
             if (vrow < p.rows_view) tc_store<I8>(p, b, vrow, sum);
         }
+        TC_CTA_MARK(6)
     } else if (ks > 1) {
         // every rank's accumulator is in its shared memory -> each rank sums
         // rows [rank 128 / ks, (rank + 1) 128 / ks) over ranks 0 .. ks-1
@@ -861,7 +862,12 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     // PRMT byte tables: bf16 {00 3F BF 00 | 00 80 80 00}; int8 {00 01 FF 00}
     p.tab0 = I8 ? 0x00FF0100u : 0x00BF3F00u;
     p.tab1 = 0x00808000u;
-    const size_t smem = tc_smem_bytes(p.N, esize);
+    // exactly one CTA per SM: each allocates all 512 TMEM columns, and a
+    // second resident CTA would block in tcgen05.alloc while its cluster
+    // partners wait for it at the cluster barrier.  Shared memory above half
+    // the SM's 228 KB guarantees it (registers alone would not for small
+    // int8 batches).
+    const size_t smem = std::max<size_t>(tc_smem_bytes(p.N, esize), 116 * 1024);
     if (smem > 227 * 1024) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     // programmatic dependent launch (PDL): the prologue overlaps the previous
@@ -888,6 +894,13 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
         auto kern = rsr_tc_kernel<NPV, I8>;                                                    \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
         int ks = tc_ks_cached(key_np, tiles, p.S, smem);                                       \
+        if (ks == 0) { /* first launch of this shape: one CTA per SM, checked once */          \
+            int per_sm = 0;                                                                    \
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS,       \
+                                                              smem) != cudaSuccess ||          \
+                per_sm != 1)                                                                   \
+                return RSR_ERR_INVALID;                                                        \
+        }                                                                                      \
         for (int c = 8; ks == 0 && c >= 2; --c) {                                              \
             if (forced_ks > 0 ? c != forced_ks : (c > p.S || tiles * c > sm_count())) continue; \
             attrs[1].val.clusterDim.x = c;                                                     \

@@ -43,8 +43,9 @@ c = np.array(cb[:], dtype=np.int64).reshape(1024, 8)
 c = c[c[:, 0] > 0]
 flags = np.zeros(len(c), np.int64)
 if (c[:, 6] > 0).all():
-    print(f"cluster reduction: loads+stores median {np.median(c[:,6]-c[:,5])/1e3:.2f} us, "
-          f"2nd barrier {np.median(c[:,7]-c[:,6])/1e3:.2f} us, then to exit {np.median(c[:,3]-c[:,7])/1e3:.2f} us")
+    last = np.where(c[:, 7] > 0, c[:, 7], c[:, 6])
+    print(f"cluster reduction: sums+stores median {np.median(c[:,6]-c[:,5])/1e3:.2f} us, "
+          f"then to exit {np.median(c[:,3]-last)/1e3:.2f} us")
 base = c[:, 0].min()
 c = (c[:, [0, 1, 2, 4, 5, 3]] - base) / 1e3
 print(f"CTAs {len(c)}: entry max {c[:,0].max():.2f} us; setup {np.median(c[:,1]-c[:,0]):.2f}; loop median {np.median(c[:,2]-c[:,1]):.2f} max {np.max(c[:,2]-c[:,1]):.2f}; "
