@@ -711,6 +711,37 @@ def main():
                "d2h_bytes_per_step": int(yh.nbytes),
                "api": "paper_2603_27462_b200.rsr_matvec(artifact, numpy float32 vector in "
                       "pinned memory) -> numpy float32"}
+    elif world > 1:
+        # sharded: every rank takes the host vector (pinned) to its GPU, runs
+        # ShardedMatrix.matvec (local multiply + all-gather + reassembly) and
+        # reads the full result back to the host; max over ranks
+        vh = torch.from_numpy(vf.copy()).pin_memory()
+        if cfg["vdtype"] == "bf16":
+            vh = vh.to(torch.bfloat16).pin_memory()
+        vd = torch.empty_like(vh, device=dev)
+        yh = torch.empty(m, dtype=torch.float32).pin_memory()
+        bufs = sm.buffers(torch.float32)
+
+        def e2e_step():
+            vd.copy_(vh, non_blocking=True)
+            yh.copy_(sm.matvec(vd, buffers=bufs), non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        for _ in range(5):
+            e2e_step()
+        dist.barrier()
+        ne = max(10, min(args.steps, 50))
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            e2e_step()
+        tt = torch.tensor([(time.perf_counter() - t0) / ne], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+        e2e = {"value": 1.0 / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(vh.numel() * vh.element_size()),
+               "d2h_bytes_per_step": int(yh.numel() * 4),
+               "api": "shard.ShardedMatrix.matvec on every rank: pinned host vector -> device, "
+                      "local multiply + NCCL all-gather + reassembly, full y -> pinned host; "
+                      "max over ranks"}
 
     if rank != 0:
         if dist:
