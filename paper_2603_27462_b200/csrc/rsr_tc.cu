@@ -530,32 +530,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                            "r"(owner));
         mbar_wait_parity(bar_done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int c = 0; c < N; c += 8) {
-            uint32_t r[8];
+        // 16 accumulator columns per TMEM load (one wait each)
+        for (int c = 0; c < N; c += 16) {
+            uint32_t r[16];
             asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+                "%10, %11, %12, %13, %14, %15}, [%16];"
                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                  "=r"(r[6]), "=r"(r[7])
+                  "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                  "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
                 : "r"(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (ks == 1) {
                 if (valid) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
+                    for (int j = 0; j < 16; ++j)
                         if (c + j < p.B)
                             tc_store<I8>(p, c + j, vrow, r[j]);
                 }
             } else if (PUSH) {
+                const uint32_t dst = owin + (uint32_t)(((rank * p.B + c) * RM + orow) * 4);
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+                for (int j = 0; j < 16; ++j)
                     if (c + j < p.B)
                         asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(
-                                         owin + (uint32_t)(((rank * p.B + c + j) * RM + orow) * 4)),
+                                         dst + (uint32_t)(j * RM * 4)),
                                      "r"(r[j])
                                      : "memory");
             } else {
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+                for (int j = 0; j < 16; ++j)
                     reinterpret_cast<uint32_t *>(acc_sm)[(c + j) * TC_M + row_t] = r[j];
             }
         }
@@ -567,8 +571,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         TC_CTA_MARK(5)
         const int rbase = rank * TC_M / ks, rows = (rank + 1) * TC_M / ks - rbase;
         const uint32_t *recv = reinterpret_cast<const uint32_t *>(tc_smem + p.recv_off);
-        for (int e = tid; e < p.B * rows; e += TC_THREADS) {
-            const int b = e / rows, rr = e - b * rows;
+        // thread = (row rr, vectors b0, b0 + bstep, ...): no divisions in the
+        // loop, consecutive threads on consecutive rows (coalesced Y stores)
+        const int bstep = TC_THREADS / rows, rr = tid % rows, b0 = tid / rows;
+        if (b0 < bstep)
+#pragma unroll 4
+        for (int b = b0; b < p.B; b += bstep) {
             uint32_t sum;
             if (I8) {
                 sum = 0u;
