@@ -571,6 +571,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         TC_CTA_MARK(5)
         const int rbase = rank * TC_M / ks, rows = (rank + 1) * TC_M / ks - rbase;
         const uint32_t *recv = reinterpret_cast<const uint32_t *>(tc_smem + p.recv_off);
+        // 32-bit outputs with 16-byte aligned rows: a thread takes four
+        // consecutive rows (one 16-byte shared load per rank, one 16-byte
+        // store); otherwise one row
+        const bool vec4 = !(I8 && p.dq_scales) && (rows & 3) == 0 && (rbase & 3) == 0 &&
+                          (p.ldy & 3) == 0 && (reinterpret_cast<uintptr_t>(p.Y) & 15) == 0 &&
+                          (RM & 3) == 0;
+        if (vec4) {
+            const int r4 = rows >> 2, bstep = TC_THREADS / r4, rq = tid % r4, b0 = tid / r4;
+            const int64_t vrow = r_first + rbase + 4 * rq;
+            if (b0 < bstep)
+                for (int b = b0; b < p.B; b += bstep) {
+                    uint4 acc = *reinterpret_cast<const uint4 *>(recv + b * RM + 4 * rq);
+                    for (int q = 1; q < ks; ++q) {
+                        const uint4 x =
+                            *reinterpret_cast<const uint4 *>(recv + (q * p.B + b) * RM + 4 * rq);
+                        if (I8) {
+                            acc.x += x.x, acc.y += x.y, acc.z += x.z, acc.w += x.w;
+                        } else {
+                            acc.x = __float_as_uint(__uint_as_float(acc.x) + __uint_as_float(x.x));
+                            acc.y = __float_as_uint(__uint_as_float(acc.y) + __uint_as_float(x.y));
+                            acc.z = __float_as_uint(__uint_as_float(acc.z) + __uint_as_float(x.z));
+                            acc.w = __float_as_uint(__uint_as_float(acc.w) + __uint_as_float(x.w));
+                        }
+                    }
+                    uint32_t *yo = reinterpret_cast<uint32_t *>(p.Y) + (int64_t)b * p.ldy + vrow;
+                    if (vrow + 3 < p.rows_view) {
+                        *reinterpret_cast<uint4 *>(yo) = acc;
+                    } else {
+                        const uint32_t v4[4] = {acc.x, acc.y, acc.z, acc.w};
+                        for (int j = 0; j < 4 && vrow + j < p.rows_view; ++j) yo[j] = v4[j];
+                    }
+                }
+        } else {
         // thread = (row rr, vectors b0, b0 + bstep, ...): no divisions in the
         // loop, consecutive threads on consecutive rows (coalesced Y stores)
         const int bstep = TC_THREADS / rows, rr = tid % rows, b0 = tid / rows;
@@ -588,6 +621,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             }
             const int64_t vrow = r_first + rbase + rr;
             if (vrow < p.rows_view) tc_store<I8>(p, b, vrow, sum);
+        }
         }
         TC_CTA_MARK(6)
     } else if (ks > 1) {
