@@ -56,11 +56,16 @@ CONFIGS = {
     "c5": dict(workload="ternary 131072x131072 RSR matvec, bf16 vector, row-block sharded "
                         "+ NCCL all-gather of outputs",
                m=131072, n=131072, bitwidth="ternary", k=6, vdtype="bf16", gen="hash",
-               tile_width=32704),  # widest halfword-format tile (5 tiles; the last 256 wide)
+               # 8 tiles of 16384 columns (measured on one GPU, tools/c5_tile_width.py:
+               # 1.084 ms vs 1.186 at 21846, 1.361 at 32704 -- wide tiles' 64 KB v images
+               # leave fewer warps per SM -- and 1.475 at 13108; 7.7% more artifact
+               # bytes than at 32704)
+               tile_width=16384),
 }
 METRIC = "ternary matvec/s & %HBM roofline at 16384^2; BitNet-2B-shape decode tok/s"
 UNIT = "matvec/s"
 L2_DEFEAT = "rotating >= 3 copies of the chunk stream (each step's inputs exceed L2)"
+L2_LARGE = "none needed: each step streams > 3x the 126 MB L2 (C5: 6.4 GB, 0.8 GB per rank at 8)"
 
 
 def make_config(cname: str, cfg: dict, world: int) -> dict:
@@ -71,7 +76,7 @@ def make_config(cname: str, cfg: dict, world: int) -> dict:
             "seed": 0, "density": 0.5,
             "generator": "rsrmv random_matrix (numpy)" if cfg["gen"] == "numpy"
             else "counter-based splitmix64 (device; CPU restatement in oracle/)",
-            "l2_defeat": L2_DEFEAT,
+            "l2_defeat": L2_LARGE if cname == "c5" else L2_DEFEAT,
             "parallelism": f"rowblock{world}" if world > 1 else "single"}
 
 
@@ -604,7 +609,9 @@ def main():
     # L2 defeat: rotate copies of the local stream
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     sb = a.stream_bytes()
-    ncopies = int(max(3, min(16, -(-3 * l2 // max(sb, 1)))))
+    # a stream far larger than L2 needs no rotation (rotating three 6.4 GB
+    # copies only adds TLB pressure a single artifact does not have)
+    ncopies = 1 if sb > 3 * l2 else int(max(3, min(16, -(-3 * l2 // max(sb, 1)))))
     copies = [(a.entries_d, a.e_off_d)] + [(a.entries_d.clone(), a.e_off_d.clone())
                                            for _ in range(ncopies - 1)]
     views = [a.view(entries=e, e_off=o) for e, o in copies]

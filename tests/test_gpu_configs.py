@@ -92,12 +92,12 @@ def test_c4_ternary_8192_k5_full_size(rsr):
     assert float_ok(y, yr, np.abs(orc.decode(p)).astype(np.float64), vr).all()
 
 
-@pytest.mark.parametrize("strip,tw", [(0, None), (1, None), (2, 32704), (3, 32704)])
+@pytest.mark.parametrize("strip,tw", [(0, None), (1, None), (2, 32704), (3, 32704), (4, 16384)])
 def test_c5_sampled_strips_vs_oracle(rsr, strip, tw):
     """C5 (ternary 131072 columns, k=6): random row strips of the device
     generator vs the oracle's restatement of it, at the reference's default
-    tiles (4 x 32768, format 0) and the bench's halfword-format tiles
-    (32704 wide: 5 tiles, the last 256 columns)."""
+    tiles (4 x 32768, format 0), the widest halfword-format tiles (32704: 5
+    tiles, the last 256 columns) and the bench's 8 x 16384."""
     import torch
     from paper_2603_27462_b200.devicepack import random_ternary_device
     n, k, rows = 131072, 6, 36
@@ -107,7 +107,7 @@ def test_c5_sampled_strips_vs_oracle(rsr, strip, tw):
     host = orc.random_ternary_rows(row0, rows, n, 0, 0.5)
     assert np.array_equal(dev.device_data().cpu().numpy(), host.data)
     a = rsr.preprocess(dev, k, tw)
-    assert a.plan.tile_count == (4 if tw is None else 5)
+    assert a.plan.tile_count == {None: 4, 32704: 5, 16384: 8}[tw]
     assert a.format == (0 if tw is None else 3)
     ref = orc.preprocess(host, k, tw)
     assert np.array_equal(a.words, ref.words) and np.array_equal(a.perm, ref.perm)
