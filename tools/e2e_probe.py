@@ -34,3 +34,25 @@ def dev_sync():
     torch.cuda.synchronize()
 print(f"device-only launch + sync            {t(dev_sync):7.1f} us")
 print(f"launch only (back to back)           {t(lambda: kn.matvec_into(a, dv, y)):7.1f} us")
+
+# round-trip latency floor: an empty kernel + stream sync, and the same with
+# an event polled in a loop (no blocking wait)
+x = torch.zeros(1, device="cuda")
+s = torch.cuda.current_stream()
+def empty_sync():
+    x.add_(1)
+    s.synchronize()
+print(f"empty kernel + stream sync           {t(empty_sync):7.1f} us")
+ev = torch.cuda.Event()
+def empty_poll():
+    x.add_(1)
+    ev.record(s)
+    while not ev.query():
+        pass
+print(f"empty kernel + event poll            {t(empty_poll):7.1f} us")
+def dev_poll():
+    kn.matvec_into(a, dv, y)
+    ev.record(s)
+    while not ev.query():
+        pass
+print(f"device-only launch + event poll      {t(dev_poll):7.1f} us")
