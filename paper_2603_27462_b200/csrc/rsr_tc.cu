@@ -19,22 +19,23 @@
 // Tile: M = 128 rows (TMEM lanes), K = 128 columns per step, N = vectors
 // padded to 16 .. 256.  One 576-thread CTA per SM (all 512 TMEM columns),
 // warp-specialized:
-//   warp 16 (producer)  lanes 0-7 each own a step of a ring of up to 16 load
-//                       slots: one cp.async.bulk of the step's 128 code rows
-//                       (4 KB) and the step's B tile as 2-d TMA boxes of V
-//                       itself (SWIZZLE_128B K-major; vectors >= B and
-//                       columns >= n zero-filled), all on the slot's "full"
-//                       mbarrier (complete_tx);
+//   warp 16 (producer)  lanes 0-7 each own a step: one cp.async.bulk of the
+//                       step's 128 code rows (4 KB) into a codes ring of up
+//                       to 16 slots (freed by the expanders once they have
+//                       read them), and the step's B tile as 2-d TMA boxes of
+//                       V itself (SWIZZLE_128B K-major; vectors >= B and
+//                       columns >= n zero-filled) into a B ring paired with
+//                       the TMEM A ring (freed by the MMA's one commit);
 //   warps 0-15 (expand) 2 step groups x 2 column halves x 4 TMEM lane
 //                       quarters; thread = (row, 64 columns): one 16-byte
 //                       code load -> 32 bf16-pair words (shift, mask, IMAD,
 //                       2 PRMT per pair) or 16 int8-quad words (mask + PRMT)
 //                       -> one tcgen05.st into the row's TMEM lane, in an A
 //                       ring of TMEM stages (64 / 32 columns per step);
-//   warp 17 (MMA)       one thread waits on the A stage (its expanders waited
-//                       on the load slot), issues 8 x K16 (bf16) / 4 x K32
-//                       (int8) MMAs, commits to the slot's and the stage's
-//                       "empty" barriers.
+//   warp 17 (MMA)       one thread waits on the A stage and its B tile,
+//                       issues 8 x K16 (bf16) / 4 x K32 (int8) MMAs and one
+//                       commit that frees both (a commit costs the pipe ~45
+//                       cycles, so one per step, not two).
 // The A tile never touches shared memory (round 1 staged it there: 32 KB of
 // shared traffic per step and ~22 us at C4 for every B).  Split-K runs
 // inside thread-block clusters (below); the tensor pipe's A rate -- ~45
@@ -294,7 +295,7 @@ template <int NP, bool I8>
 __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_constant__ TcParams p) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ __align__(8) uint64_t bars[2 * TC_LMAX + 2 * TC_AMAX + 2];
+    __shared__ __align__(8) uint64_t bars[2 * TC_LMAX + 3 * TC_AMAX + 1];
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
     constexpr int N = 16 * NP;
@@ -309,12 +310,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * (I8 ? 1 : 2);
     constexpr uint32_t ASC = I8 ? 32u : 64u;  // TMEM columns per A stage
     constexpr uint32_t C_BYTES = TC_M * TC_RB;
-    constexpr uint32_t SLOT = B_BYTES + C_BYTES;
+    // shared memory: the codes ring [LS x 4 KB] (freed by the expanders),
+    // then the B ring [AS x B tile] that pairs with the TMEM A ring (one MMA
+    // commit frees both), then (N <= 64) the reduction's receive buffer
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tc_smem);
+    const uint32_t bbase = sbase + (uint32_t)LS * C_BYTES;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
-    const uint32_t bar_full = bar0, bar_empty = bar0 + 8 * TC_LMAX;
-    const uint32_t bar_aready = bar0 + 16 * TC_LMAX, bar_aempty = bar_aready + 8 * TC_AMAX;
-    const uint32_t bar_done = bar_aempty + 8 * TC_AMAX;  // accumulator complete
+    const uint32_t bar_cfull = bar0, bar_cempty = bar0 + 8 * TC_LMAX;
+    const uint32_t bar_bfull = bar0 + 16 * TC_LMAX, bar_aready = bar_bfull + 8 * TC_AMAX;
+    const uint32_t bar_free = bar_aready + 8 * TC_AMAX;
+    const uint32_t bar_done = bar_free + 8 * TC_AMAX;  // accumulator complete
 
     if (warp == TC_EXP_WARPS + 1) {  // TMEM: accumulators + the A ring
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -322,13 +327,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                      "r"(p.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // barriers, one per thread: full (the producer's expect_tx), empty /
-    // aempty / done (an MMA commit), aready (the 256 threads of an expander
-    // group)
-    if (tid < 2 * TC_LMAX + 2 * TC_AMAX + 2) {
-        const uint32_t cnt =
-            (tid >= 2 * TC_LMAX && tid < 2 * TC_LMAX + TC_AMAX) ? 8u * 32u : 1u;
-        mbar_init(bar0 + 8 * tid, cnt);
+    // barriers, one per thread: codes full / B full (the producer's
+    // expect_tx), codes empty and A ready (the 256 threads of an expander
+    // group), stage free / done (an MMA commit)
+    if (tid < 2 * TC_LMAX + 3 * TC_AMAX + 1) {
+        const bool grp = (tid >= TC_LMAX && tid < 2 * TC_LMAX) ||
+                         (tid >= 2 * TC_LMAX + TC_AMAX && tid < 2 * TC_LMAX + 2 * TC_AMAX);
+        mbar_init(bar0 + 8 * tid, grp ? 8u * 32u : 1u);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         // lane per step, each its own slot): the step's code rows (bulk
         // copy) and its B tile straight from V (two 2-d TMAs, one per 64
         // columns) ----
-        const int J = min(LS, 8);
+        const int J = min(min(LS, AS), 8);
         const unsigned char *kb = reinterpret_cast<const unsigned char *>(p.km);
         if (lane == 0)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tm_v))
@@ -352,26 +357,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         // point overlapped its tail
         asm volatile("griddepcontrol.wait;" ::: "memory");
         if ((int)lane < J) {
-            int s = (int)lane;
-            uint32_t par = 0;
+            int s = (int)lane, a = (int)lane;
+            uint32_t par = 0, apar = 0;
             const int64_t w = w0 + lane;
             int64_t t = w / p.S, st = w - t * p.S;
             for (int64_t it = lane; it < nst; it += J) {
-                if (it >= LS) mbar_wait_parity(bar_empty + 8 * s, par ^ 1u);
                 const int64_t r_first = t * TC_M;
                 const uint32_t kbytes =
                     (uint32_t)min((int64_t)TC_M, p.rows_view - r_first) * TC_RB;
                 TC_MARK(it < 64, it * 8 + 2)
-                const uint32_t sa = sbase + s * SLOT, fb = bar_full + 8 * s;
-                mbar_expect_tx(fb, kbytes + B_BYTES);
-                bulk_g2s(sa + B_BYTES, kb + (st * p.rows_pad + p.row0 + r_first) * TC_RB, kbytes,
-                         fb);
-                tma_2d(sa, &p.tm_v, (int)st * TC_K, 0, fb);
-                if (!I8) tma_2d(sa + B_BYTES / 2, &p.tm_v, (int)st * TC_K + 64, 0, fb);
+                // codes: the slot's previous step has been read by its expanders
+                if (it >= LS) mbar_wait_parity(bar_cempty + 8 * s, par ^ 1u);
+                mbar_expect_tx(bar_cfull + 8 * s, kbytes);
+                bulk_g2s(sbase + s * C_BYTES, kb + (st * p.rows_pad + p.row0 + r_first) * TC_RB,
+                         kbytes, bar_cfull + 8 * s);
+                // B tile: the stage's previous MMAs are complete
+                if (it >= AS) mbar_wait_parity(bar_free + 8 * a, apar ^ 1u);
+                const uint32_t ba = bbase + a * B_BYTES, fb = bar_bfull + 8 * a;
+                mbar_expect_tx(fb, B_BYTES);
+                tma_2d(ba, &p.tm_v, (int)st * TC_K, 0, fb);
+                if (!I8) tma_2d(ba + B_BYTES / 2, &p.tm_v, (int)st * TC_K + 64, 0, fb);
                 s += J;
                 if (s >= LS) {
                     s -= LS;
                     par ^= 1u;
+                }
+                a += J;
+                if (a >= AS) {
+                    a -= AS;
+                    apar ^= 1u;
                 }
                 st += J;
                 while (st >= p.S) {
@@ -391,8 +405,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             // B K-major SWIZZLE_128B (layout type 2 at [61,64)): rows of 128 B,
             // SBO = 8 rows (1024 B); a K = 16 slice starts 32 B further into
             // its 64-column half (the swizzle applies to the absolute address)
-            const uint64_t db0 = smem_desc(sbase, 16, 1024) | ((uint64_t)2 << 61);
-            int s = 0, a = 0;
+            const uint64_t db0 = smem_desc(bbase, 16, 1024) | ((uint64_t)2 << 61);
+            int a = 0;
             uint32_t apar = 0;
 #ifdef RSR_TC_DBG
             long long c_prev = 0;
@@ -405,16 +419,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 const long long dstep = it ? c0 - c_prev : 0;
                 c_prev = c0;
 #endif
-                // A stage ready: its expanders waited on the load slot's full
-                // barrier (the TMA'd B tile) before arriving, so this one wait
-                // orders both operands before the MMAs
+                // A stage expanded, B tile landed
                 mbar_wait_parity(bar_aready + 8 * a, apar);
+                mbar_wait_parity(bar_bfull + 8 * a, apar);
 #ifdef RSR_TC_DBG
                 const long long c2 = clock64();
 #endif
                 TC_MARK(it < 64, it * 8 + 3)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t db = db0 + ((s * SLOT) >> 4);
+                const uint64_t db = db0 + ((a * B_BYTES) >> 4);
                 const uint32_t ta = tmem_d + p.a_col + ASC * a;
                 const uint32_t td = tmem_d;
                 if (I8) {
@@ -431,8 +444,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                             db + (uint64_t)(((kk >> 2) * (B_BYTES / 2) + (kk & 3) * 32) >> 4), idesc,
                             (!first || kk > 0) ? 1u : 0u);
                 }
-                mma_commit(bar_empty + 8 * s);
-                mma_commit(bar_aempty + 8 * a);
+                // one commit frees the A stage and its B tile
+                mma_commit(bar_free + 8 * a);
                 if (it + 1 == nst) mma_commit(bar_done);
 #ifdef RSR_TC_DBG
                 if (blockIdx.x == 0 && it < 64) {
@@ -442,7 +455,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                     tc_mma_cyc[it * 3 + 2] = c3 - c2;
                 }
 #endif
-                if (++s == LS) s = 0;
                 if (++a == AS) {
                     a = 0;
                     apar ^= 1u;
@@ -460,25 +472,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         const uint32_t tab0 = __shfl_sync(RSR_FULL_MASK, p.tab0, 0);
         const uint32_t tab1 = __shfl_sync(RSR_FULL_MASK, p.tab1, 0);
         const uint32_t c0404 = __shfl_sync(RSR_FULL_MASK, 0x04040404u, 0);
-        const unsigned char *codes0 = tc_smem + B_BYTES + row * TC_RB + hh * 16;
+        const unsigned char *codes0 = tc_smem + row * TC_RB + hh * 16;
         // this warp's steps it = h, h + TC_GROUPS, ...: load slot it % LS, A stage it % AS
         int s = h % LS, a = h % AS;
         uint32_t par = (uint32_t)(h / LS) & 1u, apar = (uint32_t)(h / AS) & 1u;
         for (int64_t it = h; it < nst; it += TC_GROUPS) {
-            mbar_wait_parity(bar_full + 8 * s, par);
+            mbar_wait_parity(bar_cfull + 8 * s, par);
             TC_MARK(tid == 0 && it < 64, it * 8 + 0)
-            const uint4 x = *reinterpret_cast<const uint4 *>(codes0 + s * SLOT);
+            const uint4 x = *reinterpret_cast<const uint4 *>(codes0 + s * C_BYTES);
+            mbar_arrive(bar_cempty + 8 * s);  // (release: the load is ordered before)
             if (I8) {
                 uint32_t w[16];
                 expand64_i8(x, w, tab0);
-                if (it >= AS) mbar_wait_parity(bar_aempty + 8 * a, apar ^ 1u);
+                if (it >= AS) mbar_wait_parity(bar_free + 8 * a, apar ^ 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 tmem_st16(t_row + ASC * a, w);
             } else {
                 uint32_t w[32];
                 expand64(x, w, tab0, tab1, c0404);
                 TC_MARK(tid == 0 && it < 64, it * 8 + 4)
-                if (it >= AS) mbar_wait_parity(bar_aempty + 8 * a, apar ^ 1u);
+                if (it >= AS) mbar_wait_parity(bar_free + 8 * a, apar ^ 1u);
                 TC_MARK(tid == 0 && it < 64, it * 8 + 5)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 tmem_st32(t_row + ASC * a, w);
@@ -686,23 +699,30 @@ static int tc_np(int B) {
     return np;
 }
 
-// load-ring slot: the B tile (N x 128 elements of esize bytes) + 128 code rows
-static size_t tc_slot_bytes(int N, int esize) {
-    return (size_t)N * TC_K * esize + (size_t)TC_M * TC_RB;
-}
-
-// N <= 64: the cluster reduction's receive buffer after the ring, sized for
-// any ks <= 8 (ks x B x ceil(128 / ks) words <= N x 135)
+// N <= 64: the cluster reduction's receive buffer after the rings, sized
+// for any ks <= 8 (ks x B x ceil(128 / ks) words <= N x 135)
 static size_t tc_recv_bytes(int N) { return N <= 64 ? (size_t)N * (TC_M + 7) * 4 : 0; }
 
-static int tc_load_stages(int N, int esize) {
-    return (int)std::max<size_t>(
-        TC_GROUPS, std::min<size_t>(TC_LMAX, (216 * 1024 - tc_recv_bytes(N)) /
-                                                 tc_slot_bytes(N, esize)));
-}
+struct TcRings {
+    int ls, as;  // codes-ring depth (4 KB slots), A / B-ring depth (TMEM stage + B tile)
+    size_t smem;
+};
 
-static size_t tc_smem_bytes(int N, int esize) {
-    return tc_load_stages(N, esize) * tc_slot_bytes(N, esize) + tc_recv_bytes(N);
+// Ring depths within 216 KB of shared memory and the TMEM left after the
+// accumulator: the A / B ring as deep as both allow (at most TC_AMAX), the
+// codes ring with the rest (at most TC_LMAX); both at least TC_GROUPS.
+static TcRings tc_rings(int N, bool i8) {
+    const size_t bbytes = (size_t)N * TC_K * (i8 ? 1 : 2), cbytes = (size_t)TC_M * TC_RB;
+    const size_t budget = 216 * 1024 - tc_recv_bytes(N);
+    const int a_col = std::max(N, 64), asc = i8 ? 32 : 64;
+    TcRings r;
+    r.as = std::min<int>(TC_AMAX, (512 - a_col) / asc);
+    r.as = std::max<int>(TC_GROUPS,
+                         std::min<int>(r.as, (int)((budget - TC_GROUPS * cbytes) / bbytes)));
+    r.ls = (int)std::max<size_t>(TC_GROUPS,
+                                 std::min<size_t>(TC_LMAX, (budget - r.as * bbytes) / cbytes));
+    r.smem = r.ls * cbytes + r.as * bbytes + tc_recv_bytes(N);
+    return r;
 }
 
 static int64_t tc_view_rows(int64_t block_begin, int64_t n_blocks, int32_t k, int64_t m) {
@@ -868,7 +888,7 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     const size_t wsb = rsr_matmul_tc_workspace_bytes(m, n, k, block_begin, n_blocks, B);
     if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
         return RSR_ERR_WORKSPACE;
-    const int np = tc_np(B), esize = I8 ? 1 : 2;
+    const int np = tc_np(B);
     TcParams p;
     p.km = (const uint32_t *)keymat;
     if (!tc_encode_v(&p.tm_v, V, n, B, ldv, 16 * np, I8)) return RSR_ERR_INVALID;
@@ -885,14 +905,14 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     p.B = B;
     p.N = 16 * np;
     p.S = tc_steps(n);
-    p.ls = tc_load_stages(p.N, esize);
-    p.recv_off = (uint32_t)(p.ls * tc_slot_bytes(p.N, esize));
     // TMEM (all 512 columns): the accumulator [0, N) (64-column aligned),
     // then the A ring: one step's 128 K elements per stage (64 columns of
     // bf16 pairs, 32 of int8 quads)
-    const int asc = I8 ? 32 : 64;
+    const TcRings rings = tc_rings(p.N, I8);
+    p.ls = rings.ls;
+    p.as = rings.as;
+    p.recv_off = (uint32_t)(rings.smem - tc_recv_bytes(p.N));
     p.a_col = (uint32_t)std::max(p.N, 64);
-    p.as = std::min<int>(TC_AMAX, (int)(512 - p.a_col) / asc);
     p.tmem_cols = 512;
     {
         static const int forced_as = [] {
@@ -909,7 +929,7 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     // partners wait for it at the cluster barrier.  Shared memory above half
     // the SM's 228 KB guarantees it (registers alone would not for small
     // int8 batches).
-    const size_t smem = std::max<size_t>(tc_smem_bytes(p.N, esize), 116 * 1024);
+    const size_t smem = std::max<size_t>(rings.smem, 116 * 1024);
     if (smem > 227 * 1024) return RSR_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     // programmatic dependent launch (PDL): the prologue overlaps the previous
