@@ -1,5 +1,5 @@
 """Per-step timeline of CTA (0,0) of the tcgen05 batched kernel (debug build
-with -DRSR_TC_DBG: librsr_b200_tcdbg.so).  usage: python tools/tc_timeline.py [B]"""
+with -DRSR_TC_DBG: librsr_b200_tcdbg.so).  usage: python tools/tc_timeline.py [B] [i8]"""
 import ctypes
 import os
 import sys
@@ -13,11 +13,16 @@ import paper_2603_27462_b200 as rsr
 from paper_2603_27462_b200 import _lib
 from paper_2603_27462_b200 import kernels as kn
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+I8 = len(sys.argv) > 2 and sys.argv[2] == "i8"
 m = n = 8192
 data = bench.random_packed(m, n, "ternary", 0)
 a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", data), 5)
-V = torch.randn(B, n, device="cuda").to(torch.bfloat16)
-Y = torch.empty(B, m, device="cuda")
+if I8:
+    V = torch.randint(-128, 128, (B, n), dtype=torch.int8, device="cuda")
+    Y = torch.empty(B, m, dtype=torch.int32, device="cuda")
+else:
+    V = torch.randn(B, n, device="cuda").to(torch.bfloat16)
+    Y = torch.empty(B, m, device="cuda")
 for _ in range(3):
     kn.matmul_into(a, V, Y, method="tc")
 torch.cuda.synchronize()
