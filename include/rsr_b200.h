@@ -261,9 +261,11 @@ rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint
 size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t block_begin,
                                      int64_t n_blocks, int32_t B);
 /* int8 batches on tcgen05 kind::i8 (s8 x s8 -> s32, exact): the same code
- * matrix in the int8 path's permuted order (rsr_keymat_build_i8, same size:
- * column 4w + i of a 16-column word in nibble i + 4 (w / 2) at bit offset
- * 2 (w % 2)); rsr_matmul_tc_i8: Y[b] (int32) = A . V[b] for int8
+ * matrix in the int8 path's order (rsr_keymat_build_i8, the size
+ * rsr_keymat_bytes gives -- it is sized for this layout): 256-column steps,
+ * u32 [ceil(cols/256)][round8(bc*k)][16], column 4w + i of a 16-column word
+ * in nibble i + 4 (w / 2) at bit offset 2 (w % 2) (the bf16 layout uses a
+ * prefix of the same size); rsr_matmul_tc_i8: Y[b] (int32) = A . V[b] for int8
  * V[b*ldv + col] (V 16-byte aligned, ldv a multiple of 16), bit-exact with
  * the integer path of rsr_matvec per column.                                */
 rsr_status rsr_keymat_build_i8(const uint64_t *words, const int64_t *go, const uint16_t *perm,

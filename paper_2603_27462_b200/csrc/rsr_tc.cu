@@ -42,10 +42,12 @@
 // cycles per M128 x K16 / K32 instruction at N <= 64 -- is the bound
 // (profiles/r02_umma_microbench.txt).
 //
-// Code matrix layout [step = col / 128][row][8 x u32]: u32 q holds columns
-// 16q .. 16q + 15 of the step, permuted so the expansion needs one shift +
-// mask per pair of words (bf16: tc_code_bit; int8: tc_code_bit_i8).  A
-// tile's step is one contiguous run of rows.
+// Code matrix layout [step][row][u32]: bf16 steps of 128 columns (8 words
+// per row), int8 steps of 256 (16 words: the int8 expansion and MMAs are
+// half as long per column, so the per-step overheads are paid half as
+// often); u32 q holds columns 16q .. 16q + 15 of the step, permuted so the
+// expansion needs one shift + mask per pair of words (bf16: tc_code_bit;
+// int8: tc_code_bit_i8).  A tile's step is one contiguous run of rows.
 #include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime)
 
 #include <cstdio>
@@ -59,8 +61,8 @@
 namespace rsr {
 
 constexpr int TC_M = 128;           // tile rows = TMEM lanes
-constexpr int TC_K = 128;           // columns per pipeline step
-constexpr int TC_RB = 32;           // code bytes per (step, row): 128 x 2 bits
+constexpr int TC_K = 128;           // columns per pipeline step (bf16; int8 steps are 2 x TC_K)
+constexpr int TC_RB = 32;           // code bytes per (step, row): 128 x 2 bits (int8: 2 x)
 constexpr int TC_LMAX = 16;         // load-ring depth (at most)
 constexpr int TC_AMAX = 16;         // A-ring depth in TMEM (at most)
 constexpr int TC_MAXK = 16;         // rows per block (16-bit pos / neg masks)
@@ -68,7 +70,10 @@ constexpr int TC_GROUPS = 2;        // expander step groups (8 warps: 2 column h
 constexpr int TC_EXP_WARPS = 8 * TC_GROUPS;
 constexpr int TC_THREADS = TC_EXP_WARPS * 32 + 64;  // expanders, producer, MMA
 
-__host__ __device__ inline int64_t tc_steps(int64_t n) { return (n + TC_K - 1) / TC_K; }
+__host__ __device__ inline int64_t tc_steps(int64_t n, bool i8 = false) {
+    const int ks = i8 ? 2 * TC_K : TC_K;
+    return (n + ks - 1) / ks;
+}
 __host__ __device__ inline int64_t tc_rows_pad(int64_t bc, int k) { return (bc * k + 7) / 8 * 8; }
 
 // bit offset of column c (c % 16 within its u32) in the permuted code word
@@ -110,10 +115,11 @@ __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t 
                 const int64_t col = c0 + cols[j];
                 const uint32_t bit =
                     I8 ? tc_code_bit_i8((uint32_t)col & 15) : tc_code_bit((uint32_t)col & 15);
-                uint32_t *dst = km32 + ((col >> 7) * rows_pad + r0) * 8 + ((col & 127) >> 4);
+                uint32_t *dst = I8 ? km32 + ((col >> 8) * rows_pad + r0) * 16 + ((col & 255) >> 4)
+                                   : km32 + ((col >> 7) * rows_pad + r0) * 8 + ((col & 127) >> 4);
                 for (int i = 0; i < k; ++i) {
                     const uint32_t code = ((pos >> i) & 1u) | (((neg >> i) & 1u) << 1);
-                    if (code) atomicOr(dst + (int64_t)i * 8, code << bit);
+                    if (code) atomicOr(dst + (int64_t)i * (I8 ? 16 : 8), code << bit);
                 }
             }
         }
@@ -307,9 +313,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     const int64_t nst = w1 - w0;
 
     // smem: per load stage [B tile: 2 K-halves x N x 128 B][codes 128 rows x 32 B]
-    constexpr uint32_t B_BYTES = (uint32_t)N * TC_K * (I8 ? 1 : 2);
-    constexpr uint32_t ASC = I8 ? 32u : 64u;  // TMEM columns per A stage
-    constexpr uint32_t C_BYTES = TC_M * TC_RB;
+    // int8 steps take 256 columns: the same 256-byte B rows and twice the
+    // code bytes, so the per-step overheads are paid half as often
+    constexpr int KS = I8 ? 2 * TC_K : TC_K;   // columns per step
+    constexpr int RB = I8 ? 2 * TC_RB : TC_RB;  // code bytes per (step, row)
+    constexpr uint32_t B_BYTES = (uint32_t)N * KS * (I8 ? 1 : 2);
+    constexpr uint32_t ASC = 64u;  // TMEM columns per A stage (128 bf16 pairs / 256 int8 quads)
+    constexpr uint32_t C_BYTES = TC_M * RB;
     // shared memory: the codes ring [LS x 4 KB] (freed by the expanders),
     // then the B ring [AS x B tile] that pairs with the TMEM A ring (one MMA
     // commit frees both), then (N <= 64) the reduction's receive buffer
@@ -364,19 +374,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             for (int64_t it = lane; it < nst; it += J) {
                 const int64_t r_first = t * TC_M;
                 const uint32_t kbytes =
-                    (uint32_t)min((int64_t)TC_M, p.rows_view - r_first) * TC_RB;
+                    (uint32_t)min((int64_t)TC_M, p.rows_view - r_first) * RB;
                 TC_MARK(it < 64, it * 8 + 2)
                 // codes: the slot's previous step has been read by its expanders
                 if (it >= LS) mbar_wait_parity(bar_cempty + 8 * s, par ^ 1u);
                 mbar_expect_tx(bar_cfull + 8 * s, kbytes);
-                bulk_g2s(sbase + s * C_BYTES, kb + (st * p.rows_pad + p.row0 + r_first) * TC_RB,
+                bulk_g2s(sbase + s * C_BYTES, kb + (st * p.rows_pad + p.row0 + r_first) * RB,
                          kbytes, bar_cfull + 8 * s);
                 // B tile: the stage's previous MMAs are complete
                 if (it >= AS) mbar_wait_parity(bar_free + 8 * a, apar ^ 1u);
                 const uint32_t ba = bbase + a * B_BYTES, fb = bar_bfull + 8 * a;
                 mbar_expect_tx(fb, B_BYTES);
-                tma_2d(ba, &p.tm_v, (int)st * TC_K, 0, fb);
-                if (!I8) tma_2d(ba + B_BYTES / 2, &p.tm_v, (int)st * TC_K + 64, 0, fb);
+                // two boxes of 128 bytes of columns (64 bf16 / 128 int8)
+                tma_2d(ba, &p.tm_v, (int)st * KS, 0, fb);
+                tma_2d(ba + B_BYTES / 2, &p.tm_v, (int)st * KS + KS / 2, 0, fb);
                 s += J;
                 if (s >= LS) {
                     s -= LS;
@@ -431,11 +442,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 const uint32_t ta = tmem_d + p.a_col + ASC * a;
                 const uint32_t td = tmem_d;
                 if (I8) {
-                    // K = 32 int8 per MMA: 32 B into the 128-byte swizzled rows
+                    // K = 32 int8 per MMA: 32 B into a half's 128-byte swizzled rows
 #pragma unroll
-                    for (int kk = 0; kk < TC_K / 32; ++kk)
-                        mma_i8_ts(td, ta + 8u * kk, db + (uint64_t)((kk * 32) >> 4), idesc,
-                                  (!first || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < KS / 32; ++kk)
+                        mma_i8_ts(td, ta + 8u * kk,
+                                  db + (uint64_t)(((kk >> 2) * (B_BYTES / 2) + (kk & 3) * 32) >> 4),
+                                  idesc, (!first || kk > 0) ? 1u : 0u);
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < TC_K / 16; ++kk)
@@ -472,7 +484,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
         const uint32_t tab0 = __shfl_sync(RSR_FULL_MASK, p.tab0, 0);
         const uint32_t tab1 = __shfl_sync(RSR_FULL_MASK, p.tab1, 0);
         const uint32_t c0404 = __shfl_sync(RSR_FULL_MASK, 0x04040404u, 0);
-        const unsigned char *codes0 = tc_smem + row * TC_RB + hh * 16;
+        const unsigned char *codes0 = tc_smem + row * RB + hh * (RB / 2);
         // this warp's steps it = h, h + TC_GROUPS, ...: load slot it % LS, A stage it % AS
         int s = h % LS, a = h % AS;
         uint32_t par = (uint32_t)(h / LS) & 1u, apar = (uint32_t)(h / AS) & 1u;
@@ -480,13 +492,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             mbar_wait_parity(bar_cfull + 8 * s, par);
             TC_MARK(tid == 0 && it < 64, it * 8 + 0)
             const uint4 x = *reinterpret_cast<const uint4 *>(codes0 + s * C_BYTES);
-            mbar_arrive(bar_cempty + 8 * s);  // (release: the load is ordered before)
+            uint4 x2 = make_uint4(0, 0, 0, 0);
+            if (I8) x2 = *reinterpret_cast<const uint4 *>(codes0 + s * C_BYTES + 16);
+            mbar_arrive(bar_cempty + 8 * s);  // (release: the loads are ordered before)
             if (I8) {
-                uint32_t w[16];
-                expand64_i8(x, w, tab0);
+                // 128 columns: two code words -> 32 int8-quad words
+                uint32_t w[32];
+                expand64_i8(x, *reinterpret_cast<uint32_t(*)[16]>(&w[0]), tab0);
+                expand64_i8(x2, *reinterpret_cast<uint32_t(*)[16]>(&w[16]), tab0);
                 if (it >= AS) mbar_wait_parity(bar_free + 8 * a, apar ^ 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                tmem_st16(t_row + ASC * a, w);
+                tmem_st32(t_row + ASC * a, w);
             } else {
                 uint32_t w[32];
                 expand64(x, w, tab0, tab1, c0404);
@@ -712,9 +728,9 @@ struct TcRings {
 // accumulator: the A / B ring as deep as both allow (at most TC_AMAX), the
 // codes ring with the rest (at most TC_LMAX); both at least TC_GROUPS.
 static TcRings tc_rings(int N, bool i8) {
-    const size_t bbytes = (size_t)N * TC_K * (i8 ? 1 : 2), cbytes = (size_t)TC_M * TC_RB;
+    const size_t bbytes = (size_t)N * TC_K * 2, cbytes = (size_t)TC_M * TC_RB * (i8 ? 2 : 1);
     const size_t budget = 216 * 1024 - tc_recv_bytes(N);
-    const int a_col = std::max(N, 64), asc = i8 ? 32 : 64;
+    const int a_col = std::max(N, 64), asc = 64;
     TcRings r;
     r.as = std::min<int>(TC_AMAX, (512 - a_col) / asc);
     r.as = std::max<int>(TC_GROUPS,
@@ -782,7 +798,9 @@ int rsr_tc_debug(unsigned long long *out) {
 size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int32_t k) {
     (void)bitwidth;
     if (k < 1 || k > TC_MAXK || block_count < 0 || cols < 0) return 0;
-    return (size_t)tc_steps(cols) * tc_rows_pad(block_count, k) * TC_RB;
+    // sized for the int8 layout (256-column steps), which the bf16 one
+    // (128-column steps) never exceeds
+    return (size_t)tc_steps(cols, true) * tc_rows_pad(block_count, k) * (2 * TC_RB);
 }
 
 }  // extern "C"
@@ -904,7 +922,7 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     p.rows_pad = tc_rows_pad(bc, k);
     p.B = B;
     p.N = 16 * np;
-    p.S = tc_steps(n);
+    p.S = tc_steps(n, I8);
     // TMEM (all 512 columns): the accumulator [0, N) (64-column aligned),
     // then the A ring: one step's 128 K elements per stage (64 columns of
     // bf16 pairs, 32 of int8 quads)

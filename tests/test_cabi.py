@@ -58,8 +58,8 @@ def test_host_queries_need_no_gpu():
     assert L.rsr_matvec(ctypes.byref(v), None, 0, None, 0, None, 0, None) == _lib.RSR_ERR_INVALID
     # tensor-core code matrix: u16 per (8-row group, column), columns padded to 64
     assert L.rsr_keymat_bytes(1639, 8192, 1, 5) == 128 * 1025 * 64 * 2   # C4: 16.8 MB
-    assert L.rsr_keymat_bytes(3, 65, 0, 8) == 2 * 3 * 64 * 2
-    assert L.rsr_keymat_bytes(10, 100, 1, 9) == 2 * 96 * 16                # k = 9: rows padded to 8
+    assert L.rsr_keymat_bytes(3, 65, 0, 8) == 24 * 64                      # one 256-column step, 24 rows
+    assert L.rsr_keymat_bytes(10, 100, 1, 9) == 96 * 64                    # k = 9: rows padded to 8
     assert L.rsr_keymat_bytes(10, 100, 1, 17) == 0                         # k > 16: no tc path
     assert L.rsr_matmul_tc(None, 8, 8, 1, 2, 0, 4, None, 1, 8, 1, None, 8, None, 0,
                            None) == _lib.RSR_ERR_INVALID
