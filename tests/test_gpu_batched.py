@@ -255,3 +255,23 @@ def test_code_matrix_layout_i8(rsr, m, n, k, bw, tw):
         bit = 4 * (i + 4 * (w // 2)) + 2 * (w % 2)
         exp[c // 256, :m, (c % 256) // 16] |= code[:, c] << bit
     assert np.array_equal(km.reshape(steps, rows_pad, 16).astype(np.int64), exp)
+
+
+@pytest.mark.parametrize("offset,pad", [(1, 3), (16, 16), (0, 7)])
+def test_tensor_core_int8_strided_vectors(rsr, offset, pad):
+    """int8 rows off a 16-byte boundary or with a pitch not a multiple of 16
+    are re-laid before the TMA loads; every column stays exact."""
+    import torch
+    from paper_2603_27462_b200 import kernels as kn
+    m, n, k, B = 300, 1000, 5, 6
+    p = orc.random_matrix(m, n, "ternary", 43)
+    ref = orc.preprocess(p, k)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", p.data), k)
+    rng = np.random.default_rng(offset + pad)
+    big = torch.from_numpy(rng.integers(-128, 128, (B, offset + n + pad)).astype(np.int8)).cuda()
+    V = big[:, offset:offset + n]
+    Y = torch.empty(B, m, dtype=torch.int32, device="cuda")
+    kn.matmul_into(a, V, Y, method="tc")
+    Vh = V.cpu().numpy()
+    for b in range(B):
+        assert np.array_equal(Y[b].cpu().numpy(), orc.matvec_i8(ref, Vh[b])), b
