@@ -69,19 +69,19 @@ class GraphDecoder:
         """Greedy tokens after the prompt; returns (tokens list, seconds of decode)."""
         self.reset()
         self.prefill(prompt_ids)
-        toks = []
+        out = torch.empty(steps, dtype=torch.long, device=self.tok.device)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(steps):
+        for i in range(steps):
             self.tok.copy_(self.next_tok)
+            out[i].copy_(self.tok[0, 0])  # this step's input token (device copy)
             if self.graph is not None:
                 self.graph.replay()
             else:
                 self._step()
-            toks.append(self.tok)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        return [int(t.item()) for t in toks], dt
+        return out.tolist(), dt
 
     @torch.no_grad()
     def time_steps(self, prompt_ids: torch.Tensor, steps: int) -> float:
