@@ -705,19 +705,35 @@ def main():
     # ---- e2e through the public API with host buffers (rank 0, 1 GPU)
     e2e = None
     if rank == 0 and world == 1:
-        vh = torch.from_numpy(vf.copy()).pin_memory().numpy()  # the step's input, pinned
-        for _ in range(5):
-            rsr.rsr_matvec(a, vh)
-        torch.cuda.synchronize()
-        ne = max(20, min(args.steps, 200))
-        t0 = time.perf_counter()
-        for _ in range(ne):
-            yh = rsr.rsr_matvec(a, vh)
-        e2e_s = (time.perf_counter() - t0) / ne
-        e2e = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(vh.nbytes),
-               "d2h_bytes_per_step": int(yh.nbytes),
-               "api": "paper_2603_27462_b200.rsr_matvec(artifact, numpy float32 vector in "
-                      "pinned memory) -> numpy float32"}
+        def host_rate(vh):
+            for _ in range(5):
+                rsr.rsr_matvec(a, vh)
+            torch.cuda.synchronize()
+            ne = max(20, min(args.steps, 200))
+            t0 = time.perf_counter()
+            for _ in range(ne):
+                yh = rsr.rsr_matvec(a, vh)
+            return ne / (time.perf_counter() - t0), yh
+        # the step's input in pinned host memory, in the workload's vector
+        # dtype: a bf16 tensor for bf16 configs (numpy has no bf16), numpy
+        # float32 otherwise -- the reference's own call, timed beside it
+        vh32 = torch.from_numpy(vf.copy()).pin_memory().numpy()
+        rate32, yh = host_rate(vh32)
+        if cfg["vdtype"] == "bf16":
+            vhb = torch.from_numpy(vf.copy()).to(torch.bfloat16).pin_memory()
+            rate, yh = host_rate(vhb)
+            vin_bytes = vhb.numel() * 2
+            api = ("paper_2603_27462_b200.rsr_matvec(artifact, bf16 vector in pinned host "
+                   "memory) -> numpy float32")
+        else:
+            rate, vin_bytes = rate32, vh32.nbytes
+            api = ("paper_2603_27462_b200.rsr_matvec(artifact, numpy float32 vector in "
+                   "pinned memory) -> numpy float32")
+        e2e = {"value": rate, "unit": UNIT, "h2d_bytes_per_step": int(vin_bytes),
+               "d2h_bytes_per_step": int(yh.nbytes), "api": api,
+               "numpy_f32": {"value": rate32, "h2d_bytes_per_step": int(vh32.nbytes),
+                             "api": "rsr_matvec(artifact, numpy float32 vector, pinned): "
+                                    "the float32 kernel"}}
     elif world > 1:
         # sharded: every rank takes the host vector (pinned) to its GPU, runs
         # ShardedMatrix.matvec (local multiply + all-gather + reassembly) and

@@ -248,6 +248,9 @@ def rsr_matvec(a: RsrArtifact, v, counter: OpCounter | None = None,
     int8 vectors take the exact integer path (int32 result); real vectors
     the float path (float32 result, fp32 accumulation -- see DESIGN.md for
     the stated tolerance).  ``threads`` is accepted for API compatibility.
+    Host vectors (numpy float32 / int8, or a CPU torch bfloat16 tensor --
+    numpy has no bf16) return a numpy result; device tensors stay on the
+    device.
     """
     if type(v) is np.ndarray and v.ndim == 1 and v.shape[0] == a.n and \
             (v.dtype == np.float32 or v.dtype == np.int8):
@@ -260,6 +263,13 @@ def rsr_matvec(a: RsrArtifact, v, counter: OpCounter | None = None,
         if vn.ndim == 1 and vn.shape[0] == a.n and vn.dtype in (np.int8, np.float32):
             _count(a, counter)
             return _matvec_host(a, np.ascontiguousarray(vn))
+    elif v.device.type == "cpu" and v.dtype == torch.bfloat16 and v.dim() == 1 \
+            and v.shape[0] == a.n:
+        # a bf16 host vector (numpy has no bf16): host in, host out in one C
+        # call, the bf16 kernel reading the halfwords as they are
+        _count(a, counter)
+        with _host_lock(a):
+            return _matvec_host_locked(a, v.contiguous().view(torch.int16).numpy(), bf16=True)
     vt, host = _prepare_vec(a, v)
     _count(a, counter)
     if vt.dtype == torch.int8:
@@ -309,13 +319,14 @@ def _matvec_host(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
         return _matvec_host_locked(a, vn)
 
 
-def _matvec_host_locked(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
+def _matvec_host_locked(a: RsrArtifact, vn: np.ndarray, bf16: bool = False) -> np.ndarray:
     is_int = vn.dtype == np.int8
-    key = "_host_call_i8" if is_int else "_host_call_f32"
+    key = "_host_call_i8" if is_int else ("_host_call_bf16" if bf16 else "_host_call_f32")
     hc = a.__dict__.get(key)
     if hc is None or hc[0] is not a._view:
         import torch
-        dv = torch.empty(a.n, dtype=torch.int8 if is_int else torch.float32, device=a.device)
+        dv = torch.empty(a.n, dtype=torch.int8 if is_int else
+                         (torch.bfloat16 if bf16 else torch.float32), device=a.device)
         ydt = torch.int32 if is_int else torch.float32
         dy = torch.empty(a.m, dtype=ydt, device=a.device)
         # pinned landing buffer: mapped into the device address space, the
@@ -327,7 +338,8 @@ def _matvec_host_locked(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
         if dev_idx is None:
             dev_idx = torch.cuda.current_device()
         hc = a.__dict__[key] = (
-            a._view, _lib.lib().rsr_matvec_host, st.ref, _lib.RSR_I8 if is_int else _lib.RSR_F32,
+            a._view, _lib.lib().rsr_matvec_host, st.ref,
+            _lib.RSR_I8 if is_int else (_lib.RSR_BF16 if bf16 else _lib.RSR_F32),
             hy, hy.ctypes.data, dv.data_ptr(), dy.data_ptr(), st,
             torch._C._cuda_getCurrentRawStream, dev_idx, (dv, dy))
     _, fn, ref, code, hy, hyp, dvp, dyp, st, cur_stream, dev_idx, _keep = hc

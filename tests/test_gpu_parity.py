@@ -245,3 +245,20 @@ def test_fused_bf16_vector_bit_exact(rsr, n):
         torch.bfloat16)
     y = rsr.rsr_matvec_fused(a, vb.cuda()).cpu().numpy()
     assert np.array_equal(y, orc.fused_matvec(ref, vb.float().numpy()))
+
+
+def test_bf16_host_vector_round_trip(rsr):
+    """A CPU bf16 tensor (pinned or pageable) goes host in / host out through
+    the bf16 kernel: bit-identical to the same vector on the device."""
+    import torch
+    p = orc.random_matrix(300, 1000, "ternary", 5)
+    a = rsr.preprocess(rsr.PackedMatrix(300, 1000, "ternary", p.data), 5)
+    vb = torch.from_numpy(orc.random_vector(1000, 5) * 3).to(torch.bfloat16)
+    yd = rsr.rsr_matvec(a, vb.cuda()).cpu().numpy()
+    for vh in (vb, vb.pin_memory()):
+        y = rsr.rsr_matvec(a, vh)
+        assert isinstance(y, np.ndarray) and y.dtype == np.float32
+        assert np.array_equal(y, yd)
+    ref = orc.preprocess(p, 5)
+    vr = vb.float().numpy()
+    assert float_ok(y, orc.matvec_f64(ref, vr), orc.decode(p), vr).all()
