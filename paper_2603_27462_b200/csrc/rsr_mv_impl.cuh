@@ -51,7 +51,7 @@ enum StreamFormat {
 enum VKind {
     VK_DEFAULT = 0,  // formats 0-2: f32 (float) / int32 or int8 (integer paths)
     VK_BF16 = 1,     // bf16 halfwords; gathers add them with add.f32.bf16
-    VK_F32X2 = 2,    // f32 words at byte 2*entry (float32 / float16 vectors)
+    VK_F32X2 = 2,    // f32 words, even / odd columns in two images (float32 / float16 vectors)
     VK_I16 = 3       // int16 halfwords (int8 and quantized vectors)
 };
 // Format 3: the 32 zero words the padding entries name sit right after the

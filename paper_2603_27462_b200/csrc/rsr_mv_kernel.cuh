@@ -90,6 +90,17 @@ rsr_mv_kernel(MvParams p) {
     Acc *__restrict__ xch = reinterpret_cast<Acc *>(mv_smem + off);  // team exchange [W][16]
     Acc *bk = buckets + (size_t)warp * p.nkeys;
     const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(vsm);
+    // Format 3 with f32 staging (VK_F32X2): column c's word at byte
+    // 4*(c/2) + (c odd ? x2h_bytes : 0), i.e. entry e = 2c maps to
+    // (e & ~3) + (e & 2) * x2h_bytes / 2.  Word bits 2-6 then equal the
+    // entry's, so the f32 gathers hit the banks the stream builder matched
+    // for 2-byte staging (a plain 4*c image would put c and c + 32 on one
+    // bank).  x2h_bytes = the zero words' byte + 128 (a multiple of 128).
+    constexpr bool X2S = FH && VK == VK_F32X2;
+    const uint32_t x2h_bytes = X2S ? h_zero_b(tn) + 128u : 0u;
+    auto f32_slot = [&](int64_t c) -> size_t {
+        return X2S ? (size_t)((c >> 1) << 2) + (size_t)(c & 1) * x2h_bytes : (size_t)c * 4;
+    };
     uint32_t bkbase = (uint32_t)__cvta_generic_to_shared(bk);
 
     // Teams (bucket path): `team` consecutive warps share one cell; warp `sub`
@@ -280,6 +291,8 @@ rsr_mv_kernel(MvParams p) {
         }
         vstaged_float = true;
     } else if constexpr (MODE == MODE_FLOAT && SMEM_V && VSZ == 4) {
+        // (format 3, f32 staging: even columns' words from byte 0, odd
+        // columns' from byte x2h_bytes -- see f32x2_byte)
         const int esz = p.vdtype == RSR_F32 ? 4 : 2;
         const int epv = 16 / esz;  // elements per 16-byte load
         const char *src = reinterpret_cast<const char *>(p.v) + c0 * esz;
@@ -300,7 +313,34 @@ rsr_mv_kernel(MvParams p) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int64_t i = i0 + u * nt;
-                    if (i < nvec) {
+                    if (i < nvec && X2S) {
+                        // elements c = i*epv ..: evens to byte 2c, odds to
+                        // x2h_bytes + 2c (c even)
+                        const uint32_t w4[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+                        unsigned char *ev = vsm + 2 * i * epv;
+                        unsigned char *od = ev + x2h_bytes;
+                        if (esz == 4) {
+                            *reinterpret_cast<float2 *>(ev) =
+                                make_float2(__uint_as_float(w4[0]), __uint_as_float(w4[2]));
+                            *reinterpret_cast<float2 *>(od) =
+                                make_float2(__uint_as_float(w4[1]), __uint_as_float(w4[3]));
+                        } else {
+                            float e4[4], o4[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (p.vdtype == RSR_BF16) {
+                                    e4[q] = __uint_as_float(w4[q] << 16);
+                                    o4[q] = __uint_as_float(w4[q] & 0xFFFF0000u);
+                                } else {
+                                    const __half2 h2 = *reinterpret_cast<const __half2 *>(&w4[q]);
+                                    e4[q] = __low2float(h2);
+                                    o4[q] = __high2float(h2);
+                                }
+                            }
+                            *reinterpret_cast<float4 *>(ev) = make_float4(e4[0], e4[1], e4[2], e4[3]);
+                            *reinterpret_cast<float4 *>(od) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+                        }
+                    } else if (i < nvec) {
                         float *d = reinterpret_cast<float *>(vsm) + i * epv;
                         const uint32_t w4[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
                         if (esz == 4) {
@@ -330,7 +370,7 @@ rsr_mv_kernel(MvParams p) {
                 }
             }
             for (int64_t i = nvec * epv + threadIdx.x; i < tn; i += nt)  // tail
-                reinterpret_cast<float *>(vsm)[i] = load_as_f32(p.v, p.vdtype, c0 + i);
+                *reinterpret_cast<float *>(vsm + f32_slot(i)) = load_as_f32(p.v, p.vdtype, c0 + i);
             vstaged_float = true;
         }
     }
@@ -452,7 +492,7 @@ rsr_mv_kernel(MvParams p) {
             // (not reached: the bf16 copy above always stages)
         } else if constexpr (MODE == MODE_FLOAT) {
             for_each_v_real(p.v, p.vdtype, c0, tn,
-                       [&](int64_t i, float x) { reinterpret_cast<float *>(vsm)[i] = x; });
+                       [&](int64_t i, float x) { *reinterpret_cast<float *>(vsm + f32_slot(i)) = x; });
         } else {
             auto put = [&](int64_t i, float x) {
                 const int8_t q = MODE == MODE_INT ? (int8_t)x : quantize_one(x, scale);
@@ -475,9 +515,10 @@ rsr_mv_kernel(MvParams p) {
     if constexpr (FH) {
         // format 3: every column is in the stream; padding names one of 32
         // zero words after the image (one per bank)
-        constexpr int NZ = VK == VK_F32X2 ? 64 : 32;  // (a CTA may have a single warp)
-        for (int i = threadIdx.x; i < NZ; i += blockDim.x)
-            reinterpret_cast<uint32_t *>(vsm + (VK == VK_F32X2 ? 2 : 1) * h_zero_b(tn))[i] = 0u;
+        // (f32 staging: the padding entries' words sit right after the
+        // even-column image, at the same byte -- f32x2_byte(zero entry))
+        for (int i = threadIdx.x; i < 32; i += blockDim.x)  // (a CTA may have a single warp)
+            reinterpret_cast<uint32_t *>(vsm + h_zero_b(tn))[i] = 0u;
     } else if constexpr (SMEM_V) {
         if constexpr (MODE == MODE_FLOAT) v0 = load_as_f32(p.v, p.vdtype, c0);
         else if constexpr (MODE == MODE_INT) v0 = (Acc)__ldg(reinterpret_cast<const int8_t *>(p.v) + c0);
@@ -639,11 +680,17 @@ rsr_mv_kernel(MvParams p) {
         constexpr bool X2 = FH && VK == VK_F32X2;
         auto is_key = [](uint32_t x) -> uint32_t { return SC ? (x & 1u) : (x & 0x8000u); };
         auto key_off = [](uint32_t x) -> uint32_t { return SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * 4u; };
-        auto lo_off = [](uint32_t x) -> uint32_t {
-            return X2 ? (x & 0xFFFEu) << 1 : (FH ? (x & 0xFFFFu) : (SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ));
+        const uint32_t x2h = x2h_bytes >> 1;
+        auto lo_off = [x2h](uint32_t x) -> uint32_t {
+            return X2 ? (x & 0xFFFCu) + (x & 2u) * x2h
+                      : (FH ? (x & 0xFFFFu) : (SC ? (x & 0xFFFCu) : (x & 0x7FFFu) * VSZ));
         };
-        auto hi_off = [](uint32_t x) -> uint32_t {
-            return X2 ? (x >> 15) & 0x1FFFEu : (SC ? (x >> 16) : (x >> 16) * VSZ);
+        auto hi_off = [x2h](uint32_t x) -> uint32_t {
+            if constexpr (X2) {
+                const uint32_t e = x >> 16;
+                return (e & 0xFFFCu) + (e & 2u) * x2h;
+            }
+            return SC ? (x >> 16) : (x >> 16) * VSZ;
         };
         auto gat = [&](uint32_t off) -> Acc {
             if constexpr (FH && VK == VK_I16) return lds_s16(vbase + off);
