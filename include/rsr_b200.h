@@ -157,6 +157,20 @@ rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtyp
                       int32_t accumulate, void *workspace, size_t workspace_bytes,
                       rsr_stream_t stream);
 
+/* rsr_matvec_peers: rsr_matvec fused with the sharded path's all-gather
+ * (SURVEY 8e): the multiply's epilogue (or, with tile_count > 1, its tile
+ * finalize) stores every output row of the view to each of npeers buffers
+ * instead of one y.  y_peers is a DEVICE array of npeers pointers, each to
+ * this view's first row inside one rank's full output buffer -- peer memory
+ * mapped into this device's address space (e.g. torch symmetric memory),
+ * this rank's own buffer included.  No accumulate.  Stream-ordered like
+ * rsr_matvec; the caller synchronizes the ranks (a barrier over the same
+ * peers) before any rank reads its full output.  Replaces rsr_matvec +
+ * ncclAllGather of the y slices.                                            */
+rsr_status rsr_matvec_peers(const rsr_stream_view *view, const void *v, int32_t v_dtype,
+                            void *const *y_peers, int32_t npeers, void *workspace,
+                            size_t workspace_bytes, rsr_stream_t stream);
+
 /* rsr_matvec_host: the synchronous host-buffer form behind the Python API's
  * numpy path -- copies v_host (n elements of v_dtype; pinned memory for full
  * speed) to dev_v, multiplies into dev_y, copies the view's rows back to

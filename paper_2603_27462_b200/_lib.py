@@ -67,6 +67,7 @@ SIGNATURES = {
     "rsr_stream_build": (I32, [P, P, P, P, I64, I64, I64, I64, I32, I32, I32, P, P, P, P, P]),
     "rsr_matvec_workspace_bytes": (SZ, [ctypes.POINTER(StreamView)]),
     "rsr_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, P, I32, P, SZ, P]),
+    "rsr_matvec_peers": (I32, [ctypes.POINTER(StreamView), P, I32, P, I32, P, SZ, P]),
     "rsr_matvec_host": (I32, [ctypes.POINTER(StreamView), P, I32, P, P, P, P, SZ, P]),
     "rsr_fused_matvec_host": (I32, [ctypes.POINTER(StreamView), P, I32, F64, P, P, P, P, SZ, P]),
     "rsr_fused_matvec": (I32, [ctypes.POINTER(StreamView), P, I32, F64, P, P, I32, P, P, SZ, P]),

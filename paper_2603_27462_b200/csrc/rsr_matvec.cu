@@ -19,15 +19,15 @@ __global__ void tile_finalize_kernel(MvParams p, int64_t rows_view) {
         for (int64_t t = 0; t < p.tc; ++t) s += part[t * rows_view + r];
         if (MODE == MODE_FLOAT) {
             float *y = reinterpret_cast<float *>(p.y);
-            y[r] = p.accumulate ? y[r] + s : s;
+            put_row<float>(p, r, p.accumulate ? y[r] + (float)s : (float)s);
         } else if (MODE == MODE_INT) {
             int32_t *y = reinterpret_cast<int32_t *>(p.y);
-            y[r] = p.accumulate ? y[r] + s : s;
+            put_row<int32_t>(p, r, p.accumulate ? y[r] + (int32_t)s : (int32_t)s);
         } else {
             const double beta = p.row_beta ? p.row_beta[p.blk0 * p.k + r] : p.beta;
             const float o = (float)((double)s * (beta / *p.scale_dev));
-            if (p.out_bf16) reinterpret_cast<__nv_bfloat16 *>(p.y)[r] = __float2bfloat16_rn(o);
-            else reinterpret_cast<float *>(p.y)[r] = o;
+            if (p.out_bf16) put_row<__nv_bfloat16>(p, r, __float2bfloat16_rn(o));
+            else put_row<float>(p, r, o);
         }
     }
 }
@@ -123,10 +123,12 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
                             int accumulate, double beta, double *scale_out, void *ws,
                             size_t ws_bytes, cudaStream_t s, const double *row_beta = nullptr,
                             int out_bf16 = 0, const uint16_t *norm_w = nullptr,
-                            float norm_eps = 0.f) {
+                            float norm_eps = 0.f, void *const *y_peers = nullptr,
+                            int npeers = 0) {
     rsr_status st = check_view(vw);
     if (st != RSR_OK) return st;
-    if (!v || !y) return RSR_ERR_INVALID;
+    if (!v || (!y && !npeers)) return RSR_ERR_INVALID;
+    if (npeers && (!y_peers || npeers < 0 || accumulate)) return RSR_ERR_INVALID;
     if (vw->n_blocks == 0) return RSR_OK;
     DeviceGuard guard(vw->device);
     const bool need_ws = vw->tile_count > 1 || vw->format == FMT_U32;
@@ -154,6 +156,8 @@ static rsr_status launch_mv(const rsr_stream_view *vw, const void *v, int vdtype
     p.out_bf16 = out_bf16;
     p.norm_w = norm_w;
     p.norm_eps = norm_eps;
+    p.y_peers = y_peers;
+    p.npeers = npeers;
     p.scale_dev = scale_out;
     p.probe = g_probe;
     {
@@ -331,6 +335,21 @@ rsr_status rsr_matvec(const rsr_stream_view *view, const void *v, int32_t v_dtyp
     if (v_dtype == RSR_F32 || v_dtype == RSR_BF16 || v_dtype == RSR_F16)
         return launch_mv<MODE_FLOAT>(view, v, v_dtype, y, accumulate, 1.0, nullptr, workspace,
                                      workspace_bytes, s);
+    return RSR_ERR_INVALID;
+}
+
+rsr_status rsr_matvec_peers(const rsr_stream_view *view, const void *v, int32_t v_dtype,
+                            void *const *y_peers, int32_t npeers, void *workspace,
+                            size_t workspace_bytes, rsr_stream_t stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (npeers < 1 || !y_peers) return RSR_ERR_INVALID;
+    if (v_dtype == RSR_I8)
+        return launch_mv<MODE_INT>(view, v, v_dtype, nullptr, 0, 1.0, nullptr, workspace,
+                                   workspace_bytes, s, nullptr, 0, nullptr, 0.f, y_peers, npeers);
+    if (v_dtype == RSR_F32 || v_dtype == RSR_BF16 || v_dtype == RSR_F16)
+        return launch_mv<MODE_FLOAT>(view, v, v_dtype, nullptr, 0, 1.0, nullptr, workspace,
+                                     workspace_bytes, s, nullptr, 0, nullptr, 0.f, y_peers,
+                                     npeers);
     return RSR_ERR_INVALID;
 }
 

@@ -94,7 +94,22 @@ struct MvParams {
     unsigned long long *probe;  // debug timeline (rsr_debug_set_probe), null in production
     const uint16_t *norm_w;  // fused: RMSNorm weight (bf16, n) applied before quantizing, or null
     float norm_eps;
+    // all-gather over peer memory (rsr_matvec_peers): every output row is
+    // stored to each of npeers buffers (this view's row 0 inside each
+    // rank's full output; peers mapped into this device's address space)
+    void *const *y_peers;
+    int npeers;
 };
+
+// The output store: this view's row r into y, or into every peer's buffer.
+template <class T>
+__device__ __forceinline__ void put_row(const MvParams &p, int64_t r, T x) {
+    if (p.npeers) {
+        for (int j = 0; j < p.npeers; ++j) reinterpret_cast<T *>(p.y_peers[j])[r] = x;
+    } else {
+        reinterpret_cast<T *>(p.y)[r] = x;
+    }
+}
 
 // CTA-wide sum of one float per thread, fixed order (identical in every CTA
 // of the same shape); the result is broadcast to every thread.

@@ -651,15 +651,15 @@ rsr_mv_kernel(MvParams p) {
                 reinterpret_cast<Acc *>(p.part)[t * rows_view + r] = mine;
             } else if constexpr (MODE == MODE_FLOAT) {
                 float *y = reinterpret_cast<float *>(p.y);
-                y[r] = p.accumulate ? y[r] + (float)mine : (float)mine;
+                put_row<float>(p, r, p.accumulate ? y[r] + (float)mine : (float)mine);
             } else if constexpr (MODE == MODE_INT) {
                 int32_t *y = reinterpret_cast<int32_t *>(p.y);
-                y[r] = p.accumulate ? y[r] + (int32_t)mine : (int32_t)mine;
+                put_row<int32_t>(p, r, p.accumulate ? y[r] + (int32_t)mine : (int32_t)mine);
             } else {
                 const double beta = p.row_beta ? p.row_beta[grow0 + lane] : p.beta;
                 const float o = (float)((double)(int32_t)mine * (beta / scale));
-                if (p.out_bf16) reinterpret_cast<__nv_bfloat16 *>(p.y)[r] = __float2bfloat16_rn(o);
-                else reinterpret_cast<float *>(p.y)[r] = o;
+                if (p.out_bf16) put_row<__nv_bfloat16>(p, r, __float2bfloat16_rn(o));
+                else put_row<float>(p, r, o);
             }
         }
     };

@@ -1,4 +1,5 @@
-"""Row-block sharding across GPUs with an NCCL all-gather of output slices.
+"""Row-block sharding across GPUs; the output slices are all-gathered either
+by the multiply itself over peer memory (gather="peer") or by NCCL.
 
 SURVEY.md section 8e / row K10 (not in the reference, which is one CPU
 process).  Row blocks own disjoint output rows (_native.py:
@@ -11,6 +12,16 @@ shard).
 
 Each rank materializes only its own strip of the matrix (``strip_fn``), so a
 131072^2 matrix never exists on one device when sharded.
+
+Gather.  gather="nccl": local multiply into a padded slice, one
+all_gather_into_tensor, an index_select back to row order.  gather="peer":
+the full output lives in symmetric memory (torch.distributed.
+_symmetric_memory: every rank's buffer mapped into every device's address
+space), and the multiply's epilogue stores each row straight into all ranks'
+buffers at its global row (rsr_matvec_peers) -- the all-gather rides on the
+multiply's own stores over NVLink, no separate collective and no reassembly
+-- followed by one symmetric-memory barrier.  Two buffers alternate, so a
+result stays valid until the call after next.
 
 Balance.  By default the ranks get equal numbers of row blocks, which for
 matrices with uniform density (the synthetic C5 matrix) is also an equal
@@ -51,6 +62,11 @@ def row_ranges(m: int, k: int, world: int, weights=None) -> list[tuple[int, int]
     return [(b0 * k, min(b1 * k, m)) for b0, b1 in block_ranges(bc, world, weights)]
 
 
+def peer_row_addresses(base_ptrs, r0: int, elem_size: int) -> list[int]:
+    """Address of global row r0 inside each rank's full output buffer."""
+    return [int(b) + int(r0) * int(elem_size) for b in base_ptrs]
+
+
 def gather_index(ranges: list[tuple[int, int]], pad: int):
     """Index of the full output's rows inside the flattened [world, pad]
     all-gather buffer."""
@@ -67,8 +83,12 @@ class ShardedMatrix:
 
     def __init__(self, m: int, n: int, bitwidth: str, k: int, strip_fn, rank: int, world: int,
                  device=None, group=None, weight_scale: float = 1.0, weights=None,
-                 tile_width: int | None = None):
+                 tile_width: int | None = None, gather: str = "nccl"):
         import torch
+        if gather not in ("nccl", "peer"):
+            raise ValueError("gather must be 'nccl' or 'peer'")
+        self.gather = gather
+        self._peer: dict = {}
         self.m, self.n, self.k, self.bitwidth = m, n, k, bitwidth
         self.rank, self.world, self.group = rank, world, group
         self.plan = make_plan(m, n, k, bitwidth, tile_width)
@@ -102,11 +122,41 @@ class ShardedMatrix:
             matvec_into(self.local, v, y_local[:rows])
         return y_local
 
+    def _peer_state(self, dtype):
+        """Symmetric-memory output buffers for `dtype` (collective on first
+        use: every rank must make the same calls in the same order)."""
+        st = self._peer.get(dtype)
+        if st is None:
+            import torch
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+            group = self.group if self.group is not None else dist.group.WORLD
+            esz = torch.empty((), dtype=dtype).element_size()
+            bufs = []
+            for _ in range(2):
+                y = symm.empty(self.m, dtype=dtype, device=self.device)
+                h = symm.rendezvous(y, group)
+                rows = torch.tensor(peer_row_addresses(h.buffer_ptrs, self.r0, esz),
+                                    dtype=torch.int64, device=self.device)
+                bufs.append((y, h, rows))
+            st = self._peer[dtype] = {"bufs": bufs, "i": 0}
+        return st
+
     def matvec(self, v, fused: bool = False, buffers=None):
-        """Full y on every rank: local multiply + all-gather (NCCL)."""
+        """Full y on every rank: local multiply + all-gather (peer stores in
+        the multiply, or NCCL)."""
         import torch
         import torch.distributed as dist
         odt = torch.int32 if (v.dtype == torch.int8 and not fused) else torch.float32
+        if self.gather == "peer" and not fused:
+            from .kernels import matvec_peers_into
+            st = self._peer_state(odt)
+            y, h, rows = st["bufs"][st["i"]]
+            st["i"] ^= 1
+            if self.local is not None:
+                matvec_peers_into(self.local, v, rows, self.world)
+            h.barrier(channel=0)
+            return y
         y_local, y_all = buffers if buffers is not None else self.buffers(odt)
         self.local_matvec(v, y_local, fused)
         if self.world > 1:

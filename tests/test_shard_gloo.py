@@ -78,3 +78,52 @@ def test_block_ranges_balance_and_cover():
     assert shard.row_ranges(12, 4, 2, np.array([5.0, 1.0, 1.0])) == [(0, 4), (4, 12)]
     idx = shard.gather_index([(0, 4), (4, 10)], 6)
     assert list(idx) == [0, 1, 2, 3, 6, 7, 8, 9, 10, 11]
+
+
+def _peer_worker(rank, world, port, m, n, k, q):
+    """gather="peer" host logic: every rank's strip lands, through
+    peer_row_addresses, at its global rows of every rank's full buffer (peer
+    memory emulated: the stores are exchanged with all_gather_object and
+    applied at the computed addresses of a flat buffer per rank)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = orc.random_matrix(m, n, "ternary", 11)
+        r0, r1 = shard.row_ranges(m, k, world)[rank]
+        vi = np.random.default_rng(5).integers(-128, 128, n).astype(np.int8)
+        rows = np.zeros(0, np.int32)
+        if r1 > r0:
+            rows = orc.matvec_i8(orc.preprocess(orc.Packed(r1 - r0, n, "ternary",
+                                                           full.data[r0:r1]), k), vi)
+        esz, base = 4, 1 << 20  # every rank's buffer at the same fake base
+        addrs = shard.peer_row_addresses([base * (j + 1) for j in range(world)], r0, esz)
+        sent = [None] * world
+        dist.all_gather_object(sent, (addrs, rows))
+        mine = np.full(m, -7, np.int64)
+        for peer_addrs, peer_rows in sent:  # the stores other ranks made into my buffer
+            start = (peer_addrs[rank] - base * (rank + 1)) // esz
+            mine[start:start + len(peer_rows)] = peer_rows
+        q.put((rank, mine))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,k", [(37, 300, 5), (5, 50, 4)])
+def test_peer_gather_addresses_gloo_world2(m, n, k):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, m, n, k, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = orc.random_matrix(m, n, "ternary", 11)
+    ref = orc.matvec_i8(orc.preprocess(full, k),
+                        np.random.default_rng(5).integers(-128, 128, n).astype(np.int8))
+    for r in range(world):
+        assert np.array_equal(outs[r], ref)
