@@ -6,8 +6,10 @@ Workloads (BASELINE.json configs):
       (rsrmv bench.py:102-113), seed 0.  A step is one matvec.
   c5  (default at N>1) ternary 131072x131072, k=6, row-block sharded across
       the ranks (each rank generates and preprocesses only its strip with the
-      device generator) + NCCL all-gather of the output slices + reassembly
-      of the full output in row order.  Strong scaling: every step is one
+      device generator); the output slices are all-gathered by the multiply
+      itself, storing its rows into every rank's symmetric-memory output
+      (--gather peer, then one barrier), or by NCCL + reassembly in row order
+      (--gather nccl).  Strong scaling: every step is one
       full 131072^2 matvec for the whole job.  The N > 1 line also carries
       the same matrix on rank 0's GPU alone, timed in the same run
       (`c5_1gpu`, `scaling_vs_1gpu_same_run`): the N = 1 bench line is the
@@ -54,7 +56,7 @@ CONFIGS = {
     "c4": dict(workload="ternary 8192x8192 RSR matvec, bf16 vector, single vector",
                m=8192, n=8192, bitwidth="ternary", k=5, vdtype="bf16", gen="numpy"),
     "c5": dict(workload="ternary 131072x131072 RSR matvec, bf16 vector, row-block sharded "
-                        "+ NCCL all-gather of outputs",
+                        "+ all-gather of outputs",
                m=131072, n=131072, bitwidth="ternary", k=6, vdtype="bf16", gen="hash",
                # 8 tiles of 16384 columns (measured on one GPU, tools/c5_tile_width.py:
                # 1.084 ms vs 1.186 at 21846, 1.361 at 32704 -- wide tiles' 64 KB v images
@@ -520,6 +522,9 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="one GPU: time the K steps as one CUDA-graph replay (pays the graph "
                          "launch once: slower than queued launches at K = 20, faster at 200)")
+    ap.add_argument("--gather", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: all-gather of the output slices by the multiply's own peer "
+                         "stores into symmetric memory (default) or by NCCL")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip cublas_bf16 / c4 / traffic sub-measurements")
     ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
@@ -626,16 +631,60 @@ def main():
     sptr = stream.cuda_stream
     y_full = torch.empty(m, dtype=torch.float32, device=dev)
 
-    def step(i, sp=None):
-        kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies],
-                       stream=sptr if sp is None else sp)
-        if world > 1:
-            dist.all_gather_into_tensor(y_all, y_local)
-            torch.index_select(y_all, 0, sm.index, out=y_full)  # full y in row order
+    # N > 1: the all-gather rides on the multiply's own stores into every
+    # rank's symmetric-memory output (--gather peer, rsr_matvec_peers) plus
+    # one barrier; NCCL all-gather + reassembly if that is unavailable
+    gather = "none"
+    if world > 1:
+        gather = args.gather
+        if gather == "peer":
+            ok = 1
+            try:
+                sm.gather = "peer"
+                pst = sm._peer_state(torch.float32)
+            except Exception as e:  # all ranks fall back together
+                print(f"[bench] symmetric-memory gather unavailable: {e}", file=sys.stderr)
+                ok = 0
+            okt = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            if not int(okt.item()):
+                gather, sm.gather = "nccl", "nccl"
+    if gather == "peer":
+        def step(i, sp=None):
+            y, h, prow = pst["bufs"][i & 1]
+            kn.matvec_peers_into(a, vt, prow, world, view=views[i % ncopies],
+                                 stream=sptr if sp is None else sp)
+            h.barrier(channel=0)  # every rank's rows are in y (row order)
+    else:
+        def step(i, sp=None):
+            kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies],
+                           stream=sptr if sp is None else sp)
+            if world > 1:
+                dist.all_gather_into_tensor(y_all, y_local)
+                torch.index_select(y_all, 0, sm.index, out=y_full)  # full y in row order
 
     for i in range(warmup):
         step(i)
     torch.cuda.synchronize()
+    if gather == "peer":
+        # one-time check against the NCCL gather; every rank falls back
+        # together if any rank's peer-gathered output differs
+        y_peer = pst["bufs"][(warmup - 1) & 1][0].clone()
+        kn.matvec_into(a, vt, y_local[:rows], view=views[0], stream=sptr)
+        dist.all_gather_into_tensor(y_all, y_local)
+        torch.index_select(y_all, 0, sm.index, out=y_full)
+        okt = torch.tensor([int(torch.equal(y_peer, y_full))], dtype=torch.int32, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if not int(okt.item()):
+            print("[bench] peer gather differs from NCCL: using NCCL", file=sys.stderr)
+            gather, sm.gather = "nccl_fallback", "nccl"
+
+            def step(i, sp=None):
+                kn.matvec_into(a, vt, y_local[:rows], view=views[i % ncopies],
+                               stream=sptr if sp is None else sp)
+                dist.all_gather_into_tensor(y_all, y_local)
+                torch.index_select(y_all, 0, sm.index, out=y_full)
+        torch.cuda.synchronize()
 
     # per-launch kernel durations (CUDA events on the launching stream)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -763,7 +812,9 @@ def main():
                "h2d_bytes_per_step": int(vh.numel() * vh.element_size()),
                "d2h_bytes_per_step": int(yh.numel() * 4),
                "api": "shard.ShardedMatrix.matvec on every rank: pinned host vector -> device, "
-                      "local multiply + NCCL all-gather + reassembly, full y -> pinned host; "
+                      + ("multiply storing into every rank's symmetric-memory output + barrier"
+                         if gather == "peer" else "local multiply + NCCL all-gather + reassembly")
+                      + ", full y -> pinned host; "
                       "max over ranks"}
 
     if rank != 0:
@@ -854,6 +905,8 @@ def main():
                                "the same call again (warm allocator)",
             "gpu_launches": args.steps * launches_per_step,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
+    if world > 1:
+        line["gather"] = gather
     line.update(extras)
     line["decode"] = decode
     line["clocks"] = clk.summary()

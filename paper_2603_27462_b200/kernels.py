@@ -153,14 +153,14 @@ def matvec_into(a: RsrArtifact, vt, y, accumulate: bool = False, view=None, stre
     return y
 
 
-def matvec_peers_into(a: RsrArtifact, vt, peer_rows, npeers: int, stream=None):
+def matvec_peers_into(a: RsrArtifact, vt, peer_rows, npeers: int, view=None, stream=None):
     """Multiply and all-gather in one launch (rsr_matvec_peers): every output
     row is stored to each of `npeers` buffers.  peer_rows: int64 device
     tensor of npeers addresses, each this artifact's row 0 inside one rank's
     full output (peer memory mapped here, e.g. symmetric memory).  The caller
     synchronizes the ranks before reading (shard.ShardedMatrix does)."""
     from .matcore import _dtype_code
-    st = _launch_state(a, None)
+    st = _launch_state(a, view)
     s = _lib.current_stream_ptr(a.device) if stream is None else stream
     ws, wsb = st.workspace(s) if st.wsb else (0, 0)
     _lib.check(_lib.lib().rsr_matvec_peers(st.ref, vt.data_ptr(), _dtype_code(vt),
