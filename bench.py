@@ -637,6 +637,8 @@ def main():
     gather = "none"
     if world > 1:
         gather = args.gather
+        if os.environ.get("RSR_BENCH_ONE_DEVICE"):
+            gather = "nccl"  # ranks sharing one GPU must not spin on each other's barrier
         if gather == "peer":
             ok = 1
             try:
