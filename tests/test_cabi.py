@@ -56,6 +56,12 @@ def test_host_queries_need_no_gpu():
     assert L.rsr_group_count(None, 4, 4, 1, 1, 11, 4, None, None, None, None, None, 0,
                              None) == _lib.RSR_ERR_K_TOO_LARGE
     assert L.rsr_matvec(ctypes.byref(v), None, 0, None, 0, None, 0, None) == _lib.RSR_ERR_INVALID
+    # the peer-store form needs a peer table and at least one peer
+    assert L.rsr_matvec_peers(ctypes.byref(v), None, 0, None, 2, None, 0, None) == \
+        _lib.RSR_ERR_INVALID
+    fake = (ctypes.c_void_p * 1)(1)
+    assert L.rsr_matvec_peers(ctypes.byref(v), None, 0, fake, 0, None, 0, None) == \
+        _lib.RSR_ERR_INVALID
     # tensor-core code matrix: u16 per (8-row group, column), columns padded to 64
     assert L.rsr_keymat_bytes(1639, 8192, 1, 5) == 128 * 1025 * 64 * 2   # C4: 16.8 MB
     assert L.rsr_keymat_bytes(3, 65, 0, 8) == 24 * 64                      # one 256-column step, 24 rows
