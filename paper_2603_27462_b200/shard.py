@@ -144,7 +144,9 @@ class ShardedMatrix:
 
     def matvec(self, v, fused: bool = False, buffers=None):
         """Full y on every rank: local multiply + all-gather (peer stores in
-        the multiply, or NCCL)."""
+        the multiply, or NCCL).  With gather="peer" the result is one of two
+        alternating symmetric-memory buffers: valid until the call after
+        next (clone it to keep it longer)."""
         import torch
         import torch.distributed as dist
         odt = torch.int32 if (v.dtype == torch.int8 and not fused) else torch.float32
