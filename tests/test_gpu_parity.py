@@ -195,6 +195,27 @@ def test_c2_full_size_bit_exact_vs_reference(rsr):
                           gd.large_output(name + "_fused_bf16v"))
 
 
+@pytest.mark.parametrize("seed", [1, 2])
+def test_c2_full_size_other_seeds_vs_oracle(rsr, seed):
+    """C2 at seeds 1 and 2 as well -- the GPU artifact equals the
+    oracle's preprocess array for array, the int path is exact, the float
+    path meets the tolerance and the fused path equals the oracle's."""
+    import torch
+    p = orc.random_matrix(16384, 16384, "ternary", seed)
+    a = rsr.preprocess(rsr.PackedMatrix(16384, 16384, "ternary", p.data), 6)
+    ref = orc.preprocess(p, 6)
+    for name in ("words", "perm", "group_offsets", "perm_offsets"):
+        assert np.array_equal(getattr(a, name), getattr(ref, name)), name
+    vi = gd.int_vector(16384, seed)
+    assert np.array_equal(rsr.rsr_matvec(a, vi), orc.matvec_i8(ref, vi, threads=8))
+    vf = orc.random_vector(16384, seed)
+    vb = torch.from_numpy(vf).cuda().to(torch.bfloat16)
+    vr = gd.bf16_round(vf)
+    y = rsr.rsr_matvec(a, vb).cpu().numpy()
+    assert float_ok(y, orc.matvec_f64(ref, vr, threads=8), orc.decode(p), vr).all()
+    assert np.array_equal(rsr.rsr_matvec_fused(a, vb).cpu().numpy(), orc.fused_matvec(ref, vr))
+
+
 @pytest.mark.parametrize("n,tw,k,bw", [(40000, None, 5, "ternary"), (65536, None, 4, "binary"),
                                        (70000, None, 6, "ternary"), (30000, 20000, 7, "ternary"),
                                        (3000, None, 9, "ternary"), (2000, None, 13, "binary"),
