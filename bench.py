@@ -339,6 +339,8 @@ def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
     views = [a.view(entries=e, e_off=o) for e, o in copies]
     km = a.keymat()
     kms = [km] + ([km.clone() for _ in range(3)] if km is not None else [])
+    kw = a.keymat("wide")  # B <= 16: the 256-column-step kernel's code matrix
+    kmw = [kw] + ([kw.clone() for _ in range(3)] if kw is not None else [])
     dense = dense_device(pm).to(torch.bfloat16)
     Wb = [dense, dense.clone()]  # 2 x 134 MB > L2
     Wi = [dense.to(torch.int8), dense.to(torch.int8)]  # 2 x 67 MB
@@ -351,6 +353,7 @@ def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
         def ours(i):
             if kms:
                 a.__dict__["_keymat"] = kms[i % 4]
+                a.__dict__["_keymat_wide"] = kmw[i % 4]
             kn.matmul_into(a, V, Y, view=views[i % 4])
         us = graph_time_us(ours)
         Yd = torch.empty(B, m, dtype=torch.bfloat16, device="cuda")
@@ -380,6 +383,7 @@ def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
         rows.append(row)
     if kms:
         a.__dict__["_keymat"] = kms[0]
+        a.__dict__["_keymat_wide"] = kmw[0]
     del Wb, Wi, dense
     torch.cuda.empty_cache()
     return {"workload": "ternary 8192x8192, k=5, bf16 vectors [B, 8192] -> f32 [B, 8192]",

@@ -282,6 +282,20 @@ size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t bl
  * prefix of the same size); rsr_matmul_tc_i8: Y[b] (int32) = A . V[b] for int8
  * V[b*ldv + col] (V 16-byte aligned, ldv a multiple of 16), bit-exact with
  * the integer path of rsr_matvec per column.                                */
+/* rsr_keymat_build_wide / rsr_matmul_tc_wide: bf16 batches of B <= 16 with
+ * 256-column pipeline steps (half the per-step commits and barriers of
+ * rsr_matmul_tc): the code matrix in the int8 path's layout (256-column
+ * steps, rsr_keymat_bytes) with the bf16 path's bit order.  Same arguments,
+ * results and determinism as rsr_matmul_tc.                                 */
+rsr_status rsr_keymat_build_wide(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                                 const int64_t *po, int64_t block_count, int64_t tile_count,
+                                 int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
+                                 void *keymat_wide, rsr_stream_t stream);
+rsr_status rsr_matmul_tc_wide(const void *keymat_wide, int64_t m, int64_t n, int32_t bitwidth,
+                              int32_t k, int64_t block_begin, int64_t n_blocks, const void *V,
+                              int32_t v_dtype, int64_t ldv, int32_t B, float *Y, int64_t ldy,
+                              void *workspace, size_t workspace_bytes, rsr_stream_t stream);
+
 rsr_status rsr_keymat_build_i8(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                                const int64_t *po, int64_t block_count, int64_t tile_count,
                                int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,

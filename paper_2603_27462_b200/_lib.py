@@ -78,6 +78,9 @@ SIGNATURES = {
     "rsr_matmul_tc_workspace_bytes": (SZ, [I64, I64, I32, I64, I64, I32]),
     "rsr_matmul_tc": (I32, [P, I64, I64, I32, I32, I64, I64, P, I32, I64, I32, P, I64, P, SZ, P]),
     "rsr_keymat_build_i8": (I32, [P, P, P, P, I64, I64, I64, I64, I32, I32, P, P]),
+    "rsr_keymat_build_wide": (I32, [P, P, P, P, I64, I64, I64, I64, I32, I32, P, P]),
+    "rsr_matmul_tc_wide": (I32, [P, I64, I64, I32, I32, I64, I64, P, I32, I64, I32, P, I64, P, SZ,
+                                 P]),
     "rsr_matmul_tc_i8": (I32, [P, I64, I64, I32, I32, I64, I64, P, I64, I32, P, I64, P, SZ, P]),
     "rsr_matmul_tc_i8_dequant": (I32, [P, I64, I64, I32, I32, I64, I64, P, I64, I32, P, P, F64,
                                        P, I32, I64, P, SZ, P]),

@@ -95,7 +95,7 @@ __device__ __forceinline__ uint32_t tc_code_bit_i8(uint32_t c) {
 // ---- code matrix: KM[step][row][q] (see the header) from the artifact's
 // groups: each column of a cell's group carries the group's pattern key; row
 // r0 + i gets code (pos_i, neg_i)
-template <bool I8>
+template <bool I8, bool W2 = false>
 __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t *__restrict__ go,
                               const uint16_t *__restrict__ perm, const int64_t *__restrict__ po,
                               int64_t bc, int64_t tc, int64_t tw, int k, int64_t rows_pad,
@@ -115,11 +115,12 @@ __global__ void keymat_kernel(const uint64_t *__restrict__ words, const int64_t 
                 const int64_t col = c0 + cols[j];
                 const uint32_t bit =
                     I8 ? tc_code_bit_i8((uint32_t)col & 15) : tc_code_bit((uint32_t)col & 15);
-                uint32_t *dst = I8 ? km32 + ((col >> 8) * rows_pad + r0) * 16 + ((col & 255) >> 4)
-                                   : km32 + ((col >> 7) * rows_pad + r0) * 8 + ((col & 127) >> 4);
+                uint32_t *dst = I8 || W2
+                                    ? km32 + ((col >> 8) * rows_pad + r0) * 16 + ((col & 255) >> 4)
+                                    : km32 + ((col >> 7) * rows_pad + r0) * 8 + ((col & 127) >> 4);
                 for (int i = 0; i < k; ++i) {
                     const uint32_t code = ((pos >> i) & 1u) | (((neg >> i) & 1u) << 1);
-                    if (code) atomicOr(dst + (int64_t)i * (I8 ? 16 : 8), code << bit);
+                    if (code) atomicOr(dst + (int64_t)i * (I8 || W2 ? 16 : 8), code << bit);
                 }
             }
         }
@@ -297,7 +298,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32
 // (DSMEM stores, one cluster barrier); larger N parks the accumulator in the
 // CTA's idle load ring and the owners read it through DSMEM.  No partials
 // in global memory, one launch per call.
-template <int NP, bool I8>
+template <int NP, bool I8, bool W2 = false>
 __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_constant__ TcParams p) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     __shared__ uint32_t tmem_base_sh;
@@ -315,10 +316,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     // smem: per load stage [B tile: 2 K-halves x N x 128 B][codes 128 rows x 32 B]
     // int8 steps take 256 columns: the same 256-byte B rows and twice the
     // code bytes, so the per-step overheads are paid half as often
-    constexpr int KS = I8 ? 2 * TC_K : TC_K;   // columns per step
-    constexpr int RB = I8 ? 2 * TC_RB : TC_RB;  // code bytes per (step, row)
+    // W2 (bf16, N = 16): 256-column steps too -- a 128-column TMEM stage,
+    // four 64-column B boxes, 16 MMAs per commit
+    constexpr int KS = I8 || W2 ? 2 * TC_K : TC_K;   // columns per step
+    constexpr int RB = I8 || W2 ? 2 * TC_RB : TC_RB;  // code bytes per (step, row)
     constexpr uint32_t B_BYTES = (uint32_t)N * KS * (I8 ? 1 : 2);
-    constexpr uint32_t ASC = 64u;  // TMEM columns per A stage (128 bf16 pairs / 256 int8 quads)
+    constexpr int NBOX = (int)(KS * (I8 ? 1 : 2) / 128);  // 128-byte column boxes per B row
+    // TMEM columns per A stage (128 bf16 pairs / 256 int8 quads; W2: 256 bf16)
+    constexpr uint32_t ASC = W2 ? 128u : 64u;
     constexpr uint32_t C_BYTES = TC_M * RB;
     // shared memory: the codes ring [LS x 4 KB] (freed by the expanders),
     // then the B ring [AS x B tile] that pairs with the TMEM A ring (one MMA
@@ -385,9 +390,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 if (it >= AS) mbar_wait_parity(bar_free + 8 * a, apar ^ 1u);
                 const uint32_t ba = bbase + a * B_BYTES, fb = bar_bfull + 8 * a;
                 mbar_expect_tx(fb, B_BYTES);
-                // two boxes of 128 bytes of columns (64 bf16 / 128 int8)
-                tma_2d(ba, &p.tm_v, (int)st * KS, 0, fb);
-                tma_2d(ba + B_BYTES / 2, &p.tm_v, (int)st * KS + KS / 2, 0, fb);
+                // boxes of 128 bytes of columns (64 bf16 / 128 int8)
+#pragma unroll
+                for (int j = 0; j < NBOX; ++j)
+                    tma_2d(ba + j * (B_BYTES / NBOX), &p.tm_v, (int)st * KS + j * (KS / NBOX), 0,
+                           fb);
                 s += J;
                 if (s >= LS) {
                     s -= LS;
@@ -450,11 +457,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                                   idesc, (!first || kk > 0) ? 1u : 0u);
                 } else {
 #pragma unroll
-                    for (int kk = 0; kk < TC_K / 16; ++kk)
+                    for (int kk = 0; kk < KS / 16; ++kk)
                         mma_bf16_ts(
                             td, ta + 8u * kk,
-                            db + (uint64_t)(((kk >> 2) * (B_BYTES / 2) + (kk & 3) * 32) >> 4), idesc,
-                            (!first || kk > 0) ? 1u : 0u);
+                            db + (uint64_t)(((kk >> 2) * (B_BYTES / NBOX) + (kk & 3) * 32) >> 4),
+                            idesc, (!first || kk > 0) ? 1u : 0u);
                 }
                 // one commit frees the A stage and its B tile
                 mma_commit(bar_free + 8 * a);
@@ -493,7 +500,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
             TC_MARK(tid == 0 && it < 64, it * 8 + 0)
             const uint4 x = *reinterpret_cast<const uint4 *>(codes0 + s * C_BYTES);
             uint4 x2 = make_uint4(0, 0, 0, 0);
-            if (I8) x2 = *reinterpret_cast<const uint4 *>(codes0 + s * C_BYTES + 16);
+            if (I8 || W2) x2 = *reinterpret_cast<const uint4 *>(codes0 + s * C_BYTES + 16);
             mbar_arrive(bar_cempty + 8 * s);  // (release: the loads are ordered before)
             if (I8) {
                 // 128 columns: two code words -> 32 int8-quad words
@@ -511,6 +518,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
                 TC_MARK(tid == 0 && it < 64, it * 8 + 5)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 tmem_st32(t_row + ASC * a, w);
+                if (W2) {  // the half's second 64 columns
+                    expand64(x2, w, tab0, tab1, c0404);
+                    tmem_st32(t_row + ASC * a + 32u, w);
+                }
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             TC_MARK(tid == 0 && it < 64, it * 8 + 6)
@@ -727,10 +738,11 @@ struct TcRings {
 // Ring depths within 216 KB of shared memory and the TMEM left after the
 // accumulator: the A / B ring as deep as both allow (at most TC_AMAX), the
 // codes ring with the rest (at most TC_LMAX); both at least TC_GROUPS.
-static TcRings tc_rings(int N, bool i8) {
-    const size_t bbytes = (size_t)N * TC_K * 2, cbytes = (size_t)TC_M * TC_RB * (i8 ? 2 : 1);
+static TcRings tc_rings(int N, bool i8, bool w2 = false) {
+    const size_t bbytes = (size_t)N * TC_K * 2 * (w2 ? 2 : 1);
+    const size_t cbytes = (size_t)TC_M * TC_RB * (i8 || w2 ? 2 : 1);
     const size_t budget = 216 * 1024 - tc_recv_bytes(N);
-    const int a_col = std::max(N, 64), asc = 64;
+    const int a_col = std::max(N, 64), asc = w2 ? 128 : 64;
     TcRings r;
     r.as = std::min<int>(TC_AMAX, (512 - a_col) / asc);
     r.as = std::max<int>(TC_GROUPS,
@@ -805,7 +817,7 @@ size_t rsr_keymat_bytes(int64_t block_count, int64_t cols, int32_t bitwidth, int
 
 }  // extern "C"
 
-template <bool I8>
+template <bool I8, bool W2 = false>
 static rsr_status keymat_build(const uint64_t *words, const int64_t *go, const uint16_t *perm,
                                const int64_t *po, int64_t block_count, int64_t tile_count,
                                int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
@@ -817,7 +829,7 @@ static rsr_status keymat_build(const uint64_t *words, const int64_t *go, const u
     cudaMemsetAsync(keymat, 0, bytes, s);
     const int64_t cells = block_count * tile_count;
     const int grid = (int)std::min<int64_t>((cells * 32 + 255) / 256, (int64_t)sm_count() * 16);
-    keymat_kernel<I8><<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count,
+    keymat_kernel<I8, W2><<<grid, 256, 0, s>>>(words, go, perm, po, block_count, tile_count,
                                            tile_width, k, tc_rows_pad(block_count, k),
                                            (uint32_t *)keymat);
     return launch_status();
@@ -831,6 +843,14 @@ rsr_status rsr_keymat_build(const uint64_t *words, const int64_t *go, const uint
                             void *keymat, rsr_stream_t stream) {
     return keymat_build<false>(words, go, perm, po, block_count, tile_count, tile_width, cols,
                                bitwidth, k, keymat, stream);
+}
+
+rsr_status rsr_keymat_build_wide(const uint64_t *words, const int64_t *go, const uint16_t *perm,
+                                 const int64_t *po, int64_t block_count, int64_t tile_count,
+                                 int64_t tile_width, int64_t cols, int32_t bitwidth, int32_t k,
+                                 void *keymat, rsr_stream_t stream) {
+    return keymat_build<false, true>(words, go, perm, po, block_count, tile_count, tile_width,
+                                     cols, bitwidth, k, keymat, stream);
 }
 
 rsr_status rsr_keymat_build_i8(const uint64_t *words, const int64_t *go, const uint16_t *perm,
@@ -887,7 +907,7 @@ size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t bl
 
 }  // extern "C"
 
-template <bool I8>
+template <bool I8, bool W2 = false>
 static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
                             int64_t block_begin, int64_t n_blocks, const void *V, int64_t ldv,
                             int32_t B, void *Y, int64_t ldy, void *workspace,
@@ -907,6 +927,7 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
         return RSR_ERR_WORKSPACE;
     const int np = tc_np(B);
+    if (W2 && np != 1) return RSR_ERR_INVALID;  // the wide steps serve N = 16 only
     TcParams p;
     p.km = (const uint32_t *)keymat;
     if (!tc_encode_v(&p.tm_v, V, n, B, ldv, 16 * np, I8)) return RSR_ERR_INVALID;
@@ -922,11 +943,11 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     p.rows_pad = tc_rows_pad(bc, k);
     p.B = B;
     p.N = 16 * np;
-    p.S = tc_steps(n, I8);
+    p.S = tc_steps(n, I8 || W2);
     // TMEM (all 512 columns): the accumulator [0, N) (64-column aligned),
     // then the A ring: one step's 128 K elements per stage (64 columns of
     // bf16 pairs, 32 of int8 quads)
-    const TcRings rings = tc_rings(p.N, I8);
+    const TcRings rings = tc_rings(p.N, I8, W2);
     p.ls = rings.ls;
     p.as = rings.as;
     p.recv_off = (uint32_t)(rings.smem - tc_recv_bytes(p.N));
@@ -968,10 +989,10 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
         const char *e = getenv("RSR_TC_KSPLIT");
         return e ? atoi(e) : 0;
     }();
-    const int key_np = np + (I8 ? 1000 : 0);
+    const int key_np = np + (I8 ? 1000 : 0) + (W2 ? 2000 : 0);
 #define RSR_TC_LAUNCH(NPV)                                                                      \
     {                                                                                          \
-        auto kern = rsr_tc_kernel<NPV, I8>;                                                    \
+        auto kern = rsr_tc_kernel<NPV, I8, W2>;                                                    \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
         int ks = tc_ks_cached(key_np, tiles, p.S, smem);                                       \
         if (ks == 0) { /* first launch of this shape: one CTA per SM, checked once */          \
@@ -1002,12 +1023,16 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
         cfg.gridDim = dim3((unsigned)(tiles * ks));                                            \
         cudaLaunchKernelEx(&cfg, kern, p);                                                     \
     }
-    switch (np) {
-        case 1: RSR_TC_LAUNCH(1) break;
-        case 2: RSR_TC_LAUNCH(2) break;
-        case 4: RSR_TC_LAUNCH(4) break;
-        case 8: RSR_TC_LAUNCH(8) break;
-        default: RSR_TC_LAUNCH(16) break;
+    if constexpr (W2) {
+        RSR_TC_LAUNCH(1)
+    } else {
+        switch (np) {
+            case 1: RSR_TC_LAUNCH(1) break;
+            case 2: RSR_TC_LAUNCH(2) break;
+            case 4: RSR_TC_LAUNCH(4) break;
+            case 8: RSR_TC_LAUNCH(8) break;
+            default: RSR_TC_LAUNCH(16) break;
+        }
     }
 #undef RSR_TC_LAUNCH
     return launch_status();
@@ -1023,6 +1048,18 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
     if (v_dtype != RSR_BF16) return RSR_ERR_INVALID;
     return tc_launch<false>(keymat, m, n, k, block_begin, n_blocks, V, ldv, B, Y, ldy, workspace,
                             workspace_bytes, stream);
+}
+
+// bf16 batches of B <= 16 over the wide code matrix (rsr_keymat_build_wide):
+// 256-column steps, half the per-step commits and barriers
+rsr_status rsr_matmul_tc_wide(const void *keymat_wide, int64_t m, int64_t n, int32_t bitwidth,
+                              int32_t k, int64_t block_begin, int64_t n_blocks, const void *V,
+                              int32_t v_dtype, int64_t ldv, int32_t B, float *Y, int64_t ldy,
+                              void *workspace, size_t workspace_bytes, rsr_stream_t stream) {
+    (void)bitwidth;
+    if (v_dtype != RSR_BF16 || B > 16) return RSR_ERR_INVALID;
+    return tc_launch<false, true>(keymat_wide, m, n, k, block_begin, n_blocks, V, ldv, B, Y, ldy,
+                                  workspace, workspace_bytes, stream);
 }
 
 rsr_status rsr_matmul_tc_i8(const void *keymat_i8, int64_t m, int64_t n, int32_t bitwidth,

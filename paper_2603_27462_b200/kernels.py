@@ -431,6 +431,9 @@ def _fused_host_locked(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
 # CUDA-core batched stream kernel covers the rest
 SINGLE_MAX_BATCH = 2
 TC_MIN_BATCH = 2
+# bf16 batches up to this size take the 256-column-step kernel (N = 16);
+# RSR_TC_WIDE=0 turns it off (A/B experiments)
+TC_WIDE_MAX_BATCH = 16 if os.environ.get("RSR_TC_WIDE", "1") != "0" else 0
 
 
 def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "auto"):
@@ -471,6 +474,13 @@ def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "au
                                               Vt.data_ptr(), Vt.stride(0), B, Y.data_ptr(),
                                               Y.stride(0), _lib.ptr(ws), wsb, s),
                            "rsr_matmul_tc_i8")
+            elif B <= TC_WIDE_MAX_BATCH:
+                # 256-column steps over the wide code matrix (N = 16)
+                _lib.check(L.rsr_matmul_tc_wide(_lib.ptr(a.keymat("wide")), a.m, a.n,
+                                                vw.bitwidth, a.k, vw.row_begin_block,
+                                                vw.n_blocks, Vt.data_ptr(), _lib.RSR_BF16,
+                                                Vt.stride(0), B, Y.data_ptr(), Y.stride(0),
+                                                _lib.ptr(ws), wsb, s), "rsr_matmul_tc_wide")
             else:
                 _lib.check(L.rsr_matmul_tc(_lib.ptr(a.keymat()), a.m, a.n, vw.bitwidth, a.k,
                                            vw.row_begin_block, vw.n_blocks, Vt.data_ptr(),

@@ -238,10 +238,12 @@ class RsrArtifact:
         (device u32 [ceil(n/128)][round8(bc*k)][8], 128 columns per row and
         step, in the permuted order of csrc/rsr_tc.cu for the bf16 ("bf16")
         or the int8 ("i8") tensor-core multiply: a tile's step is one
-        contiguous run of rows), built on first use; None when k > 16."""
-        attr = "_keymat" if kind == "bf16" else "_keymat_i8"
-        if kind not in ("bf16", "i8"):
+        contiguous run of rows; "wide": the bf16 order in the int8 path's
+        256-column steps, for bf16 batches of at most 16 vectors), built on
+        first use; None when k > 16."""
+        if kind not in ("bf16", "i8", "wide"):
             raise ValueError(f"unknown code-matrix kind {kind!r}")
+        attr = {"bf16": "_keymat", "i8": "_keymat_i8", "wide": "_keymat_wide"}[kind]
         if attr not in self.__dict__:
             import torch
             L = _lib.lib()
@@ -251,7 +253,8 @@ class RsrArtifact:
             km = None
             if nb:
                 km = torch.empty(nb, dtype=torch.uint8, device=self.device)
-                build = L.rsr_keymat_build if kind == "bf16" else L.rsr_keymat_build_i8
+                build = {"bf16": L.rsr_keymat_build, "i8": L.rsr_keymat_build_i8,
+                         "wide": L.rsr_keymat_build_wide}[kind]
                 _lib.check(build(
                     _lib.ptr(self.words_d), _lib.ptr(self.go_d), _lib.ptr(self.perm_d),
                     _lib.ptr(self.po_d), p.block_count, p.tile_count, p.tile_width, self.n,

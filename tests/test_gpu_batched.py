@@ -257,6 +257,62 @@ def test_code_matrix_layout_i8(rsr, m, n, k, bw, tw):
     assert np.array_equal(km.reshape(steps, rows_pad, 16).astype(np.int64), exp)
 
 
+@pytest.mark.parametrize("m,n,k,bw,tw", [
+    (101, 300, 5, "ternary", None),
+    (50, 333, 12, "binary", 100),
+    (37, 5000, 3, "ternary", 2048),
+])
+def test_code_matrix_layout_wide(rsr, m, n, k, bw, tw):
+    """The wide bf16 code matrix (B <= 16): the int8 layout's 256-column
+    steps, u32 [col // 256][row][(col % 256) // 16], with the bf16 bit order
+    of test_code_matrix_layout inside each 16-column word."""
+    p = orc.random_matrix(m, n, bw, 5 * m + n)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, bw, p.data), k, tw)
+    km = a.keymat("wide").cpu().numpy().view(np.uint32)
+    dense = orc.decode(p).astype(np.int64)
+    code = np.where(dense == 1, 1, np.where(dense == -1, 2, 0))
+    steps, rows_pad = (n + 255) // 256, (a.plan.block_count * k + 7) // 8 * 8
+    assert km.size == steps * rows_pad * 16
+    exp = np.zeros((steps, rows_pad, 16), np.int64)
+    for c in range(n):
+        j = (c % 16) // 2
+        bit = 8 * (2 * (j // 4) + c % 2) + 2 * (j % 4)
+        exp[c // 256, :m, (c % 256) // 16] |= code[:, c] << bit
+    assert np.array_equal(km.reshape(steps, rows_pad, 16).astype(np.int64), exp)
+
+
+@pytest.mark.parametrize("m,n,B", [(300, 1000, 16), (1000, 9000, 3), (130, 264, 1), (64, 4096, 9)])
+def test_tensor_core_wide_steps_match_narrow(rsr, m, n, B):
+    """bf16 batches of B <= 16 take 256-column steps (rsr_matmul_tc_wide):
+    each column within the float tolerance of the exact product, and within
+    a few fp32 ulps of the 128-column-step kernel (same products, the step
+    boundaries move the partial sums)."""
+    import torch
+    from paper_2603_27462_b200 import _lib
+    p = orc.random_matrix(m, n, "ternary", m + 3 * n)
+    a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", p.data), 5)
+    V = torch.randn(B, n, device="cuda").to(torch.bfloat16)
+    L = _lib.lib()
+    Yw = torch.empty(B, m, device="cuda")
+    Yn = torch.empty(B, m, device="cuda")
+    ws = torch.empty(256, dtype=torch.uint8, device="cuda")
+    s = _lib.current_stream_ptr(a.device)
+    for fn, km, Y in ((L.rsr_matmul_tc_wide, a.keymat("wide"), Yw), (L.rsr_matmul_tc, a.keymat(), Yn)):
+        assert fn(_lib.ptr(km), m, n, 1, 5, 0, a.plan.block_count, V.data_ptr(), _lib.RSR_BF16,
+                  V.stride(0), B, Y.data_ptr(), Y.stride(0), ws.data_ptr(), 256, s) == 0
+    torch.cuda.synchronize()
+    dense = orc.decode(p).astype(np.float64)
+    Vh = V.float().cpu().numpy().astype(np.float64)
+    ref = Vh @ dense.T
+    cond = np.abs(Vh) @ np.abs(dense).T
+    for Y in (Yw, Yn):
+        err = np.abs(Y.cpu().numpy() - ref)
+        assert (err <= 1e-6 * cond + 1e-6 * np.abs(ref)).all()
+    assert L.rsr_matmul_tc_wide(_lib.ptr(a.keymat("wide")), m, n, 1, 5, 0, a.plan.block_count,
+                                V.data_ptr(), _lib.RSR_BF16, V.stride(0), 17, Yw.data_ptr(),
+                                Yw.stride(0), ws.data_ptr(), 256, s) == _lib.RSR_ERR_INVALID
+
+
 @pytest.mark.parametrize("offset,pad", [(1, 3), (16, 16), (0, 7)])
 def test_tensor_core_int8_strided_vectors(rsr, offset, pad):
     """int8 rows off a 16-byte boundary or with a pitch not a multiple of 16

@@ -15,6 +15,7 @@ m = n = 8192
 data = bench.random_packed(m, n, "ternary", 0)
 a = rsr.preprocess(rsr.PackedMatrix(m, n, "ternary", data), 5)
 kms = [a.keymat()] + [a.keymat().clone() for _ in range(3)]
+kmw = [a.keymat("wide")] + [a.keymat("wide").clone() for _ in range(3)]
 tag = os.path.basename(os.environ.get("RSR_B200_LIB", "librsr_b200.so"))
 
 
@@ -46,5 +47,6 @@ for B in [int(x) for x in sys.argv[1:]]:
 
     def tc(i):
         a.__dict__["_keymat"] = kms[i % 4]
+        a.__dict__["_keymat_wide"] = kmw[i % 4]  # (B <= 16: the 256-column-step kernel)
         kn.matmul_into(a, V, Y, method="tc")
     print(f"{tag} B={B:4d} tc {graph_us(tc):8.2f} us", flush=True)
