@@ -339,7 +339,7 @@ def c4_bench(Bs=(1, 2, 4, 8, 16, 32, 64)):
     views = [a.view(entries=e, e_off=o) for e, o in copies]
     km = a.keymat()
     kms = [km] + ([km.clone() for _ in range(3)] if km is not None else [])
-    kw = a.keymat("wide")  # B <= 16: the 256-column-step kernel's code matrix
+    kw = a.keymat("wide")  # B <= 32: the 256-column-step kernel's code matrix
     kmw = [kw] + ([kw.clone() for _ in range(3)] if kw is not None else [])
     dense = dense_device(pm).to(torch.bfloat16)
     Wb = [dense, dense.clone()]  # 2 x 134 MB > L2

@@ -282,7 +282,7 @@ size_t rsr_matmul_tc_workspace_bytes(int64_t m, int64_t n, int32_t k, int64_t bl
  * prefix of the same size); rsr_matmul_tc_i8: Y[b] (int32) = A . V[b] for int8
  * V[b*ldv + col] (V 16-byte aligned, ldv a multiple of 16), bit-exact with
  * the integer path of rsr_matvec per column.                                */
-/* rsr_keymat_build_wide / rsr_matmul_tc_wide: bf16 batches of B <= 16 with
+/* rsr_keymat_build_wide / rsr_matmul_tc_wide: bf16 batches of B <= 32 with
  * 256-column pipeline steps (half the per-step commits and barriers of
  * rsr_matmul_tc): the code matrix in the int8 path's layout (256-column
  * steps, rsr_keymat_bytes) with the bf16 path's bit order.  Same arguments,

@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rsr_tc_kernel(const __grid_cons
     // smem: per load stage [B tile: 2 K-halves x N x 128 B][codes 128 rows x 32 B]
     // int8 steps take 256 columns: the same 256-byte B rows and twice the
     // code bytes, so the per-step overheads are paid half as often
-    // W2 (bf16, N = 16): 256-column steps too -- a 128-column TMEM stage,
+    // W2 (bf16, N <= 32): 256-column steps too -- a 128-column TMEM stage,
     // four 64-column B boxes, 16 MMAs per commit
     constexpr int KS = I8 || W2 ? 2 * TC_K : TC_K;   // columns per step
     constexpr int RB = I8 || W2 ? 2 * TC_RB : TC_RB;  // code bytes per (step, row)
@@ -927,7 +927,9 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
     if (!workspace || workspace_bytes < wsb || (reinterpret_cast<uintptr_t>(workspace) & 255))
         return RSR_ERR_WORKSPACE;
     const int np = tc_np(B);
-    if (W2 && np != 1) return RSR_ERR_INVALID;  // the wide steps serve N = 16 only
+    // the wide steps serve N <= 32 (at N = 64 the 3-deep A ring they leave
+    // costs what the halved per-step overheads save)
+    if (W2 && np > 2) return RSR_ERR_INVALID;
     TcParams p;
     p.km = (const uint32_t *)keymat;
     if (!tc_encode_v(&p.tm_v, V, n, B, ldv, 16 * np, I8)) return RSR_ERR_INVALID;
@@ -1024,7 +1026,7 @@ static rsr_status tc_launch(const void *keymat, int64_t m, int64_t n, int32_t k,
         cudaLaunchKernelEx(&cfg, kern, p);                                                     \
     }
     if constexpr (W2) {
-        RSR_TC_LAUNCH(1)
+        if (np == 1) RSR_TC_LAUNCH(1) else RSR_TC_LAUNCH(2)
     } else {
         switch (np) {
             case 1: RSR_TC_LAUNCH(1) break;
@@ -1050,14 +1052,14 @@ rsr_status rsr_matmul_tc(const void *keymat, int64_t m, int64_t n, int32_t bitwi
                             workspace_bytes, stream);
 }
 
-// bf16 batches of B <= 16 over the wide code matrix (rsr_keymat_build_wide):
+// bf16 batches of B <= 32 over the wide code matrix (rsr_keymat_build_wide):
 // 256-column steps, half the per-step commits and barriers
 rsr_status rsr_matmul_tc_wide(const void *keymat_wide, int64_t m, int64_t n, int32_t bitwidth,
                               int32_t k, int64_t block_begin, int64_t n_blocks, const void *V,
                               int32_t v_dtype, int64_t ldv, int32_t B, float *Y, int64_t ldy,
                               void *workspace, size_t workspace_bytes, rsr_stream_t stream) {
     (void)bitwidth;
-    if (v_dtype != RSR_BF16 || B > 16) return RSR_ERR_INVALID;
+    if (v_dtype != RSR_BF16 || B > 32) return RSR_ERR_INVALID;
     return tc_launch<false, true>(keymat_wide, m, n, k, block_begin, n_blocks, V, ldv, B, Y, ldy,
                                   workspace, workspace_bytes, stream);
 }

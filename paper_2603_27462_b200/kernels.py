@@ -431,9 +431,10 @@ def _fused_host_locked(a: RsrArtifact, vn: np.ndarray) -> np.ndarray:
 # CUDA-core batched stream kernel covers the rest
 SINGLE_MAX_BATCH = 2
 TC_MIN_BATCH = 2
-# bf16 batches up to this size take the 256-column-step kernel (N = 16);
+# bf16 batches up to this size take the 256-column-step kernel (N <= 32);
 # RSR_TC_WIDE=0 turns it off (A/B experiments)
-TC_WIDE_MAX_BATCH = 16 if os.environ.get("RSR_TC_WIDE", "1") != "0" else 0
+TC_WIDE_MAX_BATCH = int(os.environ.get("RSR_TC_WIDE_MAX", "32")) \
+    if os.environ.get("RSR_TC_WIDE", "1") != "0" else 0
 
 
 def matmul_into(a: RsrArtifact, Vt, Y, view=None, stream=None, method: str = "auto"):

@@ -239,7 +239,7 @@ class RsrArtifact:
         step, in the permuted order of csrc/rsr_tc.cu for the bf16 ("bf16")
         or the int8 ("i8") tensor-core multiply: a tile's step is one
         contiguous run of rows; "wide": the bf16 order in the int8 path's
-        256-column steps, for bf16 batches of at most 16 vectors), built on
+        256-column steps, for bf16 batches of at most 32 vectors), built on
         first use; None when k > 16."""
         if kind not in ("bf16", "i8", "wide"):
             raise ValueError(f"unknown code-matrix kind {kind!r}")

@@ -263,7 +263,7 @@ def test_code_matrix_layout_i8(rsr, m, n, k, bw, tw):
     (37, 5000, 3, "ternary", 2048),
 ])
 def test_code_matrix_layout_wide(rsr, m, n, k, bw, tw):
-    """The wide bf16 code matrix (B <= 16): the int8 layout's 256-column
+    """The wide bf16 code matrix (B <= 32): the int8 layout's 256-column
     steps, u32 [col // 256][row][(col % 256) // 16], with the bf16 bit order
     of test_code_matrix_layout inside each 16-column word."""
     p = orc.random_matrix(m, n, bw, 5 * m + n)
@@ -281,9 +281,10 @@ def test_code_matrix_layout_wide(rsr, m, n, k, bw, tw):
     assert np.array_equal(km.reshape(steps, rows_pad, 16).astype(np.int64), exp)
 
 
-@pytest.mark.parametrize("m,n,B", [(300, 1000, 16), (1000, 9000, 3), (130, 264, 1), (64, 4096, 9)])
+@pytest.mark.parametrize("m,n,B", [(300, 1000, 16), (1000, 9000, 3), (130, 264, 1), (64, 4096, 9),
+                                   (500, 2000, 32), (257, 1024, 17)])
 def test_tensor_core_wide_steps_match_narrow(rsr, m, n, B):
-    """bf16 batches of B <= 16 take 256-column steps (rsr_matmul_tc_wide):
+    """bf16 batches of B <= 32 take 256-column steps (rsr_matmul_tc_wide):
     each column within the float tolerance of the exact product, and within
     a few fp32 ulps of the 128-column-step kernel (same products, the step
     boundaries move the partial sums)."""
@@ -309,7 +310,7 @@ def test_tensor_core_wide_steps_match_narrow(rsr, m, n, B):
         err = np.abs(Y.cpu().numpy() - ref)
         assert (err <= 1e-6 * cond + 1e-6 * np.abs(ref)).all()
     assert L.rsr_matmul_tc_wide(_lib.ptr(a.keymat("wide")), m, n, 1, 5, 0, a.plan.block_count,
-                                V.data_ptr(), _lib.RSR_BF16, V.stride(0), 17, Yw.data_ptr(),
+                                V.data_ptr(), _lib.RSR_BF16, V.stride(0), 33, Yw.data_ptr(),
                                 Yw.stride(0), ws.data_ptr(), 256, s) == _lib.RSR_ERR_INVALID
 
 

@@ -47,6 +47,6 @@ for B in [int(x) for x in sys.argv[1:]]:
 
     def tc(i):
         a.__dict__["_keymat"] = kms[i % 4]
-        a.__dict__["_keymat_wide"] = kmw[i % 4]  # (B <= 16: the 256-column-step kernel)
+        a.__dict__["_keymat_wide"] = kmw[i % 4]  # (B <= 32: the 256-column-step kernel)
         kn.matmul_into(a, V, Y, method="tc")
     print(f"{tag} B={B:4d} tc {graph_us(tc):8.2f} us", flush=True)
